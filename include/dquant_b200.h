@@ -1,0 +1,199 @@
+/*
+ * dquant_b200.h -- C ABI of the B200-native DecoQuant hot path.
+ *
+ * Plain pointers and sizes only: every tensor argument is a DEVICE pointer
+ * (cudaMalloc / torch CUDA storage) unless its name starts with h_, every
+ * `stream` is a cudaStream_t passed as void*.  Calls are stream-ordered and
+ * never allocate: scratch comes from a caller-owned workspace whose size the
+ * matching *_workspace_size query returns.  No global mutable state beyond a
+ * thread-local error string.
+ *
+ * Status: every entry point returns DQ_OK (0) or a DQ_ERR_* code; the message
+ * is in dq_last_error().  Errors that depend on DEVICE data (non-finite input,
+ * out-of-range codes) are reported through a caller-provided device int32
+ * `flags` word (DQ_FLAG_* bits), which the host reads after the stream is
+ * synchronised -- this keeps the hot path free of host round trips.
+ *
+ * Reference interface replaced (the reference is pure Python; its "operator
+ * API" is the dquant module surface, /root/reference/pkg/src/dquant/__init__.py:10-77):
+ *   dq_plan_shapes ................ mpo.plan_shapes            mpo.py:73-96
+ *   dq_pack / dq_unpack ............ quantize.pack/unpack/unpack_range  quantize.py:66-120
+ *   dq_quantize_rtn ................ quantize.quantize_rtn      quantize.py:123-151
+ *   dq_dequantize .................. quantize.dequantize        quantize.py:154-157
+ *   dq_decompose_batched ........... mpo.decompose (n=2)        mpo.py:153-178
+ *   dq_deco_quantize_batched ....... compress.deco_quantize     compress.py:85-94
+ *   dq_deco_dequantize_batched ..... compress.deco_dequantize + mpo.reconstruct
+ *                                                              compress.py:105-107, mpo.py:181-198
+ *   dq_fused_matmul_t .............. compress.fused_matmul_t    compress.py:195-231
+ *   dq_fused_matmul ................ compress.fused_matmul      compress.py:159-192
+ *   dq_relayout .................... QuantizedTensor.payload wire order  quantize.py:11-14
+ *   dq_decode_attention ............ KvCache.attention_scores + softmax + per-segment
+ *                                    fused_matmul (kvcache.py:188-217, compress.py:159-192)
+ *   dq_tail_append ................. LayerCache.append (tail write)  kvcache.py:116-123
+ */
+#ifndef DQUANT_B200_H
+#define DQUANT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mirrors dquant/errors.py:4-61 class names) ---------- */
+#define DQ_OK 0
+#define DQ_ERR_UNSUPPORTED_BITS 1 /* UnsupportedBits   errors.py:28 */
+#define DQ_ERR_SHAPE_MISMATCH 2   /* ShapeMismatch     errors.py:8  */
+#define DQ_ERR_CORRUPT_PAYLOAD 3  /* CorruptPayload    errors.py:36 */
+#define DQ_ERR_NONFINITE 4        /* NonFiniteInput    errors.py:24 */
+#define DQ_ERR_RANGE_OVERFLOW 5   /* RangeOverflow     errors.py:32 */
+#define DQ_ERR_INVALID_ARG 6      /* bad pointer / size / workspace */
+#define DQ_ERR_CUDA 7             /* CUDA runtime error (message has details) */
+#define DQ_ERR_UNSUPPORTED 8      /* valid request outside this build's kernels */
+
+/* ---- device-side flag bits written into the caller's `flags` word ------ */
+#define DQ_FLAG_NONFINITE 1u
+#define DQ_FLAG_RANGE_OVERFLOW 2u
+#define DQ_FLAG_JACOBI_NOCONV 4u
+
+/* ---- dtypes ------------------------------------------------------------ */
+#define DQ_F32 0
+#define DQ_F16 1
+
+/* ---- packed large-core layouts ------------------------------------------
+ * DQ_LAYOUT_REF  : the reference wire order, codes of core1 (r, i2, j2) in
+ *                  row-major order, payload_size(r*i2*j2, bits) bytes
+ *                  (quantize.py:11-14, 66-82).
+ * DQ_LAYOUT_KROW : device K layout, (r, i2p, j2) with i2p = i2 rounded up to
+ *                  a multiple of 64 and zero codes in the padding.  Equal to
+ *                  DQ_LAYOUT_REF whenever i2 % 64 == 0.  Needs j2*bits % 8 == 0.
+ * DQ_LAYOUT_VCOL : device V layout, (r, j2, i2p): the b index is innermost so
+ *                  the PV contraction streams codes along its reduction axis.
+ */
+#define DQ_LAYOUT_REF 0
+#define DQ_LAYOUT_KROW 1
+#define DQ_LAYOUT_VCOL 2
+
+/* ---- n=2 plan (mpo.py:73-96 with n=2; r = bond, mpo.py:54-63) ---------- */
+typedef struct dq_plan2 {
+  int64_t i1, i2, j1, j2, r;
+} dq_plan2;
+
+const char* dq_last_error(void);
+int dq_version(void);
+
+/* host-only: general n (i_factors/j_factors hold n entries each) */
+int dq_plan_shapes(int64_t rows, int64_t cols, int32_t n, int64_t* h_i_factors, int64_t* h_j_factors);
+int dq_make_plan2(int64_t rows, int64_t cols, dq_plan2* h_plan);
+/* bytes of one packed large core in `layout` (host-only) */
+int dq_layout_bytes(const dq_plan2* h_plan, int32_t bits, int32_t layout, int64_t* h_bytes);
+
+/* ---- K1 codec ---------------------------------------------------------- */
+int dq_pack(const int8_t* codes, int64_t count, int32_t bits, uint8_t* payload, int32_t* flags, void* stream);
+int dq_unpack(const uint8_t* payload, int64_t payload_bytes, int64_t start, int64_t count, int32_t bits,
+              int8_t* codes, void* stream);
+
+/* ---- K2 quantizer: one symmetric scale per tensor ---------------------- */
+int dq_quantize_workspace_size(int64_t count, size_t* h_bytes);
+int dq_quantize_rtn(const float* t, int64_t count, int32_t bits, float* scale, uint8_t* payload, int32_t* flags,
+                    void* workspace, size_t workspace_bytes, void* stream);
+int dq_dequantize(const uint8_t* payload, int64_t count, int32_t bits, const float* scale, float* out, void* stream);
+
+/* ---- K3 write path: batched n=2 TT-SVD (+ quantize) -------------------
+ * blocks: nblk matrices of rows x cols (row-major, dtype in_dtype), contiguous.
+ * core0 : nblk x (i1*j1*r) f32 (shape (1,i1,j1,r) each)
+ * core1 : nblk x (r*i2*j2) f32 (shape (r,i2,j2,1) each)
+ * payload: nblk packed cores, block k at payload + k*payload_stride, in `layout`
+ * scale : nblk f32
+ */
+int dq_decompose_workspace_size(int64_t nblk, int64_t rows, int64_t cols, size_t* h_bytes);
+int dq_decompose_batched(const void* blocks, int32_t in_dtype, int64_t nblk, int64_t rows, int64_t cols,
+                         float* core0, float* core1, int32_t* flags, void* workspace, size_t workspace_bytes,
+                         void* stream);
+/* same as dq_decompose_batched with an explicit n=2 plan (any split whose bond r <= 64) */
+int dq_decompose_plan_batched(const void* blocks, int32_t in_dtype, int64_t nblk, const dq_plan2* h_plan,
+                              float* core0, float* core1, int32_t* flags, void* workspace, size_t workspace_bytes,
+                              void* stream);
+int dq_deco_quantize_batched(const void* blocks, int32_t in_dtype, int64_t nblk, int64_t rows, int64_t cols,
+                             int32_t bits, int32_t layout, float* core0, uint8_t* payload, int64_t payload_stride,
+                             float* scale, int32_t* flags, void* workspace, size_t workspace_bytes, void* stream);
+/* fp16 copy of core0 in the attention-friendly layout g0h[a][r][c] (i1 x r x j1) */
+int dq_core0_to_f16(const float* core0, int64_t nblk, const dq_plan2* h_plan, uint16_t* g0h, void* stream);
+
+/* ---- K4 reconstruct (dequant + contraction), batched ------------------- */
+int dq_deco_dequantize_batched(const float* core0, const uint8_t* payload, int64_t payload_stride, int32_t layout,
+                               const float* scale, int64_t nblk, int64_t rows, int64_t cols, int32_t bits,
+                               void* out, int32_t out_dtype, void* stream);
+
+/* layout conversion of packed cores (e.g. device layouts -> reference wire order) */
+int dq_relayout(const uint8_t* src, int32_t src_layout, int64_t src_stride, uint8_t* dst, int32_t dst_layout,
+                int64_t dst_stride, int64_t nblk, const dq_plan2* h_plan, int32_t bits, void* stream);
+
+/* ---- generic fused reads (any n=2 plan with i1*j1 <= 64) -----------------
+ * x: p x cols (f32) -> out: p x rows (f32) = x @ W^T
+ * x: p x rows (f32) -> out: p x cols (f32) = x @ W
+ */
+int dq_fused_matmul_t(const float* x, int64_t p, const float* core0, const uint8_t* payload, int32_t layout,
+                      const float* scale, int64_t rows, int64_t cols, int32_t bits, float* out, void* stream);
+int dq_fused_matmul(const float* x, int64_t p, const float* core0, const uint8_t* payload, int32_t layout,
+                    const float* scale, int64_t rows, int64_t cols, int32_t bits, float* out, void* stream);
+
+/* ---- K5 fused dequant + decode attention (D = 128, j = (8,16)) -----------
+ * One "unit" is one (sequence, kv head) of one layer; g query heads attend to it.
+ * A unit owns zero or more compressed segments (prefill segment, sealed chunks)
+ * and an fp16 tail.  Segment s of the work list belongs to unit seg_unit[s].
+ */
+typedef struct dq_segment {
+  const uint8_t* k_codes; /* DQ_LAYOUT_KROW */
+  const uint8_t* v_codes; /* DQ_LAYOUT_VCOL */
+  const uint16_t* k_g0;   /* fp16 [i1][r][8]  (dq_core0_to_f16 layout) */
+  const uint16_t* v_g0;   /* fp16 [i1][r][8] */
+  float k_scale, v_scale;
+  int32_t T;          /* tokens in the segment */
+  int32_t i1, i2, r;  /* plan of (T,128) */
+  int32_t i2p;        /* padded i2 of the device layouts */
+  int32_t unit;       /* owning unit */
+  int32_t token0;     /* first token index of the segment inside its unit */
+  int32_t pad_;
+} dq_segment;
+
+typedef struct dq_attn_args {
+  const uint16_t* q;      /* fp16 [units][g][128] */
+  uint16_t* out;          /* fp16 [units][g][128] */
+  const dq_segment* segs; /* device array [nseg] */
+  int32_t nseg;
+  int32_t units;
+  int32_t g;              /* query heads per kv head (1..8) */
+  int32_t bits;           /* 2, 4 or 8 */
+  const uint16_t* tail_k; /* fp16 [units][tail_cap][128] (may be null if tail_len==0) */
+  const uint16_t* tail_v;
+  const int32_t* tail_len; /* device [units] */
+  int32_t tail_cap;
+  int32_t chunk_b;        /* b rows per split work item (multiple of 64) */
+  float sm_scale;         /* softmax scale, 1/sqrt(128) for the reference scores */
+  /* work list (built by dq_attention_plan) */
+  const int32_t* work;    /* device int32 [nwork][2] = (segment, b0) */
+  int32_t nwork;
+  int32_t max_parts;      /* partial slots per unit (>= work items of any unit + 1) */
+  const int32_t* unit_part0; /* device [units]: first partial slot of each unit */
+  const int32_t* work_part;  /* device [nwork]: partial slot of each work item */
+  const int32_t* unit_nparts;/* device [units] */
+  float* part_o;          /* workspace [total_parts][g][128] f32 */
+  float* part_ml;         /* workspace [total_parts][g][2]   f32 (max, sum) */
+} dq_attn_args;
+
+/* host helper: fill work/partial tables (host arrays) for a host copy of the segment table */
+int dq_attention_plan(const dq_segment* h_segs, int32_t nseg, int32_t units, int32_t chunk_b, int32_t* h_work,
+                      int32_t* h_nwork, int32_t* h_work_part, int32_t* h_unit_part0, int32_t* h_unit_nparts,
+                      int32_t* h_total_parts);
+int dq_decode_attention(const dq_attn_args* h_args, void* stream);
+
+/* append one token row per unit into the fp16 tail (kvcache.py:116-123) */
+int dq_tail_append(const uint16_t* k_rows, const uint16_t* v_rows, int32_t units, uint16_t* tail_k,
+                   uint16_t* tail_v, int32_t* tail_len, int32_t tail_cap, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DQUANT_B200_H */

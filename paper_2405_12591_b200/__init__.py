@@ -1,0 +1,63 @@
+"""B200-native DecoQuant (arXiv 2405.12591): MPO decomposition + local-tensor quantization
+of KV caches, with a fused dequant decode-attention kernel for sm_100a.
+
+Drop-in for the hot path of the reference ``dquant`` package: the names below
+mirror ``dquant/__init__.py:10-77`` for the codec, the MPO factorisation, the
+DecoQuant protocol and the KV cache.  Compute runs in ``libdquant_b200.so``
+(hand-written CUDA, C ABI in include/dquant_b200.h); there is no CPU fallback.
+The batched decode hot path is ``DecodeKvCache`` (attention.py).
+
+Out of scope for this build: the analysis sweeps, the
+DQT1/DQZ1 file formats, the CLI and the dense tensor primitives.
+"""
+
+from .compress import (
+    CompressionReport,
+    QuantizedMpo,
+    WorkingSetMeter,
+    compression_report,
+    deco_dequantize,
+    deco_quantize,
+    fused_matmul,
+    fused_matmul_t,
+)
+from .kvcache import CacheConfig, KvCache, MemoryLedger, simulate_generation
+from .mpo import MpoChain, ShapePlan, decompose, plan_shapes, reconstruct, split_large_small
+from .quantize import QuantizedTensor, dequantize, pack, quantize_rtn, unpack
+
+__all__ = [
+    "CacheConfig",
+    "CompressionReport",
+    "DecodeKvCache",
+    "KvCache",
+    "MemoryLedger",
+    "MpoChain",
+    "QuantizedMpo",
+    "QuantizedTensor",
+    "ShapePlan",
+    "WorkingSetMeter",
+    "compression_report",
+    "deco_dequantize",
+    "deco_quantize",
+    "decompose",
+    "dequantize",
+    "fused_matmul",
+    "fused_matmul_t",
+    "pack",
+    "plan_shapes",
+    "quantize_rtn",
+    "reconstruct",
+    "simulate_generation",
+    "split_large_small",
+    "unpack",
+]
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    if name == "DecodeKvCache":
+        from .attention import DecodeKvCache
+
+        return DecodeKvCache
+    raise AttributeError(name)

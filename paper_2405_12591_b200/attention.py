@@ -1,0 +1,290 @@
+"""Batched device KV cache + fused DecoQuant decode attention (the hot path).
+
+One *unit* is one (sequence, kv-head) pair of a layer.  ``DecodeKvCache`` keeps,
+for every layer, the reference cache lifecycle (kvcache.py:94-128) for all units
+at once:
+
+* ``prefill(layer, K, V)``: the whole prompt of every unit becomes ONE segment
+  (kvcache.py:99-114), compressed by K3 (csrc/factor.cu) straight into the
+  device layouts the attention kernel streams (K: DQ_LAYOUT_KROW, V: DQ_LAYOUT_VCOL).
+* ``append_token(layer, k, v)``: fp16 tail write (kvcache.py:116-123); when the
+  tail reaches ``chunk_len`` it is sealed into a new segment (kvcache.py:124-128).
+* ``attend(layer, q)``: softmax(q K^T / sqrt(128)) V over every segment and the
+  tail, by K5 (csrc/attention.cu) -- the reference's ``attention_scores``
+  (kvcache.py:188-217) followed by softmax and the per-segment PV ``fused_matmul``
+  (compress.py:159-192), fused, with no full-precision K/V anywhere in HBM.
+
+``export_segment`` returns a segment in the reference's ``QuantizedMpo`` form
+(wire-order payload), so the device cache interoperates byte-exactly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check, lib, ptr, stream_ptr
+from .compress import QuantizedMpo, deco_quantize_batched
+from .errors import AlreadyPrefilled, DimMismatch, LayerOutOfRange, ShapeMismatch, Unsupported
+from .mpo import plan_shapes
+from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_size
+
+HEAD_DIM = 128
+DEFAULT_CHUNK_B = 256
+MAX_BLOCKS_PER_CALL = 512  # bounds the K3 fp32 core1 scratch
+
+
+@dataclass
+class SegmentGroup:
+    """Segment index s of every unit of a layer (same T, same plan)."""
+
+    T: int
+    plan: _lib.Plan2
+    i2p: int
+    k_payload: torch.Tensor  # (units, kbytes) u8, KROW
+    v_payload: torch.Tensor  # (units, vbytes) u8, VCOL
+    k_core0: torch.Tensor    # (units, 1, i1, 8, r) f32
+    v_core0: torch.Tensor
+    k_g0h: torch.Tensor      # (units, i1*r*8) f16, [a][r][c]
+    v_g0h: torch.Tensor
+    k_scale: torch.Tensor    # (units,) f32
+    v_scale: torch.Tensor
+    token0: int
+
+    def reference_bytes(self, bits: int) -> int:
+        """compression_report().bytes_compressed of one unit's K (or V) block (compress.py:234-248)."""
+        p = self.plan
+        return payload_size(p.r * p.i2 * p.j2, bits) + 2 + 2 * (p.i1 * p.j1 * p.r)
+
+    def stream_bytes(self) -> int:
+        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp16 G0, scales."""
+        return (self.k_payload.shape[1] + self.v_payload.shape[1] + 2 * (self.k_g0h.shape[1] + self.v_g0h.shape[1])
+                + 8)
+
+
+class _Layer:
+    def __init__(self):
+        self.groups: list[SegmentGroup] = []
+        self.tokens_sealed = 0
+        self.tail_len = 0  # host mirror (all units append in lock step)
+        self.args = None   # cached AttnArgs
+        self.keep = []     # tensors referenced by args
+
+
+def compress_blocks(blocks: torch.Tensor, bits: int, layout: int):
+    """K3 over (nblk, T, 128) fp16/fp32 CUDA blocks in slices of MAX_BLOCKS_PER_CALL.
+
+    Returns (payload (nblk, bytes), core0 f32, g0h f16 [a][r][c], scale f32, plan).
+    """
+    nblk = blocks.shape[0]
+    outs = []
+    for s in range(0, nblk, MAX_BLOCKS_PER_CALL):
+        res = deco_quantize_batched(blocks[s:s + MAX_BLOCKS_PER_CALL], bits, layout)
+        _lib.raise_flags(res["flags"], "deco_quantize")
+        outs.append(res)
+    p = outs[0]["plan"]
+    payload = torch.cat([o["payload"] for o in outs]) if len(outs) > 1 else outs[0]["payload"]
+    core0 = torch.cat([o["core0"] for o in outs]) if len(outs) > 1 else outs[0]["core0"]
+    scale = torch.cat([o["scale"] for o in outs]) if len(outs) > 1 else outs[0]["scale"]
+    g0h = torch.empty((nblk, p.i1 * p.r * p.j1), dtype=torch.float16, device=blocks.device)
+    check(lib().dq_core0_to_f16(ptr(core0), nblk, ctypes.byref(p), ptr(g0h), stream_ptr()), "core0_to_f16")
+    return payload, core0, g0h, scale, p
+
+
+class DecodeKvCache:
+    """Device DecoQuant KV cache for ``layers`` x ``units`` with fused decode attention.
+
+    ``g`` query heads share each kv head (GQA group).  ``bits`` in {2, 4, 8}.
+    """
+
+    def __init__(self, layers: int, units: int, g: int = 1, bits: int = 4, chunk_len: int = 1024,
+                 dim: int = HEAD_DIM, chunk_b: int = DEFAULT_CHUNK_B, sm_scale: float | None = None):
+        if dim != HEAD_DIM:
+            raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
+        if bits not in SUPPORTED_BITS:
+            raise UnsupportedBits(f"bits must be in {SUPPORTED_BITS}")
+        if layers < 1 or units < 1 or chunk_len < 1:
+            raise ShapeMismatch("layers, units and chunk_len must be >= 1")
+        self.device = _lib.require_cuda()
+        self.layers, self.units, self.g, self.bits = layers, units, g, bits
+        self.chunk_len, self.dim, self.chunk_b = chunk_len, dim, chunk_b
+        self.sm_scale = float(sm_scale) if sm_scale is not None else float(1.0 / math.sqrt(dim))
+        self._layers = [_Layer() for _ in range(layers)]
+        shape = (layers, units, chunk_len, dim)
+        self.tail_k = torch.zeros(shape, dtype=torch.float16, device=self.device)
+        self.tail_v = torch.zeros(shape, dtype=torch.float16, device=self.device)
+        self.tail_len = torch.zeros((layers, units), dtype=torch.int32, device=self.device)
+        self.bytes_moved_read = 0
+
+    # ---- lifecycle -----------------------------------------------------------
+    def _layer(self, layer: int) -> _Layer:
+        if not 0 <= layer < self.layers:
+            raise LayerOutOfRange(f"layer {layer} outside 0..{self.layers - 1}")
+        return self._layers[layer]
+
+    def tokens(self, layer: int) -> int:
+        lay = self._layer(layer)
+        return lay.tokens_sealed + lay.tail_len
+
+    def _add_group(self, layer: int, keys: torch.Tensor, values: torch.Tensor):
+        lay = self._layer(layer)
+        T = keys.shape[1]
+        kp, kc0, kg, ks, p = compress_blocks(keys, self.bits, _lib.LAYOUT_KROW)
+        vp, vc0, vg, vs, _ = compress_blocks(values, self.bits, _lib.LAYOUT_VCOL)
+        i2p = -(-p.i2 // _lib.I2_PAD) * _lib.I2_PAD
+        lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, lay.tokens_sealed))
+        lay.tokens_sealed += T
+        lay.args = None
+
+    def prefill(self, layer: int, keys: torch.Tensor, values: torch.Tensor):
+        """keys/values: (units, T, 128) CUDA fp16 or fp32.  One segment per unit (kvcache.py:99-114)."""
+        lay = self._layer(layer)
+        if lay.tokens_sealed or lay.tail_len:
+            raise AlreadyPrefilled("layer already holds tokens")
+        if keys.shape != values.shape or keys.ndim != 3 or keys.shape[0] != self.units:
+            raise DimMismatch(f"keys and values must both be ({self.units}, T, {self.dim})")
+        if keys.shape[2] != self.dim:
+            raise DimMismatch(f"row width {keys.shape[2]} differs from dim {self.dim}")
+        if keys.shape[1] == 0:
+            return
+        self._add_group(layer, keys.to(self.device), values.to(self.device))
+
+    def append_token(self, layer: int, k_rows: torch.Tensor, v_rows: torch.Tensor):
+        """k_rows/v_rows: (units, 128).  Seals the tail at chunk_len (kvcache.py:116-128)."""
+        lay = self._layer(layer)
+        if k_rows.shape != (self.units, self.dim) or v_rows.shape != (self.units, self.dim):
+            raise DimMismatch(f"rows must be ({self.units}, {self.dim})")
+        k = k_rows.to(self.device, torch.float16).contiguous()
+        v = v_rows.to(self.device, torch.float16).contiguous()
+        check(lib().dq_tail_append(ptr(k), ptr(v), self.units, ptr(self.tail_k[layer]), ptr(self.tail_v[layer]),
+                                   ptr(self.tail_len[layer]), self.chunk_len, stream_ptr()), "tail_append")
+        lay.tail_len += 1
+        if lay.tail_len == self.chunk_len:
+            self._add_group(layer, self.tail_k[layer], self.tail_v[layer])
+            self.tail_len[layer].zero_()
+            lay.tail_len = 0
+
+    # ---- attention -----------------------------------------------------------
+    def _build_args(self, layer: int):
+        lay = self._layers[layer]
+        segs = []
+        scales = [(grp.k_scale.cpu(), grp.v_scale.cpu()) for grp in lay.groups]
+        for grp, (ks, vs) in zip(lay.groups, scales):
+            p = grp.plan
+            kb, vb = grp.k_payload.shape[1], grp.v_payload.shape[1]
+            gb = grp.k_g0h.shape[1] * 2
+            for u in range(self.units):
+                s = _lib.Segment()
+                s.k_codes = grp.k_payload.data_ptr() + u * kb
+                s.v_codes = grp.v_payload.data_ptr() + u * vb
+                s.k_g0 = grp.k_g0h.data_ptr() + u * gb
+                s.v_g0 = grp.v_g0h.data_ptr() + u * gb
+                s.k_scale = float(ks[u])
+                s.v_scale = float(vs[u])
+                s.T, s.i1, s.i2, s.r, s.i2p = grp.T, p.i1, p.i2, p.r, grp.i2p
+                s.unit, s.token0 = u, grp.token0
+                segs.append(s)
+        nseg = len(segs)
+        seg_arr = (_lib.Segment * max(nseg, 1))(*segs)
+        # work plan (host) -> device tables
+        max_work = sum(-(-grp.plan.i2 // self.chunk_b) for grp in lay.groups) * self.units
+        work = (ctypes.c_int32 * max(2 * max_work, 2))()
+        work_part = (ctypes.c_int32 * max(max_work, 1))()
+        unit_part0 = (ctypes.c_int32 * self.units)()
+        unit_nparts = (ctypes.c_int32 * self.units)()
+        nwork, total = ctypes.c_int32(), ctypes.c_int32()
+        check(lib().dq_attention_plan(seg_arr, nseg, self.units, self.chunk_b, work, ctypes.byref(nwork), work_part,
+                                      unit_part0, unit_nparts, ctypes.byref(total)), "attention_plan")
+        dev = self.device
+
+        def i32(arr, n):
+            return torch.tensor(list(arr)[:n], dtype=torch.int32).to(dev)
+
+        seg_dev = torch.frombuffer(bytearray(bytes(seg_arr)), dtype=torch.uint8).to(dev)
+        work_dev = i32(work, 2 * nwork.value)
+        wpart_dev = i32(work_part, nwork.value)
+        p0_dev = i32(unit_part0, self.units)
+        np_dev = i32(unit_nparts, self.units)
+        tp = max(total.value, 1)
+        part_o = torch.empty((tp, self.g, self.dim), dtype=torch.float32, device=dev)
+        part_ml = torch.empty((tp, self.g, 2), dtype=torch.float32, device=dev)
+        a = _lib.AttnArgs()
+        a.segs = seg_dev.data_ptr()
+        a.nseg = nseg
+        a.units = self.units
+        a.g = self.g
+        a.bits = self.bits
+        a.tail_k = self.tail_k[layer].data_ptr()
+        a.tail_v = self.tail_v[layer].data_ptr()
+        a.tail_len = self.tail_len[layer].data_ptr()
+        a.tail_cap = self.chunk_len
+        a.chunk_b = self.chunk_b
+        a.sm_scale = self.sm_scale
+        a.work = work_dev.data_ptr() if nwork.value else None
+        a.nwork = nwork.value
+        a.max_parts = tp
+        a.unit_part0 = p0_dev.data_ptr()
+        a.work_part = wpart_dev.data_ptr() if nwork.value else None
+        a.unit_nparts = np_dev.data_ptr()
+        a.part_o = part_o.data_ptr()
+        a.part_ml = part_ml.data_ptr()
+        lay.args = a
+        lay.keep = [seg_dev, work_dev, wpart_dev, p0_dev, np_dev, part_o, part_ml]
+
+    def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """q: (units, g, 128) fp16 CUDA -> (units, g, 128) fp16."""
+        lay = self._layer(layer)
+        if q.shape != (self.units, self.g, self.dim):
+            raise DimMismatch(f"q must be ({self.units}, {self.g}, {self.dim})")
+        if lay.args is None:
+            self._build_args(layer)
+        q = q.to(self.device, torch.float16).contiguous()
+        if out is None:
+            out = torch.empty_like(q)
+        a = lay.args
+        a.q = q.data_ptr()
+        a.out = out.data_ptr()
+        check(lib().dq_decode_attention(ctypes.byref(a), stream_ptr()), "decode_attention")
+        self.bytes_moved_read += self.read_bytes(layer)
+        return out
+
+    # ---- accounting ----------------------------------------------------------
+    def read_bytes(self, layer: int) -> int:
+        """Algorithmic HBM bytes one ``attend(layer)`` streams (all units)."""
+        lay = self._layers[layer]
+        seg = sum(g.stream_bytes() for g in lay.groups) * self.units
+        tail = 2 * lay.tail_len * self.dim * 2 * self.units
+        qo = 2 * self.units * self.g * self.dim * 2
+        return seg + tail + qo
+
+    def ledger(self):
+        """(bytes_fp16_equivalent, bytes_actual) with the reference's accounting (kvcache.py:130-141)."""
+        fp16 = actual = 0
+        for lay in self._layers:
+            tokens = lay.tokens_sealed + lay.tail_len
+            fp16 += 2 * tokens * self.dim * 2 * self.units
+            actual += sum(2 * g.reference_bytes(self.bits) for g in lay.groups) * self.units
+            actual += 2 * lay.tail_len * self.dim * 2 * self.units
+        return fp16, actual
+
+    def export_segment(self, layer: int, index: int, unit: int, which: str = "k") -> QuantizedMpo:
+        """Segment ``index`` of ``unit`` as a reference-form QuantizedMpo (wire-order payload)."""
+        grp = self._layer(layer).groups[index]
+        p = grp.plan
+        src = grp.k_payload if which == "k" else grp.v_payload
+        layout = _lib.LAYOUT_KROW if which == "k" else _lib.LAYOUT_VCOL
+        nbytes = payload_size(p.r * p.i2 * p.j2, self.bits)
+        dst = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        check(lib().dq_relayout(ptr(src[unit]), layout, src.shape[1], ptr(dst), _lib.LAYOUT_REF, nbytes, 1,
+                                ctypes.byref(p), self.bits, stream_ptr()), "relayout")
+        core0 = (grp.k_core0 if which == "k" else grp.v_core0)[unit].reshape(1, p.i1, p.j1, p.r)
+        scale = float((grp.k_scale if which == "k" else grp.v_scale)[unit].item())
+        qt = QuantizedTensor((p.r, p.i2, p.j2, 1), self.bits, scale, data=dst, torch_out=True)
+        return QuantizedMpo(plan=plan_shapes(grp.T, self.dim, 2), bits=self.bits, local_tensors=(core0, qt))
+
+
+__all__ = ["DecodeKvCache", "SegmentGroup", "compress_blocks", "HEAD_DIM"]

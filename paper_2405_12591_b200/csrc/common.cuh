@@ -1,0 +1,113 @@
+// Shared helpers for the DecoQuant sm_100a kernels (see include/dquant_b200.h).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/dquant_b200.h"
+
+namespace dq {
+
+// ---- error plumbing (thread-local message behind dq_last_error) ----------
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+
+#define DQ_CUDA_TRY(expr)                                                              \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return ::dq::fail(DQ_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,        \
+                        cudaGetErrorString(e_));                                       \
+  } while (0)
+
+#define DQ_LAUNCH_CHECK() DQ_CUDA_TRY(cudaGetLastError())
+
+inline bool bits_ok(int bits) { return bits == 2 || bits == 4 || bits == 8; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// The device layouts pad i2 to a multiple of this many rows (include/dquant_b200.h).
+constexpr int kI2Pad = 64;
+
+// mpo.py:66-70 / 73-96 with n=2
+int64_t largest_divisor_le(int64_t x, int64_t cap = 8);
+dq_plan2 make_plan2(int64_t rows, int64_t cols);
+
+// ---- element addressing of packed large cores ---------------------------
+struct CoreGeom {
+  int32_t r, i2, j2, i2p;  // i2p == i2 for DQ_LAYOUT_REF
+  int32_t layout;
+  int32_t bits;
+};
+
+inline CoreGeom make_geom(const dq_plan2& p, int bits, int layout) {
+  CoreGeom g;
+  g.r = (int32_t)p.r;
+  g.i2 = (int32_t)p.i2;
+  g.j2 = (int32_t)p.j2;
+  g.i2p = layout == DQ_LAYOUT_REF ? (int32_t)p.i2 : (int32_t)round_up(p.i2, kI2Pad);
+  g.layout = layout;
+  g.bits = bits;
+  return g;
+}
+
+// number of code slots (including padding) of one packed core
+__host__ __device__ inline int64_t geom_slots(const CoreGeom& g) { return (int64_t)g.r * g.i2p * g.j2; }
+
+// linear code slot of logical element (rr, b, e)
+__host__ __device__ inline int64_t geom_slot(const CoreGeom& g, int rr, int b, int e) {
+  if (g.layout == DQ_LAYOUT_VCOL) return ((int64_t)rr * g.j2 + e) * g.i2p + b;
+  return ((int64_t)rr * g.i2p + b) * g.j2 + e;
+}
+
+// inverse: logical element of a slot; returns false for padding slots
+__host__ __device__ inline bool geom_coords(const CoreGeom& g, int64_t slot, int& rr, int& b, int& e) {
+  if (g.layout == DQ_LAYOUT_VCOL) {
+    b = (int)(slot % g.i2p);
+    int64_t t = slot / g.i2p;
+    e = (int)(t % g.j2);
+    rr = (int)(t / g.j2);
+  } else {
+    e = (int)(slot % g.j2);
+    int64_t t = slot / g.j2;
+    b = (int)(t % g.i2p);
+    rr = (int)(t / g.i2p);
+  }
+  return b < g.i2;
+}
+
+__host__ __device__ inline int64_t payload_bytes(int64_t count, int bits) { return (count * bits + 7) / 8; }
+
+// signed code at slot (two's complement in `bits`, earliest element in the low bits)
+__device__ __forceinline__ int read_code(const uint8_t* p, int64_t slot, int bits) {
+  const int per = 8 / bits;
+  const unsigned byte = p[slot / per];
+  const unsigned raw = (byte >> ((slot % per) * bits)) & ((1u << bits) - 1u);
+  const int sign = 1 << (bits - 1);
+  return (int)(raw ^ sign) - sign;
+}
+
+// ---- bit-exact replica of quantize.py:144-145 ---------------------------
+// y = t * qmax / amax in fp64 (product first), code = copysign(floor(|y| + 0.5), y), clipped.
+__device__ __forceinline__ int rtn_code(float t, int qmax, double amax) {
+  const double y = __ddiv_rn(__dmul_rn((double)t, (double)qmax), amax);
+  double c = floor(__dadd_rn(fabs(y), 0.5));
+  if (c > (double)qmax) c = (double)qmax;
+  return y < 0.0 ? -(int)c : (int)c;
+}
+
+// quantize.py:135-140: f32(amax/qmax), or 1.0 when amax == 0 or the step underflows
+__host__ __device__ inline float rtn_scale(double amax, int qmax, bool* degenerate) {
+  float s = amax > 0.0 ? (float)(amax / (double)qmax) : 1.0f;
+  const bool deg = (amax == 0.0) || (s == 0.0f);
+  if (deg) s = 1.0f;
+  if (degenerate) *degenerate = deg;
+  return s;
+}
+
+}  // namespace dq

@@ -1,0 +1,564 @@
+// K3 quantize-on-write: batched n=2 TT-SVD of K/V blocks in fp64, fused with the
+// symmetric quantizer and packing (mpo.py:153-178 + compress.py:85-94 + quantize.py:123-151).
+//
+// For a block M (rows x cols) with plan i=(i1,i2), j=(j1,j2) the interleaved matrix
+//   A[(a,c),(b,e)] = M[a*i2+b, c*j2+e]          (mpo.py:144-150, never materialised)
+// is (m = i1*j1) x (n = i2*j2).  Its SVD is taken in Gram form on the short side
+// (r = min(m,n) <= 64 because i1, j1 <= 8):
+//   case A (m <= n):  G = A A^T (r x r), G = U diag(lambda) U^T,
+//                     core0 = U sqrt(s), core1 = diag(s^-1/2) U^T A     (= sqrt(s) V^T)
+//   case B (m >  n):  H = A^T A, H = V diag(lambda) V^T,
+//                     core1 = sqrt(s) V^T, core0 = A V diag(s^-1/2)     (= U sqrt(s))
+// with s = sqrt(lambda).  The eigensolver is a CTA-level parallel cyclic Jacobi
+// (round-robin pairing, 32 disjoint rotations per round) in fp64 shared memory:
+// the rotation angles are exactly those of one-sided (Hestenes) Jacobi on the rows
+// of X, applied to the Gram form.  Everything runs in fp64 because one flipped
+// int4 code moves the reconstruction by ~1e-3 relative.
+//
+// Sign convention: each singular vector is oriented so that its largest-magnitude
+// entry of core0's column is positive (LAPACK's is implementation-defined; parity
+// tests align signs per bond index).
+#include "common.cuh"
+
+namespace dq {
+
+namespace {
+
+constexpr int kR = 64;       // max bond dimension handled (i1, j1 <= 8)
+constexpr int kTile = 64;    // contraction tile
+constexpr int kThreads = 256;
+constexpr int kMaxSweeps = 40;
+
+struct Dims {
+  int rows, cols;
+  int i1, i2, j1, j2;
+  int m, n, r, kd;  // kd = contraction length of the Gram = max(m, n)
+  bool caseA;       // m <= n
+  int dtype;
+  int64_t bstride;  // elements per block
+};
+
+Dims make_dims(const dq_plan2& p, int64_t rows, int64_t cols, int dtype) {
+  Dims d;
+  d.rows = (int)rows;
+  d.cols = (int)cols;
+  d.i1 = (int)p.i1;
+  d.i2 = (int)p.i2;
+  d.j1 = (int)p.j1;
+  d.j2 = (int)p.j2;
+  d.m = d.i1 * d.j1;
+  d.n = d.i2 * d.j2;
+  d.r = (int)p.r;
+  d.caseA = d.m <= d.n;
+  d.kd = d.caseA ? d.n : d.m;
+  d.dtype = dtype;
+  d.bstride = rows * cols;
+  return d;
+}
+
+__device__ __forceinline__ double load_m(const void* base, int dtype, int64_t off) {
+  if (dtype == DQ_F16) return (double)__half2float(((const __half*)base)[off]);
+  return (double)((const float*)base)[off];
+}
+
+// A[row][col] of the interleaved matrix
+__device__ __forceinline__ double load_a(const void* blk, const Dims& d, int row, int col) {
+  const int a = row / d.j1, c = row - a * d.j1;
+  const int b = col / d.j2, e = col - b * d.j2;
+  return load_m(blk, d.dtype, (int64_t)(a * d.i2 + b) * d.cols + c * d.j2 + e);
+}
+
+// X[p][k]: the Gram operand (X = A in case A, A^T in case B), r x kd
+__device__ __forceinline__ double load_x(const void* blk, const Dims& d, int p, int k) {
+  return d.caseA ? load_a(blk, d, p, k) : load_a(blk, d, k, p);
+}
+
+__device__ __forceinline__ const void* block_ptr(const void* in, const Dims& d, int64_t blk) {
+  const size_t es = d.dtype == DQ_F16 ? 2 : 4;
+  return (const char*)in + (size_t)blk * d.bstride * es;
+}
+
+// ---- Gram: G[blk] += X[:, k0:k1] X[:, k0:k1]^T  (upper 4x4 tiles only) ------
+__global__ void __launch_bounds__(kThreads) gram_kernel(const void* __restrict__ in, Dims d, int kchunk,
+                                                        double* __restrict__ G, int32_t* flags) {
+  __shared__ double xs[kTile][kR + 2];  // xs[k][p]
+  const int64_t blk = blockIdx.x;
+  const void* base = block_ptr(in, d, blk);
+  const int k_begin = blockIdx.y * kchunk;
+  const int k_end = min(d.kd, k_begin + kchunk);
+  const int tp = threadIdx.x >> 4, tq = threadIdx.x & 15;
+  const bool active = tq >= tp;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  bool nonfinite = false;
+  for (int k0 = k_begin; k0 < k_end; k0 += kTile) {
+    for (int idx = threadIdx.x; idx < kR * kTile; idx += kThreads) {
+      const int p = idx / kTile, kk = idx - p * kTile;
+      const int k = k0 + kk;
+      double v = 0.0;
+      if (p < d.r && k < k_end) {
+        v = load_x(base, d, p, k);
+        nonfinite |= !isfinite(v);
+      }
+      xs[kk][p] = v;
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll 4
+      for (int kk = 0; kk < kTile; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          a[i] = xs[kk][tp * 4 + i];
+          b[i] = xs[kk][tq * 4 + i];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+  if (nonfinite && flags) atomicOr(flags, (int)DQ_FLAG_NONFINITE);
+  if (!active) return;
+  double* g = G + blk * kR * kR;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int p = tp * 4 + i, q = tq * 4 + j;
+      if (p < d.r && q < d.r && p <= q) atomicAdd(&g[p * kR + q], acc[i][j]);
+    }
+}
+
+// ---- parallel cyclic Jacobi eigensolver on one r x r Gram per CTA ---------
+struct JacobiSmem {
+  double g[kR][kR + 1];
+  double v[kR][kR + 1];
+  double c[kR / 2], s[kR / 2];
+  int pp[kR / 2], qq[kR / 2];
+  double lam[kR];
+  int perm[kR];
+  int rotations;
+};
+
+__global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restrict__ G, Dims d,
+                                                          double* __restrict__ U, double* __restrict__ lam_out,
+                                                          int32_t* flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  JacobiSmem& sm = *reinterpret_cast<JacobiSmem*>(smem_raw);
+  const int64_t blk = blockIdx.x;
+  const int r = d.r;
+  const int N = (r + 1) & ~1;  // even number of players (a dummy index when r is odd)
+  const int npairs = N / 2;
+  const double* g = G + blk * kR * kR;
+  for (int idx = threadIdx.x; idx < kR * kR; idx += blockDim.x) {
+    const int p = idx / kR, q = idx % kR;
+    double val = 0.0;
+    if (p < r && q < r) val = p <= q ? g[p * kR + q] : g[q * kR + p];
+    sm.g[p][q] = val;
+    sm.v[p][q] = p == q ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  bool converged = false;
+  for (int sweep = 0; sweep < kMaxSweeps && !converged; ++sweep) {
+    if (threadIdx.x == 0) sm.rotations = 0;
+    __syncthreads();
+    for (int round = 0; round < N - 1; ++round) {
+      if (threadIdx.x < npairs) {
+        const int i = threadIdx.x;
+        // circle method: slot 0 fixed, slots 1..N-1 rotate by `round`
+        const int sa = i, sb = N - 1 - i;
+        int pa = sa == 0 ? 0 : ((sa - 1 + round) % (N - 1)) + 1;
+        int pb = ((sb - 1 + round) % (N - 1)) + 1;
+        int p = min(pa, pb), q = max(pa, pb);
+        double cc = 1.0, ss = 0.0;
+        if (q < r) {
+          const double app = sm.g[p][p], aqq = sm.g[q][q], apq = sm.g[p][q];
+          const double thr = 1e-16 * sqrt(fabs(app) * fabs(aqq));
+          if (apq != 0.0 && fabs(apq) > thr) {
+            // sym.schur2 (Golub & Van Loan 8.4.2)
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            cc = 1.0 / sqrt(1.0 + t * t);
+            ss = t * cc;
+            if (ss != 0.0) atomicAdd(&sm.rotations, 1);
+          }
+        }
+        sm.pp[i] = p;
+        sm.qq[i] = q;
+        sm.c[i] = cc;
+        sm.s[i] = ss;
+      }
+      __syncthreads();
+      // rows: G <- J^T G
+      for (int idx = threadIdx.x; idx < npairs * N; idx += blockDim.x) {
+        const int i = idx / N, k = idx - i * N;
+        const double ss = sm.s[i];
+        if (ss == 0.0 || k >= r || sm.qq[i] >= r) continue;
+        const int p = sm.pp[i], q = sm.qq[i];
+        const double cc = sm.c[i];
+        const double gp = sm.g[p][k], gq = sm.g[q][k];
+        sm.g[p][k] = cc * gp - ss * gq;
+        sm.g[q][k] = ss * gp + cc * gq;
+      }
+      __syncthreads();
+      // columns: G <- G J, V <- V J
+      for (int idx = threadIdx.x; idx < npairs * N; idx += blockDim.x) {
+        const int i = idx / N, k = idx - i * N;
+        const double ss = sm.s[i];
+        if (ss == 0.0 || k >= r || sm.qq[i] >= r) continue;
+        const int p = sm.pp[i], q = sm.qq[i];
+        const double cc = sm.c[i];
+        const double gp = sm.g[k][p], gq = sm.g[k][q];
+        sm.g[k][p] = cc * gp - ss * gq;
+        sm.g[k][q] = ss * gp + cc * gq;
+        const double vp = sm.v[k][p], vq = sm.v[k][q];
+        sm.v[k][p] = cc * vp - ss * vq;
+        sm.v[k][q] = ss * vp + cc * vq;
+      }
+      __syncthreads();
+    }
+    converged = sm.rotations == 0;
+    __syncthreads();
+  }
+  if (!converged && threadIdx.x == 0 && flags) atomicOr(flags, (int)DQ_FLAG_JACOBI_NOCONV);
+
+  // sort eigenvalues descending (ties by index), orient each vector
+  if (threadIdx.x < r) {
+    const int i = threadIdx.x;
+    const double li = sm.g[i][i];
+    int rank = 0;
+    for (int j = 0; j < r; ++j) {
+      const double lj = sm.g[j][j];
+      rank += (lj > li) || (lj == li && j < i);
+    }
+    sm.perm[rank] = i;
+  }
+  __syncthreads();
+  double* u = U + blk * kR * kR;
+  for (int col = threadIdx.x / 32; col < r; col += blockDim.x / 32) {
+    const int src = sm.perm[col];
+    // largest |v| entry (first on ties) decides the sign
+    double best = -1.0;
+    int bidx = 0;
+    for (int p = threadIdx.x & 31; p < r; p += 32) {
+      const double a = fabs(sm.v[p][src]);
+      if (a > best) { best = a; bidx = p; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    }
+    const double sgn = sm.v[bidx][src] < 0.0 ? -1.0 : 1.0;
+    for (int p = threadIdx.x & 31; p < r; p += 32) u[p * kR + col] = sgn * sm.v[p][src];
+    if ((threadIdx.x & 31) == 0) lam_out[blk * kR + col] = sm.g[src][src];
+  }
+}
+
+// singular value from an eigenvalue, with rank-deficiency cut (see file header)
+__device__ __forceinline__ double sval(const double* lam, int k) {
+  const double l0 = lam[0];
+  const double lk = lam[k];
+  if (!(lk > 0.0) || lk <= 1e-13 * l0) return 0.0;
+  return sqrt(lk);
+}
+
+// ---- case A projection: core1 = diag(s^-1/2) U^T A, core0 = U sqrt(s) ---------
+// grid (nblk, nsplit over the n columns); thread tile 4 (bond) x 4 (columns)
+__global__ void __launch_bounds__(kThreads) project_a_kernel(const void* __restrict__ in, Dims d, int cchunk,
+                                                             const double* __restrict__ U,
+                                                             const double* __restrict__ lam,
+                                                             float* __restrict__ core0, float* __restrict__ core1,
+                                                             unsigned* __restrict__ amax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double (*ws)[kR + 2] = reinterpret_cast<double (*)[kR + 2]>(smem_raw);  // ws[p][k] = U[p][k] / sqrt(s_k)
+  double (*xs)[kTile + 2] =
+      reinterpret_cast<double (*)[kTile + 2]>(smem_raw + sizeof(double) * kR * (kR + 2));  // xs[p][col]
+  const int64_t blk = blockIdx.x;
+  const void* base = block_ptr(in, d, blk);
+  const double* u = U + blk * kR * kR;
+  const double* lm = lam + blk * kR;
+  const int r = d.r;
+  for (int idx = threadIdx.x; idx < kR * kR; idx += kThreads) {
+    const int p = idx / kR, k = idx % kR;
+    double v = 0.0;
+    if (p < r && k < r) {
+      const double s = sval(lm, k);
+      v = s > 0.0 ? u[p * kR + k] / sqrt(s) : 0.0;
+    }
+    ws[p][k] = v;
+  }
+  if (blockIdx.y == 0) {
+    for (int idx = threadIdx.x; idx < r * r; idx += kThreads) {
+      const int p = idx / r, k = idx % r;
+      core0[blk * (int64_t)d.m * r + idx] = (float)(u[p * kR + k] * sqrt(sval(lm, k)));
+    }
+  }
+  const int c_begin = blockIdx.y * cchunk;
+  const int c_end = min(d.n, c_begin + cchunk);
+  const int tk = threadIdx.x >> 4, tc = threadIdx.x & 15;
+  float local_max = 0.f;
+  float* out = core1 + blk * (int64_t)r * d.n;
+  for (int c0 = c_begin; c0 < c_end; c0 += kTile) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kR * kTile; idx += kThreads) {
+      const int p = idx / kTile, cc = idx - p * kTile;
+      const int col = c0 + cc;
+      xs[p][cc] = (p < r && col < c_end) ? load_a(base, d, p, col) : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int p = 0; p < r; ++p) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = ws[p][tk * 4 + i];
+        b[i] = xs[p][tc * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = tk * 4 + i;
+      if (k >= r) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = c0 + tc * 4 + j;
+        if (col < c_end) {
+          const float v = (float)acc[i][j];
+          out[(int64_t)k * d.n + col] = v;
+          local_max = fmaxf(local_max, fabsf(v));
+        }
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) local_max = fmaxf(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&amax[blk], __float_as_uint(local_max));
+}
+
+// ---- case B (n < m, tiny blocks): core1 = sqrt(s) V^T, core0 = A V diag(s^-1/2) ----
+__global__ void __launch_bounds__(kThreads) project_b_kernel(const void* __restrict__ in, Dims d,
+                                                             const double* __restrict__ V,
+                                                             const double* __restrict__ lam,
+                                                             float* __restrict__ core0, float* __restrict__ core1,
+                                                             unsigned* __restrict__ amax) {
+  const int64_t blk = blockIdx.x;
+  const void* base = block_ptr(in, d, blk);
+  const double* v = V + blk * kR * kR;
+  const double* lm = lam + blk * kR;
+  const int r = d.r;  // == n
+  float local_max = 0.f;
+  for (int idx = threadIdx.x; idx < r * d.n; idx += kThreads) {
+    const int k = idx / d.n, col = idx % d.n;
+    const float val = (float)(sqrt(sval(lm, k)) * v[col * kR + k]);
+    core1[blk * (int64_t)r * d.n + idx] = val;
+    local_max = fmaxf(local_max, fabsf(val));
+  }
+  for (int idx = threadIdx.x; idx < d.m * r; idx += kThreads) {
+    const int row = idx / r, k = idx % r;
+    const double s = sval(lm, k);
+    double acc = 0.0;
+    if (s > 0.0)
+      for (int col = 0; col < d.n; ++col) acc = fma(load_a(base, d, row, col), v[col * kR + k], acc);
+    core0[blk * (int64_t)d.m * r + idx] = s > 0.0 ? (float)(acc / sqrt(s)) : 0.f;
+  }
+  for (int o = 16; o; o >>= 1) local_max = fmaxf(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&amax[blk], __float_as_uint(local_max));
+}
+
+// ---- quantize + pack core1 into the requested layout (quantize.py:123-151) ----
+__global__ void quantize_core_kernel(const float* __restrict__ core1, int64_t core_elems, CoreGeom geom,
+                                     int64_t out_bytes, const unsigned* __restrict__ amax,
+                                     uint8_t* __restrict__ payload, int64_t payload_stride,
+                                     float* __restrict__ scale, int32_t* flags) {
+  const int64_t blk = blockIdx.y;
+  const int bits = geom.bits;
+  const int per = 8 / bits;
+  const int qmax = (1 << (bits - 1)) - 1;
+  const unsigned mask = (1u << bits) - 1u;
+  const float amax_f = __uint_as_float(amax[blk]);
+  if (!isfinite(amax_f)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && flags) atomicOr(flags, (int)DQ_FLAG_NONFINITE);
+  }
+  const double am = (double)amax_f;
+  bool degenerate;
+  const float sc = rtn_scale(am, qmax, &degenerate);
+  if (blockIdx.x == 0 && threadIdx.x == 0) scale[blk] = sc;
+  const float* src = core1 + blk * core_elems;
+  uint8_t* dst = payload + blk * payload_stride;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < out_bytes; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned v = 0;
+    if (!degenerate) {
+      for (int k = 0; k < per; ++k) {
+        const int64_t slot = i * per + k;
+        if (slot >= geom_slots(geom)) break;
+        int rr, b, e;
+        if (!geom_coords(geom, slot, rr, b, e)) continue;
+        const float t = src[((int64_t)rr * geom.i2 + b) * geom.j2 + e];
+        v |= ((unsigned)rtn_code(t, qmax, am) & mask) << (k * bits);
+      }
+    }
+    dst[i] = (uint8_t)v;
+  }
+}
+
+struct Workspace {
+  double* G;
+  double* U;
+  double* lam;
+  unsigned* amax;
+  float* core1;  // optional scratch
+};
+
+size_t ws_bytes(int64_t nblk, const Dims& d, bool need_core1) {
+  size_t b = 0;
+  b += (size_t)nblk * kR * kR * 8 * 2;  // G, U
+  b += (size_t)nblk * kR * 8;           // lam
+  b += round_up(nblk * 4, 256);         // amax
+  if (need_core1) b += (size_t)nblk * d.r * d.n * 4;
+  return b;
+}
+
+Workspace carve(void* base, int64_t nblk, const Dims& d, bool need_core1) {
+  Workspace w;
+  char* p = (char*)base;
+  w.G = (double*)p;
+  p += (size_t)nblk * kR * kR * 8;
+  w.U = (double*)p;
+  p += (size_t)nblk * kR * kR * 8;
+  w.lam = (double*)p;
+  p += (size_t)nblk * kR * 8;
+  w.amax = (unsigned*)p;
+  p += round_up(nblk * 4, 256);
+  w.core1 = need_core1 ? (float*)p : nullptr;
+  return w;
+}
+
+int check_args(const void* blocks, int32_t dtype, int64_t nblk, int64_t rows, int64_t cols) {
+  if (rows < 1 || cols < 1) return fail(DQ_ERR_SHAPE_MISMATCH, "dimensions must be >= 1");
+  if (nblk < 0 || (nblk && !blocks)) return fail(DQ_ERR_INVALID_ARG, "bad block arguments");
+  if (dtype != DQ_F32 && dtype != DQ_F16) return fail(DQ_ERR_INVALID_ARG, "unknown input dtype %d", dtype);
+  if (rows * cols > (int64_t)1 << 31) return fail(DQ_ERR_UNSUPPORTED, "block too large");
+  return DQ_OK;
+}
+
+// gram -> jacobi -> projection (core0 f32 + core1 f32 + amax)
+int factor_core(const void* blocks, const Dims& d, int64_t nblk, float* core0, float* core1, const Workspace& w,
+                int32_t* flags, cudaStream_t s) {
+  DQ_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)nblk * kR * kR * 8, s));
+  DQ_CUDA_TRY(cudaMemsetAsync(w.amax, 0, (size_t)nblk * 4, s));
+  // split the contraction so that the batch fills ~2 waves of 148 SMs
+  const int64_t target = 296;
+  int64_t splits = ceil_div(target, nblk);
+  int64_t chunk = round_up(ceil_div(d.kd, splits), kTile);
+  if (chunk < 4 * kTile) chunk = 4 * kTile;
+  splits = ceil_div(d.kd, chunk);
+  gram_kernel<<<dim3((unsigned)nblk, (unsigned)splits), kThreads, 0, s>>>(blocks, d, (int)chunk, w.G, flags);
+  DQ_LAUNCH_CHECK();
+  constexpr int kProjSmem = (int)(sizeof(double) * kR * (kR + 2) + sizeof(double) * kR * (kTile + 2));
+  static bool attr_set = false;
+  if (!attr_set) {
+    DQ_CUDA_TRY(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(JacobiSmem)));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(project_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kProjSmem));
+    attr_set = true;
+  }
+  jacobi_kernel<<<(unsigned)nblk, kThreads, sizeof(JacobiSmem), s>>>(w.G, d, w.U, w.lam, flags);
+  DQ_LAUNCH_CHECK();
+  if (d.caseA) {
+    int64_t csplits = ceil_div(target, nblk);
+    int64_t cchunk = round_up(ceil_div(d.n, csplits), kTile);
+    if (cchunk < 4 * kTile) cchunk = 4 * kTile;
+    csplits = ceil_div(d.n, cchunk);
+    project_a_kernel<<<dim3((unsigned)nblk, (unsigned)csplits), kThreads, kProjSmem, s>>>(blocks, d, (int)cchunk, w.U,
+                                                                                   w.lam, core0, core1, w.amax);
+  } else {
+    project_b_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(blocks, d, w.U, w.lam, core0, core1, w.amax);
+  }
+  DQ_LAUNCH_CHECK();
+  return DQ_OK;
+}
+
+}  // namespace
+
+}  // namespace dq
+
+using namespace dq;
+
+extern "C" int dq_decompose_workspace_size(int64_t nblk, int64_t rows, int64_t cols, size_t* bytes) {
+  if (!bytes) return fail(DQ_ERR_INVALID_ARG, "null output");
+  if (rows < 1 || cols < 1) return fail(DQ_ERR_SHAPE_MISMATCH, "dimensions must be >= 1");
+  Dims d = make_dims(make_plan2(rows, cols), rows, cols, DQ_F32);
+  *bytes = ws_bytes(nblk, d, true);
+  return DQ_OK;
+}
+
+extern "C" int dq_decompose_plan_batched(const void* blocks, int32_t dtype, int64_t nblk, const dq_plan2* hp,
+                                         float* core0, float* core1, int32_t* flags, void* ws, size_t wsb,
+                                         void* stream) {
+  if (!hp) return fail(DQ_ERR_INVALID_ARG, "null plan");
+  const int64_t rows = hp->i1 * hp->i2, cols = hp->j1 * hp->j2;
+  int st = check_args(blocks, dtype, nblk, rows, cols);
+  if (st) return st;
+  if (hp->i1 < 1 || hp->i2 < 1 || hp->j1 < 1 || hp->j2 < 1) return fail(DQ_ERR_SHAPE_MISMATCH, "factors must be >= 1");
+  const int64_t left = hp->i1 * hp->j1, right = hp->i2 * hp->j2;
+  if ((left < right ? left : right) > kR) return fail(DQ_ERR_UNSUPPORTED, "bond dimension %lld > %d",
+                                                      (long long)(left < right ? left : right), kR);
+  if (hp->r != (left < right ? left : right)) return fail(DQ_ERR_SHAPE_MISMATCH, "plan bond does not follow the bond law");
+  if (nblk == 0) return DQ_OK;
+  Dims d = make_dims(*hp, rows, cols, dtype);
+  if (!core0 || !core1 || !ws || wsb < ws_bytes(nblk, d, false))
+    return fail(DQ_ERR_INVALID_ARG, "dq_decompose_batched: missing output or workspace too small");
+  Workspace w = carve(ws, nblk, d, false);
+  return factor_core(blocks, d, nblk, core0, core1, w, flags, (cudaStream_t)stream);
+}
+
+extern "C" int dq_deco_quantize_batched(const void* blocks, int32_t dtype, int64_t nblk, int64_t rows, int64_t cols,
+                                        int32_t bits, int32_t layout, float* core0, uint8_t* payload,
+                                        int64_t payload_stride, float* scale, int32_t* flags, void* ws, size_t wsb,
+                                        void* stream) {
+  if (!bits_ok(bits)) return fail(DQ_ERR_UNSUPPORTED_BITS, "bits must be one of (2, 4, 8), got %d", bits);
+  int st = check_args(blocks, dtype, nblk, rows, cols);
+  if (st) return st;
+  if (nblk == 0) return DQ_OK;
+  dq_plan2 p = make_plan2(rows, cols);
+  Dims d = make_dims(p, rows, cols, dtype);
+  int64_t out_bytes;
+  st = dq_layout_bytes(&p, bits, layout, &out_bytes);
+  if (st) return st;
+  if (payload_stride < out_bytes) return fail(DQ_ERR_INVALID_ARG, "payload_stride smaller than one core");
+  if (!core0 || !payload || !scale || !ws || wsb < ws_bytes(nblk, d, true))
+    return fail(DQ_ERR_INVALID_ARG, "dq_deco_quantize_batched: missing output or workspace too small");
+  Workspace w = carve(ws, nblk, d, true);
+  cudaStream_t s = (cudaStream_t)stream;
+  st = factor_core(blocks, d, nblk, core0, w.core1, w, flags, s);
+  if (st) return st;
+  CoreGeom g = make_geom(p, bits, layout);
+  int64_t gx = ceil_div(out_bytes, kThreads);
+  if (gx > 64) gx = 64;
+  quantize_core_kernel<<<dim3((unsigned)gx, (unsigned)nblk), kThreads, 0, s>>>(
+      w.core1, (int64_t)d.r * d.n, g, out_bytes, w.amax, payload, payload_stride, scale, flags);
+  DQ_LAUNCH_CHECK();
+  return DQ_OK;
+}
+
+extern "C" int dq_decompose_batched(const void* blocks, int32_t dtype, int64_t nblk, int64_t rows, int64_t cols,
+                                    float* core0, float* core1, int32_t* flags, void* ws, size_t wsb, void* stream) {
+  if (rows < 1 || cols < 1) return fail(DQ_ERR_SHAPE_MISMATCH, "dimensions must be >= 1");
+  const dq_plan2 p = make_plan2(rows, cols);
+  return dq_decompose_plan_batched(blocks, dtype, nblk, &p, core0, core1, flags, ws, wsb, stream);
+}

@@ -108,6 +108,16 @@ def main():
             "bytes_compressed": rep.bytes_compressed,
         }
 
+    # ---- the reference's outlier matrix (test_compress.py:47-53) and its errors
+    sm = dquant.synth_activations(256, 256, outlier_cols=8, outlier_scale=20.0, seed=11)
+    arrays["synth256"] = sm
+    rec = compress.deco_dequantize(compress.deco_quantize(sm, 4))
+    direct = quantize.dequantize(quantize.quantize_rtn(sm, 4))
+    meta["synth256"] = {
+        "deco_err": float(np.linalg.norm(sm.astype(np.float64) - rec) / np.linalg.norm(sm)),
+        "direct_err": float(np.linalg.norm(sm.astype(np.float64) - direct) / np.linalg.norm(sm)),
+    }
+
     # ---- KV cache lifecycle (kvcache.py:94-225)
     cfg = kvcache.CacheConfig(layers=2, dim=128, bits=4, chunk_len=32)
     cache = kvcache.KvCache(cfg)

@@ -1,0 +1,155 @@
+"""K5 fused decode attention and the generic fused reads against the CPU oracle.
+
+Tolerance (north_star): relative Frobenius error <= 1e-3 of the attention output
+against the oracle's fp64 composition (scores kvcache.py:188-217 -> softmax ->
+per-segment x@W compress.py:159-192 + tail).  Inputs are fp16-rounded so both
+sides see identical K/V/q values.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import dquant_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def dq():
+    import paper_2405_12591_b200 as dq
+
+    return dq
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(a), 1e-30))
+
+
+@pytest.mark.parametrize("name", ["c1h0", "out512", "b2_256", "b8_256", "odd1009", "r1023", "tiny8", "s37x41",
+                                  "s64x48", "d64_512"])
+def test_generic_fused_reads_golden(golden, dq, name):
+    """fused_matmul / fused_matmul_t on the reference's own encoding vs its outputs."""
+    g, meta = golden
+    info = meta["blocks"][name]
+    bits = info["bits"]
+    core1 = g[f"{name}_core1"]
+    qt = dq.quantize_rtn(core1, bits)
+    plan = dq.plan_shapes(*info["shape"], 2)
+    q = dq.QuantizedMpo(plan=plan, bits=bits, local_tensors=(g[f"{name}_core0"], qt))
+    assert qt.payload == g[f"{name}_payload"].tobytes()
+    assert rel(g[f"{name}_mmt"], dq.fused_matmul_t(g[f"{name}_xt"], q)) < 1e-5
+    assert rel(g[f"{name}_mm"], dq.fused_matmul(g[f"{name}_x"], q)) < 1e-5
+    meter = dq.WorkingSetMeter()
+    dq.fused_matmul(g[f"{name}_x"], q, meter)
+    assert 0 < meter.peak_elements <= 64 * 64
+
+
+def _oracle_attend(k, v, q, bits, segs_T, tail):
+    """k, v: (T_total, 128) fp32; segments of lengths segs_T then `tail` dense rows."""
+    lay = O.LayerOracle(128, bits, 1 << 30)
+    off = 0
+    for i, T in enumerate(segs_T):
+        blk_k, blk_v = k[off:off + T], v[off:off + T]
+        if i == 0:
+            lay.prefill(blk_k, blk_v)
+        else:
+            lay.k_segs.append(O.encode(blk_k, bits))
+            lay.v_segs.append(O.encode(blk_v, bits))
+            lay.rows.append(T)
+        off += T
+    for t in range(tail):
+        lay.tail_k.append(k[off + t])
+        lay.tail_v.append(v[off + t])
+    return lay.attend(q)
+
+
+@pytest.mark.parametrize("bits,g,T,units", [
+    (4, 1, 4096, 4), (4, 1, 1024, 3), (4, 2, 2048, 2), (4, 4, 1024, 2), (2, 1, 2048, 2), (8, 1, 1024, 2),
+    (4, 1, 1009, 2), (4, 1, 1023, 2), (4, 1, 8192, 1),
+])
+def test_decode_attention_prefill_only(dq, bits, g, T, units):
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(T + 7 * g + bits)
+    k = rng.standard_normal((units, T, 128)).astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = rng.standard_normal((units, g, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=bits)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), bits,
+                             [T], 0)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
+def test_decode_attention_segments_and_tail(dq):
+    """prefill 1500 + 2 sealed chunks of 256 + tail 77, g=2, int4, outlier columns."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    units, g, chunk = 3, 2, 256
+    rng = np.random.default_rng(5)
+    P, steps = 1500, 2 * chunk + 77
+    total = P + steps
+    k = rng.standard_normal((units, total, 128)).astype(np.float32)
+    k[:, :, [3, 77]] *= 15.0  # outlier channels
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, total, 128)).astype(np.float16)
+    q = rng.standard_normal((units, g, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=2, units=units, g=g, bits=4, chunk_len=chunk)
+    kd, vd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    cache.prefill(1, kd[:, :P], vd[:, :P])
+    for t in range(P, total):
+        cache.append_token(1, kd[:, t], vd[:, t])
+    assert cache.tokens(1) == total
+    assert len(cache._layers[1].groups) == 3 and cache._layers[1].tail_len == 77
+    out = cache.attend(1, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), 4,
+                             [P, chunk, chunk], 77)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+    # ledger: reference accounting (kvcache.py:130-141)
+    fp16, actual = cache.ledger()
+    assert fp16 == 2 * total * 128 * 2 * units
+    assert actual / fp16 < 0.32
+
+
+def test_tail_only_and_empty(dq):
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    cache = DecodeKvCache(layers=1, units=2, g=1, bits=4, chunk_len=64)
+    q = torch.randn(2, 1, 128, device="cuda", dtype=torch.float16)
+    assert torch.count_nonzero(cache.attend(0, q)) == 0
+    rng = np.random.default_rng(2)
+    k = rng.standard_normal((2, 10, 128)).astype(np.float16)
+    v = rng.standard_normal((2, 10, 128)).astype(np.float16)
+    for t in range(10):
+        cache.append_token(0, torch.from_numpy(k[:, t]).cuda(), torch.from_numpy(v[:, t]).cuda())
+    out = cache.attend(0, q).float().cpu().numpy()
+    qn = q.float().cpu().numpy()
+    for u in range(2):
+        s = qn[u].astype(np.float64) @ k[u].astype(np.float64).T / np.sqrt(128)
+        p = np.exp(s - s.max())
+        p /= p.sum()
+        assert rel(p @ v[u].astype(np.float64), out[u]) < TOL
+
+
+def test_export_segment_wire_format(dq):
+    """Device layouts -> reference wire order: same bytes as deco_quantize on the same block."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(9)
+    k = rng.standard_normal((2, 1009, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=2, g=1, bits=4)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(k).cuda())
+    for which in ("k", "v"):
+        seg = cache.export_segment(0, 0, 1, which)
+        direct = dq.deco_quantize(k[1].astype(np.float32), 4)
+        assert seg.local_tensors[1].payload == direct.local_tensors[1].payload
+        assert seg.local_tensors[1].scale == direct.local_tensors[1].scale
+        assert rel(dq.deco_dequantize(direct), dq.deco_dequantize(seg).cpu().numpy()) < 1e-6
