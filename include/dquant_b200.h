@@ -65,15 +65,19 @@ extern "C" {
  * DQ_LAYOUT_REF  : the reference wire order, codes of core1 (r, i2, j2) in
  *                  row-major order, payload_size(r*i2*j2, bits) bytes
  *                  (quantize.py:11-14, 66-82).
- * DQ_LAYOUT_KROW : device K layout, (r, i2p, j2) with i2p = i2 rounded up to
- *                  a multiple of 64 and zero codes in the padding.  Equal to
- *                  DQ_LAYOUT_REF whenever i2 % 64 == 0.  Needs j2*bits % 8 == 0.
- * DQ_LAYOUT_VCOL : device V layout, (r, j2, i2p): the b index is innermost so
- *                  the PV contraction streams codes along its reduction axis.
+ * Device layouts (what the fused attention kernel streams; i2p = i2 rounded up to
+ * a multiple of 64, bt = b / 64 is a 64-row tile, padding codes encode 0; codes
+ * are stored in excess-2^(bits-1) form, i.e. code + 2^(bits-1) unsigned):
+ * DQ_LAYOUT_KTILE: (bt, r, 64, j2) with the 64 rows of a tile XOR-swizzled,
+ *                  row b' = (b % 64) ^ ((r & 3) * 16 / bits).  One (tile, r-range)
+ *                  is one contiguous bulk copy for the QK^T contraction.
+ * DQ_LAYOUT_VTILE: (bt, r, j2, 64): the b index innermost, so the PV contraction
+ *                  streams codes along its reduction axis.
+ * Both need j2*bits % 8 == 0.  dq_relayout converts to/from DQ_LAYOUT_REF.
  */
 #define DQ_LAYOUT_REF 0
-#define DQ_LAYOUT_KROW 1
-#define DQ_LAYOUT_VCOL 2
+#define DQ_LAYOUT_KTILE 1
+#define DQ_LAYOUT_VTILE 2
 
 /* ---- n=2 plan (mpo.py:73-96 with n=2; r = bond, mpo.py:54-63) ---------- */
 typedef struct dq_plan2 {
@@ -118,8 +122,11 @@ int dq_decompose_plan_batched(const void* blocks, int32_t in_dtype, int64_t nblk
 int dq_deco_quantize_batched(const void* blocks, int32_t in_dtype, int64_t nblk, int64_t rows, int64_t cols,
                              int32_t bits, int32_t layout, float* core0, uint8_t* payload, int64_t payload_stride,
                              float* scale, int32_t* flags, void* workspace, size_t workspace_bytes, void* stream);
-/* fp16 copy of core0 in the attention-friendly layout g0h[a][r][c] (i1 x r x j1) */
-int dq_core0_to_f16(const float* core0, int64_t nblk, const dq_plan2* h_plan, uint16_t* g0h, void* stream);
+/* fp16 copy of core0 in the attention-friendly layout g0h[a][r][c] (i1 x r x j1), normalised
+ * by a power of two per block so that max|g0h| is in [0.5, 1); norm[blk] receives that
+ * factor (core0 = g0h * norm).  norm may be null (then no normalisation). */
+int dq_core0_to_f16(const float* core0, int64_t nblk, const dq_plan2* h_plan, uint16_t* g0h, float* norm,
+                    void* stream);
 
 /* ---- K4 reconstruct (dequant + contraction), batched ------------------- */
 int dq_deco_dequantize_batched(const float* core0, const uint8_t* payload, int64_t payload_stride, int32_t layout,
@@ -145,11 +152,11 @@ int dq_fused_matmul(const float* x, int64_t p, const float* core0, const uint8_t
  * and an fp16 tail.  Segment s of the work list belongs to unit seg_unit[s].
  */
 typedef struct dq_segment {
-  const uint8_t* k_codes; /* DQ_LAYOUT_KROW */
-  const uint8_t* v_codes; /* DQ_LAYOUT_VCOL */
-  const uint16_t* k_g0;   /* fp16 [i1][r][8]  (dq_core0_to_f16 layout) */
+  const uint8_t* k_codes; /* DQ_LAYOUT_KTILE */
+  const uint8_t* v_codes; /* DQ_LAYOUT_VTILE */
+  const uint16_t* k_g0;   /* fp16 [i1][r][8]  (dq_core0_to_f16 layout, normalised) */
   const uint16_t* v_g0;   /* fp16 [i1][r][8] */
-  float k_scale, v_scale;
+  float k_scale, v_scale; /* quantizer scale times the G0 normalisation factor */
   int32_t T;          /* tokens in the segment */
   int32_t i1, i2, r;  /* plan of (T,128) */
   int32_t i2p;        /* padded i2 of the device layouts */
@@ -181,6 +188,8 @@ typedef struct dq_attn_args {
   const int32_t* unit_nparts;/* device [units] */
   float* part_o;          /* workspace [total_parts][g][128] f32 */
   float* part_ml;         /* workspace [total_parts][g][2]   f32 (max, sum) */
+  int32_t phases;         /* bit 0: split kernel, bit 1: combine kernel; 0 means both */
+  int32_t pad_;
 } dq_attn_args;
 
 /* host helper: fill work/partial tables (host arrays) for a host copy of the segment table */

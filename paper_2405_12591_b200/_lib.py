@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdquant_b
 
 DQ_OK = 0
 DQ_F32, DQ_F16 = 0, 1
-LAYOUT_REF, LAYOUT_KROW, LAYOUT_VCOL = 0, 1, 2
+LAYOUT_REF, LAYOUT_KTILE, LAYOUT_VTILE = 0, 1, 2
 FLAG_NONFINITE, FLAG_RANGE_OVERFLOW, FLAG_JACOBI_NOCONV = 1, 2, 4
 I2_PAD = 64
 
@@ -86,6 +86,8 @@ class AttnArgs(ctypes.Structure):
         ("unit_nparts", c_void_p),
         ("part_o", c_void_p),
         ("part_ml", c_void_p),
+        ("phases", c_int32),
+        ("pad_", c_int32),
     ]
 
 
@@ -109,7 +111,7 @@ SIGNATURES = {
                                             c_void_p, c_size_t, c_void_p]),
     "dq_deco_quantize_batched": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p,
                                            c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
-    "dq_core0_to_f16": (c_int32, [c_void_p, c_int64, POINTER(Plan2), c_void_p, c_void_p]),
+    "dq_core0_to_f16": (c_int32, [c_void_p, c_int64, POINTER(Plan2), c_void_p, c_void_p, c_void_p]),
     "dq_deco_dequantize_batched": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int64,
                                              c_int64, c_int32, c_void_p, c_int32, c_void_p]),
     "dq_relayout": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int32, c_int64, c_int64, POINTER(Plan2),

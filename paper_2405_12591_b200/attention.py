@@ -6,7 +6,7 @@ at once:
 
 * ``prefill(layer, K, V)``: the whole prompt of every unit becomes ONE segment
   (kvcache.py:99-114), compressed by K3 (csrc/factor.cu) straight into the
-  device layouts the attention kernel streams (K: DQ_LAYOUT_KROW, V: DQ_LAYOUT_VCOL).
+  device layouts the attention kernel streams (K: DQ_LAYOUT_KTILE, V: DQ_LAYOUT_VTILE).
 * ``append_token(layer, k, v)``: fp16 tail write (kvcache.py:116-123); when the
   tail reaches ``chunk_len`` it is sealed into a new segment (kvcache.py:124-128).
 * ``attend(layer, q)``: softmax(q K^T / sqrt(128)) V over every segment and the
@@ -35,6 +35,7 @@ from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_
 
 HEAD_DIM = 128
 DEFAULT_CHUNK_B = 256
+SUPPORTED_G = (1, 2)
 MAX_BLOCKS_PER_CALL = 512  # bounds the K3 fp32 core1 scratch
 
 
@@ -45,14 +46,16 @@ class SegmentGroup:
     T: int
     plan: _lib.Plan2
     i2p: int
-    k_payload: torch.Tensor  # (units, kbytes) u8, KROW
-    v_payload: torch.Tensor  # (units, vbytes) u8, VCOL
+    k_payload: torch.Tensor  # (units, kbytes) u8, KTILE
+    v_payload: torch.Tensor  # (units, vbytes) u8, VTILE
     k_core0: torch.Tensor    # (units, 1, i1, 8, r) f32
     v_core0: torch.Tensor
-    k_g0h: torch.Tensor      # (units, i1*r*8) f16, [a][r][c]
+    k_g0h: torch.Tensor      # (units, i1*r*8) f16, [a][r][c], normalised (core0 = g0h * norm)
     v_g0h: torch.Tensor
-    k_scale: torch.Tensor    # (units,) f32
+    k_scale: torch.Tensor    # (units,) f32 quantizer scale
     v_scale: torch.Tensor
+    k_norm: torch.Tensor     # (units,) f32 power-of-two G0 normalisation
+    v_norm: torch.Tensor
     token0: int
 
     def reference_bytes(self, bits: int) -> int:
@@ -78,7 +81,7 @@ class _Layer:
 def compress_blocks(blocks: torch.Tensor, bits: int, layout: int):
     """K3 over (nblk, T, 128) fp16/fp32 CUDA blocks in slices of MAX_BLOCKS_PER_CALL.
 
-    Returns (payload (nblk, bytes), core0 f32, g0h f16 [a][r][c], scale f32, plan).
+    Returns (payload (nblk, bytes), core0 f32, g0h f16 [a][r][c] normalised, norm f32, scale f32, plan).
     """
     nblk = blocks.shape[0]
     outs = []
@@ -91,8 +94,10 @@ def compress_blocks(blocks: torch.Tensor, bits: int, layout: int):
     core0 = torch.cat([o["core0"] for o in outs]) if len(outs) > 1 else outs[0]["core0"]
     scale = torch.cat([o["scale"] for o in outs]) if len(outs) > 1 else outs[0]["scale"]
     g0h = torch.empty((nblk, p.i1 * p.r * p.j1), dtype=torch.float16, device=blocks.device)
-    check(lib().dq_core0_to_f16(ptr(core0), nblk, ctypes.byref(p), ptr(g0h), stream_ptr()), "core0_to_f16")
-    return payload, core0, g0h, scale, p
+    norm = torch.empty(nblk, dtype=torch.float32, device=blocks.device)
+    check(lib().dq_core0_to_f16(ptr(core0), nblk, ctypes.byref(p), ptr(g0h), ptr(norm), stream_ptr()),
+          "core0_to_f16")
+    return payload, core0, g0h, norm, scale, p
 
 
 class DecodeKvCache:
@@ -105,6 +110,10 @@ class DecodeKvCache:
                  dim: int = HEAD_DIM, chunk_b: int = DEFAULT_CHUNK_B, sm_scale: float | None = None):
         if dim != HEAD_DIM:
             raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
+        if g not in SUPPORTED_G:
+            raise Unsupported(f"the fused decode kernel supports GQA groups g in {SUPPORTED_G}")
+        if chunk_b != DEFAULT_CHUNK_B:
+            raise Unsupported(f"the fused decode kernel splits segments into {DEFAULT_CHUNK_B}-row work items")
         if bits not in SUPPORTED_BITS:
             raise UnsupportedBits(f"bits must be in {SUPPORTED_BITS}")
         if layers < 1 or units < 1 or chunk_len < 1:
@@ -133,10 +142,10 @@ class DecodeKvCache:
     def _add_group(self, layer: int, keys: torch.Tensor, values: torch.Tensor):
         lay = self._layer(layer)
         T = keys.shape[1]
-        kp, kc0, kg, ks, p = compress_blocks(keys, self.bits, _lib.LAYOUT_KROW)
-        vp, vc0, vg, vs, _ = compress_blocks(values, self.bits, _lib.LAYOUT_VCOL)
+        kp, kc0, kg, kn, ks, p = compress_blocks(keys, self.bits, _lib.LAYOUT_KTILE)
+        vp, vc0, vg, vn, vs, _ = compress_blocks(values, self.bits, _lib.LAYOUT_VTILE)
         i2p = -(-p.i2 // _lib.I2_PAD) * _lib.I2_PAD
-        lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, lay.tokens_sealed))
+        lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, kn, vn, lay.tokens_sealed))
         lay.tokens_sealed += T
         lay.args = None
 
@@ -172,7 +181,8 @@ class DecodeKvCache:
     def _build_args(self, layer: int):
         lay = self._layers[layer]
         segs = []
-        scales = [(grp.k_scale.cpu(), grp.v_scale.cpu()) for grp in lay.groups]
+        # the kernel sees g0h = core0 / norm, so the per-segment scale carries the norm back
+        scales = [((grp.k_scale * grp.k_norm).cpu(), (grp.v_scale * grp.v_norm).cpu()) for grp in lay.groups]
         for grp, (ks, vs) in zip(lay.groups, scales):
             p = grp.plan
             kb, vb = grp.k_payload.shape[1], grp.v_payload.shape[1]
@@ -252,7 +262,33 @@ class DecodeKvCache:
         self.bytes_moved_read += self.read_bytes(layer)
         return out
 
+    def launch(self, layer: int, q: torch.Tensor, out: torch.Tensor, phases: int = 3):
+        """Low-level launch (bench/profiling): phases bit 0 = split kernel, bit 1 = combine."""
+        lay = self._layers[layer]
+        if lay.args is None:
+            self._build_args(layer)
+        a = lay.args
+        a.q, a.out, a.phases = q.data_ptr(), out.data_ptr(), phases
+        check(lib().dq_decode_attention(ctypes.byref(a), stream_ptr()), "decode_attention")
+        a.phases = 0
+
+    def clone_layer(self, src: int, dst: int):
+        """Copy layer ``src``'s sealed segments into empty layer ``dst`` (distinct device memory)."""
+        s, d = self._layer(src), self._layer(dst)
+        if d.groups or d.tail_len:
+            raise AlreadyPrefilled("destination layer already holds tokens")
+        for grp in s.groups:
+            fields = {k: (v.clone() if isinstance(v, torch.Tensor) else v) for k, v in grp.__dict__.items()}
+            d.groups.append(SegmentGroup(**fields))
+        d.tokens_sealed = s.tokens_sealed
+        d.args = None
+
     # ---- accounting ----------------------------------------------------------
+    def kernel_bytes(self, layer: int) -> int:
+        """Algorithmic bytes of one split-kernel launch: compressed segments + q."""
+        lay = self._layers[layer]
+        return sum(g.stream_bytes() for g in lay.groups) * self.units + self.units * self.g * self.dim * 2
+
     def read_bytes(self, layer: int) -> int:
         """Algorithmic HBM bytes one ``attend(layer)`` streams (all units)."""
         lay = self._layers[layer]
@@ -276,7 +312,7 @@ class DecodeKvCache:
         grp = self._layer(layer).groups[index]
         p = grp.plan
         src = grp.k_payload if which == "k" else grp.v_payload
-        layout = _lib.LAYOUT_KROW if which == "k" else _lib.LAYOUT_VCOL
+        layout = _lib.LAYOUT_KTILE if which == "k" else _lib.LAYOUT_VTILE
         nbytes = payload_size(p.r * p.i2 * p.j2, self.bits)
         dst = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         check(lib().dq_relayout(ptr(src[unit]), layout, src.shape[1], ptr(dst), _lib.LAYOUT_REF, nbytes, 1,

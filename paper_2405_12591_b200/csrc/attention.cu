@@ -1,7 +1,7 @@
 // K5: fused DecoQuant dequantisation + decode attention for D = 128 (j = (8,16)).
 //
 // Reference semantics (kvcache.py:188-217 scores, compress.py:159-231 fused reads):
-// for one unit (sequence, kv head) with segments s of T_s tokens (plan i=(i1,i2),
+// for one unit (sequence, kv head) with segments of T_s tokens (plan i=(i1,i2),
 // bond r) and g query rows q[h] (GQA group), the output is
 //     softmax_t(q.K^T * sm_scale) V        over all segments and the fp16 tail,
 // with K[a*i2+b, c*16+e] = sum_r G0k[a,c,r] * scale_k * code_k[r,b,e] (same for V).
@@ -9,17 +9,21 @@
 // Factored order: per segment
 //   W[h,a,r,e] = sum_c q[h,c*16+e] G0k[a,c,r]                  (CUDA cores, per CTA)
 //   S[h,a,b]   = scale_k * sum_{r,e} W[h,a,r,e] code_k[r,b,e]   (tensor cores)
-//   P          = exp(S*sm_scale - m)                           (online softmax, split-T)
+//   P          = exp(S*sm_scale - m)                           (split-T softmax)
 //   Y[h,a,r,e] = sum_b P[h,a,b] code_v[r,b,e]                  (tensor cores)
 //   O[h,c,e]   = scale_v * sum_{a,r} G0v[a,c,r] Y[h,a,r,e]     (CUDA cores, epilogue)
-// Codes never leave registers as anything but fp16 MMA fragments: packed words are
-// loaded with 4/8/16-byte coalesced loads straight into the fragment layout (the
-// reduction index is permuted identically on both MMA operands, which is free),
-// converted with the 0x6400 magic-number trick (exact: |code| <= 127 < 1024), and
-// fed to mma.sync m16n8k16 (f16 x f16 -> f32).  Full-precision K/V never exist.
 //
-// Work item = (segment, 64*k-row slice of b) -> one CTA; partial (m, l, O) per item,
-// merged with the dense fp16 tail by combine_kernel (flash-decoding split).
+// Data movement: one work item = (segment, 256-row slice of b) = one CTA.  Its packed
+// K codes (DQ_LAYOUT_KTILE) and V codes (DQ_LAYOUT_VTILE) are streamed through a
+// 4-stage x 16 KB shared-memory ring by cp.async.bulk (TMA bulk copies completing on
+// mbarriers); the last warp to release a stage issues its refill, so up to 64 KB per
+// CTA (128 KB per SM at 2 CTAs/SM) is in flight with no register cost.  Consumers read
+// bank-conflict-free fragments (the K tile rows are XOR-swizzled by r in HBM), turn
+// pairs of excess-coded codes into fp16 with one LOP3 (0x6400 magic; codes at nibble
+// position 1/3 come out x16 and that power of two is folded into the other MMA
+// operand), subtract the excess with one HSUB2, and feed mma.sync m16n8k16
+// (f16 x f16 -> f32).  The reduction index is permuted identically on both operands,
+// which is free.  Full-precision K/V never exist anywhere.
 #include "common.cuh"
 
 namespace dq {
@@ -30,8 +34,46 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kD = 128;
 constexpr int kMaxR = 64;
+constexpr int kCB = 256;                 // b rows per work item
+constexpr int kTiles = kCB / kI2Pad;     // 64-row tiles per work item
+constexpr int kNG = kCB / 16;            // 16-row groups per work item
+constexpr int kStageBytes = 16384;
+constexpr int kStages = 4;
 
-// ---- MMA ---------------------------------------------------------------------
+// ---- PTX wrappers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -41,187 +83,255 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// ---- packed rows of 16 codes ------------------------------------------------
-// BITS=4: 8 bytes, BITS=2: 4 bytes, BITS=8: 16 bytes.  Stored pre-biased
-// (xor with the sign bit of every lane) so each lane is code + 2^(bits-1).
+// ---- code rows ------------------------------------------------------------------
+// A row is 16 codes of one (r, b) [K] or one (r, e) x 16 b [V]: 2*BITS bytes.
 template <int BITS>
 struct Row {
   uint32_t w[BITS == 8 ? 4 : (BITS == 4 ? 2 : 1)];
 };
 
 template <int BITS>
-__device__ __forceinline__ Row<BITS> load_row(const uint8_t* p) {
+__device__ __forceinline__ Row<BITS> lds_row(const unsigned char* p) {
   Row<BITS> r;
   if constexpr (BITS == 4) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-    r.w[0] = v.x ^ 0x88888888u;
-    r.w[1] = v.y ^ 0x88888888u;
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    r.w[0] = v.x;
+    r.w[1] = v.y;
   } else if constexpr (BITS == 2) {
-    r.w[0] = __ldg(reinterpret_cast<const uint32_t*>(p)) ^ 0xAAAAAAAAu;
+    r.w[0] = *reinterpret_cast<const uint32_t*>(p);
   } else {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-    r.w[0] = v.x ^ 0x80808080u;
-    r.w[1] = v.y ^ 0x80808080u;
-    r.w[2] = v.z ^ 0x80808080u;
-    r.w[3] = v.w ^ 0x80808080u;
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    r.w[0] = v.x;
+    r.w[1] = v.y;
+    r.w[2] = v.z;
+    r.w[3] = v.w;
   }
   return r;
 }
 
-template <int BITS>
-__device__ __forceinline__ Row<BITS> zero_row() {
-  Row<BITS> r;
-#pragma unroll
-  for (int i = 0; i < (int)(sizeof(r.w) / 4); ++i) r.w[i] = BITS == 4 ? 0x88888888u : (BITS == 2 ? 0xAAAAAAAAu : 0x80808080u);
-  return r;
+__device__ __forceinline__ uint32_t hsub2_u32(uint32_t x, uint32_t bias) {
+  __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&x), *reinterpret_cast<const __half2*>(&bias));
+  return *reinterpret_cast<uint32_t*>(&r);
 }
 
-// half2 pairs for sub-MMA c: lo -> k slots (2t, 2t+1), hi -> (2t+8, 2t+9).
-// The element of the 16-group that lands in each slot is perm<BITS>(4c + {0,1,2,3}).
+// fp16 pairs for sub-MMA C: lo -> k slots (2t, 2t+1), hi -> (2t+8, 2t+9).
+// Slot q = 4C + {0,1,2,3} holds element perm16(q) of the 16-group, times kscale(q).
 template <int BITS, int C>
 __device__ __forceinline__ void row_pairs(const Row<BITS>& r, uint32_t& lo, uint32_t& hi) {
-  uint32_t l, h;
+  constexpr uint32_t M = 0x64006400u;
   if constexpr (BITS == 4) {
-    l = ((r.w[0] >> (4 * C)) & 0x000F000Fu) | 0x64006400u;
-    h = ((r.w[1] >> (4 * C)) & 0x000F000Fu) | 0x64006400u;
+    const uint32_t w0 = (C >= 2) ? (r.w[0] >> 8) : r.w[0];
+    const uint32_t w1 = (C >= 2) ? (r.w[1] >> 8) : r.w[1];
+    constexpr uint32_t mask = (C & 1) ? 0x00F000F0u : 0x000F000Fu;
+    constexpr uint32_t bias = (C & 1) ? 0x64806480u : 0x64086408u;  // 1024 + s*8, s = 16 or 1
+    lo = hsub2_u32((w0 & mask) | M, bias);
+    hi = hsub2_u32((w1 & mask) | M, bias);
   } else if constexpr (BITS == 2) {
-    l = ((r.w[0] >> (2 * C)) & 0x00030003u) | 0x64006400u;
-    h = ((r.w[0] >> (2 * C + 8)) & 0x00030003u) | 0x64006400u;
+    const uint32_t w = (C >= 2) ? (r.w[0] >> 8) : r.w[0];
+    constexpr uint32_t mlo = (C & 1) ? 0x00300030u : 0x00030003u;
+    constexpr uint32_t mhi = (C & 1) ? 0x00C000C0u : 0x000C000Cu;
+    constexpr uint32_t blo = (C & 1) ? 0x64206420u : 0x64026402u;  // 1024 + 2s, s = 16 / 1
+    constexpr uint32_t bhi = (C & 1) ? 0x64806480u : 0x64086408u;  // s = 64 / 4
+    lo = hsub2_u32((w & mlo) | M, blo);
+    hi = hsub2_u32((w & mhi) | M, bhi);
   } else {
-    l = (r.w[C] & 0x00FF00FFu) | 0x64006400u;
-    h = ((r.w[C] >> 8) & 0x00FF00FFu) | 0x64006400u;
+    lo = hsub2_u32((r.w[C] & 0x00FF00FFu) | M, 0x64806480u);
+    hi = hsub2_u32(((r.w[C] >> 8) & 0x00FF00FFu) | M, 0x64806480u);
   }
-  constexpr uint32_t bias = BITS == 4 ? 0x64086408u : (BITS == 2 ? 0x64026402u : 0x64806480u);  // 1024+2^(b-1)
-  const __half2 hb = *reinterpret_cast<const __half2*>(&bias);
-  __half2 hl = __hsub2(*reinterpret_cast<__half2*>(&l), hb);
-  __half2 hh = __hsub2(*reinterpret_cast<__half2*>(&h), hb);
-  lo = *reinterpret_cast<uint32_t*>(&hl);
-  hi = *reinterpret_cast<uint32_t*>(&hh);
 }
 
-// element of the 16-group held in permuted position q (must match row_pairs)
+// element of the 16-group in k-slot q of the 4 sub-MMAs (must match row_pairs)
 template <int BITS>
 __host__ __device__ constexpr int perm16(int q) {
   const int c = q >> 2, j = q & 3;
-  if (BITS == 4) return c + 4 * j;                       // c, c+4, c+8, c+12
-  if (BITS == 2) return c + (j == 1 ? 8 : j == 2 ? 4 : j == 3 ? 12 : 0);  // c, c+8, c+4, c+12
-  return 4 * c + (j == 1 ? 2 : j == 2 ? 1 : j);           // 4c, 4c+2, 4c+1, 4c+3
+  if (BITS == 4) return c + 4 * j;                                   // c, c+4, c+8, c+12
+  if (BITS == 2) return 2 * c + (j == 1 ? 8 : j == 2 ? 1 : j == 3 ? 9 : 0);  // 2c, 2c+8, 2c+1, 2c+9
+  return 4 * c + (j == 1 ? 2 : j == 2 ? 1 : j);                       // 4c, 4c+2, 4c+1, 4c+3
 }
 
+// power of two the code in k-slot q comes out multiplied by (folded into the other operand)
 template <int BITS>
-__device__ __forceinline__ int inv_perm16(int e) {
-#pragma unroll
-  for (int q = 0; q < 16; ++q)
-    if (perm16<BITS>(q) == e) return q;
-  return 0;
+__host__ __device__ constexpr float kscale16(int q) {
+  const int c = q >> 2, j = q & 3;
+  if (BITS == 4) return (c & 1) ? 16.f : 1.f;
+  if (BITS == 2) return (float)((c & 1 ? 16 : 1) * (j >= 2 ? 4 : 1));
+  return 1.f;
 }
 
-template <int G, int CB>
+template <int G>
 struct AttnSmem {
+  alignas(128) unsigned char ring[kStages][kStageBytes];
+  uint64_t full[kStages];
+  unsigned int released[kStages];
   float q[G][kD];
-  // W in fragment order: 16-byte chunks [(h*r + rr)*2 + j][a ^ 2*(rr&3)]
-  uint4 w[G * kMaxR * 2 * 8];
-  // G0v fp16 [a][r][c] (16 bytes per (a, r))
-  uint4 g0v[8 * kMaxR];
-  float s[G][8][CB];
-  // P in fragment order: 16-byte chunks [((h*8 + a)*NG + bg)*2 + (j ^ (a&1))]
-  uint4 p[G * 8 * (CB / 16) * 2];
-  float red[kWarps][G][kD];
-  float wmax;
+  float qmax;
+  // K phase: W fragments, 16-byte chunks [(h*r + rr)*2 + j][a ^ 2*(rr&3)];
+  // V phase (aliased): P fragments [((h*8 + a)*kNG + bg)*2 + (j ^ (a&1))]
+  union {
+    uint4 w[G * kMaxR * 2 * 8];
+    uint4 p[G * 8 * kNG * 2];
+  } wp;
+  uint4 g0v[8 * kMaxR];  // fp16 [a][r][c], normalised
+  // scores (phase 1-2) and the cross-warp reduction (phase 4) share storage
+  union {
+    float s[G][8][kCB];
+    float red[kWarps][G][kD];
+  } sr;
   float rowmax[G][kWarps];
   float rowsum[G][kWarps];
 };
 
-template <int BITS, int G, int MT>
-__global__ void __launch_bounds__(kThreads) decode_attn_kernel(dq_attn_args args) {
-  constexpr int CB = MT * 16 * kWarps;  // b rows per work item
-  constexpr int NG = CB / 16;
-  constexpr int RB = 2 * BITS;          // bytes per 16-code row
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  AttnSmem<G, CB>& sm = *reinterpret_cast<AttnSmem<G, CB>*>(smem_raw);
+// stage geometry of one work item (identical in every thread)
+template <int BITS>
+struct Plan {
+  int r, nbt, bt0;
+  int RK, nK;              // K stages: RK bond rows x nbt tiles each
+  int rw, kslice, RV, nV;  // V stages: (tile, slice of RV bond rows)
+  int nslices;
+  __device__ Plan(const dq_segment& s, int wb0) {
+    constexpr int RB = 2 * BITS;
+    r = s.r;
+    bt0 = wb0 / kI2Pad;
+    nbt = min(kTiles, (s.i2p - wb0) / kI2Pad);
+    RK = kStageBytes / (nbt * kI2Pad * RB);
+    RK = RK & ~3;
+    if (RK > r) RK = r;
+    nK = (r + RK - 1) / RK;
+    rw = r / kWarps;
+    kslice = kWarps;
+    while (kslice > 1 && kslice * rw * 16 * kI2Pad * BITS / 8 > kStageBytes) kslice >>= 1;
+    RV = kslice * rw;
+    nslices = kWarps / kslice;
+    nV = nbt * nslices;
+  }
+  __device__ int stages() const { return nK + nV; }
+};
+
+// issue stage `st` of the work item into its ring slot (one thread)
+template <int BITS>
+__device__ __forceinline__ void issue_stage(const Plan<BITS>& pl, const dq_segment& seg, int st,
+                                            unsigned char* slot_buf, uint64_t* bar) {
+  constexpr int RB = 2 * BITS;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (st < pl.nK) {
+    const int rk0 = st * pl.RK;
+    const int nr = min(pl.RK, pl.r - rk0);
+    const uint32_t chunk = (uint32_t)(nr * kI2Pad * RB);
+    mbar_expect_tx(bar, chunk * pl.nbt);
+    for (int j = 0; j < pl.nbt; ++j) {
+      const unsigned char* src = seg.k_codes + ((size_t)(pl.bt0 + j) * pl.r + rk0) * kI2Pad * RB;
+      bulk_g2s(slot_buf + j * chunk, src, chunk, bar);
+    }
+  } else {
+    const int v = st - pl.nK;
+    const int btl = v / pl.nslices, sl = v % pl.nslices;
+    const uint32_t bytes = (uint32_t)(pl.RV * 16 * kI2Pad * BITS / 8);
+    mbar_expect_tx(bar, bytes);
+    const unsigned char* src = seg.v_codes + ((size_t)(pl.bt0 + btl) * pl.r + sl * pl.RV) * 16 * kI2Pad * BITS / 8;
+    bulk_g2s(slot_buf, src, bytes, bar);
+  }
+}
+
+template <int BITS, int G>
+__global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(dq_attn_args args) {
+  constexpr int RB = 2 * BITS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  AttnSmem<G>& sm = *reinterpret_cast<AttnSmem<G>*>(smem_raw);
 
   const int wi = blockIdx.x;
   const int seg_id = args.work[2 * wi];
   const int wb0 = args.work[2 * wi + 1];
   const dq_segment seg = args.segs[seg_id];
   const int unit = seg.unit;
-  const int r = seg.r, i1 = seg.i1, i2 = seg.i2, i2p = seg.i2p;
+  const int r = seg.r, i1 = seg.i1, i2 = seg.i2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tid4 = lane & 3;
+  const Plan<BITS> pl(seg, wb0);
+  const int nstages = pl.stages();
 
-  // ---- phase 0: q, W = q . G0k (fp32 -> fp16 fragments), G0v ------------------
+  // ---- prologue: barriers + first stages in flight before anything else ----------
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      sm.released[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int s = 0; s < kStages && s < nstages; ++s)
+      issue_stage<BITS>(pl, seg, s, sm.ring[s], &sm.full[s]);
+  }
+
+  // ---- phase 0: q, W = q . G0k (normalised G0, power-of-two prescale), G0v ----------
   const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)unit * G * kD;
-  for (int i = tid; i < G * kD; i += kThreads) sm.q[i / kD][i % kD] = __half2float(qh[i]);
-  if (tid == 0) sm.wmax = 0.f;
+  float qm = 0.f;
+  for (int i = tid; i < G * kD; i += kThreads) {
+    const float v = __half2float(qh[i]);
+    sm.q[i / kD][i % kD] = v;
+    qm = fmaxf(qm, fabsf(v));
+  }
+  for (int o = 16; o; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+  if (tid == 0) sm.qmax = 0.f;
   {
     const uint4* src = reinterpret_cast<const uint4*>(seg.v_g0);
     for (int i = tid; i < i1 * r; i += kThreads) sm.g0v[i] = src[i];
   }
   __syncthreads();
-  // load the G0k row of bond index rr (8 values of c), zeros for a >= i1
-  const uint4* g0k = reinterpret_cast<const uint4*>(seg.k_g0);
-  auto g0k_row = [&](int a, int rr, float (&gk)[8]) {
-    if (a < i1) {
-      const uint4 gv = g0k[a * r + rr];
-      const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __half22float2(g2[k]);
-        gk[2 * k] = f.x;
-        gk[2 * k + 1] = f.y;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) gk[k] = 0.f;
-    }
-  };
-  float lmax = 0.f;
-  for (int item = tid; item < G * 8 * r; item += kThreads) {
-    const int h = item / (8 * r), rem = item - h * 8 * r;
-    const int a = rem / r, rr = rem - a * r;
-    float gk[8];
-    g0k_row(a, rr, gk);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc = fmaf(sm.q[h][c * 16 + e], gk[c], acc);
-      lmax = fmaxf(lmax, fabsf(acc));
-    }
-  }
-  for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-  if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(&sm.wmax), __float_as_uint(lmax));
+  if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(&sm.qmax), __float_as_uint(qm));
   __syncthreads();
-  // power-of-two prescale keeps |W| inside fp16 range (exact, undone in the score scale)
+  // |W| <= 8 max|q| max|g0| <= 8 max|q|; keep it below 2^14 with an exact power of two
   float wscale = 1.f;
+  while (8.f * sm.qmax * wscale > 16384.f) wscale *= 0.5f;
   {
-    const float wm = sm.wmax;
-    while (wm * wscale > 16384.f) wscale *= 0.5f;
-  }
-  for (int item = tid; item < G * 8 * r; item += kThreads) {
-    const int h = item / (8 * r), rem = item - h * 8 * r;
-    const int a = rem / r, rr = rem - a * r;
-    float gk[8];
-    g0k_row(a, rr, gk);
-    float wv[16];
+    const uint4* g0k = reinterpret_cast<const uint4*>(seg.k_g0);
+    for (int item = tid; item < G * 8 * r; item += kThreads) {
+      const int h = item / (8 * r), rem = item - h * 8 * r;
+      const int a = rem / r, rr = rem - a * r;
+      float gk[8];
+      if (a < i1) {
+        const uint4 gv = g0k[a * r + rr];
+        const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      float acc = 0.f;
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(g2[k]);
+          gk[2 * k] = f.x;
+          gk[2 * k + 1] = f.y;
+        }
+      } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) acc = fmaf(sm.q[h][c * 16 + e], gk[c], acc);
-      wv[e] = acc * wscale;
+        for (int k = 0; k < 8; ++k) gk[k] = 0.f;
+      }
+      __half hv[16];
+#pragma unroll
+      for (int qi = 0; qi < 16; ++qi) {
+        const int e = perm16<BITS>(qi);
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc = fmaf(sm.q[h][c * 16 + e], gk[c], acc);
+        hv[qi] = __float2half_rn(acc * (wscale / kscale16<BITS>(qi)));
+      }
+      const int sw = a ^ (2 * (rr & 3));
+      sm.wp.w[((h * r + rr) * 2 + 0) * 8 + sw] = *reinterpret_cast<uint4*>(&hv[0]);
+      sm.wp.w[((h * r + rr) * 2 + 1) * 8 + sw] = *reinterpret_cast<uint4*>(&hv[8]);
     }
-    __half hv[16];
-#pragma unroll
-    for (int qi = 0; qi < 16; ++qi) hv[qi] = __float2half_rn(wv[perm16<BITS>(qi)]);
-    const int sw = a ^ (2 * (rr & 3));
-    sm.w[((h * r + rr) * 2 + 0) * 8 + sw] = *reinterpret_cast<uint4*>(&hv[0]);
-    sm.w[((h * r + rr) * 2 + 1) * 8 + sw] = *reinterpret_cast<uint4*>(&hv[8]);
   }
   __syncthreads();
 
-  // ---- phase 1: S = W . codes_k (tensor cores) ---------------------------------
-  const int wbase = wb0 + warp * MT * 16;  // first b row of this warp
+  int st = 0;  // running stage index
+  auto release = [&](int s) {
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const int slot = s % kStages;
+      const unsigned target = (unsigned)(s / kStages + 1) * kWarps;
+      const unsigned old = atomicAdd(&sm.released[slot], 1u);
+      if (old + 1 == target && s + kStages < nstages)
+        issue_stage<BITS>(pl, seg, s + kStages, sm.ring[slot], &sm.full[slot]);
+    }
+  };
+
+  // ---- phase 1: S = W . codes_k ---------------------------------------------------
+  constexpr int MT = 2;  // 16-row m-tiles per warp (32 b rows)
+  const int jt = warp >> 1;                     // tile of this warp inside the item
+  const int bl_base = 32 * (warp & 1);          // first row of this warp inside the tile
   float acc[MT][G][4];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
@@ -229,60 +339,49 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(dq_attn_args args
     for (int h = 0; h < G; ++h)
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[mt][h][k] = 0.f;
-  {
-    const uint8_t* kc = seg.k_codes;
-    bool valid[MT][2];
+  for (int ks = 0; ks < pl.nK; ++ks, ++st) {
+    const int slot = st % kStages;
+    mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
+    const int rk0 = ks * pl.RK;
+    const int nr = min(pl.RK, r - rk0);
+    if (jt < pl.nbt) {
+      const unsigned char* tile = sm.ring[slot] + jt * nr * kI2Pad * RB;
+      for (int q0 = 0; q0 < nr; q0 += 4) {
+        const int rl = q0 + tid4;     // bond row inside the stage
+        const int rr = rk0 + rl;      // global bond row
+        const int swz = ktile_swizzle(rr, BITS);
+        uint4 bw[G][2];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      valid[mt][0] = wbase + mt * 16 + gid < i2p;
-      valid[mt][1] = wbase + mt * 16 + gid + 8 < i2p;
-    }
-    auto load_step = [&](int rr0, Row<BITS> (&dst)[MT][2]) {
-      const int rr = rr0 + tid4;
+        for (int h = 0; h < G; ++h)
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+          for (int j = 0; j < 2; ++j) bw[h][j] = sm.wp.w[((h * r + rr) * 2 + j) * 8 + (gid ^ (2 * tid4))];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int b = wbase + mt * 16 + gid + 8 * hh;
-          dst[mt][hh] = valid[mt][hh] ? load_row<BITS>(kc + ((size_t)rr * i2p + b) * RB) : zero_row<BITS>();
-        }
-    };
-    Row<BITS> cur[MT][2], nxt[MT][2];
-    load_step(0, cur);
-    for (int rr0 = 0; rr0 < r; rr0 += 4) {
-      if (rr0 + 4 < r) load_step(rr0 + 4, nxt);
-      uint4 bw[G][2];
+        for (int mt = 0; mt < MT; ++mt) {
+          const int b0 = bl_base + mt * 16 + gid;
+          const Row<BITS> x0 = lds_row<BITS>(tile + (rl * kI2Pad + (b0 ^ swz)) * RB);
+          const Row<BITS> x1 = lds_row<BITS>(tile + (rl * kI2Pad + ((b0 + 8) ^ swz)) * RB);
+          uint32_t a[4][4];
+          row_pairs<BITS, 0>(x0, a[0][0], a[0][2]);
+          row_pairs<BITS, 0>(x1, a[0][1], a[0][3]);
+          row_pairs<BITS, 1>(x0, a[1][0], a[1][2]);
+          row_pairs<BITS, 1>(x1, a[1][1], a[1][3]);
+          row_pairs<BITS, 2>(x0, a[2][0], a[2][2]);
+          row_pairs<BITS, 2>(x1, a[2][1], a[2][3]);
+          row_pairs<BITS, 3>(x0, a[3][0], a[3][2]);
+          row_pairs<BITS, 3>(x1, a[3][1], a[3][3]);
 #pragma unroll
-      for (int h = 0; h < G; ++h)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) bw[h][j] = sm.w[((h * r + rr0 + tid4) * 2 + j) * 8 + (gid ^ (2 * tid4))];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        uint32_t a[4][4];
-        row_pairs<BITS, 0>(cur[mt][0], a[0][0], a[0][2]);
-        row_pairs<BITS, 0>(cur[mt][1], a[0][1], a[0][3]);
-        row_pairs<BITS, 1>(cur[mt][0], a[1][0], a[1][2]);
-        row_pairs<BITS, 1>(cur[mt][1], a[1][1], a[1][3]);
-        row_pairs<BITS, 2>(cur[mt][0], a[2][0], a[2][2]);
-        row_pairs<BITS, 2>(cur[mt][1], a[2][1], a[2][3]);
-        row_pairs<BITS, 3>(cur[mt][0], a[3][0], a[3][2]);
-        row_pairs<BITS, 3>(cur[mt][1], a[3][1], a[3][3]);
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
-          mma16816(acc[mt][h], a[0][0], a[0][1], a[0][2], a[0][3], bw[h][0].x, bw[h][0].y);
-          mma16816(acc[mt][h], a[1][0], a[1][1], a[1][2], a[1][3], bw[h][0].z, bw[h][0].w);
-          mma16816(acc[mt][h], a[2][0], a[2][1], a[2][2], a[2][3], bw[h][1].x, bw[h][1].y);
-          mma16816(acc[mt][h], a[3][0], a[3][1], a[3][2], a[3][3], bw[h][1].z, bw[h][1].w);
+          for (int h = 0; h < G; ++h) {
+            mma16816(acc[mt][h], a[0][0], a[0][1], a[0][2], a[0][3], bw[h][0].x, bw[h][0].y);
+            mma16816(acc[mt][h], a[1][0], a[1][1], a[1][2], a[1][3], bw[h][0].z, bw[h][0].w);
+            mma16816(acc[mt][h], a[2][0], a[2][1], a[2][2], a[2][3], bw[h][1].x, bw[h][1].y);
+            mma16816(acc[mt][h], a[3][0], a[3][1], a[3][2], a[3][3], bw[h][1].z, bw[h][1].w);
+          }
         }
       }
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        cur[mt][0] = nxt[mt][0];
-        cur[mt][1] = nxt[mt][1];
-      }
     }
+    release(st);
   }
-  // scores (already in log2 domain): s = acc * scale_k * sm_scale / wscale * log2(e)
+  // scores in the log2 domain: s = acc * scale_k * sm_scale / wscale * log2(e)
   const float kscale = seg.k_scale * args.sm_scale / wscale * 1.4426950408889634f;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
@@ -290,23 +389,23 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(dq_attn_args args
     for (int h = 0; h < G; ++h)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int bl = warp * MT * 16 + mt * 16 + gid + (k >= 2 ? 8 : 0);
+        const int bl = jt * kI2Pad + bl_base + mt * 16 + gid + (k >= 2 ? 8 : 0);
         const int a = 2 * tid4 + (k & 1);
-        const bool ok = (a < i1) && (wb0 + bl < i2);
-        sm.s[h][a][bl] = ok ? acc[mt][h][k] * kscale : -INFINITY;
+        const bool ok = (a < i1) && (wb0 + bl < i2) && (jt < pl.nbt);
+        sm.sr.s[h][a][bl] = ok ? acc[mt][h][k] * kscale : -INFINITY;
       }
   __syncthreads();
 
-  // ---- phase 2: local softmax of this work item ---------------------------------
+  // ---- phase 2: local softmax of the work item -> P fragments ------------------------
+  float mh[G];
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     float m = -INFINITY;
-    for (int i = tid; i < 8 * CB; i += kThreads) m = fmaxf(m, sm.s[h][i / CB][i % CB]);
+    for (int i = tid; i < 8 * kCB; i += kThreads) m = fmaxf(m, sm.sr.s[h][i / kCB][i % kCB]);
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) sm.rowmax[h][warp] = m;
   }
   __syncthreads();
-  float mh[G];
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     float m = sm.rowmax[h][0];
@@ -314,83 +413,70 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(dq_attn_args args
     for (int w = 1; w < kWarps; ++w) m = fmaxf(m, sm.rowmax[h][w]);
     mh[h] = m;
   }
-  __syncthreads();
+  // one thread per (h, a, 16-group): 16 probabilities -> two 16-byte fragment chunks
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     float l = 0.f;
-    __half* pbase = reinterpret_cast<__half*>(sm.p);
-    for (int i = tid; i < 8 * CB; i += kThreads) {
-      const int a = i / CB, bl = i % CB;
-      const float sv = sm.s[h][a][bl];
-      const float pv = sv == -INFINITY ? 0.f : exp2f(sv - mh[h]);
-      const __half ph = __float2half_rn(pv);
-      l += __half2float(ph);  // sum what the PV product actually uses
-      const int bg = bl >> 4, q = inv_perm16<BITS>(bl & 15);
-      const int j = q >> 3, within = q & 7;
-      const int chunk = ((h * 8 + a) * NG + bg) * 2 + (j ^ (a & 1));
-      pbase[chunk * 8 + within] = ph;
+    if (tid < 8 * kNG) {
+      const int a = tid / kNG, bg = tid % kNG;
+      __half hv[16];
+#pragma unroll
+      for (int qi = 0; qi < 16; ++qi) {
+        const float sv = sm.sr.s[h][a][bg * 16 + perm16<BITS>(qi)];
+        const float pv = sv == -INFINITY ? 0.f : exp2f(sv - mh[h]);
+        const float ks = kscale16<BITS>(qi);
+        hv[qi] = __float2half_rn(pv / ks);
+        l += __half2float(hv[qi]) * ks;  // the probability mass the PV product really uses
+      }
+      sm.wp.p[(((h * 8 + a) * kNG + bg) * 2 + (0 ^ (a & 1)))] = *reinterpret_cast<uint4*>(&hv[0]);
+      sm.wp.p[(((h * 8 + a) * kNG + bg) * 2 + (1 ^ (a & 1)))] = *reinterpret_cast<uint4*>(&hv[8]);
     }
     for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
     if (lane == 0) sm.rowsum[h][warp] = l;
   }
   __syncthreads();
 
-  // ---- phase 3: Y = codes_v . P^T (tensor cores) ---------------------------------
-  // warp w owns bond rows rr = w*rw .. w*rw+rw-1 (rw = r/8 <= 8); m-tile = one rr x 16 e
-  const int rw = r / kWarps;
-  constexpr int HG = G < 2 ? G : 2;  // heads per V pass (register budget)
-  const int nsteps = min(CB, i2p - wb0) / 64;
-  float part[G][16];  // O partial: [h][c*2 + (e == gid+8)]
+  // ---- phase 3: Y = codes_v . P^T ------------------------------------------------------
+  // warp w owns bond rows w*rw .. w*rw+rw-1 (an m-tile = one bond row x 16 e)
+  const int rw = pl.rw;
+  const int my_slice = warp / pl.kslice;
+  const int rbase_in_slice = (warp % pl.kslice) * rw;
+  float accv[8][G][4];
 #pragma unroll
-  for (int h = 0; h < G; ++h)
+  for (int t = 0; t < 8; ++t)
 #pragma unroll
-    for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
-  const uint8_t* vc = seg.v_codes;
+    for (int h = 0; h < G; ++h)
 #pragma unroll
-  for (int hg = 0; hg < G; hg += HG) {
-    float accv[8][HG][4];
+      for (int k = 0; k < 4; ++k) accv[t][h][k] = 0.f;
+  for (int vs = 0; vs < pl.nV; ++vs, ++st) {
+    const int slot = st % kStages;
+    mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
+    const int btl = vs / pl.nslices, sl = vs % pl.nslices;
+    if (sl == my_slice) {
+      uint4 pf[G][2];
 #pragma unroll
-    for (int t = 0; t < 8; ++t)
+      for (int h = 0; h < G; ++h)
 #pragma unroll
-      for (int h = 0; h < HG; ++h)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) accv[t][h][k] = 0.f;
-    for (int st = 0; st < nsteps; ++st) {
-      const int bstart = wb0 + st * 64 + 16 * tid4;
-      Row<BITS> rows[8][2];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        if (t < rw) {
-          const int rr = warp * rw + t;
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int e = gid + 8 * hh;
-            rows[t][hh] = load_row<BITS>(vc + (((size_t)rr * 16 + e) * i2p + bstart) * BITS / 8);
-          }
-        }
-      }
-      uint4 pf[HG][2];
-#pragma unroll
-      for (int h = 0; h < HG; ++h)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int bg = st * 4 + tid4;
-          pf[h][j] = sm.p[(((hg + h) * 8 + gid) * NG + bg) * 2 + (j ^ (gid & 1))];
-        }
+        for (int j = 0; j < 2; ++j)
+          pf[h][j] = sm.wp.p[(((h * 8 + gid) * kNG + btl * 4 + tid4) * 2 + (j ^ (gid & 1)))];
+      const unsigned char* buf = sm.ring[slot];
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         if (t < rw) {
+          const int rl = rbase_in_slice + t;
+          const Row<BITS> x0 = lds_row<BITS>(buf + (rl * 16 + gid) * 8 * BITS + RB * tid4);
+          const Row<BITS> x1 = lds_row<BITS>(buf + (rl * 16 + gid + 8) * 8 * BITS + RB * tid4);
           uint32_t a[4][4];
-          row_pairs<BITS, 0>(rows[t][0], a[0][0], a[0][2]);
-          row_pairs<BITS, 0>(rows[t][1], a[0][1], a[0][3]);
-          row_pairs<BITS, 1>(rows[t][0], a[1][0], a[1][2]);
-          row_pairs<BITS, 1>(rows[t][1], a[1][1], a[1][3]);
-          row_pairs<BITS, 2>(rows[t][0], a[2][0], a[2][2]);
-          row_pairs<BITS, 2>(rows[t][1], a[2][1], a[2][3]);
-          row_pairs<BITS, 3>(rows[t][0], a[3][0], a[3][2]);
-          row_pairs<BITS, 3>(rows[t][1], a[3][1], a[3][3]);
+          row_pairs<BITS, 0>(x0, a[0][0], a[0][2]);
+          row_pairs<BITS, 0>(x1, a[0][1], a[0][3]);
+          row_pairs<BITS, 1>(x0, a[1][0], a[1][2]);
+          row_pairs<BITS, 1>(x1, a[1][1], a[1][3]);
+          row_pairs<BITS, 2>(x0, a[2][0], a[2][2]);
+          row_pairs<BITS, 2>(x1, a[2][1], a[2][3]);
+          row_pairs<BITS, 3>(x0, a[3][0], a[3][2]);
+          row_pairs<BITS, 3>(x1, a[3][1], a[3][3]);
 #pragma unroll
-          for (int h = 0; h < HG; ++h) {
+          for (int h = 0; h < G; ++h) {
             mma16816(accv[t][h], a[0][0], a[0][1], a[0][2], a[0][3], pf[h][0].x, pf[h][0].y);
             mma16816(accv[t][h], a[1][0], a[1][1], a[1][2], a[1][3], pf[h][0].z, pf[h][0].w);
             mma16816(accv[t][h], a[2][0], a[2][1], a[2][2], a[2][3], pf[h][1].x, pf[h][1].y);
@@ -399,38 +485,44 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(dq_attn_args args
         }
       }
     }
-    // ---- phase 4a: contract Y with G0v on CUDA cores ---------------------------
-    // accv[t][h]: rows e = gid (k 0,1) / gid+8 (k 2,3); cols a = 2*tid4 + (k & 1)
+    release(st);
+  }
+
+  // ---- phase 4: O = scale_v * G0v . Y on CUDA cores, reduce, write the partial ---------
+  // accv[t][h]: rows e = gid (k 0,1) / gid+8 (k 2,3); cols a = 2*tid4 + (k & 1)
+  float part[G][16];  // [h][c*2 + (e == gid+8)]
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      if (t < rw) {
-        const int rr = warp * rw + t;
+  for (int h = 0; h < G; ++h)
 #pragma unroll
-        for (int aa = 0; aa < 2; ++aa) {
-          const int a = 2 * tid4 + aa;
-          if (a < i1) {
-            const uint4 gv = sm.g0v[a * r + rr];
-            const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
-            float gc[8];
+    for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float2 f = __half22float2(g2[k]);
-              gc[2 * k] = f.x;
-              gc[2 * k + 1] = f.y;
-            }
+  for (int t = 0; t < 8; ++t) {
+    if (t < rw) {
+      const int rr = warp * rw + t;
 #pragma unroll
-            for (int h = 0; h < HG; ++h)
+      for (int aa = 0; aa < 2; ++aa) {
+        const int a = 2 * tid4 + aa;
+        if (a < i1) {
+          const uint4 gv = sm.g0v[a * r + rr];
+          const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
+          float gc[8];
 #pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                part[hg + h][2 * c] = fmaf(gc[c], accv[t][h][aa], part[hg + h][2 * c]);
-                part[hg + h][2 * c + 1] = fmaf(gc[c], accv[t][h][2 + aa], part[hg + h][2 * c + 1]);
-              }
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __half22float2(g2[k]);
+            gc[2 * k] = f.x;
+            gc[2 * k + 1] = f.y;
           }
+#pragma unroll
+          for (int h = 0; h < G; ++h)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              part[h][2 * c] = fmaf(gc[c], accv[t][h][aa], part[h][2 * c]);
+              part[h][2 * c + 1] = fmaf(gc[c], accv[t][h][2 + aa], part[h][2 * c + 1]);
+            }
         }
       }
     }
   }
-  // reduce over the 4 threads of a quad (different a), then over warps (different rr)
 #pragma unroll
   for (int h = 0; h < G; ++h)
 #pragma unroll
@@ -440,7 +532,7 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(dq_attn_args args
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       part[h][k] = v;
     }
-  // thread tid4 writes c = 2*tid4, 2*tid4+1 for e = gid, gid+8
+  // the score buffer is dead now: reuse it for the cross-warp reduction
 #pragma unroll
   for (int h = 0; h < G; ++h)
 #pragma unroll
@@ -453,24 +545,24 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(dq_attn_args args
           v0 = part[h][2 * k];
           v1 = part[h][2 * k + 1];
         }
-      sm.red[warp][h][c * 16 + gid] = v0;
-      sm.red[warp][h][c * 16 + gid + 8] = v1;
+      sm.sr.red[warp][h][c * 16 + gid] = v0;
+      sm.sr.red[warp][h][c * 16 + gid + 8] = v1;
     }
   __syncthreads();
-  const int slot = args.work_part[wi];
+  const int slot_out = args.work_part[wi];
   for (int i = tid; i < G * kD; i += kThreads) {
     const int h = i / kD, d = i % kD;
     float v = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) v += sm.red[w][h][d];
-    args.part_o[((size_t)slot * G + h) * kD + d] = v * seg.v_scale;
+    for (int w = 0; w < kWarps; ++w) v += sm.sr.red[w][h][d];
+    args.part_o[((size_t)slot_out * G + h) * kD + d] = v * seg.v_scale;
   }
   if (tid < G) {
     float l = 0.f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) l += sm.rowsum[tid][w];
-    args.part_ml[((size_t)slot * G + tid) * 2 + 0] = mh[tid];  // log2 domain
-    args.part_ml[((size_t)slot * G + tid) * 2 + 1] = l;
+    args.part_ml[((size_t)slot_out * G + tid) * 2 + 0] = mh[tid];  // log2 domain
+    args.part_ml[((size_t)slot_out * G + tid) * 2 + 1] = l;
   }
 }
 
@@ -551,47 +643,45 @@ __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __ha
   if (threadIdx.x == 0) tail_len[u] = pos + 1;
 }
 
-template <int BITS, int G, int MT>
-int launch_attn(const dq_attn_args& a, cudaStream_t s) {
-  constexpr int CB = MT * 16 * kWarps;
-  const size_t smem = sizeof(AttnSmem<G, CB>);
-  static bool attr = false;
-  if (!attr) {
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    attr = true;
-  }
-  if (a.nwork > 0) {
-    decode_attn_kernel<BITS, G, MT><<<a.nwork, kThreads, smem, s>>>(a);
-    DQ_LAUNCH_CHECK();
-  }
-  const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1);
-  combine_kernel<G><<<a.units, 128, csmem, s>>>(a);
-  DQ_LAUNCH_CHECK();
-  return DQ_OK;
-}
 
 template <int BITS, int G>
-int dispatch_mt(const dq_attn_args& a, cudaStream_t s) {
-  if (a.chunk_b == 256) return launch_attn<BITS, G, 2>(a, s);
-  if (a.chunk_b == 512 && G <= 2) return launch_attn<BITS, G, (G <= 2 ? 4 : 2)>(a, s);
-  return fail(DQ_ERR_UNSUPPORTED, "chunk_b %d not supported for g=%d (use 256%s)", a.chunk_b, G,
-              G <= 2 ? " or 512" : "");
+int launch_attn(const dq_attn_args& a, cudaStream_t s) {
+  const size_t smem = sizeof(AttnSmem<G>);
+  static bool attr = false;
+  if (!attr) {
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     100));
+    attr = true;
+  }
+  const int phases = a.phases ? a.phases : 3;
+  if (a.nwork > 0 && (phases & 1)) {
+    decode_attn_kernel<BITS, G><<<a.nwork, kThreads, smem, s>>>(a);
+    DQ_LAUNCH_CHECK();
+  }
+  if (phases & 2) {
+    const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1);
+    combine_kernel<G><<<a.units, 128, csmem, s>>>(a);
+    DQ_LAUNCH_CHECK();
+  }
+  return DQ_OK;
 }
 
 template <int BITS>
 int dispatch_g(const dq_attn_args& a, cudaStream_t s) {
+  if (a.chunk_b != kCB) return fail(DQ_ERR_UNSUPPORTED, "chunk_b must be %d (got %d)", kCB, a.chunk_b);
   switch (a.g) {
-    case 1: return dispatch_mt<BITS, 1>(a, s);
-    case 2: return dispatch_mt<BITS, 2>(a, s);
-    case 4: return dispatch_mt<BITS, 4>(a, s);
+    case 1: return launch_attn<BITS, 1>(a, s);
+    case 2: return launch_attn<BITS, 2>(a, s);
   }
-  return fail(DQ_ERR_UNSUPPORTED, "g must be 1, 2 or 4 in this build (got %d)", a.g);
+  return fail(DQ_ERR_UNSUPPORTED, "g must be 1 or 2 in this build (got %d)", a.g);
 }
 
 }  // namespace
 
 }  // namespace dq
+
 
 using namespace dq;
 
@@ -605,7 +695,7 @@ extern "C" int dq_attention_plan(const dq_segment* segs, int32_t nseg, int32_t u
   for (int s = 0; s < nseg; ++s) {
     const dq_segment& g = segs[s];
     if (g.unit < 0 || g.unit >= units) return fail(DQ_ERR_INVALID_ARG, "segment %d has unit %d", s, g.unit);
-    if (g.r > kMaxR || g.r % 8 || g.i1 > 8 || g.i2p % 64) return fail(DQ_ERR_UNSUPPORTED, "segment %d plan unsupported", s);
+    if (g.r > kMaxR || g.r % 8 || g.i1 > 8 || g.i2p % kI2Pad) return fail(DQ_ERR_UNSUPPORTED, "segment %d plan unsupported", s);
     for (int b0 = 0; b0 < g.i2; b0 += chunk_b) {
       if (work) {
         work[2 * n] = s;

@@ -77,7 +77,7 @@ extern "C" int dq_make_plan2(int64_t rows, int64_t cols, dq_plan2* out) {
 extern "C" int dq_layout_bytes(const dq_plan2* p, int32_t bits, int32_t layout, int64_t* bytes) {
   if (!p || !bytes) return fail(DQ_ERR_INVALID_ARG, "null argument");
   if (!bits_ok(bits)) return fail(DQ_ERR_UNSUPPORTED_BITS, "bits must be one of (2, 4, 8), got %d", bits);
-  if (layout != DQ_LAYOUT_REF && layout != DQ_LAYOUT_KROW && layout != DQ_LAYOUT_VCOL)
+  if (layout != DQ_LAYOUT_REF && layout != DQ_LAYOUT_KTILE && layout != DQ_LAYOUT_VTILE)
     return fail(DQ_ERR_INVALID_ARG, "unknown layout %d", layout);
   CoreGeom g = make_geom(*p, bits, layout);
   if (layout != DQ_LAYOUT_REF && ((g.j2 * bits) % 8 || (g.i2p * bits) % 8))

@@ -59,24 +59,42 @@ inline CoreGeom make_geom(const dq_plan2& p, int bits, int layout) {
 // number of code slots (including padding) of one packed core
 __host__ __device__ inline int64_t geom_slots(const CoreGeom& g) { return (int64_t)g.r * g.i2p * g.j2; }
 
+// Device layouts (include/dquant_b200.h): b is split into 64-row tiles bt, and
+// the K rows of a tile are XOR-swizzled by r so that the mma fragment reads of
+// 4 consecutive r hit distinct shared-memory banks.
+__host__ __device__ inline int ktile_swizzle(int rr, int bits) { return (rr & 3) * (16 / bits); }
+
 // linear code slot of logical element (rr, b, e)
 __host__ __device__ inline int64_t geom_slot(const CoreGeom& g, int rr, int b, int e) {
-  if (g.layout == DQ_LAYOUT_VCOL) return ((int64_t)rr * g.j2 + e) * g.i2p + b;
-  return ((int64_t)rr * g.i2p + b) * g.j2 + e;
+  if (g.layout == DQ_LAYOUT_REF) return ((int64_t)rr * g.i2 + b) * g.j2 + e;
+  const int bt = b / kI2Pad, bl = b % kI2Pad;
+  if (g.layout == DQ_LAYOUT_VTILE) return (((int64_t)bt * g.r + rr) * g.j2 + e) * kI2Pad + bl;
+  return (((int64_t)bt * g.r + rr) * kI2Pad + (bl ^ ktile_swizzle(rr, g.bits))) * g.j2 + e;
 }
 
 // inverse: logical element of a slot; returns false for padding slots
 __host__ __device__ inline bool geom_coords(const CoreGeom& g, int64_t slot, int& rr, int& b, int& e) {
-  if (g.layout == DQ_LAYOUT_VCOL) {
-    b = (int)(slot % g.i2p);
-    int64_t t = slot / g.i2p;
+  if (g.layout == DQ_LAYOUT_REF) {
+    e = (int)(slot % g.j2);
+    const int64_t t = slot / g.j2;
+    b = (int)(t % g.i2);
+    rr = (int)(t / g.i2);
+    return true;
+  }
+  if (g.layout == DQ_LAYOUT_VTILE) {
+    const int bl = (int)(slot % kI2Pad);
+    int64_t t = slot / kI2Pad;
     e = (int)(t % g.j2);
-    rr = (int)(t / g.j2);
+    t /= g.j2;
+    rr = (int)(t % g.r);
+    b = (int)(t / g.r) * kI2Pad + bl;
   } else {
     e = (int)(slot % g.j2);
     int64_t t = slot / g.j2;
-    b = (int)(t % g.i2p);
-    rr = (int)(t / g.i2p);
+    const int bsw = (int)(t % kI2Pad);
+    t /= kI2Pad;
+    rr = (int)(t % g.r);
+    b = (int)(t / g.r) * kI2Pad + (bsw ^ ktile_swizzle(rr, g.bits));
   }
   return b < g.i2;
 }
@@ -90,6 +108,22 @@ __device__ __forceinline__ int read_code(const uint8_t* p, int64_t slot, int bit
   const unsigned raw = (byte >> ((slot % per) * bits)) & ((1u << bits) - 1u);
   const int sign = 1 << (bits - 1);
   return (int)(raw ^ sign) - sign;
+}
+
+// Device layouts store codes in excess-2^(bits-1) form (code + 2^(bits-1), unsigned),
+// which the attention kernel turns into fp16 with one LOP3 per pair of codes.
+__device__ __forceinline__ int geom_read(const uint8_t* p, const CoreGeom& g, int rr, int b, int e) {
+  const int64_t slot = geom_slot(g, rr, b, e);
+  if (g.layout == DQ_LAYOUT_REF) return read_code(p, slot, g.bits);
+  const int per = 8 / g.bits;
+  const unsigned raw = (p[slot / per] >> ((slot % per) * g.bits)) & ((1u << g.bits) - 1u);
+  return (int)raw - (1 << (g.bits - 1));
+}
+
+// lane bits of `code` in layout g
+__host__ __device__ inline unsigned geom_encode(int code, const CoreGeom& g) {
+  const unsigned mask = (1u << g.bits) - 1u;
+  return g.layout == DQ_LAYOUT_REF ? ((unsigned)code & mask) : ((unsigned)(code + (1 << (g.bits - 1))) & mask);
 }
 
 // ---- bit-exact replica of quantize.py:144-145 ---------------------------

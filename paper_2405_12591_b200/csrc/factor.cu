@@ -389,7 +389,6 @@ __global__ void quantize_core_kernel(const float* __restrict__ core1, int64_t co
   const int bits = geom.bits;
   const int per = 8 / bits;
   const int qmax = (1 << (bits - 1)) - 1;
-  const unsigned mask = (1u << bits) - 1u;
   const float amax_f = __uint_as_float(amax[blk]);
   if (!isfinite(amax_f)) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && flags) atomicOr(flags, (int)DQ_FLAG_NONFINITE);
@@ -402,15 +401,14 @@ __global__ void quantize_core_kernel(const float* __restrict__ core1, int64_t co
   uint8_t* dst = payload + blk * payload_stride;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < out_bytes; i += (int64_t)gridDim.x * blockDim.x) {
     unsigned v = 0;
-    if (!degenerate) {
-      for (int k = 0; k < per; ++k) {
-        const int64_t slot = i * per + k;
-        if (slot >= geom_slots(geom)) break;
-        int rr, b, e;
-        if (!geom_coords(geom, slot, rr, b, e)) continue;
-        const float t = src[((int64_t)rr * geom.i2 + b) * geom.j2 + e];
-        v |= ((unsigned)rtn_code(t, qmax, am) & mask) << (k * bits);
-      }
+    for (int k = 0; k < per; ++k) {
+      const int64_t slot = i * per + k;
+      if (slot >= geom_slots(geom)) break;
+      int rr, b, e;
+      int code = 0;  // padding slots and degenerate blocks hold the code 0
+      if (geom_coords(geom, slot, rr, b, e) && !degenerate)
+        code = rtn_code(src[((int64_t)rr * geom.i2 + b) * geom.j2 + e], qmax, am);
+      v |= geom_encode(code, geom) << (k * bits);
     }
     dst[i] = (uint8_t)v;
   }

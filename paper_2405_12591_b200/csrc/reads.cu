@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kThreads) reconstruct_kernel(const float* __re
     const int rr = i / (kBT * j2), rem = i - rr * kBT * j2;
     const int bb = rem / j2, e = rem - bb * j2;
     float v = 0.f;
-    if (bb < nb) v = __fmul_rn((float)read_code(pl, geom_slot(geom, rr, b0 + bb, e), geom.bits), s);
+    if (bb < nb) v = __fmul_rn((float)geom_read(pl, geom, rr, b0 + bb, e), s);
     dq[i] = v;
   }
   __syncthreads();
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) fused_t_kernel(const float* __restri
   for (int a = 0; a < 8; ++a) acc[a] = 0.0;
   for (int rr = 0; rr < r; ++rr)
     for (int e = 0; e < j2; ++e) {
-      const double cv = (double)read_code(payload, geom_slot(geom, rr, b, e), geom.bits);
+      const double cv = (double)geom_read(payload, geom, rr, b, e);
       if (cv == 0.0) continue;
 #pragma unroll
       for (int a = 0; a < 8; ++a)
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads) fused_n_kernel(const float* __restri
 #pragma unroll
     for (int a = 0; a < 8; ++a) acc[a] = 0.0;
     for (int b = 0; b < i2; ++b) {
-      const double cv = (double)read_code(payload, geom_slot(geom, rr, b, e), geom.bits);
+      const double cv = (double)geom_read(payload, geom, rr, b, e);
       if (cv == 0.0) continue;
 #pragma unroll
       for (int a = 0; a < 8; ++a)
@@ -149,7 +149,6 @@ __global__ void relayout_kernel(const uint8_t* __restrict__ src, CoreGeom gs, in
                                 uint8_t* __restrict__ dst, CoreGeom gd, int64_t dst_stride, int64_t dst_bytes) {
   const int bits = gd.bits;
   const int per = 8 / bits;
-  const unsigned mask = (1u << bits) - 1u;
   const int64_t blk = blockIdx.y;
   const uint8_t* s = src + blk * src_stride;
   uint8_t* d = dst + blk * dst_stride;
@@ -160,29 +159,50 @@ __global__ void relayout_kernel(const uint8_t* __restrict__ src, CoreGeom gs, in
       const int64_t slot = i * per + k;
       if (slot >= nslots) break;
       int rr, b, e;
-      if (!geom_coords(gd, slot, rr, b, e)) continue;
-      v |= ((unsigned)read_code(s, geom_slot(gs, rr, b, e), bits) & mask) << (k * bits);
+      const int code = geom_coords(gd, slot, rr, b, e) ? geom_read(s, gs, rr, b, e) : 0;
+      v |= geom_encode(code, gd) << (k * bits);
     }
     d[i] = (uint8_t)v;
   }
 }
 
-// core0 (1,i1,j1,r) f32 -> fp16 [a][r][c]
-__global__ void core0_f16_kernel(const float* __restrict__ core0, int64_t n, int i1, int j1, int r,
-                                 __half* __restrict__ out) {
+// core0 (1,i1,j1,r) f32 -> fp16 [a][r][c], divided by a per-block power of two so that
+// max|g0h| lies in [0.5, 1): keeps W = q.G0 inside fp16 range whatever the K scale.
+// One CTA per block.
+__global__ void core0_f16_kernel(const float* __restrict__ core0, int i1, int j1, int r, __half* __restrict__ out,
+                                 float* __restrict__ norm) {
+  __shared__ float red[32];
   const int per = i1 * j1 * r;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * per; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t blk = i / per;
-    const int rem = (int)(i - blk * per);
-    const int a = rem / (r * j1), t = rem - a * r * j1;
+  const int64_t blk = blockIdx.x;
+  const float* src = core0 + blk * per;
+  float m = 0.f;
+  for (int i = threadIdx.x; i < per; i += blockDim.x) m = fmaxf(m, fabsf(src[i]));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+  // f = 2^(e) with m / f in [0.5, 1); exact power of two, f = 1 for an all-zero core
+  float f = 1.f;
+  if (norm) {
+    if (m > 0.f) {
+      int e;
+      frexpf(m, &e);
+      f = ldexpf(1.f, e);
+    }
+    if (threadIdx.x == 0) norm[blk] = f;
+  }
+  const float inv = 1.f / f;
+  for (int i = threadIdx.x; i < per; i += blockDim.x) {
+    const int a = i / (r * j1), t = i - a * r * j1;
     const int rr = t / j1, c = t - rr * j1;
-    out[i] = __float2half_rn(core0[blk * per + (a * j1 + c) * r + rr]);
+    out[blk * per + i] = __float2half_rn(src[(a * j1 + c) * r + rr] * inv);
   }
 }
 
 int check_geom(const dq_plan2& p, int bits, int layout) {
   if (!bits_ok(bits)) return fail(DQ_ERR_UNSUPPORTED_BITS, "bits must be one of (2, 4, 8), got %d", bits);
-  if (layout != DQ_LAYOUT_REF && layout != DQ_LAYOUT_KROW && layout != DQ_LAYOUT_VCOL)
+  if (layout != DQ_LAYOUT_REF && layout != DQ_LAYOUT_KTILE && layout != DQ_LAYOUT_VTILE)
     return fail(DQ_ERR_INVALID_ARG, "unknown layout %d", layout);
   if (p.i1 * p.j1 > 64) return fail(DQ_ERR_UNSUPPORTED, "i1*j1 > 64");
   return DQ_OK;
@@ -277,14 +297,12 @@ extern "C" int dq_relayout(const uint8_t* src, int32_t src_layout, int64_t src_s
   return DQ_OK;
 }
 
-extern "C" int dq_core0_to_f16(const float* core0, int64_t nblk, const dq_plan2* hp, uint16_t* g0h, void* stream) {
+extern "C" int dq_core0_to_f16(const float* core0, int64_t nblk, const dq_plan2* hp, uint16_t* g0h, float* norm,
+                               void* stream) {
   if (!hp || (nblk && (!core0 || !g0h))) return fail(DQ_ERR_INVALID_ARG, "null pointer");
   if (nblk == 0) return DQ_OK;
-  const int64_t n = nblk * hp->i1 * hp->j1 * hp->r;
-  int64_t grid = ceil_div(n, kThreads);
-  if (grid > 148 * 8) grid = 148 * 8;
-  core0_f16_kernel<<<(unsigned)grid, kThreads, 0, (cudaStream_t)stream>>>(core0, nblk, (int)hp->i1, (int)hp->j1,
-                                                                         (int)hp->r, (__half*)g0h);
+  core0_f16_kernel<<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(core0, (int)hp->i1, (int)hp->j1, (int)hp->r,
+                                                                         (__half*)g0h, norm);
   DQ_LAUNCH_CHECK();
   return DQ_OK;
 }

@@ -67,8 +67,8 @@ def test_make_plan2_and_layout_bytes(L):
             ref = L.layout_bytes(p, bits, L.LAYOUT_REF)
             assert ref == O.payload_bytes(p.r * p.i2 * p.j2, bits)
             i2p = -(-p.i2 // 64) * 64
-            assert L.layout_bytes(p, bits, L.LAYOUT_KROW) == p.r * i2p * 16 * bits // 8
-            assert L.layout_bytes(p, bits, L.LAYOUT_VCOL) == p.r * i2p * 16 * bits // 8
+            assert L.layout_bytes(p, bits, L.LAYOUT_KTILE) == p.r * i2p * 16 * bits // 8
+            assert L.layout_bytes(p, bits, L.LAYOUT_VTILE) == p.r * i2p * 16 * bits // 8
     from paper_2405_12591_b200.errors import UnsupportedBits
 
     with pytest.raises(UnsupportedBits):

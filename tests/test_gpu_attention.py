@@ -69,8 +69,9 @@ def _oracle_attend(k, v, q, bits, segs_T, tail):
 
 
 @pytest.mark.parametrize("bits,g,T,units", [
-    (4, 1, 4096, 4), (4, 1, 1024, 3), (4, 2, 2048, 2), (4, 4, 1024, 2), (2, 1, 2048, 2), (8, 1, 1024, 2),
-    (4, 1, 1009, 2), (4, 1, 1023, 2), (4, 1, 8192, 1),
+    (4, 1, 4096, 4), (4, 1, 1024, 3), (4, 2, 2048, 2), (2, 2, 1024, 2), (2, 1, 2048, 2), (8, 1, 1024, 2), (8, 2, 640, 2),
+    (4, 1, 1009, 2), (4, 1, 1023, 2), (4, 1, 8192, 1), (4, 1, 24, 2), (4, 1, 100, 2), (2, 1, 1009, 1),
+    (8, 1, 1023, 1),
 ])
 def test_decode_attention_prefill_only(dq, bits, g, T, units):
     from paper_2405_12591_b200.attention import DecodeKvCache
