@@ -38,7 +38,7 @@ constexpr int kCB = 256;                 // b rows per work item
 constexpr int kTiles = kCB / kI2Pad;     // 64-row tiles per work item
 constexpr int kNG = kCB / 16;            // 16-row groups per work item
 constexpr int kStageBytes = 16384;
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 
 // ---- PTX wrappers -------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -109,6 +109,14 @@ __device__ __forceinline__ Row<BITS> lds_row(const unsigned char* p) {
   return r;
 }
 
+// (a & b) | c in ONE LOP3: with both masks as immediates ptxas emits two (a LOP3
+// takes a single immediate), which doubles the ALU-pipe cost of the conversion.
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t hsub2_u32(uint32_t x, uint32_t bias) {
   __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&x), *reinterpret_cast<const __half2*>(&bias));
   return *reinterpret_cast<uint32_t*>(&r);
@@ -118,25 +126,26 @@ __device__ __forceinline__ uint32_t hsub2_u32(uint32_t x, uint32_t bias) {
 // Slot q = 4C + {0,1,2,3} holds element perm16(q) of the 16-group, times kscale(q).
 template <int BITS, int C>
 __device__ __forceinline__ void row_pairs(const Row<BITS>& r, uint32_t& lo, uint32_t& hi) {
-  constexpr uint32_t M = 0x64006400u;
+  const uint32_t M = 0x64006400u;
   if constexpr (BITS == 4) {
     const uint32_t w0 = (C >= 2) ? (r.w[0] >> 8) : r.w[0];
     const uint32_t w1 = (C >= 2) ? (r.w[1] >> 8) : r.w[1];
-    constexpr uint32_t mask = (C & 1) ? 0x00F000F0u : 0x000F000Fu;
+    const uint32_t mask = (C & 1) ? 0x00F000F0u : 0x000F000Fu;
     constexpr uint32_t bias = (C & 1) ? 0x64806480u : 0x64086408u;  // 1024 + s*8, s = 16 or 1
-    lo = hsub2_u32((w0 & mask) | M, bias);
-    hi = hsub2_u32((w1 & mask) | M, bias);
+    lo = hsub2_u32(and_or(w0, mask, M), bias);
+    hi = hsub2_u32(and_or(w1, mask, M), bias);
   } else if constexpr (BITS == 2) {
     const uint32_t w = (C >= 2) ? (r.w[0] >> 8) : r.w[0];
-    constexpr uint32_t mlo = (C & 1) ? 0x00300030u : 0x00030003u;
-    constexpr uint32_t mhi = (C & 1) ? 0x00C000C0u : 0x000C000Cu;
+    const uint32_t mlo = (C & 1) ? 0x00300030u : 0x00030003u;
+    const uint32_t mhi = (C & 1) ? 0x00C000C0u : 0x000C000Cu;
     constexpr uint32_t blo = (C & 1) ? 0x64206420u : 0x64026402u;  // 1024 + 2s, s = 16 / 1
     constexpr uint32_t bhi = (C & 1) ? 0x64806480u : 0x64086408u;  // s = 64 / 4
-    lo = hsub2_u32((w & mlo) | M, blo);
-    hi = hsub2_u32((w & mhi) | M, bhi);
+    lo = hsub2_u32(and_or(w, mlo, M), blo);
+    hi = hsub2_u32(and_or(w, mhi, M), bhi);
   } else {
-    lo = hsub2_u32((r.w[C] & 0x00FF00FFu) | M, 0x64806480u);
-    hi = hsub2_u32(((r.w[C] >> 8) & 0x00FF00FFu) | M, 0x64806480u);
+    const uint32_t mask = 0x00FF00FFu;
+    lo = hsub2_u32(and_or(r.w[C], mask, M), 0x64806480u);
+    hi = hsub2_u32(and_or(r.w[C] >> 8, mask, M), 0x64806480u);
   }
 }
 
@@ -147,6 +156,14 @@ __host__ __device__ constexpr int perm16(int q) {
   if (BITS == 4) return c + 4 * j;                                   // c, c+4, c+8, c+12
   if (BITS == 2) return 2 * c + (j == 1 ? 8 : j == 2 ? 1 : j == 3 ? 9 : 0);  // 2c, 2c+8, 2c+1, 2c+9
   return 4 * c + (j == 1 ? 2 : j == 2 ? 1 : j);                       // 4c, 4c+2, 4c+1, 4c+3
+}
+
+// inverse of perm16: k-slot holding element e of the 16-group
+template <int BITS>
+__host__ __device__ constexpr int inv_perm16(int e) {
+  if (BITS == 4) return 4 * (e & 3) + (e >> 2);
+  if (BITS == 2) return 4 * ((e & 7) >> 1) + 2 * (e & 1) + (e >> 3);
+  return 4 * (e >> 2) + (((e & 1) << 1) | ((e >> 1) & 1));
 }
 
 // power of two the code in k-slot q comes out multiplied by (folded into the other operand)
@@ -171,12 +188,7 @@ struct AttnSmem {
     uint4 w[G * kMaxR * 2 * 8];
     uint4 p[G * 8 * kNG * 2];
   } wp;
-  uint4 g0v[8 * kMaxR];  // fp16 [a][r][c], normalised
-  // scores (phase 1-2) and the cross-warp reduction (phase 4) share storage
-  union {
-    float s[G][8][kCB];
-    float red[kWarps][G][kD];
-  } sr;
+  float red[kWarps][G][kD];  // cross-warp reduction of the O partial (phase 4)
   float rowmax[G][kWarps];
   float rowsum[G][kWarps];
 };
@@ -233,7 +245,7 @@ __device__ __forceinline__ void issue_stage(const Plan<BITS>& pl, const dq_segme
 }
 
 template <int BITS, int G>
-__global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(dq_attn_args args) {
+__global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(dq_attn_args args) {
   constexpr int RB = 2 * BITS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   AttnSmem<G>& sm = *reinterpret_cast<AttnSmem<G>*>(smem_raw);
@@ -270,10 +282,6 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(dq_attn_args a
   }
   for (int o = 16; o; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
   if (tid == 0) sm.qmax = 0.f;
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(seg.v_g0);
-    for (int i = tid; i < i1 * r; i += kThreads) sm.g0v[i] = src[i];
-  }
   __syncthreads();
   if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(&sm.qmax), __float_as_uint(qm));
   __syncthreads();
@@ -381,56 +389,50 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(dq_attn_args a
     }
     release(st);
   }
+  // ---- phase 2: softmax of the work item straight from the accumulators ---------------
   // scores in the log2 domain: s = acc * scale_k * sm_scale / wscale * log2(e)
   const float kscale = seg.k_scale * args.sm_scale / wscale * 1.4426950408889634f;
+  float mh[G];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
+  for (int h = 0; h < G; ++h) {
+    float m = -INFINITY;
 #pragma unroll
-    for (int h = 0; h < G; ++h)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int bl = jt * kI2Pad + bl_base + mt * 16 + gid + (k >= 2 ? 8 : 0);
         const int a = 2 * tid4 + (k & 1);
         const bool ok = (a < i1) && (wb0 + bl < i2) && (jt < pl.nbt);
-        sm.sr.s[h][a][bl] = ok ? acc[mt][h][k] * kscale : -INFINITY;
+        acc[mt][h][k] = ok ? acc[mt][h][k] * kscale : -INFINITY;
+        m = fmaxf(m, acc[mt][h][k]);
       }
-  __syncthreads();
-
-  // ---- phase 2: local softmax of the work item -> P fragments ------------------------
-  float mh[G];
-#pragma unroll
-  for (int h = 0; h < G; ++h) {
-    float m = -INFINITY;
-    for (int i = tid; i < 8 * kCB; i += kThreads) m = fmaxf(m, sm.sr.s[h][i / kCB][i % kCB]);
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) sm.rowmax[h][warp] = m;
   }
-  __syncthreads();
+  __syncthreads();  // every warp is past phase 1: the W buffer may now hold P
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     float m = sm.rowmax[h][0];
 #pragma unroll
     for (int w = 1; w < kWarps; ++w) m = fmaxf(m, sm.rowmax[h][w]);
     mh[h] = m;
-  }
-  // one thread per (h, a, 16-group): 16 probabilities -> two 16-byte fragment chunks
-#pragma unroll
-  for (int h = 0; h < G; ++h) {
     float l = 0.f;
-    if (tid < 8 * kNG) {
-      const int a = tid / kNG, bg = tid % kNG;
-      __half hv[16];
+    __half* pbase = reinterpret_cast<__half*>(sm.wp.p);
 #pragma unroll
-      for (int qi = 0; qi < 16; ++qi) {
-        const float sv = sm.sr.s[h][a][bg * 16 + perm16<BITS>(qi)];
-        const float pv = sv == -INFINITY ? 0.f : exp2f(sv - mh[h]);
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int bl = jt * kI2Pad + bl_base + mt * 16 + gid + (k >= 2 ? 8 : 0);
+        const int a = 2 * tid4 + (k & 1);
+        const float sv = acc[mt][h][k];
+        const float pv = sv == -INFINITY ? 0.f : exp2f(sv - m);
+        const int qi = inv_perm16<BITS>(bl & 15);
         const float ks = kscale16<BITS>(qi);
-        hv[qi] = __float2half_rn(pv / ks);
-        l += __half2float(hv[qi]) * ks;  // the probability mass the PV product really uses
+        const __half ph = __float2half_rn(pv / ks);
+        l += __half2float(ph) * ks;  // the probability mass the PV product really uses
+        if (jt < pl.nbt)
+          pbase[((((h * 8 + a) * kNG + (bl >> 4)) * 2 + ((qi >> 3) ^ (a & 1))) << 3) + (qi & 7)] = ph;
       }
-      sm.wp.p[(((h * 8 + a) * kNG + bg) * 2 + (0 ^ (a & 1)))] = *reinterpret_cast<uint4*>(&hv[0]);
-      sm.wp.p[(((h * 8 + a) * kNG + bg) * 2 + (1 ^ (a & 1)))] = *reinterpret_cast<uint4*>(&hv[8]);
-    }
     for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
     if (lane == 0) sm.rowsum[h][warp] = l;
   }
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(dq_attn_args a
       for (int aa = 0; aa < 2; ++aa) {
         const int a = 2 * tid4 + aa;
         if (a < i1) {
-          const uint4 gv = sm.g0v[a * r + rr];
+          const uint4 gv = __ldg(reinterpret_cast<const uint4*>(seg.v_g0) + a * r + rr);  // L2-resident
           const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
           float gc[8];
 #pragma unroll
@@ -545,8 +547,8 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(dq_attn_args a
           v0 = part[h][2 * k];
           v1 = part[h][2 * k + 1];
         }
-      sm.sr.red[warp][h][c * 16 + gid] = v0;
-      sm.sr.red[warp][h][c * 16 + gid + 8] = v1;
+      sm.red[warp][h][c * 16 + gid] = v0;
+      sm.red[warp][h][c * 16 + gid + 8] = v1;
     }
   __syncthreads();
   const int slot_out = args.work_part[wi];
@@ -554,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(dq_attn_args a
     const int h = i / kD, d = i % kD;
     float v = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) v += sm.sr.red[w][h][d];
+    for (int w = 0; w < kWarps; ++w) v += sm.red[w][h][d];
     args.part_o[((size_t)slot_out * G + h) * kD + d] = v * seg.v_scale;
   }
   if (tid < G) {
