@@ -122,11 +122,11 @@ int dq_decompose_plan_batched(const void* blocks, int32_t in_dtype, int64_t nblk
 int dq_deco_quantize_batched(const void* blocks, int32_t in_dtype, int64_t nblk, int64_t rows, int64_t cols,
                              int32_t bits, int32_t layout, float* core0, uint8_t* payload, int64_t payload_stride,
                              float* scale, int32_t* flags, void* workspace, size_t workspace_bytes, void* stream);
-/* fp16 copy of core0 in the attention-friendly layout g0h[a][r][c] (i1 x r x j1), normalised
- * by a power of two per block so that max|g0h| is in [0.5, 1); norm[blk] receives that
- * factor (core0 = g0h * norm).  norm may be null (then no normalisation). */
-int dq_core0_to_f16(const float* core0, int64_t nblk, const dq_plan2* h_plan, uint16_t* g0h, float* norm,
-                    void* stream);
+/* copy of core0 (fp16 or fp32) in the attention-friendly layout out[a][r][c] (i1 x r x j1),
+ * normalised by a power of two per block so that max|out| is in [0.5, 1); norm[blk] receives
+ * that factor (core0 = out * norm).  norm may be null (then no normalisation). */
+int dq_core0_relayout(const float* core0, int64_t nblk, const dq_plan2* h_plan, void* out, int32_t out_dtype,
+                      float* norm, void* stream);
 
 /* ---- K4 reconstruct (dequant + contraction), batched ------------------- */
 int dq_deco_dequantize_batched(const float* core0, const uint8_t* payload, int64_t payload_stride, int32_t layout,
@@ -154,8 +154,8 @@ int dq_fused_matmul(const float* x, int64_t p, const float* core0, const uint8_t
 typedef struct dq_segment {
   const uint8_t* k_codes; /* DQ_LAYOUT_KTILE */
   const uint8_t* v_codes; /* DQ_LAYOUT_VTILE */
-  const uint16_t* k_g0;   /* fp16 [i1][r][8]  (dq_core0_to_f16 layout, normalised) */
-  const uint16_t* v_g0;   /* fp16 [i1][r][8] */
+  const float* k_g0;      /* fp32 [i1][r][8]  (dq_core0_relayout, normalised): score side */
+  const uint16_t* v_g0;   /* fp16 [i1][r][8]  (dq_core0_relayout, normalised): output side */
   float k_scale, v_scale; /* quantizer scale times the G0 normalisation factor */
   int32_t T;          /* tokens in the segment */
   int32_t i1, i2, r;  /* plan of (T,128) */

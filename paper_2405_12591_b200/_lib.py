@@ -111,7 +111,7 @@ SIGNATURES = {
                                             c_void_p, c_size_t, c_void_p]),
     "dq_deco_quantize_batched": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p,
                                            c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
-    "dq_core0_to_f16": (c_int32, [c_void_p, c_int64, POINTER(Plan2), c_void_p, c_void_p, c_void_p]),
+    "dq_core0_relayout": (c_int32, [c_void_p, c_int64, POINTER(Plan2), c_void_p, c_int32, c_void_p, c_void_p]),
     "dq_deco_dequantize_batched": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int64,
                                              c_int64, c_int32, c_void_p, c_int32, c_void_p]),
     "dq_relayout": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int32, c_int64, c_int64, POINTER(Plan2),

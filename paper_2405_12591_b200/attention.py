@@ -64,9 +64,9 @@ class SegmentGroup:
         return payload_size(p.r * p.i2 * p.j2, bits) + 2 + 2 * (p.i1 * p.j1 * p.r)
 
     def stream_bytes(self) -> int:
-        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp16 G0, scales."""
-        return (self.k_payload.shape[1] + self.v_payload.shape[1] + 2 * (self.k_g0h.shape[1] + self.v_g0h.shape[1])
-                + 8)
+        """Bytes K5 reads for one unit of this segment (K + V): packed cores, G0 (fp32 K, fp16 V), scales."""
+        return (self.k_payload.shape[1] + self.v_payload.shape[1] + self.k_g0h.element_size() * self.k_g0h.shape[1]
+                + self.v_g0h.element_size() * self.v_g0h.shape[1] + 8)
 
 
 class _Layer:
@@ -78,10 +78,10 @@ class _Layer:
         self.keep = []     # tensors referenced by args
 
 
-def compress_blocks(blocks: torch.Tensor, bits: int, layout: int):
+def compress_blocks(blocks: torch.Tensor, bits: int, layout: int, g0_dtype=torch.float16):
     """K3 over (nblk, T, 128) fp16/fp32 CUDA blocks in slices of MAX_BLOCKS_PER_CALL.
 
-    Returns (payload (nblk, bytes), core0 f32, g0h f16 [a][r][c] normalised, norm f32, scale f32, plan).
+    Returns (payload (nblk, bytes), core0 f32, g0 [a][r][c] normalised in g0_dtype, norm f32, scale f32, plan).
     """
     nblk = blocks.shape[0]
     outs = []
@@ -93,11 +93,12 @@ def compress_blocks(blocks: torch.Tensor, bits: int, layout: int):
     payload = torch.cat([o["payload"] for o in outs]) if len(outs) > 1 else outs[0]["payload"]
     core0 = torch.cat([o["core0"] for o in outs]) if len(outs) > 1 else outs[0]["core0"]
     scale = torch.cat([o["scale"] for o in outs]) if len(outs) > 1 else outs[0]["scale"]
-    g0h = torch.empty((nblk, p.i1 * p.r * p.j1), dtype=torch.float16, device=blocks.device)
+    g0 = torch.empty((nblk, p.i1 * p.r * p.j1), dtype=g0_dtype, device=blocks.device)
     norm = torch.empty(nblk, dtype=torch.float32, device=blocks.device)
-    check(lib().dq_core0_to_f16(ptr(core0), nblk, ctypes.byref(p), ptr(g0h), ptr(norm), stream_ptr()),
-          "core0_to_f16")
-    return payload, core0, g0h, norm, scale, p
+    code = _lib.DQ_F16 if g0_dtype == torch.float16 else _lib.DQ_F32
+    check(lib().dq_core0_relayout(ptr(core0), nblk, ctypes.byref(p), ptr(g0), code, ptr(norm), stream_ptr()),
+          "core0_relayout")
+    return payload, core0, g0, norm, scale, p
 
 
 class DecodeKvCache:
@@ -142,8 +143,10 @@ class DecodeKvCache:
     def _add_group(self, layer: int, keys: torch.Tensor, values: torch.Tensor):
         lay = self._layer(layer)
         T = keys.shape[1]
-        kp, kc0, kg, kn, ks, p = compress_blocks(keys, self.bits, _lib.LAYOUT_KTILE)
-        vp, vc0, vg, vn, vs, _ = compress_blocks(values, self.bits, _lib.LAYOUT_VTILE)
+        # fp32 G0 on the score side: scores of outlier-heavy keys are large, and the fp16
+        # rounding of G0k (2^-11) would show up as absolute logit error
+        kp, kc0, kg, kn, ks, p = compress_blocks(keys, self.bits, _lib.LAYOUT_KTILE, torch.float32)
+        vp, vc0, vg, vn, vs, _ = compress_blocks(values, self.bits, _lib.LAYOUT_VTILE, torch.float32)
         i2p = -(-p.i2 // _lib.I2_PAD) * _lib.I2_PAD
         lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, kn, vn, lay.tokens_sealed))
         lay.tokens_sealed += T
@@ -186,13 +189,14 @@ class DecodeKvCache:
         for grp, (ks, vs) in zip(lay.groups, scales):
             p = grp.plan
             kb, vb = grp.k_payload.shape[1], grp.v_payload.shape[1]
-            gb = grp.k_g0h.shape[1] * 2
+            kgb = grp.k_g0h.shape[1] * grp.k_g0h.element_size()
+            vgb = grp.v_g0h.shape[1] * grp.v_g0h.element_size()
             for u in range(self.units):
                 s = _lib.Segment()
                 s.k_codes = grp.k_payload.data_ptr() + u * kb
                 s.v_codes = grp.v_payload.data_ptr() + u * vb
-                s.k_g0 = grp.k_g0h.data_ptr() + u * gb
-                s.v_g0 = grp.v_g0h.data_ptr() + u * gb
+                s.k_g0 = grp.k_g0h.data_ptr() + u * kgb
+                s.v_g0 = grp.v_g0h.data_ptr() + u * vgb
                 s.k_scale = float(ks[u])
                 s.v_scale = float(vs[u])
                 s.T, s.i1, s.i2, s.r, s.i2p = grp.T, p.i1, p.i2, p.r, grp.i2p

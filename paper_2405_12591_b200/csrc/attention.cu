@@ -8,565 +8,29 @@
 //
 // Factored order: per segment
 //   W[h,a,r,e] = sum_c q[h,c*16+e] G0k[a,c,r]                  (CUDA cores, per CTA)
-//   S[h,a,b]   = scale_k * sum_{r,e} W[h,a,r,e] code_k[r,b,e]   (tensor cores)
+//   S[h,a,b]   = scale_k * sum_{r,e} W[h,a,r,e] code_k[r,b,e]   (int8 tensor cores)
 //   P          = exp(S*sm_scale - m)                           (split-T softmax)
-//   Y[h,a,r,e] = sum_b P[h,a,b] code_v[r,b,e]                  (tensor cores)
+//   Y[h,a,r,e] = sum_b P[h,a,b] code_v[r,b,e]                  (int8 tensor cores)
 //   O[h,c,e]   = scale_v * sum_{a,r} G0v[a,c,r] Y[h,a,r,e]     (CUDA cores, epilogue)
 //
 // Data movement: one work item = (segment, 256-row slice of b) = one CTA.  Its packed
-// K codes (DQ_LAYOUT_KTILE) and V codes (DQ_LAYOUT_VTILE) are streamed through a
-// 4-stage x 16 KB shared-memory ring by cp.async.bulk (TMA bulk copies completing on
-// mbarriers); the last warp to release a stage issues its refill, so up to 64 KB per
-// CTA (128 KB per SM at 2 CTAs/SM) is in flight with no register cost.  Consumers read
-// bank-conflict-free fragments (the K tile rows are XOR-swizzled by r in HBM), turn
-// pairs of excess-coded codes into fp16 with one LOP3 (0x6400 magic; codes at nibble
-// position 1/3 come out x16 and that power of two is folded into the other MMA
-// operand), subtract the excess with one HSUB2, and feed mma.sync m16n8k16
-// (f16 x f16 -> f32).  The reduction index is permuted identically on both operands,
-// which is free.  Full-precision K/V never exist anywhere.
-#include "common.cuh"
+// K codes (DQ_LAYOUT_KTILE) and V codes (DQ_LAYOUT_VTILE) stream through a 3-stage x
+// 16 KB shared-memory ring by cp.async.bulk (TMA bulk copies completing on mbarriers);
+// the last warp to release a stage issues its refill (3 CTAs/SM -> 144 KB in flight per
+// SM, no register cost).  Consumers read bank-conflict-free fragments (K tile rows are
+// XOR-swizzled by r in HBM) and widen codes to bytes (int4: one AND per 4 even codes,
+// one SHF+AND per 4 odd codes).  The codes multiply fixed-point W and P split into two
+// 8-bit limbs (hi*256 + lo) on the int8 tensor pipe (mma.sync m16n8k32, exact s32
+// accumulation); the excess-code offset is removed exactly in integers.  The reduction
+// index is permuted identically on both operands, which is free.  Full-precision K/V
+// never exist anywhere.
+#include "attn_kernel.cuh"
 
 namespace dq {
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kD = 128;
-constexpr int kMaxR = 64;
-constexpr int kCB = 256;                 // b rows per work item
-constexpr int kTiles = kCB / kI2Pad;     // 64-row tiles per work item
-constexpr int kNG = kCB / 16;            // 16-row groups per work item
-constexpr int kStageBytes = 16384;
-constexpr int kStages = 3;
-
-// ---- PTX wrappers -------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-// ---- code rows ------------------------------------------------------------------
-// A row is 16 codes of one (r, b) [K] or one (r, e) x 16 b [V]: 2*BITS bytes.
-template <int BITS>
-struct Row {
-  uint32_t w[BITS == 8 ? 4 : (BITS == 4 ? 2 : 1)];
-};
-
-template <int BITS>
-__device__ __forceinline__ Row<BITS> lds_row(const unsigned char* p) {
-  Row<BITS> r;
-  if constexpr (BITS == 4) {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
-    r.w[0] = v.x;
-    r.w[1] = v.y;
-  } else if constexpr (BITS == 2) {
-    r.w[0] = *reinterpret_cast<const uint32_t*>(p);
-  } else {
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
-    r.w[0] = v.x;
-    r.w[1] = v.y;
-    r.w[2] = v.z;
-    r.w[3] = v.w;
-  }
-  return r;
-}
-
-// (a & b) | c in ONE LOP3: with both masks as immediates ptxas emits two (a LOP3
-// takes a single immediate), which doubles the ALU-pipe cost of the conversion.
-__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-
-__device__ __forceinline__ uint32_t hsub2_u32(uint32_t x, uint32_t bias) {
-  __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&x), *reinterpret_cast<const __half2*>(&bias));
-  return *reinterpret_cast<uint32_t*>(&r);
-}
-
-// fp16 pairs for sub-MMA C: lo -> k slots (2t, 2t+1), hi -> (2t+8, 2t+9).
-// Slot q = 4C + {0,1,2,3} holds element perm16(q) of the 16-group, times kscale(q).
-template <int BITS, int C>
-__device__ __forceinline__ void row_pairs(const Row<BITS>& r, uint32_t& lo, uint32_t& hi) {
-  const uint32_t M = 0x64006400u;
-  if constexpr (BITS == 4) {
-    const uint32_t w0 = (C >= 2) ? (r.w[0] >> 8) : r.w[0];
-    const uint32_t w1 = (C >= 2) ? (r.w[1] >> 8) : r.w[1];
-    const uint32_t mask = (C & 1) ? 0x00F000F0u : 0x000F000Fu;
-    constexpr uint32_t bias = (C & 1) ? 0x64806480u : 0x64086408u;  // 1024 + s*8, s = 16 or 1
-    lo = hsub2_u32(and_or(w0, mask, M), bias);
-    hi = hsub2_u32(and_or(w1, mask, M), bias);
-  } else if constexpr (BITS == 2) {
-    const uint32_t w = (C >= 2) ? (r.w[0] >> 8) : r.w[0];
-    const uint32_t mlo = (C & 1) ? 0x00300030u : 0x00030003u;
-    const uint32_t mhi = (C & 1) ? 0x00C000C0u : 0x000C000Cu;
-    constexpr uint32_t blo = (C & 1) ? 0x64206420u : 0x64026402u;  // 1024 + 2s, s = 16 / 1
-    constexpr uint32_t bhi = (C & 1) ? 0x64806480u : 0x64086408u;  // s = 64 / 4
-    lo = hsub2_u32(and_or(w, mlo, M), blo);
-    hi = hsub2_u32(and_or(w, mhi, M), bhi);
-  } else {
-    const uint32_t mask = 0x00FF00FFu;
-    lo = hsub2_u32(and_or(r.w[C], mask, M), 0x64806480u);
-    hi = hsub2_u32(and_or(r.w[C] >> 8, mask, M), 0x64806480u);
-  }
-}
-
-// element of the 16-group in k-slot q of the 4 sub-MMAs (must match row_pairs)
-template <int BITS>
-__host__ __device__ constexpr int perm16(int q) {
-  const int c = q >> 2, j = q & 3;
-  if (BITS == 4) return c + 4 * j;                                   // c, c+4, c+8, c+12
-  if (BITS == 2) return 2 * c + (j == 1 ? 8 : j == 2 ? 1 : j == 3 ? 9 : 0);  // 2c, 2c+8, 2c+1, 2c+9
-  return 4 * c + (j == 1 ? 2 : j == 2 ? 1 : j);                       // 4c, 4c+2, 4c+1, 4c+3
-}
-
-// inverse of perm16: k-slot holding element e of the 16-group
-template <int BITS>
-__host__ __device__ constexpr int inv_perm16(int e) {
-  if (BITS == 4) return 4 * (e & 3) + (e >> 2);
-  if (BITS == 2) return 4 * ((e & 7) >> 1) + 2 * (e & 1) + (e >> 3);
-  return 4 * (e >> 2) + (((e & 1) << 1) | ((e >> 1) & 1));
-}
-
-// power of two the code in k-slot q comes out multiplied by (folded into the other operand)
-template <int BITS>
-__host__ __device__ constexpr float kscale16(int q) {
-  const int c = q >> 2, j = q & 3;
-  if (BITS == 4) return (c & 1) ? 16.f : 1.f;
-  if (BITS == 2) return (float)((c & 1 ? 16 : 1) * (j >= 2 ? 4 : 1));
-  return 1.f;
-}
-
-template <int G>
-struct AttnSmem {
-  alignas(128) unsigned char ring[kStages][kStageBytes];
-  uint64_t full[kStages];
-  unsigned int released[kStages];
-  float q[G][kD];
-  float qmax;
-  // K phase: W fragments, 16-byte chunks [(h*r + rr)*2 + j][a ^ 2*(rr&3)];
-  // V phase (aliased): P fragments [((h*8 + a)*kNG + bg)*2 + (j ^ (a&1))]
-  union {
-    uint4 w[G * kMaxR * 2 * 8];
-    uint4 p[G * 8 * kNG * 2];
-  } wp;
-  float red[kWarps][G][kD];  // cross-warp reduction of the O partial (phase 4)
-  float rowmax[G][kWarps];
-  float rowsum[G][kWarps];
-};
-
-// stage geometry of one work item (identical in every thread)
-template <int BITS>
-struct Plan {
-  int r, nbt, bt0;
-  int RK, nK;              // K stages: RK bond rows x nbt tiles each
-  int rw, kslice, RV, nV;  // V stages: (tile, slice of RV bond rows)
-  int nslices;
-  __device__ Plan(const dq_segment& s, int wb0) {
-    constexpr int RB = 2 * BITS;
-    r = s.r;
-    bt0 = wb0 / kI2Pad;
-    nbt = min(kTiles, (s.i2p - wb0) / kI2Pad);
-    RK = kStageBytes / (nbt * kI2Pad * RB);
-    RK = RK & ~3;
-    if (RK > r) RK = r;
-    nK = (r + RK - 1) / RK;
-    rw = r / kWarps;
-    kslice = kWarps;
-    while (kslice > 1 && kslice * rw * 16 * kI2Pad * BITS / 8 > kStageBytes) kslice >>= 1;
-    RV = kslice * rw;
-    nslices = kWarps / kslice;
-    nV = nbt * nslices;
-  }
-  __device__ int stages() const { return nK + nV; }
-};
-
-// issue stage `st` of the work item into its ring slot (one thread)
-template <int BITS>
-__device__ __forceinline__ void issue_stage(const Plan<BITS>& pl, const dq_segment& seg, int st,
-                                            unsigned char* slot_buf, uint64_t* bar) {
-  constexpr int RB = 2 * BITS;
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  if (st < pl.nK) {
-    const int rk0 = st * pl.RK;
-    const int nr = min(pl.RK, pl.r - rk0);
-    const uint32_t chunk = (uint32_t)(nr * kI2Pad * RB);
-    mbar_expect_tx(bar, chunk * pl.nbt);
-    for (int j = 0; j < pl.nbt; ++j) {
-      const unsigned char* src = seg.k_codes + ((size_t)(pl.bt0 + j) * pl.r + rk0) * kI2Pad * RB;
-      bulk_g2s(slot_buf + j * chunk, src, chunk, bar);
-    }
-  } else {
-    const int v = st - pl.nK;
-    const int btl = v / pl.nslices, sl = v % pl.nslices;
-    const uint32_t bytes = (uint32_t)(pl.RV * 16 * kI2Pad * BITS / 8);
-    mbar_expect_tx(bar, bytes);
-    const unsigned char* src = seg.v_codes + ((size_t)(pl.bt0 + btl) * pl.r + sl * pl.RV) * 16 * kI2Pad * BITS / 8;
-    bulk_g2s(slot_buf, src, bytes, bar);
-  }
-}
-
-template <int BITS, int G>
-__global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(dq_attn_args args) {
-  constexpr int RB = 2 * BITS;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  AttnSmem<G>& sm = *reinterpret_cast<AttnSmem<G>*>(smem_raw);
-
-  const int wi = blockIdx.x;
-  const int seg_id = args.work[2 * wi];
-  const int wb0 = args.work[2 * wi + 1];
-  const dq_segment seg = args.segs[seg_id];
-  const int unit = seg.unit;
-  const int r = seg.r, i1 = seg.i1, i2 = seg.i2;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tid4 = lane & 3;
-  const Plan<BITS> pl(seg, wb0);
-  const int nstages = pl.stages();
-
-  // ---- prologue: barriers + first stages in flight before anything else ----------
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.full[s], 1);
-      sm.released[s] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int s = 0; s < kStages && s < nstages; ++s)
-      issue_stage<BITS>(pl, seg, s, sm.ring[s], &sm.full[s]);
-  }
-
-  // ---- phase 0: q, W = q . G0k (normalised G0, power-of-two prescale), G0v ----------
-  const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)unit * G * kD;
-  float qm = 0.f;
-  for (int i = tid; i < G * kD; i += kThreads) {
-    const float v = __half2float(qh[i]);
-    sm.q[i / kD][i % kD] = v;
-    qm = fmaxf(qm, fabsf(v));
-  }
-  for (int o = 16; o; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
-  if (tid == 0) sm.qmax = 0.f;
-  __syncthreads();
-  if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(&sm.qmax), __float_as_uint(qm));
-  __syncthreads();
-  // |W| <= 8 max|q| max|g0| <= 8 max|q|; keep it below 2^14 with an exact power of two
-  float wscale = 1.f;
-  while (8.f * sm.qmax * wscale > 16384.f) wscale *= 0.5f;
-  {
-    const uint4* g0k = reinterpret_cast<const uint4*>(seg.k_g0);
-    for (int item = tid; item < G * 8 * r; item += kThreads) {
-      const int h = item / (8 * r), rem = item - h * 8 * r;
-      const int a = rem / r, rr = rem - a * r;
-      float gk[8];
-      if (a < i1) {
-        const uint4 gv = g0k[a * r + rr];
-        const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __half22float2(g2[k]);
-          gk[2 * k] = f.x;
-          gk[2 * k + 1] = f.y;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) gk[k] = 0.f;
-      }
-      __half hv[16];
-#pragma unroll
-      for (int qi = 0; qi < 16; ++qi) {
-        const int e = perm16<BITS>(qi);
-        float acc = 0.f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc = fmaf(sm.q[h][c * 16 + e], gk[c], acc);
-        hv[qi] = __float2half_rn(acc * (wscale / kscale16<BITS>(qi)));
-      }
-      const int sw = a ^ (2 * (rr & 3));
-      sm.wp.w[((h * r + rr) * 2 + 0) * 8 + sw] = *reinterpret_cast<uint4*>(&hv[0]);
-      sm.wp.w[((h * r + rr) * 2 + 1) * 8 + sw] = *reinterpret_cast<uint4*>(&hv[8]);
-    }
-  }
-  __syncthreads();
-
-  int st = 0;  // running stage index
-  auto release = [&](int s) {
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      const int slot = s % kStages;
-      const unsigned target = (unsigned)(s / kStages + 1) * kWarps;
-      const unsigned old = atomicAdd(&sm.released[slot], 1u);
-      if (old + 1 == target && s + kStages < nstages)
-        issue_stage<BITS>(pl, seg, s + kStages, sm.ring[slot], &sm.full[slot]);
-    }
-  };
-
-  // ---- phase 1: S = W . codes_k ---------------------------------------------------
-  constexpr int MT = 2;  // 16-row m-tiles per warp (32 b rows)
-  const int jt = warp >> 1;                     // tile of this warp inside the item
-  const int bl_base = 32 * (warp & 1);          // first row of this warp inside the tile
-  float acc[MT][G][4];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int h = 0; h < G; ++h)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[mt][h][k] = 0.f;
-  for (int ks = 0; ks < pl.nK; ++ks, ++st) {
-    const int slot = st % kStages;
-    mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
-    const int rk0 = ks * pl.RK;
-    const int nr = min(pl.RK, r - rk0);
-    if (jt < pl.nbt) {
-      const unsigned char* tile = sm.ring[slot] + jt * nr * kI2Pad * RB;
-      for (int q0 = 0; q0 < nr; q0 += 4) {
-        const int rl = q0 + tid4;     // bond row inside the stage
-        const int rr = rk0 + rl;      // global bond row
-        const int swz = ktile_swizzle(rr, BITS);
-        uint4 bw[G][2];
-#pragma unroll
-        for (int h = 0; h < G; ++h)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) bw[h][j] = sm.wp.w[((h * r + rr) * 2 + j) * 8 + (gid ^ (2 * tid4))];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int b0 = bl_base + mt * 16 + gid;
-          const Row<BITS> x0 = lds_row<BITS>(tile + (rl * kI2Pad + (b0 ^ swz)) * RB);
-          const Row<BITS> x1 = lds_row<BITS>(tile + (rl * kI2Pad + ((b0 + 8) ^ swz)) * RB);
-          uint32_t a[4][4];
-          row_pairs<BITS, 0>(x0, a[0][0], a[0][2]);
-          row_pairs<BITS, 0>(x1, a[0][1], a[0][3]);
-          row_pairs<BITS, 1>(x0, a[1][0], a[1][2]);
-          row_pairs<BITS, 1>(x1, a[1][1], a[1][3]);
-          row_pairs<BITS, 2>(x0, a[2][0], a[2][2]);
-          row_pairs<BITS, 2>(x1, a[2][1], a[2][3]);
-          row_pairs<BITS, 3>(x0, a[3][0], a[3][2]);
-          row_pairs<BITS, 3>(x1, a[3][1], a[3][3]);
-#pragma unroll
-          for (int h = 0; h < G; ++h) {
-            mma16816(acc[mt][h], a[0][0], a[0][1], a[0][2], a[0][3], bw[h][0].x, bw[h][0].y);
-            mma16816(acc[mt][h], a[1][0], a[1][1], a[1][2], a[1][3], bw[h][0].z, bw[h][0].w);
-            mma16816(acc[mt][h], a[2][0], a[2][1], a[2][2], a[2][3], bw[h][1].x, bw[h][1].y);
-            mma16816(acc[mt][h], a[3][0], a[3][1], a[3][2], a[3][3], bw[h][1].z, bw[h][1].w);
-          }
-        }
-      }
-    }
-    release(st);
-  }
-  // ---- phase 2: softmax of the work item straight from the accumulators ---------------
-  // scores in the log2 domain: s = acc * scale_k * sm_scale / wscale * log2(e)
-  const float kscale = seg.k_scale * args.sm_scale / wscale * 1.4426950408889634f;
-  float mh[G];
-#pragma unroll
-  for (int h = 0; h < G; ++h) {
-    float m = -INFINITY;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int bl = jt * kI2Pad + bl_base + mt * 16 + gid + (k >= 2 ? 8 : 0);
-        const int a = 2 * tid4 + (k & 1);
-        const bool ok = (a < i1) && (wb0 + bl < i2) && (jt < pl.nbt);
-        acc[mt][h][k] = ok ? acc[mt][h][k] * kscale : -INFINITY;
-        m = fmaxf(m, acc[mt][h][k]);
-      }
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) sm.rowmax[h][warp] = m;
-  }
-  __syncthreads();  // every warp is past phase 1: the W buffer may now hold P
-#pragma unroll
-  for (int h = 0; h < G; ++h) {
-    float m = sm.rowmax[h][0];
-#pragma unroll
-    for (int w = 1; w < kWarps; ++w) m = fmaxf(m, sm.rowmax[h][w]);
-    mh[h] = m;
-    float l = 0.f;
-    __half* pbase = reinterpret_cast<__half*>(sm.wp.p);
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int bl = jt * kI2Pad + bl_base + mt * 16 + gid + (k >= 2 ? 8 : 0);
-        const int a = 2 * tid4 + (k & 1);
-        const float sv = acc[mt][h][k];
-        const float pv = sv == -INFINITY ? 0.f : exp2f(sv - m);
-        const int qi = inv_perm16<BITS>(bl & 15);
-        const float ks = kscale16<BITS>(qi);
-        const __half ph = __float2half_rn(pv / ks);
-        l += __half2float(ph) * ks;  // the probability mass the PV product really uses
-        if (jt < pl.nbt)
-          pbase[((((h * 8 + a) * kNG + (bl >> 4)) * 2 + ((qi >> 3) ^ (a & 1))) << 3) + (qi & 7)] = ph;
-      }
-    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) sm.rowsum[h][warp] = l;
-  }
-  __syncthreads();
-
-  // ---- phase 3: Y = codes_v . P^T ------------------------------------------------------
-  // warp w owns bond rows w*rw .. w*rw+rw-1 (an m-tile = one bond row x 16 e)
-  const int rw = pl.rw;
-  const int my_slice = warp / pl.kslice;
-  const int rbase_in_slice = (warp % pl.kslice) * rw;
-  float accv[8][G][4];
-#pragma unroll
-  for (int t = 0; t < 8; ++t)
-#pragma unroll
-    for (int h = 0; h < G; ++h)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) accv[t][h][k] = 0.f;
-  for (int vs = 0; vs < pl.nV; ++vs, ++st) {
-    const int slot = st % kStages;
-    mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
-    const int btl = vs / pl.nslices, sl = vs % pl.nslices;
-    if (sl == my_slice) {
-      uint4 pf[G][2];
-#pragma unroll
-      for (int h = 0; h < G; ++h)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          pf[h][j] = sm.wp.p[(((h * 8 + gid) * kNG + btl * 4 + tid4) * 2 + (j ^ (gid & 1)))];
-      const unsigned char* buf = sm.ring[slot];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        if (t < rw) {
-          const int rl = rbase_in_slice + t;
-          const Row<BITS> x0 = lds_row<BITS>(buf + (rl * 16 + gid) * 8 * BITS + RB * tid4);
-          const Row<BITS> x1 = lds_row<BITS>(buf + (rl * 16 + gid + 8) * 8 * BITS + RB * tid4);
-          uint32_t a[4][4];
-          row_pairs<BITS, 0>(x0, a[0][0], a[0][2]);
-          row_pairs<BITS, 0>(x1, a[0][1], a[0][3]);
-          row_pairs<BITS, 1>(x0, a[1][0], a[1][2]);
-          row_pairs<BITS, 1>(x1, a[1][1], a[1][3]);
-          row_pairs<BITS, 2>(x0, a[2][0], a[2][2]);
-          row_pairs<BITS, 2>(x1, a[2][1], a[2][3]);
-          row_pairs<BITS, 3>(x0, a[3][0], a[3][2]);
-          row_pairs<BITS, 3>(x1, a[3][1], a[3][3]);
-#pragma unroll
-          for (int h = 0; h < G; ++h) {
-            mma16816(accv[t][h], a[0][0], a[0][1], a[0][2], a[0][3], pf[h][0].x, pf[h][0].y);
-            mma16816(accv[t][h], a[1][0], a[1][1], a[1][2], a[1][3], pf[h][0].z, pf[h][0].w);
-            mma16816(accv[t][h], a[2][0], a[2][1], a[2][2], a[2][3], pf[h][1].x, pf[h][1].y);
-            mma16816(accv[t][h], a[3][0], a[3][1], a[3][2], a[3][3], pf[h][1].z, pf[h][1].w);
-          }
-        }
-      }
-    }
-    release(st);
-  }
-
-  // ---- phase 4: O = scale_v * G0v . Y on CUDA cores, reduce, write the partial ---------
-  // accv[t][h]: rows e = gid (k 0,1) / gid+8 (k 2,3); cols a = 2*tid4 + (k & 1)
-  float part[G][16];  // [h][c*2 + (e == gid+8)]
-#pragma unroll
-  for (int h = 0; h < G; ++h)
-#pragma unroll
-    for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    if (t < rw) {
-      const int rr = warp * rw + t;
-#pragma unroll
-      for (int aa = 0; aa < 2; ++aa) {
-        const int a = 2 * tid4 + aa;
-        if (a < i1) {
-          const uint4 gv = __ldg(reinterpret_cast<const uint4*>(seg.v_g0) + a * r + rr);  // L2-resident
-          const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
-          float gc[8];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float2 f = __half22float2(g2[k]);
-            gc[2 * k] = f.x;
-            gc[2 * k + 1] = f.y;
-          }
-#pragma unroll
-          for (int h = 0; h < G; ++h)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              part[h][2 * c] = fmaf(gc[c], accv[t][h][aa], part[h][2 * c]);
-              part[h][2 * c + 1] = fmaf(gc[c], accv[t][h][2 + aa], part[h][2 * c + 1]);
-            }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < G; ++h)
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      float v = part[h][k];
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      part[h][k] = v;
-    }
-  // the score buffer is dead now: reuse it for the cross-warp reduction
-#pragma unroll
-  for (int h = 0; h < G; ++h)
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int c = 2 * tid4 + cc;
-      float v0 = 0.f, v1 = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (k == c) {
-          v0 = part[h][2 * k];
-          v1 = part[h][2 * k + 1];
-        }
-      sm.red[warp][h][c * 16 + gid] = v0;
-      sm.red[warp][h][c * 16 + gid + 8] = v1;
-    }
-  __syncthreads();
-  const int slot_out = args.work_part[wi];
-  for (int i = tid; i < G * kD; i += kThreads) {
-    const int h = i / kD, d = i % kD;
-    float v = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) v += sm.red[w][h][d];
-    args.part_o[((size_t)slot_out * G + h) * kD + d] = v * seg.v_scale;
-  }
-  if (tid < G) {
-    float l = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) l += sm.rowsum[tid][w];
-    args.part_ml[((size_t)slot_out * G + tid) * 2 + 0] = mh[tid];  // log2 domain
-    args.part_ml[((size_t)slot_out * G + tid) * 2 + 1] = l;
-  }
-}
+using namespace attn;
 
 // ---- combine: merge work-item partials with the dense fp16 tail ------------------
 // one CTA (128 threads) per unit; thread d owns output dim d.

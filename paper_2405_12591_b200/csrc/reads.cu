@@ -169,8 +169,8 @@ __global__ void relayout_kernel(const uint8_t* __restrict__ src, CoreGeom gs, in
 // core0 (1,i1,j1,r) f32 -> fp16 [a][r][c], divided by a per-block power of two so that
 // max|g0h| lies in [0.5, 1): keeps W = q.G0 inside fp16 range whatever the K scale.
 // One CTA per block.
-__global__ void core0_f16_kernel(const float* __restrict__ core0, int i1, int j1, int r, __half* __restrict__ out,
-                                 float* __restrict__ norm) {
+__global__ void core0_f16_kernel(const float* __restrict__ core0, int i1, int j1, int r, void* __restrict__ out,
+                                 int out_dtype, float* __restrict__ norm) {
   __shared__ float red[32];
   const int per = i1 * j1 * r;
   const int64_t blk = blockIdx.x;
@@ -196,7 +196,11 @@ __global__ void core0_f16_kernel(const float* __restrict__ core0, int i1, int j1
   for (int i = threadIdx.x; i < per; i += blockDim.x) {
     const int a = i / (r * j1), t = i - a * r * j1;
     const int rr = t / j1, c = t - rr * j1;
-    out[blk * per + i] = __float2half_rn(src[(a * j1 + c) * r + rr] * inv);
+    const float v = src[(a * j1 + c) * r + rr] * inv;
+    if (out_dtype == DQ_F16)
+      static_cast<__half*>(out)[blk * per + i] = __float2half_rn(v);
+    else
+      static_cast<float*>(out)[blk * per + i] = v;
   }
 }
 
@@ -297,12 +301,13 @@ extern "C" int dq_relayout(const uint8_t* src, int32_t src_layout, int64_t src_s
   return DQ_OK;
 }
 
-extern "C" int dq_core0_to_f16(const float* core0, int64_t nblk, const dq_plan2* hp, uint16_t* g0h, float* norm,
-                               void* stream) {
-  if (!hp || (nblk && (!core0 || !g0h))) return fail(DQ_ERR_INVALID_ARG, "null pointer");
+extern "C" int dq_core0_relayout(const float* core0, int64_t nblk, const dq_plan2* hp, void* out, int32_t out_dtype,
+                                 float* norm, void* stream) {
+  if (!hp || (nblk && (!core0 || !out))) return fail(DQ_ERR_INVALID_ARG, "null pointer");
+  if (out_dtype != DQ_F16 && out_dtype != DQ_F32) return fail(DQ_ERR_INVALID_ARG, "unknown dtype %d", out_dtype);
   if (nblk == 0) return DQ_OK;
   core0_f16_kernel<<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(core0, (int)hp->i1, (int)hp->j1, (int)hp->r,
-                                                                         (__half*)g0h, norm);
+                                                                         out, out_dtype, norm);
   DQ_LAUNCH_CHECK();
   return DQ_OK;
 }

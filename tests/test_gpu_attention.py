@@ -89,6 +89,27 @@ def test_decode_attention_prefill_only(dq, bits, g, T, units):
         assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
 
 
+@pytest.mark.parametrize("scale,bits", [(20.0, 4), (50.0, 4), (20.0, 2), (20.0, 8)])
+def test_decode_attention_outlier_channels(dq, scale, bits):
+    """Outlier key channels (LLM-like) make the softmax peaky: tolerance must still hold."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(int(scale) + bits)
+    units, T = 2, 4096
+    k = rng.standard_normal((units, T, 128)).astype(np.float32)
+    k[:, :, [3, 77]] *= scale
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = rng.standard_normal((units, 1, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=bits)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), bits,
+                             [T], 0)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
 def test_decode_attention_segments_and_tail(dq):
     """prefill 1500 + 2 sealed chunks of 256 + tail 77, g=2, int4, outlier columns."""
     from paper_2405_12591_b200.attention import DecodeKvCache
