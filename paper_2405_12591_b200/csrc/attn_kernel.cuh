@@ -39,11 +39,17 @@ struct AttnSmem {
   unsigned pmax[G][8][kTiles];  // largest probability per (h, a, tile), float bits
   // K phase: W limbs, 16-byte chunks [((h*2 + limb)*r + rr)*8 + (a ^ 2*(rr&3))];
   // V phase (aliased): P limbs [((h*2 + limb)*8 + a)*kNG + (bg ^ 4*(a&1))]
+  // K phase: W limbs; V phase + epilogue (aliased, W is dead): fp32 G0v [a][rr][c] by TMA
   union {
     uint4 w[G * 2 * kMaxR * 8];
+    float4 g0v[8 * kMaxR * 2];
+  } wg;
+  // V phase: P limbs; epilogue (aliased, P is dead): cross-warp reduction of the O partial
+  union {
     uint4 p[G * 2 * 8 * kNG];
-  } wp;
-  float red[kWarps][G][kD];  // cross-warp reduction of the O partial
+    float red[kWarps][G][kD];
+  } pr;
+  uint64_t g0bar;  // G0v prefetch
   float rowmax[G][kWarps];
 };
 
@@ -130,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
       mbar_init(&sm.full[s], 1);
       sm.released[s] = 0;
     }
+    mbar_init(&sm.g0bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     for (int s = 0; s < kStages && s < nstages; ++s) issue_stage<BITS>(pl, seg, s, sm.ring[s], &sm.full[s]);
   }
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
       int h = 0, a = 0, rr = 0;
       bool live = item < G * 8 * r;
       if (live) {
-        h = item / (8 * r);
+        h = G == 1 ? 0 : item / (8 * r);  // G == 1: lets the compiler share the q loads across items
         const int rem = item - h * 8 * r;
         a = rem / r;
         rr = rem - a * r;
@@ -170,15 +177,17 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
           gk[4] = g_hi.x, gk[5] = g_hi.y, gk[6] = g_hi.z, gk[7] = g_hi.w;
         }
       }
+      if (!live) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) gk[c] = 0.f;
+      }
       float m = 0.f;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int e = ord16<BITS>(i);
         float acc = 0.f;
-        if (live) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc = fmaf(sm.q[h][c * 16 + e], gk[c], acc);
-        }
+        for (int c = 0; c < 8; ++c) acc = fmaf(sm.q[h][c * 16 + e], gk[c], acc);
         wv[j][i] = acc;
         m = fmaxf(m, fabsf(acc));
       }
@@ -205,8 +214,8 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
         hi[i >> 2] |= (uint32_t)((wint >> 8) & 0xFF) << (8 * (i & 3));
         lo[i >> 2] |= (uint32_t)(wint & 0xFF) << (8 * (i & 3));
       }
-      sm.wp.w[w_chunk(h, 0, r, rr, a)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      sm.wp.w[w_chunk(h, 1, r, rr, a)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      sm.wg.w[w_chunk(h, 0, r, rr, a)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      sm.wg.w[w_chunk(h, 1, r, rr, a)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       if (X) atomicAdd(&sm.beta[h][a][grp], X * wsum);
     }
   }
@@ -277,8 +286,8 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
         uint4 bh[G], bl[G];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          bh[h] = sm.wp.w[w_chunk(h, 0, r, rr, gid)];
-          bl[h] = sm.wp.w[w_chunk(h, 1, r, rr, gid)];
+          bh[h] = sm.wg.w[w_chunk(h, 0, r, rr, gid)];
+          bl[h] = sm.wg.w[w_chunk(h, 1, r, rr, gid)];
         }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
@@ -319,8 +328,14 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) sm.rowmax[h][warp] = m;
   }
-  __syncthreads();  // every warp is past phase 1: the W buffer may now hold P
-  unsigned char* pb = reinterpret_cast<unsigned char*>(sm.wp.p);
+  __syncthreads();  // every warp is past phase 1: the W buffer is dead
+  if (tid == 0) {   // prefetch the fp32 G0v for the epilogue into it
+    const uint32_t gb = (uint32_t)(i1 * r * 32);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(&sm.g0bar, gb);
+    bulk_g2s(sm.wg.g0v, seg.v_g0, gb, &sm.g0bar);
+  }
+  unsigned char* pb = reinterpret_cast<unsigned char*>(sm.pr.p);
   // P = exp2(s - m) in fixed point with one scale per (h, a, 64-row tile), set by that
   // tile's largest probability: small probabilities far from the peak keep their
   // relative precision (the V side combines its accumulators per tile anyway)
@@ -412,8 +427,8 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
       float pinv[G][2];
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        ph[h] = sm.wp.p[p_chunk(h, 0, gid, btl * 4 + tid4)];
-        pl_[h] = sm.wp.p[p_chunk(h, 1, gid, btl * 4 + tid4)];
+        ph[h] = sm.pr.p[p_chunk(h, 0, gid, btl * 4 + tid4)];
+        pl_[h] = sm.pr.p[p_chunk(h, 1, gid, btl * 4 + tid4)];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           gam[h][j] = sm.gamma[h][2 * tid4 + j][btl];
@@ -432,14 +447,15 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
           row_bytes<BITS>(lds_row<BITS>(buf + (rl * 16 + gid + 8) * 8 * BITS + RB * tid4), x1);
 #pragma unroll
           for (int h = 0; h < G; ++h) {
-            int yh[4] = {0, 0, 0, 0}, yl[4] = {0, 0, 0, 0};
+            // the excess correction seeds the low-limb accumulator
+            int yh[4] = {0, 0, 0, 0}, yl[4] = {-gam[h][0], -gam[h][1], -gam[h][0], -gam[h][1]};
             imma<SA, false>(yh, x0[0], x1[0], x0[1], x1[1], ph[h].x, ph[h].y);
             imma<SA, false>(yl, x0[0], x1[0], x0[1], x1[1], pl_[h].x, pl_[h].y);
             imma<SA, false>(yh, x0[2], x1[2], x0[3], x1[3], ph[h].z, ph[h].w);
             imma<SA, false>(yl, x0[2], x1[2], x0[3], x1[3], pl_[h].z, pl_[h].w);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              accv[t][h][k] += (float)(256 * yh[k] + yl[k] - gam[h][k & 1]) * pinv[h][k & 1];
+              accv[t][h][k] += (float)(256 * yh[k] + yl[k]) * pinv[h][k & 1];
           }
         }
       }
@@ -454,7 +470,8 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
   for (int h = 0; h < G; ++h)
 #pragma unroll
     for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
-  const float4* g0v = reinterpret_cast<const float4*>(seg.v_g0);  // fp32 [a][rr][c], normalised
+  mbar_wait(&sm.g0bar, 0);  // fp32 G0v [a][rr][c] (normalised), prefetched into the W buffer
+  const float4* g0v = sm.wg.g0v;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     if (t < rw) {
@@ -463,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
       for (int aa = 0; aa < 2; ++aa) {
         const int a = 2 * tid4 + aa;
         if (a < i1) {
-          const float4 g_lo = __ldg(g0v + 2 * (a * r + rr)), g_hi = __ldg(g0v + 2 * (a * r + rr) + 1);
+          const float4 g_lo = g0v[2 * (a * r + rr)], g_hi = g0v[2 * (a * r + rr) + 1];
           const float gc[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
 #pragma unroll
           for (int h = 0; h < G; ++h)
@@ -485,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       part[h][k] = v;
     }
+  __syncthreads();  // every warp is past the V stages: the P buffer may now hold the reduction
 #pragma unroll
   for (int h = 0; h < G; ++h)
 #pragma unroll
@@ -497,8 +515,8 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
           v0 = part[h][2 * k];
           v1 = part[h][2 * k + 1];
         }
-      sm.red[warp][h][c * 16 + gid] = v0;
-      sm.red[warp][h][c * 16 + gid + 8] = v1;
+      sm.pr.red[warp][h][c * 16 + gid] = v0;
+      sm.pr.red[warp][h][c * 16 + gid + 8] = v1;
     }
   __syncthreads();
   const int slot_out = args.work_part[wi];
@@ -506,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
     const int h = i / kD, d = i % kD;
     float v = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) v += sm.red[w][h][d];
+    for (int w = 0; w < kWarps; ++w) v += sm.pr.red[w][h][d];
     args.part_o[((size_t)slot_out * G + h) * kD + d] = v * seg.v_scale;
   }
   if (tid < G) {
