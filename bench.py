@@ -394,7 +394,7 @@ def run_ours(args, cfg):
                        "blocks_per_s": 2 * units * layers / write_s},
         "e2e": {"value": global_batch / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "gpu_launches": args.steps * layers * 3,
+        "gpu_launches": args.steps * layers * 4,  # per layer: prepare, split, combine, tail append
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -188,9 +188,15 @@ typedef struct dq_attn_args {
   const int32_t* unit_nparts;/* device [units] */
   float* part_o;          /* workspace [total_parts][g][128] f32 */
   float* part_ml;         /* workspace [total_parts][g][2]   f32 (max, sum) */
-  int32_t phases;         /* bit 0: split kernel, bit 1: combine kernel; 0 means both */
+  int32_t phases;         /* bit 0: split kernel, bit 1: combine kernel, bit 2: prepare kernel; 0: all */
   int32_t pad_;
+  int64_t* trace;         /* optional (profiling): [nwork][8] global-timer stamps per work item */
+  void* wimg;             /* workspace [nseg][wimg_stride]: per-segment W images (prepare kernel) */
+  int64_t wimg_stride;    /* >= dq_attention_wimg_bytes(g) */
 } dq_attn_args;
+
+/* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */
+int dq_attention_wimg_bytes(int32_t g, int64_t* h_bytes);
 
 /* host helper: fill work/partial tables (host arrays) for a host copy of the segment table */
 int dq_attention_plan(const dq_segment* h_segs, int32_t nseg, int32_t units, int32_t chunk_b, int32_t* h_work,

@@ -88,6 +88,9 @@ class AttnArgs(ctypes.Structure):
         ("part_ml", c_void_p),
         ("phases", c_int32),
         ("pad_", c_int32),
+        ("trace", c_void_p),
+        ("wimg", c_void_p),
+        ("wimg_stride", c_int64),
     ]
 
 
@@ -123,6 +126,7 @@ SIGNATURES = {
     "dq_attention_plan": (c_int32, [POINTER(Segment), c_int32, c_int32, c_int32, POINTER(c_int32), POINTER(c_int32),
                                     POINTER(c_int32), POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
     "dq_decode_attention": (c_int32, [POINTER(AttnArgs), c_void_p]),
+    "dq_attention_wimg_bytes": (c_int32, [c_int32, POINTER(c_int64)]),
     "dq_tail_append": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
 }
 

@@ -246,8 +246,13 @@ class DecodeKvCache:
         a.unit_nparts = np_dev.data_ptr()
         a.part_o = part_o.data_ptr()
         a.part_ml = part_ml.data_ptr()
+        wib = ctypes.c_int64()
+        check(lib().dq_attention_wimg_bytes(self.g, ctypes.byref(wib)), "wimg_bytes")
+        wimg = torch.empty((max(nseg, 1), wib.value), dtype=torch.uint8, device=dev)
+        a.wimg = wimg.data_ptr()
+        a.wimg_stride = wib.value
         lay.args = a
-        lay.keep = [seg_dev, work_dev, wpart_dev, p0_dev, np_dev, part_o, part_ml]
+        lay.keep = [seg_dev, work_dev, wpart_dev, p0_dev, np_dev, part_o, part_ml, wimg]
 
     def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """q: (units, g, 128) fp16 CUDA -> (units, g, 128) fp16."""

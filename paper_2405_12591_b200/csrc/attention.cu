@@ -121,10 +121,28 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
                                      100));
     attr = true;
   }
-  const int phases = a.phases ? a.phases : 3;
-  if (a.nwork > 0 && (phases & 1)) {
-    decode_attn_kernel<BITS, G><<<a.nwork, kThreads, smem, s>>>(a);
+  const int phases = a.phases ? a.phases : 7;
+  if (a.nwork > 0 && (phases & 5)) {
+    if (!a.wimg || a.wimg_stride < kWImageBytes<G>) return fail(DQ_ERR_INVALID_ARG, "W image workspace too small");
+  }
+  if (a.nseg > 0 && a.nwork > 0 && (phases & 4)) {
+    attn_prepare_kernel<BITS, G><<<a.nseg, kPrepThreads, 0, s>>>(a);
     DQ_LAUNCH_CHECK();
+  }
+  if (a.nwork > 0 && (phases & 1)) {
+    // programmatic dependent launch: the split kernel's prologue and first code copies
+    // overlap the prepare kernel; it waits (griddepcontrol.wait) only for the W images
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.nwork);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_pdl[1];
+    attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr_pdl;
+    cfg.numAttrs = 1;
+    DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G>, a));
   }
   if (phases & 2) {
     const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1);
@@ -185,6 +203,14 @@ extern "C" int dq_attention_plan(const dq_segment* segs, int32_t nseg, int32_t u
   }
   *nwork = n;
   *total_parts = acc;
+  return DQ_OK;
+}
+
+extern "C" int dq_attention_wimg_bytes(int32_t g, int64_t* bytes) {
+  if (!bytes) return fail(DQ_ERR_INVALID_ARG, "null output");
+  if (g == 1) *bytes = kWImageBytes<1>;
+  else if (g == 2) *bytes = kWImageBytes<2>;
+  else return fail(DQ_ERR_UNSUPPORTED, "g must be 1 or 2 in this build (got %d)", g);
   return DQ_OK;
 }
 

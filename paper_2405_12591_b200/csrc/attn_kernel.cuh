@@ -2,7 +2,7 @@
 // math.  One CTA = one work item = (segment, 256-row slice of b).
 #pragma once
 
-#include "attn_frag.cuh"
+#include "attn_prepare.cuh"
 
 namespace dq {
 namespace attn {
@@ -17,10 +17,6 @@ constexpr int kNG = kCB / 16;         // 16-row groups per work item
 constexpr int kStageBytes = 16384;
 constexpr int kStages = 3;
 
-// fixed-point precision of the two-limb (hi*256 + lo) 8-bit MMA operands; int8 codes
-// use fewer bits so the s32 accumulators cannot overflow
-template <int BITS>
-constexpr int kWBits = BITS == 8 ? 13 : 15;  // |W * 2^sW| < 2^kWBits
 template <int BITS>
 constexpr int kPBits = 15;  // P / tile max in (0.5, 1] -> round(P * 2^(kPBits - e)); Y sums per 64-row tile
 
@@ -28,12 +24,10 @@ template <int G>
 struct AttnSmem {
   alignas(128) unsigned char ring[kStages][kStageBytes];
   uint64_t full[kStages];
+  uint64_t wbar;   // W image (attn_prepare.cuh) by TMA
+  uint64_t g0bar;  // G0v prefetch
   unsigned int released[kStages];
-  float q[G][kD];
-  // W is quantized per output column (h, a) and per bond-row group: group 0 = the rows of
-  // the first K stage (the largest singular values), group 1 = the rest
-  unsigned wmax[G][8][2];  // max |W| as float bits
-  int beta[G][8][2];       // excess correction of the scores: kExcess * sum_k Wint[a][k]
+  alignas(16) WMeta<G> wmeta;  // per-column W scales and excess corrections (TMA target)
   int gamma[G][8][kTiles]; // excess correction of Y per 64-row tile: kExcess * sum_b Pint[a][b]
   float lsum[G][kWarps];   // probability mass per warp
   unsigned pmax[G][8][kTiles];  // largest probability per (h, a, tile), float bits
@@ -49,7 +43,6 @@ struct AttnSmem {
     uint4 p[G * 2 * 8 * kNG];
     float red[kWarps][G][kD];
   } pr;
-  uint64_t g0bar;  // G0v prefetch
   float rowmax[G][kWarps];
 };
 
@@ -103,9 +96,6 @@ __device__ __forceinline__ void issue_stage(const Plan<BITS>& pl, const dq_segme
   }
 }
 
-__device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a) {
-  return ((h * 2 + limb) * r + rr) * 8 + (a ^ (2 * (rr & 3)));
-}
 
 __device__ __forceinline__ int p_chunk(int h, int limb, int a, int bg) {
   return ((h * 2 + limb) * 8 + a) * kNG + (bg ^ (4 * (a & 1)));
@@ -130,96 +120,38 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
   const Plan<BITS> pl(seg, wb0);
   const int nstages = pl.stages();
 
+  auto stamp = [&](int k) {  // optional per-item phase timestamps (profiling only)
+    if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + k] = global_ns();
+  };
+  stamp(0);
+  if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + 7] = sm_id();
+
   // ---- prologue: barriers + the first stages in flight before anything else ----------
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.full[s], 1);
       sm.released[s] = 0;
     }
+    mbar_init(&sm.wbar, 1);
     mbar_init(&sm.g0bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    // the code stages do not depend on the prepare kernel: start streaming right away
     for (int s = 0; s < kStages && s < nstages; ++s) issue_stage<BITS>(pl, seg, s, sm.ring[s], &sm.full[s]);
-  }
-
-  // ---- phase 0: W = q . G0k in two 8-bit limbs ----------------------------------------
-  const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)unit * G * kD;
-  for (int i = tid; i < G * kD; i += kThreads) sm.q[i / kD][i % kD] = __half2float(qh[i]);
-  if (tid < G * 8) {
-    sm.beta[tid / 8][tid % 8][0] = sm.beta[tid / 8][tid % 8][1] = 0;
-    sm.wmax[tid / 8][tid % 8][0] = sm.wmax[tid / 8][tid % 8][1] = 0u;
+    // programmatic dependent launch: everything above overlapped the prepare kernel;
+    // its output (the segment's W image: limb chunks + per-column metadata) is read below
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    const unsigned char* img = static_cast<const unsigned char*>(args.wimg) + (size_t)seg_id * args.wimg_stride;
+    const uint32_t wb = (uint32_t)(G * 2 * r * 8 * 16);
+    mbar_expect_tx(&sm.wbar, wb + (uint32_t)sizeof(WMeta<G>));
+    bulk_g2s(sm.wg.w, img, wb, &sm.wbar);
+    bulk_g2s(&sm.wmeta, img + kWChunkBytes<G>, (uint32_t)sizeof(WMeta<G>), &sm.wbar);
   }
   if (tid < G * 8 * kTiles) {
     (&sm.gamma[0][0][0])[tid] = 0;
     (&sm.pmax[0][0][0])[tid] = 0u;
   }
-  __syncthreads();
-  // W in fp32 registers first (item = (h, a, rr) -> 16 values of e), so every output
-  // column (h, a) gets its own tight fixed-point scale 2^(kWBits - e), max|W| < 2^e
-  constexpr int kItems = G * 8 * kMaxR / kThreads;  // W items per thread (upper bound)
-  float wv[kItems][16];
-  {
-    const float4* g0k = reinterpret_cast<const float4*>(seg.k_g0);  // fp32 [a][rr][c], normalised
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      const int item = tid + j * kThreads;
-      float gk[8];
-      int h = 0, a = 0, rr = 0;
-      bool live = item < G * 8 * r;
-      if (live) {
-        h = G == 1 ? 0 : item / (8 * r);  // G == 1: lets the compiler share the q loads across items
-        const int rem = item - h * 8 * r;
-        a = rem / r;
-        rr = rem - a * r;
-        live = a < i1;
-        if (live) {
-          const float4 g_lo = g0k[2 * (a * r + rr)], g_hi = g0k[2 * (a * r + rr) + 1];
-          gk[0] = g_lo.x, gk[1] = g_lo.y, gk[2] = g_lo.z, gk[3] = g_lo.w;
-          gk[4] = g_hi.x, gk[5] = g_hi.y, gk[6] = g_hi.z, gk[7] = g_hi.w;
-        }
-      }
-      if (!live) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) gk[c] = 0.f;
-      }
-      float m = 0.f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int e = ord16<BITS>(i);
-        float acc = 0.f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc = fmaf(sm.q[h][c * 16 + e], gk[c], acc);
-        wv[j][i] = acc;
-        m = fmaxf(m, fabsf(acc));
-      }
-      if (live) atomicMax(&sm.wmax[h][a][rr < pl.RK ? 0 : 1], __float_as_uint(m));
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int item = tid + j * kThreads;
-    if (item < G * 8 * r) {
-      const int h = item / (8 * r), rem = item - h * 8 * r;
-      const int a = rem / r, rr = rem - a * r;
-      const int grp = rr < pl.RK ? 0 : 1;
-      int e2;
-      frexpf(fmaxf(__uint_as_float(sm.wmax[h][a][grp]), 1e-30f), &e2);
-      const float wq = ldexpf(1.f, kWBits<BITS> - e2);
-      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-      int wsum = 0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int wint = __float2int_rn(wv[j][i] * wq);
-        wsum += wint;
-        hi[i >> 2] |= (uint32_t)((wint >> 8) & 0xFF) << (8 * (i & 3));
-        lo[i >> 2] |= (uint32_t)(wint & 0xFF) << (8 * (i & 3));
-      }
-      sm.wg.w[w_chunk(h, 0, r, rr, a)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      sm.wg.w[w_chunk(h, 1, r, rr, a)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      if (X) atomicAdd(&sm.beta[h][a][grp], X * wsum);
-    }
-  }
-  __syncthreads();
+  __syncthreads();  // barrier inits visible
+  mbar_wait(&sm.wbar, 0);
 
   int st = 0;  // running stage index
   auto release = [&](int s) {
@@ -234,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
     }
   };
 
+  stamp(1);
   // ---- phase 1: S = W . codes_k on the int8 tensor pipe --------------------------------
   constexpr int MT = 2;                   // 16-row m-tiles per warp (32 b rows)
   const int jt = warp >> 1;               // tile of this warp inside the item
@@ -258,10 +191,8 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
       int bt[2];
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        int e2;
-        frexpf(fmaxf(__uint_as_float(sm.wmax[h][2 * tid4 + j][grp]), 1e-30f), &e2);
-        cs[j] = ldexpf(kscale, e2 - kWBits<BITS>);
-        bt[j] = sm.beta[h][2 * tid4 + j][grp];
+        cs[j] = kscale * sm.wmeta.cs[h][2 * tid4 + j][grp];
+        bt[j] = sm.wmeta.beta[h][2 * tid4 + j][grp];
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -303,12 +234,14 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
             imma<SA, false>(acc_lo[mt][h], x0[2], x1[2], x0[3], x1[3], bl[h].z, bl[h].w);
           }
         }
+        if (rk0 + q0 + 4 == kGroupR) flush_group(0);  // leading bond rows carry their own W scale
       }
     }
     release(st);
-    if (ks == 0 || ks == pl.nK - 1) flush_group(ks == 0 ? 0 : 1);
   }
+  if (r > kGroupR) flush_group(1);
 
+  stamp(2);
   // ---- phase 2: softmax of the item straight from the accumulators ------------------------
   float sv[MT][G][4];
   float mh[G];
@@ -405,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
   }
   __syncthreads();  // P limbs, gamma and lsum complete
 
+  stamp(3);
   // ---- phase 3: Y = codes_v . P^T on the int8 tensor pipe ------------------------------
   // warp w owns bond rows w*rw .. w*rw+rw-1 (an m-tile = one bond row x 16 e)
   const int rw = pl.rw;
@@ -463,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
     release(st);
   }
 
+  stamp(4);
   // ---- phase 4: O = scale_v * G0v . Y on CUDA cores, reduce, write the partial ---------
   // accv[t][h]: rows e = gid (k 0,1) / gid+8 (k 2,3); cols a = 2*tid4 + (k & 1)
   float part[G][16];  // [h][c*2 + (e == gid+8)]
@@ -534,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, G == 1 ? 3 : 2) decode_attn_kernel(d
     args.part_ml[((size_t)slot_out * G + tid) * 2 + 0] = mh[tid];  // log2 domain
     args.part_ml[((size_t)slot_out * G + tid) * 2 + 1] = l;
   }
+  stamp(5);
 }
 
 }  // namespace attn

@@ -1,0 +1,143 @@
+// Prepare kernel of the fused decode attention: per segment, W = q . G0k turned into the
+// two-limb int8 B operand of the score MMAs, written as the exact shared-memory image
+// the split kernel loads with one TMA bulk copy (W depends on the segment, not on the
+// work item, so it is computed once per segment instead of once per item).
+#pragma once
+
+#include "attn_frag.cuh"
+
+namespace dq {
+namespace attn {
+
+constexpr int kPrepThreads = 256;
+constexpr int kMaxRW = 64;   // bond dimension bound of the W image
+constexpr int kGroupR = 8;   // W is quantized per column and per bond-row group: rr < 8 | rr >= 8
+
+// fixed-point precision of the two-limb (hi*256 + lo) 8-bit MMA operands; int8 codes
+// use fewer bits so the s32 accumulators cannot overflow
+template <int BITS>
+constexpr int kWBits = BITS == 8 ? 13 : 15;  // |W * 2^sW| < 2^kWBits
+
+// per-column metadata that follows the W chunks in the image
+template <int G>
+struct WMeta {
+  int beta[G][8][2];   // excess correction: kExcess * sum_k Wint[a][k] per bond-row group
+  float cs[G][8][2];   // 2^(e - kWBits): Wint -> W
+};
+
+template <int G>
+constexpr int kWChunkBytes = G * 2 * kMaxRW * 8 * 16;  // W limb chunks (bond rows >= r unused)
+template <int G>
+constexpr int kWImageBytes = kWChunkBytes<G> + (int)sizeof(WMeta<G>);
+
+// 16-byte chunk of limb `limb` of W[h][a][rr][16 e] (e in ord16 order), bank-swizzled
+__device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a) {
+  return ((h * 2 + limb) * r + rr) * 8 + (a ^ (2 * (rr & 3)));
+}
+
+template <int BITS, int G>
+__global__ void __launch_bounds__(kPrepThreads) attn_prepare_kernel(dq_attn_args args) {
+  constexpr int X = kExcess<BITS>;
+  __shared__ float q[G][128];
+  __shared__ unsigned wmax[G][8][2];
+  __shared__ WMeta<G> meta;
+  // the dependent split kernel may start its prologue (barriers, code TMA) right away
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const int s = blockIdx.x;
+  const dq_segment seg = args.segs[s];
+  const int r = seg.r, i1 = seg.i1;
+  const int tid = threadIdx.x;
+  unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
+  uint4* wout = reinterpret_cast<uint4*>(img);
+
+  // issue every global load (q and this thread's G0k rows) before the first barrier
+  constexpr int kItems = G * 8 * kMaxRW / kPrepThreads;
+  const float4* g0k = reinterpret_cast<const float4*>(seg.k_g0);  // fp32 [a][rr][c], normalised
+  float gk[kItems][8];
+  int ih[kItems], ia[kItems], irr[kItems];
+  bool ilive[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int item = tid + j * kPrepThreads;
+    int h = 0, a = 0, rr = 0;
+    bool live = item < G * 8 * r;
+    if (live) {
+      h = G == 1 ? 0 : item / (8 * r);
+      const int rem = item - h * 8 * r;
+      a = rem / r;
+      rr = rem - a * r;
+      live = a < i1;
+    }
+    ih[j] = h, ia[j] = a, irr[j] = rr, ilive[j] = live;
+    float4 g_lo = make_float4(0.f, 0.f, 0.f, 0.f), g_hi = g_lo;
+    if (live) {
+      g_lo = g0k[2 * (a * r + rr)];
+      g_hi = g0k[2 * (a * r + rr) + 1];
+    }
+    gk[j][0] = g_lo.x, gk[j][1] = g_lo.y, gk[j][2] = g_lo.z, gk[j][3] = g_lo.w;
+    gk[j][4] = g_hi.x, gk[j][5] = g_hi.y, gk[j][6] = g_hi.z, gk[j][7] = g_hi.w;
+  }
+  const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)seg.unit * G * 128;
+  for (int i = tid; i < G * 128; i += kPrepThreads) q[i / 128][i % 128] = __half2float(qh[i]);
+  if (tid < G * 16) {
+    (&meta.beta[0][0][0])[tid] = 0;
+    (&wmax[0][0][0])[tid] = 0u;
+  }
+  __syncthreads();
+  // W in fp32 registers first (item = (h, a, rr) -> 16 values of e), so every column and
+  // bond-row group gets its own tight fixed-point scale 2^(kWBits - e), max|W| < 2^e
+  float wv[kItems][16];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int h = ih[j], a = ia[j], rr = irr[j];
+    const bool live = ilive[j];
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int e = ord16<BITS>(i);
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc = fmaf(q[h][c * 16 + e], gk[j][c], acc);
+      wv[j][i] = acc;
+      m = fmaxf(m, fabsf(acc));
+    }
+    if (live) atomicMax(&wmax[h][a][rr < kGroupR ? 0 : 1], __float_as_uint(m));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int item = tid + j * kPrepThreads;
+    if (item < G * 8 * r) {
+      const int h = item / (8 * r), rem = item - h * 8 * r;
+      const int a = rem / r, rr = rem - a * r;
+      const int grp = rr < kGroupR ? 0 : 1;
+      int e2;
+      frexpf(fmaxf(__uint_as_float(wmax[h][a][grp]), 1e-30f), &e2);
+      const float wq = ldexpf(1.f, kWBits<BITS> - e2);
+      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+      int wsum = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int wint = __float2int_rn(wv[j][i] * wq);
+        wsum += wint;
+        hi[i >> 2] |= (uint32_t)((wint >> 8) & 0xFF) << (8 * (i & 3));
+        lo[i >> 2] |= (uint32_t)(wint & 0xFF) << (8 * (i & 3));
+      }
+      wout[w_chunk(h, 0, r, rr, a)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      wout[w_chunk(h, 1, r, rr, a)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
+    }
+  }
+  __syncthreads();
+  if (tid < G * 16) {
+    int e2;
+    frexpf(fmaxf(__uint_as_float((&wmax[0][0][0])[tid]), 1e-30f), &e2);
+    (&meta.cs[0][0][0])[tid] = ldexpf(1.f, e2 - kWBits<BITS>);
+  }
+  __syncthreads();
+  int* mout = reinterpret_cast<int*>(img + kWChunkBytes<G>);
+  for (int i = tid; i < (int)(sizeof(WMeta<G>) / 4); i += kPrepThreads) mout[i] = reinterpret_cast<int*>(&meta)[i];
+}
+
+}  // namespace attn
+}  // namespace dq

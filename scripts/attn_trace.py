@@ -1,0 +1,44 @@
+#!/usr/bin/env python
+"""Per-work-item phase timeline of the fused attention kernel (globaltimer stamps), C2 shapes."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2405_12591_b200 import _lib  # noqa: E402
+from paper_2405_12591_b200.attention import DecodeKvCache  # noqa: E402
+
+units, T = int(os.environ.get("UNITS", 512)), int(os.environ.get("T", 4096))
+cache = DecodeKvCache(layers=1, units=units, g=1, bits=4)
+k = torch.randn((units, T, 128), device="cuda").half()
+cache.prefill(0, k, k)
+del k
+q = torch.randn((units, 1, 128), device="cuda").half()
+out = torch.empty_like(q)
+cache.attend(0, q, out)
+a = cache._layers[0].args
+trace = torch.zeros((a.nwork, 8), dtype=torch.int64, device="cuda")
+a.trace = trace.data_ptr()
+for _ in range(3):
+    cache.launch(0, q, out, phases=1)
+torch.cuda.synchronize()
+t = trace.cpu().numpy().astype(np.float64)
+t0 = t[:, 0].min()
+ph = np.diff(t[:, :6], axis=1) / 1e3  # us
+names = ["prologue+W", "K stages", "softmax", "V stages", "epilogue"]
+print(f"items {a.nwork}, kernel span {(t[:, 5].max() - t0) / 1e3:.1f} us")
+for i, n in enumerate(names):
+    print(f"  {n:11s} mean {ph[:, i].mean():6.2f} us  p50 {np.median(ph[:, i]):6.2f}  p90 {np.percentile(ph[:, i], 90):6.2f}")
+life = (t[:, 5] - t[:, 0]) / 1e3
+print(f"  item life  mean {life.mean():6.2f} us  min {life.min():6.2f}  max {life.max():6.2f}")
+starts = np.sort((t[:, 0] - t0) / 1e3)
+print("  start-time quantiles (us):", np.round(np.percentile(starts, [0, 25, 50, 75, 90, 100]), 1))
+ends = np.sort((t[:, 5] - t0) / 1e3)
+print("  end-time quantiles (us):  ", np.round(np.percentile(ends, [0, 25, 50, 75, 90, 100]), 1))
+# concurrency over time
+grid = np.linspace(0, ends[-1], 40)
+conc = [int(((t[:, 0] - t0) / 1e3 <= x).sum() - ((t[:, 5] - t0) / 1e3 <= x).sum()) for x in grid]
+print("  resident items over time:", conc)
