@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunk-b", type=int, default=256)
+    ap.add_argument("--ctas", type=int, default=None,
+                    help="split-kernel grid: default persistent (resident CTAs), 0 = one CTA per 256-row slice")
     ap.add_argument("--layers", type=int, default=None, help="override layer count (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -257,7 +259,8 @@ def run_ours(args, cfg):
     units = global_batch * local_heads  # (sequence, local kv head) pairs on this rank
     chunk_len = 1024
 
-    cache = DecodeKvCache(layers=layers, units=units, g=g, bits=bits, chunk_len=chunk_len, chunk_b=args.chunk_b)
+    cache = DecodeKvCache(layers=layers, units=units, g=g, bits=bits, chunk_len=chunk_len, chunk_b=args.chunk_b,
+                          ctas=args.ctas)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
 
@@ -384,6 +387,7 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
                    "kv_bits": bits, "layers": layers, "kv_heads": kv_heads, "g": g,
                    "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": args.chunk_b,
+                   "split_ctas": cache.ctas,
                    "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB streamed per step per GPU"},
         "hbm_gbs_step": step_bytes / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

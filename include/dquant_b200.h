@@ -155,7 +155,7 @@ typedef struct dq_segment {
   const uint8_t* k_codes; /* DQ_LAYOUT_KTILE */
   const uint8_t* v_codes; /* DQ_LAYOUT_VTILE */
   const float* k_g0;      /* fp32 [i1][r][8]  (dq_core0_relayout, normalised): score side */
-  const uint16_t* v_g0;   /* fp16 [i1][r][8]  (dq_core0_relayout, normalised): output side */
+  const float* v_g0;      /* fp32 [i1][r][8]  (dq_core0_relayout, normalised): output side */
   float k_scale, v_scale; /* quantizer scale times the G0 normalisation factor */
   int32_t T;          /* tokens in the segment */
   int32_t i1, i2, r;  /* plan of (T,128) */
@@ -177,19 +177,20 @@ typedef struct dq_attn_args {
   const uint16_t* tail_v;
   const int32_t* tail_len; /* device [units] */
   int32_t tail_cap;
-  int32_t chunk_b;        /* b rows per split work item (multiple of 64) */
+  int32_t chunk_b;        /* max b rows per work item (sub-item) of the split kernel: 256 */
   float sm_scale;         /* softmax scale, 1/sqrt(128) for the reference scores */
   /* work list (built by dq_attention_plan) */
-  const int32_t* work;    /* device int32 [nwork][2] = (segment, b0) */
+  const int32_t* work;    /* device int32 [nwork][3] = (segment, b0, 64-row tiles) */
   int32_t nwork;
   int32_t max_parts;      /* partial slots per unit (>= work items of any unit + 1) */
   const int32_t* unit_part0; /* device [units]: first partial slot of each unit */
   const int32_t* work_part;  /* device [nwork]: partial slot of each work item */
   const int32_t* unit_nparts;/* device [units] */
+  int32_t* sched;            /* device [2] scheduler counters, zero before the first launch (self-resetting) */
   float* part_o;          /* workspace [total_parts][g][128] f32 */
   float* part_ml;         /* workspace [total_parts][g][2]   f32 (max, sum) */
   int32_t phases;         /* bit 0: split kernel, bit 1: combine kernel, bit 2: prepare kernel; 0: all */
-  int32_t pad_;
+  int32_t nctas;          /* persistent split-kernel CTAs (dq_attention_ctas); <= 0 or >= nwork: one per item */
   int64_t* trace;         /* optional (profiling): [nwork][8] global-timer stamps per work item */
   void* wimg;             /* workspace [nseg][wimg_stride]: per-segment W images (prepare kernel) */
   int64_t wimg_stride;    /* >= dq_attention_wimg_bytes(g) */
@@ -198,10 +199,15 @@ typedef struct dq_attn_args {
 /* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */
 int dq_attention_wimg_bytes(int32_t g, int64_t* h_bytes);
 
-/* host helper: fill work/partial tables (host arrays) for a host copy of the segment table */
-int dq_attention_plan(const dq_segment* h_segs, int32_t nseg, int32_t units, int32_t chunk_b, int32_t* h_work,
-                      int32_t* h_nwork, int32_t* h_work_part, int32_t* h_unit_part0, int32_t* h_unit_nparts,
-                      int32_t* h_total_parts);
+/* resident split-kernel CTAs on the current device (SMs x CTAs per SM): the persistent grid */
+int dq_attention_ctas(int32_t g, int32_t bits, int32_t* h_ctas);
+
+/* host helper: fill the work/partial tables (host arrays) for a host copy of the segment
+ * table: every segment is cut into ceil(tiles / (chunk_b / 64)) near-equal work items of
+ * 64-row b tiles.  h_work [max_work][3] may be null (count only). */
+int dq_attention_plan(const dq_segment* h_segs, int32_t nseg, int32_t units, int32_t chunk_b, int32_t max_work,
+                      int32_t* h_work, int32_t* h_nwork, int32_t* h_work_part, int32_t* h_unit_part0,
+                      int32_t* h_unit_nparts, int32_t* h_total_parts);
 int dq_decode_attention(const dq_attn_args* h_args, void* stream);
 
 /* append one token row per unit into the fp16 tail (kvcache.py:116-123) */

@@ -84,10 +84,11 @@ class AttnArgs(ctypes.Structure):
         ("unit_part0", c_void_p),
         ("work_part", c_void_p),
         ("unit_nparts", c_void_p),
+        ("sched", c_void_p),
         ("part_o", c_void_p),
         ("part_ml", c_void_p),
         ("phases", c_int32),
-        ("pad_", c_int32),
+        ("nctas", c_int32),
         ("trace", c_void_p),
         ("wimg", c_void_p),
         ("wimg_stride", c_int64),
@@ -123,8 +124,10 @@ SIGNATURES = {
                                     c_int32, c_void_p, c_void_p]),
     "dq_fused_matmul": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_int64, c_int64,
                                   c_int32, c_void_p, c_void_p]),
-    "dq_attention_plan": (c_int32, [POINTER(Segment), c_int32, c_int32, c_int32, POINTER(c_int32), POINTER(c_int32),
-                                    POINTER(c_int32), POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
+    "dq_attention_plan": (c_int32, [POINTER(Segment), c_int32, c_int32, c_int32, c_int32, POINTER(c_int32),
+                                    POINTER(c_int32), POINTER(c_int32), POINTER(c_int32), POINTER(c_int32),
+                                    POINTER(c_int32)]),
+    "dq_attention_ctas": (c_int32, [c_int32, c_int32, POINTER(c_int32)]),
     "dq_decode_attention": (c_int32, [POINTER(AttnArgs), c_void_p]),
     "dq_attention_wimg_bytes": (c_int32, [c_int32, POINTER(c_int64)]),
     "dq_tail_append": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),

@@ -101,6 +101,33 @@ def compress_blocks(blocks: torch.Tensor, bits: int, layout: int, g0_dtype=torch
     return payload, core0, g0, norm, scale, p
 
 
+@dataclass
+class WorkPlan:
+    """Host result of dq_attention_plan."""
+
+    nwork: int
+    total_parts: int
+    work: list          # [nwork * 3] = (segment, b0, tiles)
+    work_part: list     # [nwork]
+    unit_part0: list    # [units]
+    unit_nparts: list   # [units]
+
+
+def plan_work(seg_arr, nseg: int, units: int, chunk_b: int) -> WorkPlan:
+    """Split-kernel work list for a host segment table (dq_attention_plan)."""
+    nwork, total = ctypes.c_int32(), ctypes.c_int32()
+    p0 = (ctypes.c_int32 * max(units, 1))()
+    npt = (ctypes.c_int32 * max(units, 1))()
+    check(lib().dq_attention_plan(seg_arr, nseg, units, chunk_b, 0, None, ctypes.byref(nwork), None, p0, npt,
+                                  ctypes.byref(total)), "attention_plan")
+    n = nwork.value
+    work = (ctypes.c_int32 * max(3 * n, 3))()
+    wpart = (ctypes.c_int32 * max(n, 1))()
+    check(lib().dq_attention_plan(seg_arr, nseg, units, chunk_b, n, work, ctypes.byref(nwork), wpart, p0, npt,
+                                  ctypes.byref(total)), "attention_plan")
+    return WorkPlan(n, total.value, list(work)[:3 * n], list(wpart)[:n], list(p0)[:units], list(npt)[:units])
+
+
 class DecodeKvCache:
     """Device DecoQuant KV cache for ``layers`` x ``units`` with fused decode attention.
 
@@ -108,7 +135,8 @@ class DecodeKvCache:
     """
 
     def __init__(self, layers: int, units: int, g: int = 1, bits: int = 4, chunk_len: int = 1024,
-                 dim: int = HEAD_DIM, chunk_b: int = DEFAULT_CHUNK_B, sm_scale: float | None = None):
+                 dim: int = HEAD_DIM, chunk_b: int = DEFAULT_CHUNK_B, sm_scale: float | None = None,
+                 ctas: int | None = None):
         if dim != HEAD_DIM:
             raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
         if g not in SUPPORTED_G:
@@ -122,6 +150,9 @@ class DecodeKvCache:
         self.device = _lib.require_cuda()
         self.layers, self.units, self.g, self.bits = layers, units, g, bits
         self.chunk_len, self.dim, self.chunk_b = chunk_len, dim, chunk_b
+        # split-kernel grid: None = persistent (resident CTAs of this device), 0 = one CTA
+        # per work item, k > 0 = k persistent CTAs
+        self.ctas = ctas
         self.sm_scale = float(sm_scale) if sm_scale is not None else float(1.0 / math.sqrt(dim))
         self._layers = [_Layer() for _ in range(layers)]
         shape = (layers, units, chunk_len, dim)
@@ -205,25 +236,24 @@ class DecodeKvCache:
         nseg = len(segs)
         seg_arr = (_lib.Segment * max(nseg, 1))(*segs)
         # work plan (host) -> device tables
-        max_work = sum(-(-grp.plan.i2 // self.chunk_b) for grp in lay.groups) * self.units
-        work = (ctypes.c_int32 * max(2 * max_work, 2))()
-        work_part = (ctypes.c_int32 * max(max_work, 1))()
-        unit_part0 = (ctypes.c_int32 * self.units)()
-        unit_nparts = (ctypes.c_int32 * self.units)()
-        nwork, total = ctypes.c_int32(), ctypes.c_int32()
-        check(lib().dq_attention_plan(seg_arr, nseg, self.units, self.chunk_b, work, ctypes.byref(nwork), work_part,
-                                      unit_part0, unit_nparts, ctypes.byref(total)), "attention_plan")
+        if self.ctas is None:
+            c = ctypes.c_int32()
+            check(lib().dq_attention_ctas(self.g, self.bits, ctypes.byref(c)), "attention_ctas")
+            self.ctas = c.value
+        wp = plan_work(seg_arr, nseg, self.units, self.chunk_b)
         dev = self.device
 
         def i32(arr, n):
             return torch.tensor(list(arr)[:n], dtype=torch.int32).to(dev)
 
         seg_dev = torch.frombuffer(bytearray(bytes(seg_arr)), dtype=torch.uint8).to(dev)
-        work_dev = i32(work, 2 * nwork.value)
-        wpart_dev = i32(work_part, nwork.value)
-        p0_dev = i32(unit_part0, self.units)
-        np_dev = i32(unit_nparts, self.units)
-        tp = max(total.value, 1)
+        nwork = wp.nwork
+        work_dev = i32(wp.work, 3 * nwork)
+        wpart_dev = i32(wp.work_part, nwork)
+        sched = torch.zeros(2, dtype=torch.int32, device=dev)
+        p0_dev = i32(wp.unit_part0, self.units)
+        np_dev = i32(wp.unit_nparts, self.units)
+        tp = max(wp.total_parts, 1)
         part_o = torch.empty((tp, self.g, self.dim), dtype=torch.float32, device=dev)
         part_ml = torch.empty((tp, self.g, 2), dtype=torch.float32, device=dev)
         a = _lib.AttnArgs()
@@ -238,11 +268,13 @@ class DecodeKvCache:
         a.tail_cap = self.chunk_len
         a.chunk_b = self.chunk_b
         a.sm_scale = self.sm_scale
-        a.work = work_dev.data_ptr() if nwork.value else None
-        a.nwork = nwork.value
+        a.work = work_dev.data_ptr() if nwork else None
+        a.nwork = nwork
+        a.sched = sched.data_ptr()
+        a.nctas = self.ctas
         a.max_parts = tp
         a.unit_part0 = p0_dev.data_ptr()
-        a.work_part = wpart_dev.data_ptr() if nwork.value else None
+        a.work_part = wpart_dev.data_ptr() if nwork else None
         a.unit_nparts = np_dev.data_ptr()
         a.part_o = part_o.data_ptr()
         a.part_ml = part_ml.data_ptr()
@@ -252,7 +284,7 @@ class DecodeKvCache:
         a.wimg = wimg.data_ptr()
         a.wimg_stride = wib.value
         lay.args = a
-        lay.keep = [seg_dev, work_dev, wpart_dev, p0_dev, np_dev, part_o, part_ml, wimg]
+        lay.keep = [seg_dev, work_dev, wpart_dev, sched, p0_dev, np_dev, part_o, part_ml, wimg]
 
     def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """q: (units, g, 128) fp16 CUDA -> (units, g, 128) fp16."""

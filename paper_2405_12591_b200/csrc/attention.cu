@@ -13,11 +13,12 @@
 //   Y[h,a,r,e] = sum_b P[h,a,b] code_v[r,b,e]                  (int8 tensor cores)
 //   O[h,c,e]   = scale_v * sum_{a,r} G0v[a,c,r] Y[h,a,r,e]     (CUDA cores, epilogue)
 //
-// Data movement: one work item = (segment, 256-row slice of b) = one CTA.  Its packed
-// K codes (DQ_LAYOUT_KTILE) and V codes (DQ_LAYOUT_VTILE) stream through a 3-stage x
+// Data movement: a persistent grid of (SMs x resident CTAs) CTAs draws work items
+// (<= 256 rows of one segment, dq_attention_plan; one partial each) from a ticket
+// counter (attn_kernel.cuh).  The packed K codes (DQ_LAYOUT_KTILE) and V codes (DQ_LAYOUT_VTILE) stream through a 3-stage x
 // 16 KB shared-memory ring by cp.async.bulk (TMA bulk copies completing on mbarriers);
-// the last warp to release a stage issues its refill (3 CTAs/SM -> 144 KB in flight per
-// SM, no register cost).  Consumers read bank-conflict-free fragments (K tile rows are
+// the last warp to release a stage issues its refill, across sub-item boundaries (3
+// CTAs/SM -> 144 KB in flight per SM, no register cost).  Consumers read bank-conflict-free fragments (K tile rows are
 // XOR-swizzled by r in HBM) and widen codes to bytes (int4: one AND per 4 even codes,
 // one SHF+AND per 4 odd codes).  The codes multiply fixed-point W and P split into two
 // 8-bit limbs (hi*256 + lo) on the int8 tensor pipe (mma.sync m16n8k32, exact s32
@@ -25,6 +26,9 @@
 // index is permuted identically on both operands, which is free.  Full-precision K/V
 // never exist anywhere.
 #include "attn_kernel.cuh"
+
+#include <algorithm>
+#include <vector>
 
 namespace dq {
 
@@ -111,15 +115,33 @@ __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __ha
 
 
 template <int BITS, int G>
-int launch_attn(const dq_attn_args& a, cudaStream_t s) {
-  const size_t smem = sizeof(AttnSmem<G>);
+int set_attrs() {
   static bool attr = false;
   if (!attr) {
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+    const int smem = (int)sizeof(AttnSmem<G>);
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      100));
     attr = true;
+  }
+  return DQ_OK;
+}
+
+template <int BITS, int G>
+int occupancy(int* per_sm) {
+  const int rc = set_attrs<BITS, G>();
+  if (rc != DQ_OK) return rc;
+  DQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, decode_attn_kernel<BITS, G>, kCtaThreads,
+                                                            sizeof(AttnSmem<G>)));
+  return DQ_OK;
+}
+
+template <int BITS, int G>
+int launch_attn(const dq_attn_args& a, cudaStream_t s) {
+  const size_t smem = sizeof(AttnSmem<G>);
+  {
+    const int rc = set_attrs<BITS, G>();
+    if (rc != DQ_OK) return rc;
   }
   const int phases = a.phases ? a.phases : 7;
   if (a.nwork > 0 && (phases & 5)) {
@@ -133,8 +155,8 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     // programmatic dependent launch: the split kernel's prologue and first code copies
     // overlap the prepare kernel; it waits (griddepcontrol.wait) only for the W images
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)a.nwork);
-    cfg.blockDim = dim3(kThreads);
+    cfg.gridDim = dim3((unsigned)(a.nctas > 0 && a.nctas < a.nwork ? a.nctas : a.nwork));
+    cfg.blockDim = dim3(kCtaThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr_pdl[1];
@@ -169,24 +191,32 @@ int dispatch_g(const dq_attn_args& a, cudaStream_t s) {
 
 using namespace dq;
 
-extern "C" int dq_attention_plan(const dq_segment* segs, int32_t nseg, int32_t units, int32_t chunk_b, int32_t* work,
-                                 int32_t* nwork, int32_t* work_part, int32_t* unit_part0, int32_t* unit_nparts,
-                                 int32_t* total_parts) {
-  if (nseg < 0 || units < 0 || chunk_b <= 0 || chunk_b % 64) return fail(DQ_ERR_INVALID_ARG, "bad plan arguments");
+extern "C" int dq_attention_plan(const dq_segment* segs, int32_t nseg, int32_t units, int32_t chunk_b, int32_t max_work,
+                                 int32_t* work, int32_t* nwork, int32_t* work_part, int32_t* unit_part0,
+                                 int32_t* unit_nparts, int32_t* total_parts) {
+  if (nseg < 0 || units < 0 || chunk_b <= 0 || chunk_b % kI2Pad) return fail(DQ_ERR_INVALID_ARG, "bad plan arguments");
   if (!nwork || !total_parts || !unit_part0 || !unit_nparts) return fail(DQ_ERR_INVALID_ARG, "null output");
+  const int maxt = chunk_b / kI2Pad;
   for (int u = 0; u < units; ++u) unit_nparts[u] = 0;
   int n = 0;
   for (int s = 0; s < nseg; ++s) {
     const dq_segment& g = segs[s];
     if (g.unit < 0 || g.unit >= units) return fail(DQ_ERR_INVALID_ARG, "segment %d has unit %d", s, g.unit);
-    if (g.r > kMaxR || g.r % 8 || g.i1 > 8 || g.i2p % kI2Pad) return fail(DQ_ERR_UNSUPPORTED, "segment %d plan unsupported", s);
-    for (int b0 = 0; b0 < g.i2; b0 += chunk_b) {
+    if (g.r > kMaxR || g.r % 8 || g.i1 > 8 || g.i2p % kI2Pad || g.i2p < g.i2)
+      return fail(DQ_ERR_UNSUPPORTED, "segment %d plan unsupported", s);
+    // ceil(tiles / maxt) near-equal items per segment
+    const int nt = (g.i2 + kI2Pad - 1) / kI2Pad, k = (nt + maxt - 1) / maxt;
+    for (int i = 0, t = 0; i < k; ++i) {
+      const int len = nt / k + (i < nt % k ? 1 : 0);
       if (work) {
-        work[2 * n] = s;
-        work[2 * n + 1] = b0;
+        if (n >= max_work) return fail(DQ_ERR_INVALID_ARG, "work list exceeds max_work = %d", max_work);
+        work[3 * n] = s;
+        work[3 * n + 1] = t * kI2Pad;
+        work[3 * n + 2] = len;
       }
       unit_nparts[g.unit]++;
       ++n;
+      t += len;
     }
   }
   int acc = 0;
@@ -194,15 +224,33 @@ extern "C" int dq_attention_plan(const dq_segment* segs, int32_t nseg, int32_t u
     unit_part0[u] = acc;
     acc += unit_nparts[u];
   }
-  if (work_part) {
-    // second pass assigns slots in work-list order
-    int* cursor = new int[units > 0 ? units : 1];
-    for (int u = 0; u < units; ++u) cursor[u] = unit_part0[u];
-    for (int i = 0; i < n; ++i) work_part[i] = cursor[segs[work[2 * i]].unit]++;
-    delete[] cursor;
+  if (work && work_part) {
+    // partial slots per unit, in work-list order
+    std::vector<int> cursor(unit_part0, unit_part0 + units);
+    for (int i = 0; i < n; ++i) work_part[i] = cursor[segs[work[3 * i]].unit]++;
   }
   *nwork = n;
   *total_parts = acc;
+  return DQ_OK;
+}
+
+extern "C" int dq_attention_ctas(int32_t g, int32_t bits, int32_t* ctas) {
+  if (!ctas) return fail(DQ_ERR_INVALID_ARG, "null output");
+  int dev = 0, sms = 0, per_sm = 0;
+  DQ_CUDA_TRY(cudaGetDevice(&dev));
+  DQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int rc = DQ_OK;
+  switch (bits * 16 + g) {
+    case 2 * 16 + 1: rc = occupancy<2, 1>(&per_sm); break;
+    case 2 * 16 + 2: rc = occupancy<2, 2>(&per_sm); break;
+    case 4 * 16 + 1: rc = occupancy<4, 1>(&per_sm); break;
+    case 4 * 16 + 2: rc = occupancy<4, 2>(&per_sm); break;
+    case 8 * 16 + 1: rc = occupancy<8, 1>(&per_sm); break;
+    case 8 * 16 + 2: rc = occupancy<8, 2>(&per_sm); break;
+    default: return fail(DQ_ERR_UNSUPPORTED, "no split kernel for bits %d, g %d", bits, g);
+  }
+  if (rc != DQ_OK) return rc;
+  *ctas = sms * per_sm;
   return DQ_OK;
 }
 
@@ -218,7 +266,8 @@ extern "C" int dq_decode_attention(const dq_attn_args* h, void* stream) {
   if (!h) return fail(DQ_ERR_INVALID_ARG, "null args");
   const dq_attn_args& a = *h;
   if (a.units <= 0) return DQ_OK;
-  if (!a.q || !a.out || (a.nwork > 0 && (!a.segs || !a.work || !a.work_part || !a.part_o || !a.part_ml)))
+  if (!a.q || !a.out ||
+      (a.nwork > 0 && (!a.segs || !a.work || !a.work_part || !a.sched || !a.part_o || !a.part_ml)))
     return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: null pointer");
   if (!a.unit_part0 || !a.unit_nparts) return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: missing unit tables");
   cudaStream_t s = (cudaStream_t)stream;

@@ -75,12 +75,16 @@ def test_make_plan2_and_layout_bytes(L):
         L.layout_bytes(L.plan2(64, 128), 3, 0)
 
 
-def test_attention_work_plan(L):
-    """dq_attention_plan (host): every b row of every segment is covered exactly once."""
+@pytest.mark.parametrize("chunk_b", [64, 128, 256])
+def test_attention_work_plan(L, chunk_b):
+    """dq_attention_plan (host): every 64-row tile of every segment is covered exactly once by
+    items of <= chunk_b rows inside one segment; partial slots are grouped per unit."""
+    from paper_2405_12591_b200.attention import plan_work
+
     segs = []
     units = 3
     for u in range(units):
-        for T in (4096, 1024, 1009):
+        for T in (4096, 1024, 1009, 8):
             p = L.plan2(T, 128)
             s = L.Segment()
             s.T, s.i1, s.i2, s.r = T, p.i1, p.i2, p.r
@@ -88,29 +92,24 @@ def test_attention_work_plan(L):
             s.unit = u
             segs.append(s)
     arr = (L.Segment * len(segs))(*segs)
-    work = (ctypes.c_int32 * 1000)()
-    wpart = (ctypes.c_int32 * 500)()
-    p0 = (ctypes.c_int32 * units)()
-    npt = (ctypes.c_int32 * units)()
-    nwork, total = ctypes.c_int32(), ctypes.c_int32()
-    L.check(L.lib().dq_attention_plan(arr, len(segs), units, 256, work, ctypes.byref(nwork), wpart, p0, npt,
-                                      ctypes.byref(total)))
+    wp = plan_work(arr, len(segs), units, chunk_b)
     covered = {}
-    for i in range(nwork.value):
-        s, b0 = work[2 * i], work[2 * i + 1]
-        covered.setdefault(s, []).append(b0)
+    for i in range(wp.nwork):
+        s, b0, nt = wp.work[3 * i: 3 * i + 3]
+        assert b0 % 64 == 0 and 1 <= nt <= chunk_b // 64
+        covered.setdefault(s, []).extend(range(b0 // 64, b0 // 64 + nt))
     for s, seg in enumerate(segs):
-        assert sorted(covered[s]) == list(range(0, seg.i2, 256))
-    assert total.value == nwork.value
-    # partial slots are a permutation, grouped per unit
-    slots = sorted(wpart[i] for i in range(nwork.value))
-    assert slots == list(range(total.value))
-    for i in range(nwork.value):
-        u = segs[work[2 * i]].unit
-        assert p0[u] <= wpart[i] < p0[u] + npt[u]
-    bad = (ctypes.c_int32 * units)()
-    assert L.lib().dq_attention_plan(arr, len(segs), units, 100, work, ctypes.byref(nwork), wpart, p0, bad,
-                                     ctypes.byref(total)) != 0
+        tiles = -(-seg.i2 // 64)
+        assert sorted(covered[s]) == list(range(tiles))
+        sizes = [wp.work[3 * i + 2] for i in range(wp.nwork) if wp.work[3 * i] == s]
+        assert len(sizes) == -(-tiles // (chunk_b // 64)) and max(sizes) - min(sizes) <= 1
+    assert wp.total_parts == wp.nwork
+    assert sorted(wp.work_part) == list(range(wp.total_parts))
+    for i in range(wp.nwork):
+        u = segs[wp.work[3 * i]].unit
+        assert wp.unit_part0[u] <= wp.work_part[i] < wp.unit_part0[u] + wp.unit_nparts[u]
+    with pytest.raises(ValueError):  # DQ_ERR_INVALID_ARG: chunk_b not a multiple of 64
+        plan_work(arr, len(segs), units, 100)
 
 
 def test_struct_layouts(L):
