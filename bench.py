@@ -288,8 +288,9 @@ def run_ours(args, cfg):
 
     def step():
         for layer in range(layers):
-            cache.attend(layer, q[layer], out[layer])
-            cache.append_token(layer, kn[layer], vn[layer])
+            # one launch sequence per layer: attention over the cache, then the new token
+            # joins the tail (append fused into the combine kernel)
+            cache.attend(layer, q[layer], out[layer], append=(kn[layer], vn[layer]))
 
     def barrier():
         if world > 1:
@@ -344,17 +345,17 @@ def run_ours(args, cfg):
     q_h = q.cpu().pin_memory()
     kn_h, vn_h = kn.cpu().pin_memory(), vn.cpu().pin_memory()
     out_h = torch.empty(q.shape, dtype=torch.float16).pin_memory()
-    q_d = torch.empty_like(q[0])
-    k_d, v_d = torch.empty_like(kn[0]), torch.empty_like(vn[0])
+    q_d, k_d, v_d, o_d = torch.empty_like(q), torch.empty_like(kn), torch.empty_like(vn), torch.empty_like(q)
 
     def e2e_step():
+        # this step's inputs host -> device (pinned, one copy per tensor), every layer through
+        # the public API, the step's outputs device -> host
+        q_d.copy_(q_h, non_blocking=True)
+        k_d.copy_(kn_h, non_blocking=True)
+        v_d.copy_(vn_h, non_blocking=True)
         for layer in range(layers):
-            q_d.copy_(q_h[layer], non_blocking=True)
-            k_d.copy_(kn_h[layer], non_blocking=True)
-            v_d.copy_(vn_h[layer], non_blocking=True)
-            o = cache.attend(layer, q_d)
-            cache.append_token(layer, k_d, v_d)
-            out_h[layer].copy_(o, non_blocking=True)
+            cache.attend(layer, q_d[layer], o_d[layer], append=(k_d[layer], v_d[layer]))
+        out_h.copy_(o_d, non_blocking=True)
 
     e2e_steps = max(3, args.steps // 2)
     for _ in range(max(3, args.warmup // 2)):
@@ -398,7 +399,7 @@ def run_ours(args, cfg):
                        "blocks_per_s": 2 * units * layers / write_s},
         "e2e": {"value": global_batch / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "gpu_launches": args.steps * layers * 4,  # per layer: prepare, split, combine, tail append
+        "gpu_launches": args.steps * layers * 3,  # per layer: prepare, split, combine (+ fused tail append)
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -173,9 +173,9 @@ typedef struct dq_attn_args {
   int32_t units;
   int32_t g;              /* query heads per kv head (1..8) */
   int32_t bits;           /* 2, 4 or 8 */
-  const uint16_t* tail_k; /* fp16 [units][tail_cap][128] (may be null if tail_len==0) */
-  const uint16_t* tail_v;
-  const int32_t* tail_len; /* device [units] */
+  uint16_t* tail_k;       /* fp16 [units][tail_cap][128] (may be null if tail_len==0 and no append) */
+  uint16_t* tail_v;
+  int32_t* tail_len;      /* device [units] */
   int32_t tail_cap;
   int32_t chunk_b;        /* max b rows per work item (sub-item) of the split kernel: 256 */
   float sm_scale;         /* softmax scale, 1/sqrt(128) for the reference scores */
@@ -194,6 +194,8 @@ typedef struct dq_attn_args {
   int64_t* trace;         /* optional (profiling): [nwork][8] global-timer stamps per work item */
   void* wimg;             /* workspace [nseg][wimg_stride]: per-segment W images (prepare kernel) */
   int64_t wimg_stride;    /* >= dq_attention_wimg_bytes(g) */
+  const uint16_t* app_k;  /* optional fp16 [units][128]: appended to the tail AFTER the attention */
+  const uint16_t* app_v;  /*   (the combine kernel does dq_tail_append's work; null = no append) */
 } dq_attn_args;
 
 /* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */

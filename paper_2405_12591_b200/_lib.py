@@ -92,6 +92,8 @@ class AttnArgs(ctypes.Structure):
         ("trace", c_void_p),
         ("wimg", c_void_p),
         ("wimg_stride", c_int64),
+        ("app_k", c_void_p),
+        ("app_v", c_void_p),
     ]
 
 

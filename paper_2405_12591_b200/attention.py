@@ -198,13 +198,19 @@ class DecodeKvCache:
 
     def append_token(self, layer: int, k_rows: torch.Tensor, v_rows: torch.Tensor):
         """k_rows/v_rows: (units, 128).  Seals the tail at chunk_len (kvcache.py:116-128)."""
-        lay = self._layer(layer)
-        if k_rows.shape != (self.units, self.dim) or v_rows.shape != (self.units, self.dim):
-            raise DimMismatch(f"rows must be ({self.units}, {self.dim})")
-        k = k_rows.to(self.device, torch.float16).contiguous()
-        v = v_rows.to(self.device, torch.float16).contiguous()
+        self._layer(layer)
+        k, v = self._rows(k_rows, v_rows)
         check(lib().dq_tail_append(ptr(k), ptr(v), self.units, ptr(self.tail_k[layer]), ptr(self.tail_v[layer]),
                                    ptr(self.tail_len[layer]), self.chunk_len, stream_ptr()), "tail_append")
+        self._after_append(layer)
+
+    def _rows(self, k_rows: torch.Tensor, v_rows: torch.Tensor):
+        if k_rows.shape != (self.units, self.dim) or v_rows.shape != (self.units, self.dim):
+            raise DimMismatch(f"rows must be ({self.units}, {self.dim})")
+        return (k_rows.to(self.device, torch.float16).contiguous(), v_rows.to(self.device, torch.float16).contiguous())
+
+    def _after_append(self, layer: int):
+        lay = self._layers[layer]
         lay.tail_len += 1
         if lay.tail_len == self.chunk_len:
             self._add_group(layer, self.tail_k[layer], self.tail_v[layer])
@@ -286,8 +292,13 @@ class DecodeKvCache:
         lay.args = a
         lay.keep = [seg_dev, work_dev, wpart_dev, sched, p0_dev, np_dev, part_o, part_ml, wimg]
 
-    def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """q: (units, g, 128) fp16 CUDA -> (units, g, 128) fp16."""
+    def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None,
+               append: tuple[torch.Tensor, torch.Tensor] | None = None) -> torch.Tensor:
+        """q: (units, g, 128) fp16 CUDA -> (units, g, 128) fp16.
+
+        ``append=(k_rows, v_rows)`` (each (units, 128)) fuses ``append_token`` into the same
+        launch: the rows join the tail after this attention, exactly as attend + append_token.
+        """
         lay = self._layer(layer)
         if q.shape != (self.units, self.g, self.dim):
             raise DimMismatch(f"q must be ({self.units}, {self.g}, {self.dim})")
@@ -299,8 +310,16 @@ class DecodeKvCache:
         a = lay.args
         a.q = q.data_ptr()
         a.out = out.data_ptr()
-        check(lib().dq_decode_attention(ctypes.byref(a), stream_ptr()), "decode_attention")
+        if append is not None:
+            k, v = self._rows(*append)
+            a.app_k, a.app_v = k.data_ptr(), v.data_ptr()
+        try:
+            check(lib().dq_decode_attention(ctypes.byref(a), stream_ptr()), "decode_attention")
+        finally:
+            a.app_k = a.app_v = None
         self.bytes_moved_read += self.read_bytes(layer)
+        if append is not None:
+            self._after_append(layer)
         return out
 
     def launch(self, layer: int, q: torch.Tensor, out: torch.Tensor, phases: int = 3):

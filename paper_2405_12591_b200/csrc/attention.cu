@@ -98,6 +98,16 @@ __global__ void __launch_bounds__(128) combine_kernel(dq_attn_args args) {
     __half* out = reinterpret_cast<__half*>(args.out) + ((size_t)u * G + h) * kD;
     out[d] = __float2half_rn(L > 0.f ? O / L : 0.f);
   }
+  if (args.app_k) {
+    // fused dq_tail_append: the new token joins the tail after this step's attention
+    __syncthreads();  // every thread has read tail_len[u]
+    if (tl < args.tail_cap) {
+      const size_t dst = ((size_t)u * args.tail_cap + tl) * kD + d;
+      reinterpret_cast<__half*>(args.tail_k)[dst] = reinterpret_cast<const __half*>(args.app_k)[(size_t)u * kD + d];
+      reinterpret_cast<__half*>(args.tail_v)[dst] = reinterpret_cast<const __half*>(args.app_v)[(size_t)u * kD + d];
+    }
+    if (d == 0) args.tail_len[u] = tl + 1;
+  }
 }
 
 __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __half* __restrict__ v_rows,
@@ -148,7 +158,7 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     if (!a.wimg || a.wimg_stride < kWImageBytes<G>) return fail(DQ_ERR_INVALID_ARG, "W image workspace too small");
   }
   if (a.nseg > 0 && a.nwork > 0 && (phases & 4)) {
-    attn_prepare_kernel<BITS, G><<<a.nseg, kPrepThreads, 0, s>>>(a);
+    attn_prepare_kernel<BITS, G><<<a.nseg, kPrepThreadsOf<G>, 0, s>>>(a);
     DQ_LAUNCH_CHECK();
   }
   if (a.nwork > 0 && (phases & 1)) {
@@ -270,6 +280,8 @@ extern "C" int dq_decode_attention(const dq_attn_args* h, void* stream) {
       (a.nwork > 0 && (!a.segs || !a.work || !a.work_part || !a.sched || !a.part_o || !a.part_ml)))
     return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: null pointer");
   if (!a.unit_part0 || !a.unit_nparts) return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: missing unit tables");
+  if (a.app_k && (!a.app_v || !a.tail_k || !a.tail_v || !a.tail_len || a.tail_cap <= 0))
+    return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: append needs app_v and the tail buffers");
   cudaStream_t s = (cudaStream_t)stream;
   switch (a.bits) {
     case 2: return dispatch_g<2>(a, s);

@@ -9,7 +9,6 @@
 namespace dq {
 namespace attn {
 
-constexpr int kPrepThreads = 256;
 constexpr int kMaxRW = 64;   // bond dimension bound of the W image
 constexpr int kGroupR = 8;   // W is quantized per column and per bond-row group: rr < 8 | rr >= 8
 
@@ -35,108 +34,87 @@ __device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a) {
   return ((h * 2 + limb) * r + rr) * 8 + (a ^ (2 * (rr & 3)));
 }
 
+// one CTA per segment, one thread per (h, a, rr) of W (threads beyond i1 / r idle): a
+// single wave of short-lived CTAs (the kernel is pure latency: ~16 KB in, ~16 KB out)
+template <int G>
+constexpr int kPrepThreadsOf = G * 8 * kMaxRW;
+
 template <int BITS, int G>
-__global__ void __launch_bounds__(kPrepThreads) attn_prepare_kernel(dq_attn_args args) {
+__global__ void __launch_bounds__(kPrepThreadsOf<G>) attn_prepare_kernel(dq_attn_args args) {
   constexpr int X = kExcess<BITS>;
   __shared__ float q[G][128];
   __shared__ unsigned wmax[G][8][2];
   __shared__ WMeta<G> meta;
-  // the dependent split kernel may start its prologue (barriers, code TMA) right away
+  // the dependent split kernel may start its prologue (barriers, code copies) right away
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int s = blockIdx.x;
-  const dq_segment seg = args.segs[s];
-  const int r = seg.r, i1 = seg.i1;
   const int tid = threadIdx.x;
-  unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
-  uint4* wout = reinterpret_cast<uint4*>(img);
-
-  // issue every global load (q and this thread's G0k rows) before the first barrier
-  constexpr int kItems = G * 8 * kMaxRW / kPrepThreads;
+  const int h = G == 1 ? 0 : tid / (8 * kMaxRW), a = (tid / kMaxRW) % 8, rr = tid % kMaxRW;
+  const dq_segment& seg = args.segs[s];
+  const int r = seg.r, i1 = seg.i1;
+  const bool live = a < i1 && rr < r;
+  // issue the global loads first: this thread's G0k row and (spread over threads) q
   const float4* g0k = reinterpret_cast<const float4*>(seg.k_g0);  // fp32 [a][rr][c], normalised
-  float gk[kItems][8];
-  int ih[kItems], ia[kItems], irr[kItems];
-  bool ilive[kItems];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int item = tid + j * kPrepThreads;
-    int h = 0, a = 0, rr = 0;
-    bool live = item < G * 8 * r;
-    if (live) {
-      h = G == 1 ? 0 : item / (8 * r);
-      const int rem = item - h * 8 * r;
-      a = rem / r;
-      rr = rem - a * r;
-      live = a < i1;
-    }
-    ih[j] = h, ia[j] = a, irr[j] = rr, ilive[j] = live;
-    float4 g_lo = make_float4(0.f, 0.f, 0.f, 0.f), g_hi = g_lo;
-    if (live) {
-      g_lo = g0k[2 * (a * r + rr)];
-      g_hi = g0k[2 * (a * r + rr) + 1];
-    }
-    gk[j][0] = g_lo.x, gk[j][1] = g_lo.y, gk[j][2] = g_lo.z, gk[j][3] = g_lo.w;
-    gk[j][4] = g_hi.x, gk[j][5] = g_hi.y, gk[j][6] = g_hi.z, gk[j][7] = g_hi.w;
+  float4 g_lo = make_float4(0.f, 0.f, 0.f, 0.f), g_hi = g_lo;
+  if (live) {
+    g_lo = g0k[2 * (a * r + rr)];
+    g_hi = g0k[2 * (a * r + rr) + 1];
   }
-  const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)seg.unit * G * 128;
-  for (int i = tid; i < G * 128; i += kPrepThreads) q[i / 128][i % 128] = __half2float(qh[i]);
+  if (tid < G * 128) {
+    const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)seg.unit * G * 128;
+    q[tid / 128][tid % 128] = __half2float(qh[tid]);
+  }
   if (tid < G * 16) {
     (&meta.beta[0][0][0])[tid] = 0;
     (&wmax[0][0][0])[tid] = 0u;
   }
   __syncthreads();
-  // W in fp32 registers first (item = (h, a, rr) -> 16 values of e), so every column and
-  // bond-row group gets its own tight fixed-point scale 2^(kWBits - e), max|W| < 2^e
-  float wv[kItems][16];
+  const float gk[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
+  const int grp = rr < kGroupR ? 0 : 1;
+  // W[h][a][rr][e] in fp32 (e in ord16 order), then one fixed-point scale 2^(kWBits - e2)
+  // per (h, a, bond-row group) from the exact group maximum
+  float wv[16];
+  float m = 0.f;
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int h = ih[j], a = ia[j], rr = irr[j];
-    const bool live = ilive[j];
-    float m = 0.f;
+  for (int i = 0; i < 16; ++i) {
+    const int e = ord16<BITS>(i);
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc = fmaf(q[h][c * 16 + e], gk[c], acc);
+    wv[i] = acc;
+    m = fmaxf(m, fabsf(acc));
+  }
+  if (live) atomicMax(&wmax[h][a][grp], __float_as_uint(m));
+  __syncthreads();
+  int e2;
+  frexpf(fmaxf(__uint_as_float(wmax[h][a][grp]), 1e-30f), &e2);
+  if (live) {
+    const float wq = ldexpf(1.f, kWBits<BITS> - e2);
+    uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    int wsum = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int e = ord16<BITS>(i);
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc = fmaf(q[h][c * 16 + e], gk[j][c], acc);
-      wv[j][i] = acc;
-      m = fmaxf(m, fabsf(acc));
+      const int wint = __float2int_rn(wv[i] * wq);
+      wsum += wint;
+      hi[i >> 2] |= (uint32_t)((wint >> 8) & 0xFF) << (8 * (i & 3));
+      lo[i >> 2] |= (uint32_t)(wint & 0xFF) << (8 * (i & 3));
     }
-    if (live) atomicMax(&wmax[h][a][rr < kGroupR ? 0 : 1], __float_as_uint(m));
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int item = tid + j * kPrepThreads;
-    if (item < G * 8 * r) {
-      const int h = item / (8 * r), rem = item - h * 8 * r;
-      const int a = rem / r, rr = rem - a * r;
-      const int grp = rr < kGroupR ? 0 : 1;
-      int e2;
-      frexpf(fmaxf(__uint_as_float(wmax[h][a][grp]), 1e-30f), &e2);
-      const float wq = ldexpf(1.f, kWBits<BITS> - e2);
-      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-      int wsum = 0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int wint = __float2int_rn(wv[j][i] * wq);
-        wsum += wint;
-        hi[i >> 2] |= (uint32_t)((wint >> 8) & 0xFF) << (8 * (i & 3));
-        lo[i >> 2] |= (uint32_t)(wint & 0xFF) << (8 * (i & 3));
-      }
-      wout[w_chunk(h, 0, r, rr, a)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      wout[w_chunk(h, 1, r, rr, a)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
-    }
+    unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
+    uint4* wout = reinterpret_cast<uint4*>(img);
+    wout[w_chunk(h, 0, r, rr, a)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    wout[w_chunk(h, 1, r, rr, a)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
   }
   __syncthreads();
   if (tid < G * 16) {
-    int e2;
-    frexpf(fmaxf(__uint_as_float((&wmax[0][0][0])[tid]), 1e-30f), &e2);
-    (&meta.cs[0][0][0])[tid] = ldexpf(1.f, e2 - kWBits<BITS>);
+    int ex;
+    frexpf(fmaxf(__uint_as_float((&wmax[0][0][0])[tid]), 1e-30f), &ex);
+    int* mout = reinterpret_cast<int*>(static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride +
+                                       kWChunkBytes<G>);
+    const float cs = ldexpf(1.f, ex - kWBits<BITS>);
+    mout[tid] = (&meta.beta[0][0][0])[tid];                               // beta[G][8][2]
+    mout[G * 16 + tid] = __float_as_int(cs);                               // cs[G][8][2]
   }
-  __syncthreads();
-  int* mout = reinterpret_cast<int*>(img + kWChunkBytes<G>);
-  for (int i = tid; i < (int)(sizeof(WMeta<G>) / 4); i += kPrepThreads) mout[i] = reinterpret_cast<int*>(&meta)[i];
 }
 
 }  // namespace attn

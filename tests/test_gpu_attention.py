@@ -161,6 +161,30 @@ def test_tail_only_and_empty(dq):
         assert rel(p @ v[u].astype(np.float64), out[u]) < TOL
 
 
+def test_fused_append_matches_attend_then_append(dq):
+    """attend(append=(k, v)) == attend + append_token, step by step, across a tail seal."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    units, g, chunk, P, steps = 3, 2, 64, 300, 70
+    rng = np.random.default_rng(11)
+    k = torch.from_numpy(rng.standard_normal((units, P + steps, 128)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.standard_normal((units, P + steps, 128)).astype(np.float16)).cuda()
+    q = torch.from_numpy(rng.standard_normal((steps, units, g, 128)).astype(np.float16)).cuda()
+    a = DecodeKvCache(layers=1, units=units, g=g, bits=4, chunk_len=chunk)
+    b = DecodeKvCache(layers=1, units=units, g=g, bits=4, chunk_len=chunk)
+    for c in (a, b):
+        c.prefill(0, k[:, :P], v[:, :P])
+    for t in range(steps):
+        oa = a.attend(0, q[t])
+        a.append_token(0, k[:, P + t], v[:, P + t])
+        ob = b.attend(0, q[t], append=(k[:, P + t], v[:, P + t]))
+        assert torch.equal(oa, ob), t
+        assert a.tokens(0) == b.tokens(0) == P + t + 1
+    assert len(b._layers[0].groups) == 2 and b._layers[0].tail_len == steps - chunk
+    assert torch.equal(a.tail_len, b.tail_len)
+    assert torch.equal(a.tail_k[0, :, :steps - chunk], b.tail_k[0, :, :steps - chunk])
+
+
 def test_export_segment_wire_format(dq):
     """Device layouts -> reference wire order: same bytes as deco_quantize on the same block."""
     from paper_2405_12591_b200.attention import DecodeKvCache
