@@ -71,6 +71,28 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(config: str):
+    """DRAM bytes (read + write) per split-kernel launch from the newest committed ncu --set full
+    capture (profiles/rNN_ncu_decode_attn.txt, taken on C2: scripts/profile_round.sh)."""
+    import glob
+    import re
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_decode_attn.txt")))
+    if config != "c2" or not files:
+        return None, None
+    total = 0.0
+    txt = open(files[-1]).read()
+    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        hit = re.search(m + r"\s+([0-9.]+)\s+(\w+)", txt)
+        if not hit:
+            return None, None
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(hit.group(2))
+        if scale is None:
+            return None, None
+        total += float(hit.group(1)) * scale
+    return total, os.path.relpath(files[-1], ROOT)
+
+
 # ---------------------------------------------------------------------------
 # CPU side: the oracle (reference algorithm) on host cores
 # ---------------------------------------------------------------------------
@@ -339,6 +361,7 @@ def run_ours(args, cfg):
     kern_bytes = cache.kernel_bytes(0)
     achieved = kern_bytes / (kern_ms / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
+    traffic, traffic_src = ncu_traffic(args.config)
     step_bytes = sum(cache.read_bytes(layer) for layer in range(layers))
 
     # ---- end-to-end through the public API with host buffers --------------------------
@@ -392,7 +415,8 @@ def run_ours(args, cfg):
                    "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB streamed per step per GPU"},
         "hbm_gbs_step": step_bytes / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "decode_attn_kernel", "bytes_per_launch": kern_bytes,
+                     "traffic": traffic, "traffic_source": traffic_src, "kernel": "decode_attn_kernel",
+                     "bytes_per_launch": kern_bytes,
                      "launch_ms": kern_ms, "peak_kind": peak_kind},
         "memory_per_token_vs_fp16": actual_bytes / fp16_bytes,
         "write_path": {"blocks": 2 * units * layers, "block": f"{T}x128", "seconds": write_s,

@@ -64,7 +64,7 @@ class SegmentGroup:
         return payload_size(p.r * p.i2 * p.j2, bits) + 2 + 2 * (p.i1 * p.j1 * p.r)
 
     def stream_bytes(self) -> int:
-        """Bytes K5 reads for one unit of this segment (K + V): packed cores, G0 (fp32 K, fp16 V), scales."""
+        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k and G0v, scales."""
         return (self.k_payload.shape[1] + self.v_payload.shape[1] + self.k_g0h.element_size() * self.k_g0h.shape[1]
                 + self.v_g0h.element_size() * self.v_g0h.shape[1] + 8)
 

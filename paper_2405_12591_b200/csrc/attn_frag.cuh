@@ -93,6 +93,17 @@ __device__ __forceinline__ void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint
   }
 }
 
+// 2^(k - e) and 2^(e - k) for e = frexp exponent of a non-negative float x (x = m * 2^e,
+// m in [0.5, 1)), by exponent-field arithmetic; x is clamped below to 2^-100 (0 included)
+__device__ __forceinline__ float pow2_sub_exp(float x, int k) {  // 2^(k - e)
+  const int E = max((int)((__float_as_uint(x) >> 23) & 0xFF), 27);
+  return __uint_as_float((uint32_t)(k + 253 - E) << 23);
+}
+__device__ __forceinline__ float pow2_exp_sub(float x, int k) {  // 2^(e - k)
+  const int E = max((int)((__float_as_uint(x) >> 23) & 0xFF), 27);
+  return __uint_as_float((uint32_t)(E - 126 - k + 127) << 23);
+}
+
 // ---- packed code rows -----------------------------------------------------------------
 // A row is 16 codes of one (r, b) [K side] or of one (r, e) x 16 b [V side]: 2*BITS bytes,
 // excess-coded (code + 2^(bits-1)) as the device layouts store them.

@@ -414,10 +414,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       float pq[2], pinv[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        int e2;
-        frexpf(fmaxf(__uint_as_float(sm.pmax[h][2 * tid4 + q][min(jt, kTiles - 1)]), 1e-30f), &e2);
-        pq[q] = ldexpf(1.f, kPBits<BITS> - e2);
-        pinv[q] = ldexpf(1.f, e2 - kPBits<BITS>);
+        const float pm = __uint_as_float(sm.pmax[h][2 * tid4 + q][min(jt, kTiles - 1)]);
+        pq[q] = pow2_sub_exp(pm, kPBits<BITS>);
+        pinv[q] = pow2_exp_sub(pm, kPBits<BITS>);
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -463,10 +462,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 #pragma unroll
         for (int k = 0; k < 4; ++k) accv[t][h][k] = 0.f;
     const int nV = nbt * d.nslices;
-    for (int vs = 0; vs < nV; ++vs, ++st) {
+    for (int vs = 0, btl = 0, sl = 0; vs < nV; ++vs, ++st) {
       const int slot = st % kStages;
       mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
-      const int btl = vs / d.nslices, sl = vs % d.nslices;
       if (sl == my_slice) {
         uint4 ph[G], pl_[G];
         int gam[G][2];
@@ -478,9 +476,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             gam[h][q] = sm.gamma[h][2 * tid4 + q][btl];
-            int e2;
-            frexpf(fmaxf(__uint_as_float(sm.pmax[h][2 * tid4 + q][btl]), 1e-30f), &e2);
-            pinv[h][q] = ldexpf(1.f, e2 - kPBits<BITS>);
+            pinv[h][q] = pow2_exp_sub(__uint_as_float(sm.pmax[h][2 * tid4 + q][btl]), kPBits<BITS>);
           }
         }
         const unsigned char* buf = sm.ring[slot];
@@ -507,6 +503,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         }
       }
       release(st);
+      if (++sl == d.nslices) sl = 0, ++btl;
     }
 
     stamp(4);

@@ -40,7 +40,7 @@ template <int G>
 constexpr int kPrepThreadsOf = G * 8 * kMaxRW;
 
 template <int BITS, int G>
-__global__ void __launch_bounds__(kPrepThreadsOf<G>) attn_prepare_kernel(dq_attn_args args) {
+__global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 4 : 2) attn_prepare_kernel(dq_attn_args args) {
   constexpr int X = kExcess<BITS>;
   __shared__ float q[G][128];
   __shared__ unsigned wmax[G][8][2];
@@ -86,10 +86,8 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>) attn_prepare_kernel(dq_attn
   }
   if (live) atomicMax(&wmax[h][a][grp], __float_as_uint(m));
   __syncthreads();
-  int e2;
-  frexpf(fmaxf(__uint_as_float(wmax[h][a][grp]), 1e-30f), &e2);
   if (live) {
-    const float wq = ldexpf(1.f, kWBits<BITS> - e2);
+    const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a][grp]), kWBits<BITS>);
     uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
     int wsum = 0;
 #pragma unroll
@@ -107,11 +105,10 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>) attn_prepare_kernel(dq_attn
   }
   __syncthreads();
   if (tid < G * 16) {
-    int ex;
-    frexpf(fmaxf(__uint_as_float((&wmax[0][0][0])[tid]), 1e-30f), &ex);
+
     int* mout = reinterpret_cast<int*>(static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride +
                                        kWChunkBytes<G>);
-    const float cs = ldexpf(1.f, ex - kWBits<BITS>);
+    const float cs = pow2_exp_sub(__uint_as_float((&wmax[0][0][0])[tid]), kWBits<BITS>);
     mout[tid] = (&meta.beta[0][0][0])[tid];                               // beta[G][8][2]
     mout[G * 16 + tid] = __float_as_int(cs);                               // cs[G][8][2]
   }
