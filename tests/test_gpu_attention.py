@@ -73,14 +73,15 @@ def _oracle_attend(k, v, q, bits, segs_T, tail):
     (4, 1, 1009, 2), (4, 1, 1023, 2), (4, 1, 8192, 1), (4, 1, 24, 2), (4, 1, 100, 2), (2, 1, 1009, 1),
     (8, 1, 1023, 1),
 ])
-def test_decode_attention_prefill_only(dq, bits, g, T, units):
+@pytest.mark.parametrize("ctas", [None, 0, 3])  # persistent grid / one CTA per item / 3 CTAs
+def test_decode_attention_prefill_only(dq, bits, g, T, units, ctas):
     from paper_2405_12591_b200.attention import DecodeKvCache
 
     rng = np.random.default_rng(T + 7 * g + bits)
     k = rng.standard_normal((units, T, 128)).astype(np.float16)
     v = rng.standard_normal((units, T, 128)).astype(np.float16)
     q = rng.standard_normal((units, g, 128)).astype(np.float16)
-    cache = DecodeKvCache(layers=1, units=units, g=g, bits=bits)
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=bits, ctas=ctas)
     cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
     for u in range(units):
@@ -90,7 +91,8 @@ def test_decode_attention_prefill_only(dq, bits, g, T, units):
 
 
 @pytest.mark.parametrize("scale,bits", [(20.0, 4), (50.0, 4), (20.0, 2), (20.0, 8)])
-def test_decode_attention_outlier_channels(dq, scale, bits):
+@pytest.mark.parametrize("ctas", [None, 0])  # persistent grid / one CTA per item
+def test_decode_attention_outlier_channels(dq, scale, bits, ctas):
     """Outlier key channels (LLM-like) make the softmax peaky: tolerance must still hold."""
     from paper_2405_12591_b200.attention import DecodeKvCache
 
@@ -101,7 +103,7 @@ def test_decode_attention_outlier_channels(dq, scale, bits):
     k = k.astype(np.float16)
     v = rng.standard_normal((units, T, 128)).astype(np.float16)
     q = rng.standard_normal((units, 1, 128)).astype(np.float16)
-    cache = DecodeKvCache(layers=1, units=units, g=1, bits=bits)
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=bits, ctas=ctas)
     cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
     for u in range(units):
