@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunk-b", type=int, default=256)
+    ap.add_argument("--kernel-g", type=int, default=None, help="query heads per split-kernel head group (1 or 2)")
     ap.add_argument("--ctas", type=int, default=None,
                     help="split-kernel grid: default persistent (resident CTAs), 0 = one CTA per 256-row slice")
     ap.add_argument("--layers", type=int, default=None, help="override layer count (debug only)")
@@ -282,7 +283,7 @@ def run_ours(args, cfg):
     chunk_len = 1024
 
     cache = DecodeKvCache(layers=layers, units=units, g=g, bits=bits, chunk_len=chunk_len, chunk_b=args.chunk_b,
-                          ctas=args.ctas)
+                          ctas=args.ctas, kernel_g=args.kernel_g)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
 
@@ -325,7 +326,8 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    if args.steps + args.warmup + args.steps + 2 >= chunk_len:
+    appended = args.warmup + args.steps + 1 + max(3, args.warmup // 2) + max(3, args.steps // 2)
+    if appended + 1 >= chunk_len:
         raise SystemExit("steps too large: the tail would seal a chunk inside the timed region")
 
     # ---- device-resident timed region ----------------------------------------------
@@ -368,17 +370,15 @@ def run_ours(args, cfg):
     q_h = q.cpu().pin_memory()
     kn_h, vn_h = kn.cpu().pin_memory(), vn.cpu().pin_memory()
     out_h = torch.empty(q.shape, dtype=torch.float16).pin_memory()
-    q_d, k_d, v_d, o_d = torch.empty_like(q), torch.empty_like(kn), torch.empty_like(vn), torch.empty_like(q)
+
+    # the public decode-step API: host buffers in / out, the step replayed as one CUDA graph
+    # (per-layer copies on a side stream overlap the previous layer's kernels)
+    from paper_2405_12591_b200.decode_step import DecodeStepGraph
+
+    stepper = DecodeStepGraph(cache, q_h, kn_h, vn_h, out_h)
 
     def e2e_step():
-        # this step's inputs host -> device (pinned, one copy per tensor), every layer through
-        # the public API, the step's outputs device -> host
-        q_d.copy_(q_h, non_blocking=True)
-        k_d.copy_(kn_h, non_blocking=True)
-        v_d.copy_(vn_h, non_blocking=True)
-        for layer in range(layers):
-            cache.attend(layer, q_d[layer], o_d[layer], append=(k_d[layer], v_d[layer]))
-        out_h.copy_(o_d, non_blocking=True)
+        stepper.replay()
 
     e2e_steps = max(3, args.steps // 2)
     for _ in range(max(3, args.warmup // 2)):
@@ -411,7 +411,7 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
                    "kv_bits": bits, "layers": layers, "kv_heads": kv_heads, "g": g,
                    "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": args.chunk_b,
-                   "split_ctas": cache.ctas,
+                   "split_ctas": cache.ctas, "kernel_g": cache.kernel_g, "head_groups": cache.head_groups,
                    "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB streamed per step per GPU"},
         "hbm_gbs_step": step_bytes / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

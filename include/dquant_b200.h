@@ -166,7 +166,7 @@ typedef struct dq_segment {
 } dq_segment;
 
 typedef struct dq_attn_args {
-  const uint16_t* q;      /* fp16 [units][g][128] */
+  const uint16_t* q;      /* fp16 [units][g][128] (units = virtual units, see head_groups) */
   uint16_t* out;          /* fp16 [units][g][128] */
   const dq_segment* segs; /* device array [nseg] */
   int32_t nseg;
@@ -194,8 +194,13 @@ typedef struct dq_attn_args {
   int64_t* trace;         /* optional (profiling): [nwork][8] global-timer stamps per work item */
   void* wimg;             /* workspace [nseg][wimg_stride]: per-segment W images (prepare kernel) */
   int64_t wimg_stride;    /* >= dq_attention_wimg_bytes(g) */
-  const uint16_t* app_k;  /* optional fp16 [units][128]: appended to the tail AFTER the attention */
-  const uint16_t* app_v;  /*   (the combine kernel does dq_tail_append's work; null = no append) */
+  const uint16_t* app_k;  /* optional fp16 [units / head_groups][128]: appended to the tail AFTER */
+  const uint16_t* app_v;  /*   the attention (the combine kernel does dq_tail_append's work) */
+  int32_t head_groups;    /* GQA groups wider than the kernels' g: a kv head's g_total = g * head_groups
+                             query heads run as head_groups "virtual units" u * head_groups + k (each g
+                             heads, same codes; segs/q/out/partials indexed by virtual unit, the tail and
+                             the combine grid by kv head u).  0 or 1: none */
+  int32_t pad2_;
 } dq_attn_args;
 
 /* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */

@@ -94,6 +94,8 @@ class AttnArgs(ctypes.Structure):
         ("wimg_stride", c_int64),
         ("app_k", c_void_p),
         ("app_v", c_void_p),
+        ("head_groups", c_int32),
+        ("pad2_", c_int32),
     ]
 
 

@@ -35,7 +35,8 @@ from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_
 
 HEAD_DIM = 128
 DEFAULT_CHUNK_B = 256
-SUPPORTED_G = (1, 2)
+KERNEL_G = (1, 2)   # query heads per kv head the split kernel is instantiated for
+MAX_G = 16          # wider GQA groups run as g / kernel_g head groups over the same codes
 MAX_BLOCKS_PER_CALL = 512  # bounds the K3 fp32 core1 scratch
 
 
@@ -136,11 +137,11 @@ class DecodeKvCache:
 
     def __init__(self, layers: int, units: int, g: int = 1, bits: int = 4, chunk_len: int = 1024,
                  dim: int = HEAD_DIM, chunk_b: int = DEFAULT_CHUNK_B, sm_scale: float | None = None,
-                 ctas: int | None = None):
+                 ctas: int | None = None, kernel_g: int | None = None):
         if dim != HEAD_DIM:
             raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
-        if g not in SUPPORTED_G:
-            raise Unsupported(f"the fused decode kernel supports GQA groups g in {SUPPORTED_G}")
+        if not 1 <= g <= MAX_G:
+            raise Unsupported(f"GQA groups of 1..{MAX_G} query heads per kv head are supported (got {g})")
         if chunk_b != DEFAULT_CHUNK_B:
             raise Unsupported(f"the fused decode kernel splits segments into {DEFAULT_CHUNK_B}-row work items")
         if bits not in SUPPORTED_BITS:
@@ -149,6 +150,13 @@ class DecodeKvCache:
             raise ShapeMismatch("layers, units and chunk_len must be >= 1")
         self.device = _lib.require_cuda()
         self.layers, self.units, self.g, self.bits = layers, units, g, bits
+        # the split kernel runs kernel_g heads at a time; g > 2 becomes head_groups virtual
+        # units per kv head that share its segments (their re-reads of the codes are L2 hits:
+        # the work list puts a tile range's head groups next to each other)
+        self.kernel_g = kernel_g if kernel_g is not None else (2 if g % 2 == 0 else 1)
+        if self.kernel_g not in KERNEL_G or g % self.kernel_g:
+            raise Unsupported(f"kernel_g must be in {KERNEL_G} and divide g")
+        self.head_groups = g // self.kernel_g
         self.chunk_len, self.dim, self.chunk_b = chunk_len, dim, chunk_b
         # split-kernel grid: None = persistent (resident CTAs of this device), 0 = one CTA
         # per work item, k > 0 = k persistent CTAs
@@ -223,30 +231,37 @@ class DecodeKvCache:
         segs = []
         # the kernel sees g0h = core0 / norm, so the per-segment scale carries the norm back
         scales = [((grp.k_scale * grp.k_norm).cpu(), (grp.v_scale * grp.v_norm).cpu()) for grp in lay.groups]
+        hg, gk, vunits = self.head_groups, self.kernel_g, self.units * self.head_groups
         for grp, (ks, vs) in zip(lay.groups, scales):
             p = grp.plan
             kb, vb = grp.k_payload.shape[1], grp.v_payload.shape[1]
             kgb = grp.k_g0h.shape[1] * grp.k_g0h.element_size()
             vgb = grp.v_g0h.shape[1] * grp.v_g0h.element_size()
             for u in range(self.units):
-                s = _lib.Segment()
-                s.k_codes = grp.k_payload.data_ptr() + u * kb
-                s.v_codes = grp.v_payload.data_ptr() + u * vb
-                s.k_g0 = grp.k_g0h.data_ptr() + u * kgb
-                s.v_g0 = grp.v_g0h.data_ptr() + u * vgb
-                s.k_scale = float(ks[u])
-                s.v_scale = float(vs[u])
-                s.T, s.i1, s.i2, s.r, s.i2p = grp.T, p.i1, p.i2, p.r, grp.i2p
-                s.unit, s.token0 = u, grp.token0
-                segs.append(s)
+                for hk in range(hg):  # one virtual unit per head group, same codes
+                    s = _lib.Segment()
+                    s.k_codes = grp.k_payload.data_ptr() + u * kb
+                    s.v_codes = grp.v_payload.data_ptr() + u * vb
+                    s.k_g0 = grp.k_g0h.data_ptr() + u * kgb
+                    s.v_g0 = grp.v_g0h.data_ptr() + u * vgb
+                    s.k_scale = float(ks[u])
+                    s.v_scale = float(vs[u])
+                    s.T, s.i1, s.i2, s.r, s.i2p = grp.T, p.i1, p.i2, p.r, grp.i2p
+                    s.unit, s.token0 = u * hg + hk, grp.token0
+                    segs.append(s)
         nseg = len(segs)
         seg_arr = (_lib.Segment * max(nseg, 1))(*segs)
         # work plan (host) -> device tables
         if self.ctas is None:
             c = ctypes.c_int32()
-            check(lib().dq_attention_ctas(self.g, self.bits, ctypes.byref(c)), "attention_ctas")
+            check(lib().dq_attention_ctas(gk, self.bits, ctypes.byref(c)), "attention_ctas")
             self.ctas = c.value
-        wp = plan_work(seg_arr, nseg, self.units, self.chunk_b)
+        wp = plan_work(seg_arr, nseg, vunits, self.chunk_b)
+        if hg > 1:  # a tile range's head groups back to back in the ticket order (L2 reuse)
+            order = sorted(range(wp.nwork), key=lambda i: (wp.work[3 * i] // hg, wp.work[3 * i + 1],
+                                                           wp.work[3 * i] % hg))
+            wp.work = [x for i in order for x in wp.work[3 * i: 3 * i + 3]]
+            wp.work_part = [wp.work_part[i] for i in order]
         dev = self.device
 
         def i32(arr, n):
@@ -257,16 +272,17 @@ class DecodeKvCache:
         work_dev = i32(wp.work, 3 * nwork)
         wpart_dev = i32(wp.work_part, nwork)
         sched = torch.zeros(2, dtype=torch.int32, device=dev)
-        p0_dev = i32(wp.unit_part0, self.units)
-        np_dev = i32(wp.unit_nparts, self.units)
+        p0_dev = i32(wp.unit_part0, vunits)
+        np_dev = i32(wp.unit_nparts, vunits)
         tp = max(wp.total_parts, 1)
-        part_o = torch.empty((tp, self.g, self.dim), dtype=torch.float32, device=dev)
-        part_ml = torch.empty((tp, self.g, 2), dtype=torch.float32, device=dev)
+        part_o = torch.empty((tp, gk, self.dim), dtype=torch.float32, device=dev)
+        part_ml = torch.empty((tp, gk, 2), dtype=torch.float32, device=dev)
         a = _lib.AttnArgs()
         a.segs = seg_dev.data_ptr()
         a.nseg = nseg
-        a.units = self.units
-        a.g = self.g
+        a.units = vunits
+        a.g = gk
+        a.head_groups = hg
         a.bits = self.bits
         a.tail_k = self.tail_k[layer].data_ptr()
         a.tail_v = self.tail_v[layer].data_ptr()
@@ -285,7 +301,7 @@ class DecodeKvCache:
         a.part_o = part_o.data_ptr()
         a.part_ml = part_ml.data_ptr()
         wib = ctypes.c_int64()
-        check(lib().dq_attention_wimg_bytes(self.g, ctypes.byref(wib)), "wimg_bytes")
+        check(lib().dq_attention_wimg_bytes(gk, ctypes.byref(wib)), "wimg_bytes")
         wimg = torch.empty((max(nseg, 1), wib.value), dtype=torch.uint8, device=dev)
         a.wimg = wimg.data_ptr()
         a.wimg_stride = wib.value

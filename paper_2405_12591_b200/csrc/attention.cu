@@ -37,21 +37,25 @@ namespace {
 using namespace attn;
 
 // ---- combine: merge work-item partials with the dense fp16 tail ------------------
-// one CTA (128 threads) per unit; thread d owns output dim d.
+// one CTA (128 threads) per kv head unit u (all head_groups virtual units of it: they
+// share the tail, and the fused append must happen once, after every head has read it);
+// thread d owns output dim d.
 template <int G>
 __global__ void __launch_bounds__(128) combine_kernel(dq_attn_args args) {
   extern __shared__ float tail_s[];  // [tail_cap]
   __shared__ float red[4];
+  const int hg = args.head_groups > 1 ? args.head_groups : 1;
   const int u = blockIdx.x;
   const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
-  const int p0 = args.unit_part0[u], np = args.unit_nparts[u];
   const int tl = args.tail_len ? args.tail_len[u] : 0;
   const float l2e = 1.4426950408889634f;
-  for (int h = 0; h < G; ++h) {
+  for (int hh = 0; hh < G * hg; ++hh) {
+    const int v = u * hg + hh / G, h = hh % G;  // virtual unit, head inside it
+    const int p0 = args.unit_part0[v], np = args.unit_nparts[v];
     // dense tail scores (log2 domain)
     float tm = -INFINITY;
     if (tl > 0) {
-      const __half* qh = reinterpret_cast<const __half*>(args.q) + ((size_t)u * G + h) * kD;
+      const __half* qh = reinterpret_cast<const __half*>(args.q) + ((size_t)v * G + h) * kD;
       const uint2 qv = reinterpret_cast<const uint2*>(qh)[lane];
       const __half2* q2 = reinterpret_cast<const __half2*>(&qv);
       const float2 qa = __half22float2(q2[0]), qb = __half22float2(q2[1]);
@@ -95,7 +99,7 @@ __global__ void __launch_bounds__(128) combine_kernel(dq_attn_args args) {
       O += ot;
       __syncthreads();
     }
-    __half* out = reinterpret_cast<__half*>(args.out) + ((size_t)u * G + h) * kD;
+    __half* out = reinterpret_cast<__half*>(args.out) + ((size_t)v * G + h) * kD;
     out[d] = __float2half_rn(L > 0.f ? O / L : 0.f);
   }
   if (args.app_k) {
@@ -178,7 +182,8 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
   }
   if (phases & 2) {
     const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1);
-    combine_kernel<G><<<a.units, 128, csmem, s>>>(a);
+    const int hg = a.head_groups > 1 ? a.head_groups : 1;
+    combine_kernel<G><<<a.units / hg, 128, csmem, s>>>(a);
     DQ_LAUNCH_CHECK();
   }
   return DQ_OK;
@@ -280,6 +285,9 @@ extern "C" int dq_decode_attention(const dq_attn_args* h, void* stream) {
       (a.nwork > 0 && (!a.segs || !a.work || !a.work_part || !a.sched || !a.part_o || !a.part_ml)))
     return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: null pointer");
   if (!a.unit_part0 || !a.unit_nparts) return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: missing unit tables");
+  if (a.head_groups > 1 && a.units % a.head_groups)
+    return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: units (%d) not a multiple of head_groups (%d)", a.units,
+                a.head_groups);
   if (a.app_k && (!a.app_v || !a.tail_k || !a.tail_v || !a.tail_len || a.tail_cap <= 0))
     return fail(DQ_ERR_INVALID_ARG, "dq_decode_attention: append needs app_v and the tail buffers");
   cudaStream_t s = (cudaStream_t)stream;

@@ -298,9 +298,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            sacc[mt][h][k] += (float)(256 * acc_hi[mt][h][k] + acc_lo[mt][h][k] - bt[k & 1]) * cs[k & 1];
-            acc_hi[mt][h][k] = acc_lo[mt][h][k] = 0;
+          for (int k = 0; k < 4; k += 2) {
+            ffma2(sacc[mt][h][k], sacc[mt][h][k + 1], (float)(256 * acc_hi[mt][h][k] + acc_lo[mt][h][k] - bt[0]),
+                  (float)(256 * acc_hi[mt][h][k + 1] + acc_lo[mt][h][k + 1] - bt[1]), cs[0], cs[1]);
+            acc_hi[mt][h][k] = acc_lo[mt][h][k] = acc_hi[mt][h][k + 1] = acc_lo[mt][h][k + 1] = 0;
           }
       }
     };
@@ -496,8 +497,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
               imma<SA, false>(yh, x0[2], x1[2], x0[3], x1[3], ph[h].z, ph[h].w);
               imma<SA, false>(yl, x0[2], x1[2], x0[3], x1[3], pl_[h].z, pl_[h].w);
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                accv[t][h][k] += (float)(256 * yh[k] + yl[k]) * pinv[h][k & 1];
+              for (int k = 0; k < 4; k += 2)
+                ffma2(accv[t][h][k], accv[t][h][k + 1], (float)(256 * yh[k] + yl[k]),
+                      (float)(256 * yh[k + 1] + yl[k + 1]), pinv[h][0], pinv[h][1]);
             }
           }
         }
@@ -529,10 +531,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 #pragma unroll
             for (int h = 0; h < G; ++h)
 #pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                part[h][2 * c] = fmaf(gc[c], accv[t][h][aa], part[h][2 * c]);
-                part[h][2 * c + 1] = fmaf(gc[c], accv[t][h][2 + aa], part[h][2 * c + 1]);
-              }
+              for (int c = 0; c < 8; ++c)
+                ffma2(part[h][2 * c], part[h][2 * c + 1], gc[c], gc[c], accv[t][h][aa], accv[t][h][2 + aa]);
           }
         }
       }

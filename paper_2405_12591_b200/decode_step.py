@@ -1,0 +1,101 @@
+"""One multi-layer decode step as a CUDA graph: host inputs in, host outputs out.
+
+A decode step over ``DecodeKvCache`` is, per layer: copy that layer's q / k / v rows from
+pinned host memory, run the fused attention (prepare -> split -> combine, with the new
+token appended to the tail by the combine kernel), copy the output back.  Launching this
+from Python costs ~10 us of host time per op, more than the GPU needs for a layer, so the
+step is captured once and replayed:
+
+- host-to-device copies run ahead on one side stream (layer l+1's inputs land while layer
+  l computes) and device-to-host copies trail on another (layer l's output leaves while
+  layer l+1 computes);
+- the kernels keep their programmatic dependent launch edges inside the graph;
+- the host keeps the cache's token counters in step (``DecodeKvCache._after_append``).
+
+A replay that would seal a tail chunk (which re-plans the layer's segment table) is
+refused; call ``recapture()`` after sealing steps run eagerly.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .attention import DecodeKvCache
+from .errors import ShapeMismatch
+
+
+class DecodeStepGraph:
+    """Captured decode step for every layer of ``cache``.
+
+    q_h: (layers, units, g, 128), k_h / v_h: (layers, units, 128), out_h like q_h: pinned
+    host fp16 tensors the caller refills / reads between replays.
+    """
+
+    def __init__(self, cache: DecodeKvCache, q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor,
+                 out_h: torch.Tensor):
+        L, U, g, D = cache.layers, cache.units, cache.g, cache.dim
+        if q_h.shape != (L, U, g, D) or out_h.shape != q_h.shape or k_h.shape != (L, U, D) or v_h.shape != (L, U, D):
+            raise ShapeMismatch("host buffers must be q/out (layers, units, g, 128) and k/v (layers, units, 128)")
+        for t in (q_h, k_h, v_h, out_h):
+            if t.dtype != torch.float16 or not t.is_pinned():
+                raise ShapeMismatch("host buffers must be pinned fp16")
+        self.cache = cache
+        self.q_h, self.k_h, self.v_h, self.out_h = q_h, k_h, v_h, out_h
+        dev = cache.device
+        self.q_d = torch.empty(q_h.shape, dtype=torch.float16, device=dev)
+        self.k_d = torch.empty(k_h.shape, dtype=torch.float16, device=dev)
+        self.v_d = torch.empty(v_h.shape, dtype=torch.float16, device=dev)
+        self.o_d = torch.empty(q_h.shape, dtype=torch.float16, device=dev)
+        self.up = torch.cuda.Stream(device=dev)    # host -> device, runs ahead
+        self.down = torch.cuda.Stream(device=dev)  # device -> host, trails the layers
+        self.h2d = [torch.cuda.Event() for _ in range(L)]
+        self.done = [torch.cuda.Event() for _ in range(L)]
+        self.graph = None
+        self.recapture()
+
+    def _body(self):
+        cache, L = self.cache, self.cache.layers
+        compute = torch.cuda.current_stream()
+        self.up.wait_stream(compute)
+        self.down.wait_stream(compute)
+        with torch.cuda.stream(self.up):
+            for layer in range(L):
+                self.q_d[layer].copy_(self.q_h[layer], non_blocking=True)
+                self.k_d[layer].copy_(self.k_h[layer], non_blocking=True)
+                self.v_d[layer].copy_(self.v_h[layer], non_blocking=True)
+                self.h2d[layer].record(self.up)
+        for layer in range(L):
+            compute.wait_event(self.h2d[layer])
+            cache.attend(layer, self.q_d[layer], self.o_d[layer], append=(self.k_d[layer], self.v_d[layer]))
+            self.done[layer].record(compute)
+            with torch.cuda.stream(self.down):
+                self.down.wait_event(self.done[layer])
+                self.out_h[layer].copy_(self.o_d[layer], non_blocking=True)
+        compute.wait_stream(self.up)
+        compute.wait_stream(self.down)
+
+    def _sealing_ahead(self) -> bool:
+        return any(lay.tail_len + 1 >= self.cache.chunk_len for lay in self.cache._layers)
+
+    def recapture(self):
+        """(Re)build the graph: one eager step (it is a real decode step), then the capture."""
+        if self._sealing_ahead():
+            raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
+        self._body()  # eager step: builds every layer's segment table outside the capture
+        torch.cuda.synchronize()
+        if self._sealing_ahead():
+            raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
+        tails = [lay.tail_len for lay in self.cache._layers]
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._body()
+        for lay, t in zip(self.cache._layers, tails):  # the capture ran no device work
+            lay.tail_len = t
+
+    def replay(self):
+        """One decode step for every layer from the current host inputs into out_h."""
+        if self._sealing_ahead():
+            raise ShapeMismatch("a tail chunk seals on this token: run the step eagerly, then recapture()")
+        self.graph.replay()
+        for layer in range(self.cache.layers):
+            self.cache._after_append(layer)

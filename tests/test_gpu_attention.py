@@ -163,6 +163,32 @@ def test_tail_only_and_empty(dq):
         assert rel(p @ v[u].astype(np.float64), out[u]) < TOL
 
 
+@pytest.mark.parametrize("g,kernel_g", [(4, None), (8, None), (4, 1), (3, None)])
+def test_gqa_head_groups(dq, g, kernel_g):
+    """g > 2 query heads per kv head: head groups of kernel_g heads share the segments and the
+    tail; segments + fp16 tail + fused append, against the oracle."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    units, P, steps = 3, 1100, 21
+    rng = np.random.default_rng(40 + g)
+    k = rng.standard_normal((units, P + steps, 128)).astype(np.float32)
+    k[:, :, [5, 90]] *= 12.0
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, P + steps, 128)).astype(np.float16)
+    q = rng.standard_normal((units, g, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=4, chunk_len=256, kernel_g=kernel_g)
+    kd, vd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    cache.prefill(0, kd[:, :P], vd[:, :P])
+    qd = torch.from_numpy(q).cuda()
+    for t in range(P, P + steps - 1):
+        cache.attend(0, qd, append=(kd[:, t], vd[:, t]))
+    out = cache.attend(0, qd).float().cpu().numpy()
+    for u in range(units):
+        ref = _oracle_attend(k[u, :P + steps - 1].astype(np.float32), v[u, :P + steps - 1].astype(np.float32),
+                             q[u].astype(np.float32), 4, [P], steps - 1)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
 def test_fused_append_matches_attend_then_append(dq):
     """attend(append=(k, v)) == attend + append_token, step by step, across a tail seal."""
     from paper_2405_12591_b200.attention import DecodeKvCache
@@ -185,6 +211,49 @@ def test_fused_append_matches_attend_then_append(dq):
     assert len(b._layers[0].groups) == 2 and b._layers[0].tail_len == steps - chunk
     assert torch.equal(a.tail_len, b.tail_len)
     assert torch.equal(a.tail_k[0, :, :steps - chunk], b.tail_k[0, :, :steps - chunk])
+
+
+def test_decode_step_graph_matches_eager(dq):
+    """DecodeStepGraph (captured multi-layer step, host I/O) == eager attend(append=...) per layer."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+    from paper_2405_12591_b200.decode_step import DecodeStepGraph
+
+    L, U, g, P, steps = 3, 4, 2, 700, 5
+    rng = np.random.default_rng(21)
+    kv = torch.from_numpy(rng.standard_normal((L, 2, U, P, 128)).astype(np.float16)).cuda()
+    caches = [DecodeKvCache(layers=L, units=U, g=g, bits=4, chunk_len=64) for _ in range(2)]
+    for c in caches:
+        for layer in range(L):
+            c.prefill(layer, kv[layer, 0], kv[layer, 1])
+    q_h = torch.empty((L, U, g, 128), dtype=torch.float16).pin_memory()
+    k_h = torch.empty((L, U, 128), dtype=torch.float16).pin_memory()
+    v_h = torch.empty((L, U, 128), dtype=torch.float16).pin_memory()
+    out_h = torch.empty((L, U, g, 128), dtype=torch.float16).pin_memory()
+    eager, graphed = caches
+
+    def fill(t):
+        r = np.random.default_rng(100 + t)
+        q_h.copy_(torch.from_numpy(r.standard_normal((L, U, g, 128)).astype(np.float16)))
+        k_h.copy_(torch.from_numpy(r.standard_normal((L, U, 128)).astype(np.float16)))
+        v_h.copy_(torch.from_numpy(r.standard_normal((L, U, 128)).astype(np.float16)))
+
+    def eager_step():
+        return torch.stack([eager.attend(layer, q_h[layer].cuda(), append=(k_h[layer].cuda(), v_h[layer].cuda()))
+                            for layer in range(L)]).cpu()
+
+    fill(0)
+    stepper = DecodeStepGraph(graphed, q_h, k_h, v_h, out_h)  # runs step 0 eagerly, then captures
+    ref = eager_step()
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, ref)
+    for t in range(1, steps):
+        fill(t)
+        stepper.replay()
+        torch.cuda.synchronize()
+        ref = eager_step()
+        assert torch.equal(out_h, ref), t
+        assert graphed.tokens(0) == eager.tokens(0) == P + t + 1
+    assert torch.equal(graphed.tail_len, eager.tail_len)
 
 
 def test_export_segment_wire_format(dq):
