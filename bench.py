@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--chunk-b", type=int, default=256)
+    ap.add_argument("--chunk-b", type=int, default=None, help="rows per split-kernel work item (default: auto)")
     ap.add_argument("--kernel-g", type=int, default=None, help="query heads per split-kernel head group (1 or 2)")
     ap.add_argument("--ctas", type=int, default=None,
                     help="split-kernel grid: default persistent (resident CTAs), 0 = one CTA per 256-row slice")
@@ -410,7 +410,7 @@ def run_ours(args, cfg):
         "data": "synthetic: per-layer K/V ~ N(0,1) fp16 compressed by the K3 write path; q/k/v rows ~ N(0,1) fp16",
         "config": {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
                    "kv_bits": bits, "layers": layers, "kv_heads": kv_heads, "g": g,
-                   "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": args.chunk_b,
+                   "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": cache._layers[0].args.chunk_b,
                    "split_ctas": cache.ctas, "kernel_g": cache.kernel_g, "head_groups": cache.head_groups,
                    "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB streamed per step per GPU"},
         "hbm_gbs_step": step_bytes / (ms / 1e3) / 1e9,

@@ -136,14 +136,14 @@ class DecodeKvCache:
     """
 
     def __init__(self, layers: int, units: int, g: int = 1, bits: int = 4, chunk_len: int = 1024,
-                 dim: int = HEAD_DIM, chunk_b: int = DEFAULT_CHUNK_B, sm_scale: float | None = None,
+                 dim: int = HEAD_DIM, chunk_b: int | None = None, sm_scale: float | None = None,
                  ctas: int | None = None, kernel_g: int | None = None):
         if dim != HEAD_DIM:
             raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
         if not 1 <= g <= MAX_G:
             raise Unsupported(f"GQA groups of 1..{MAX_G} query heads per kv head are supported (got {g})")
-        if chunk_b != DEFAULT_CHUNK_B:
-            raise Unsupported(f"the fused decode kernel splits segments into {DEFAULT_CHUNK_B}-row work items")
+        if chunk_b is not None and (chunk_b % 64 or not 64 <= chunk_b <= DEFAULT_CHUNK_B):
+            raise Unsupported(f"work items must be 64..{DEFAULT_CHUNK_B} rows, a multiple of 64")
         if bits not in SUPPORTED_BITS:
             raise UnsupportedBits(f"bits must be in {SUPPORTED_BITS}")
         if layers < 1 or units < 1 or chunk_len < 1:
@@ -256,7 +256,10 @@ class DecodeKvCache:
             c = ctypes.c_int32()
             check(lib().dq_attention_ctas(gk, self.bits, ctypes.byref(c)), "attention_ctas")
             self.ctas = c.value
-        wp = plan_work(seg_arr, nseg, vunits, self.chunk_b)
+        # the largest items: the per-item cost (W image, softmax, epilogue) is fixed, and
+        # smaller items measured slower even where they shorten the scheduler's last round
+        chunk_b = self.chunk_b or DEFAULT_CHUNK_B
+        wp = plan_work(seg_arr, nseg, vunits, chunk_b)
         if hg > 1:  # a tile range's head groups back to back in the ticket order (L2 reuse)
             order = sorted(range(wp.nwork), key=lambda i: (wp.work[3 * i] // hg, wp.work[3 * i + 1],
                                                            wp.work[3 * i] % hg))
@@ -288,7 +291,7 @@ class DecodeKvCache:
         a.tail_v = self.tail_v[layer].data_ptr()
         a.tail_len = self.tail_len[layer].data_ptr()
         a.tail_cap = self.chunk_len
-        a.chunk_b = self.chunk_b
+        a.chunk_b = chunk_b
         a.sm_scale = self.sm_scale
         a.work = work_dev.data_ptr() if nwork else None
         a.nwork = nwork

@@ -191,7 +191,9 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
 
 template <int BITS>
 int dispatch_g(const dq_attn_args& a, cudaStream_t s) {
-  if (a.chunk_b != kCB) return fail(DQ_ERR_UNSUPPORTED, "chunk_b must be %d (got %d)", kCB, a.chunk_b);
+  if (a.chunk_b <= 0 || a.chunk_b > kCB || a.chunk_b % kI2Pad)
+    return fail(DQ_ERR_UNSUPPORTED, "chunk_b must be a multiple of %d in %d..%d (got %d)", kI2Pad, kI2Pad, kCB,
+                a.chunk_b);
   switch (a.g) {
     case 1: return launch_attn<BITS, 1>(a, s);
     case 2: return launch_attn<BITS, 2>(a, s);
