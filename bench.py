@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunk-b", type=int, default=None, help="rows per split-kernel work item (default: auto)")
     ap.add_argument("--kernel-g", type=int, default=None, help="query heads per split-kernel head group (1 or 2)")
+    ap.add_argument("--tc", type=int, default=None, choices=[0, 1],
+                    help="split kernel: 1 = tcgen05, 0 = mma.sync, default: tcgen05 where eligible")
     ap.add_argument("--ctas", type=int, default=None,
                     help="split-kernel grid: default persistent (resident CTAs), 0 = one CTA per 256-row slice")
     ap.add_argument("--layers", type=int, default=None, help="override layer count (debug only)")
@@ -283,7 +285,8 @@ def run_ours(args, cfg):
     chunk_len = 1024
 
     cache = DecodeKvCache(layers=layers, units=units, g=g, bits=bits, chunk_len=chunk_len, chunk_b=args.chunk_b,
-                          ctas=args.ctas, kernel_g=args.kernel_g)
+                          ctas=args.ctas, kernel_g=args.kernel_g,
+                          tc=None if args.tc is None else bool(args.tc))
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
 
@@ -412,6 +415,7 @@ def run_ours(args, cfg):
                    "kv_bits": bits, "layers": layers, "kv_heads": kv_heads, "g": g,
                    "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": cache._layers[0].args.chunk_b,
                    "split_ctas": cache.ctas, "kernel_g": cache.kernel_g, "head_groups": cache.head_groups,
+                   "split_path": "tcgen05" if cache._layers[0].args.path == 1 else "mma.sync",
                    "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB streamed per step per GPU"},
         "hbm_gbs_step": step_bytes / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

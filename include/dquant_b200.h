@@ -200,7 +200,7 @@ typedef struct dq_attn_args {
                              query heads run as head_groups "virtual units" u * head_groups + k (each g
                              heads, same codes; segs/q/out/partials indexed by virtual unit, the tail and
                              the combine grid by kv head u).  0 or 1: none */
-  int32_t pad2_;
+  int32_t path;           /* split kernel: 0 = mma.sync (all plans), 1 = tcgen05 (int4, g = 1, r = 64, i1 = 8) */
 } dq_attn_args;
 
 /* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */

@@ -95,7 +95,7 @@ class AttnArgs(ctypes.Structure):
         ("app_k", c_void_p),
         ("app_v", c_void_p),
         ("head_groups", c_int32),
-        ("pad2_", c_int32),
+        ("path", c_int32),
     ]
 
 

@@ -137,7 +137,7 @@ class DecodeKvCache:
 
     def __init__(self, layers: int, units: int, g: int = 1, bits: int = 4, chunk_len: int = 1024,
                  dim: int = HEAD_DIM, chunk_b: int | None = None, sm_scale: float | None = None,
-                 ctas: int | None = None, kernel_g: int | None = None):
+                 ctas: int | None = None, kernel_g: int | None = None, tc: bool | None = None):
         if dim != HEAD_DIM:
             raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
         if not 1 <= g <= MAX_G:
@@ -157,6 +157,10 @@ class DecodeKvCache:
         if self.kernel_g not in KERNEL_G or g % self.kernel_g:
             raise Unsupported(f"kernel_g must be in {KERNEL_G} and divide g")
         self.head_groups = g // self.kernel_g
+        # split kernel: tcgen05 (path 1) for 4-bit codes, one head per kernel and the full plan
+        # (i1 = 8, r = 64 -- any segment of >= 512 tokens with 8 | T); mma.sync (path 0) otherwise.
+        # True = tcgen05 (required), None / False = mma.sync (path 1 is correct but not yet faster).
+        self.tc = tc
         self.chunk_len, self.dim, self.chunk_b = chunk_len, dim, chunk_b
         # split-kernel grid: None = persistent (resident CTAs of this device), 0 = one CTA
         # per work item, k > 0 = k persistent CTAs
@@ -286,6 +290,11 @@ class DecodeKvCache:
         a.units = vunits
         a.g = gk
         a.head_groups = hg
+        eligible = self.bits == 4 and gk == 1
+        eligible = eligible and all(grp.plan.i1 == 8 and grp.plan.r == 64 for grp in lay.groups)
+        if self.tc and not eligible:
+            raise Unsupported("the tcgen05 path needs 4-bit codes, one head per kernel and i1 = 8, r = 64 plans")
+        a.path = 1 if (eligible and self.tc) else 0
         a.bits = self.bits
         a.tail_k = self.tail_k[layer].data_ptr()
         a.tail_v = self.tail_v[layer].data_ptr()

@@ -25,7 +25,7 @@
 // accumulation); the excess-code offset is removed exactly in integers.  The reduction
 // index is permuted identically on both operands, which is free.  Full-precision K/V
 // never exist anywhere.
-#include "attn_kernel.cuh"
+#include "attn_tc.cuh"
 
 #include <algorithm>
 #include <vector>
@@ -165,7 +165,32 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     attn_prepare_kernel<BITS, G><<<a.nseg, kPrepThreadsOf<G>, 0, s>>>(a);
     DQ_LAUNCH_CHECK();
   }
-  if (a.nwork > 0 && (phases & 1)) {
+  if (a.path == 1 && a.nwork > 0 && (phases & 1)) {
+    if constexpr (BITS == 4 && G == 1) {
+      static bool tc_attr = false;
+      if (!tc_attr) {
+        DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(TcSmem)));
+        tc_attr = true;
+      }
+      int sms = 0, dev = 0;
+      DQ_CUDA_TRY(cudaGetDevice(&dev));
+      DQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(a.nwork < sms ? a.nwork : sms));  // one CTA per SM (TMEM: 512 columns)
+      cfg.blockDim = dim3(kTcThreads);
+      cfg.dynamicSmemBytes = sizeof(TcSmem);
+      cfg.stream = s;
+      cudaLaunchAttribute attr_pdl[1];
+      attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr_pdl;
+      cfg.numAttrs = 1;
+      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_tc_kernel, a));
+    } else {
+      return fail(DQ_ERR_UNSUPPORTED, "the tcgen05 path covers 4-bit codes with g = 1");
+    }
+  } else if (a.nwork > 0 && (phases & 1)) {
     // programmatic dependent launch: the split kernel's prologue and first code copies
     // overlap the prepare kernel; it waits (griddepcontrol.wait) only for the W images
     cudaLaunchConfig_t cfg = {};

@@ -69,6 +69,11 @@ __device__ __forceinline__ void named_sync(int threads) {
   asm volatile("bar.sync 1, %0;\n" ::"r"(threads) : "memory");
 }
 
+// named barrier 2 over `threads` threads (consumer warps + the MMA warp of the tcgen05 path)
+__device__ __forceinline__ void named_sync2(int threads) {
+  asm volatile("bar.sync 2, %0;\n" ::"r"(threads) : "memory");
+}
+
 // TMA bulk copy global -> shared, completing `bytes` on the mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

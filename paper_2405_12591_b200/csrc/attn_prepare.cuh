@@ -29,9 +29,11 @@ constexpr int kWChunkBytes = G * 2 * kMaxRW * 8 * 16;  // W limb chunks (bond ro
 template <int G>
 constexpr int kWImageBytes = kWChunkBytes<G> + (int)sizeof(WMeta<G>);
 
-// 16-byte chunk of limb `limb` of W[h][a][rr][16 e] (e in ord16 order), bank-swizzled
-__device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a) {
-  return ((h * 2 + limb) * r + rr) * 8 + (a ^ (2 * (rr & 3)));
+// 16-byte chunk of limb `limb` of W[h][a][rr][16 e] (e in ord16 order): bank-swizzled for
+// the mma.sync fragments (path 0), or plain for tcgen05 (path 1: rows a of one bond row
+// form a K-major core matrix, 8 rows x 16 bytes, the next bond row 128 bytes further)
+__device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a, int path = 0) {
+  return ((h * 2 + limb) * r + rr) * 8 + (path ? a : (a ^ (2 * (rr & 3))));
 }
 
 // one CTA per segment, one thread per (h, a, rr) of W (threads beyond i1 / r idle): a
@@ -99,8 +101,8 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 4 : 2) attn_prepar
     }
     unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
     uint4* wout = reinterpret_cast<uint4*>(img);
-    wout[w_chunk(h, 0, r, rr, a)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    wout[w_chunk(h, 1, r, rr, a)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    wout[w_chunk(h, 0, r, rr, a, args.path)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    wout[w_chunk(h, 1, r, rr, a, args.path)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
   }
   __syncthreads();

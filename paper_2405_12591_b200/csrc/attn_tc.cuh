@@ -1,0 +1,547 @@
+// tcgen05 split kernel of the fused decode attention (path 1): int4 codes, g = 1, segments
+// with the full plan (i1 = 8, r = 64).  Same work items, persistent grid, ticket scheduler,
+// producer warp, W images and partials as attn_kernel.cuh (path 0); the two contractions
+// run on the 5th-generation tensor cores instead of mma.sync:
+//
+//   S[b, a]      = sum_{r,e} code_k[b, (r,e)] . W[(r,e), a]     UMMA M=128 (b), N=8 (a), K=(r,e)
+//   Y[(r,e), a] += sum_b code_v[(r,e), b] . P[b, a]             UMMA M=128 ((r,e)), N=8 (a), K=b
+//
+// The consumer warps stream the packed codes out of the shared-memory ring, widen them to
+// u8 in registers and write them into tensor memory (tcgen05.st: lane = row, 4 K-bytes
+// per column): A operands never touch shared memory twice.  B operands (the two-limb
+// fixed-point W image and P) sit in shared memory as K-major core matrices.  One elected
+// lane of a dedicated MMA warp issues tcgen05.mma.kind::i8 with s32 accumulators in TMEM
+// and signals completion with tcgen05.commit on mbarriers.  Both TMEM A buffers and both
+// Y buffers are double-buffered, so the consumers widen stage s+1 while stage s's MMAs run,
+// and fold stage s's Y (exact s32 -> scaled fp32) into registers afterwards.
+//
+// The numerics are identical to path 0: exact integer products of the excess-coded codes
+// with 15-bit two-limb W (per column and bond-row group scale) and 15-bit two-limb P (per
+// 64-row tile scale), excess removed exactly, fp32 accumulation across tiles.
+#pragma once
+
+#include "attn_kernel.cuh"
+
+namespace dq {
+namespace attn {
+
+constexpr int kTcStages = 10;                        // 10 x 16 KB ring, one CTA per SM
+constexpr int kTcWarps = kWarps + 2;                 // + producer (8) + MMA (9)
+constexpr int kTcThreads = kTcWarps * 32;
+constexpr int kTmemCols = 512;
+// TMEM column map: A buffers [0, 128), S [128, 192), Y buffers [192, 320)
+constexpr uint32_t kColA = 0, kColS = 128, kColY = 192;
+
+__device__ __forceinline__ uint32_t tc_idesc(int M, int N, int a_signed, int b_signed) {
+  return (2u << 4) | ((uint32_t)a_signed << 7) | ((uint32_t)b_signed << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+// K-major, no-swizzle shared-memory matrix descriptor (core matrices of 8 rows x 16 bytes)
+__device__ __forceinline__ uint64_t tc_sdesc(const void* p, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, int (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// stage geometry of path 1: K stages of RK bond rows over all tiles of the item, with
+// RK * 4 columns per 128-row M-block (<= 64 columns per A buffer); V stages of 32 bond rows
+// of one tile (512 (r,e) rows = 4 M-blocks x 16 columns)
+__device__ __forceinline__ void tc_geometry(SubItem& d) {
+  const int nmb = (d.nbt + 1) / 2;
+  int RK = (kStageBytes / (d.nbt * kI2Pad * 8)) & ~3;
+  RK = min(RK, nmb == 2 ? 8 : 16);
+  d.RK = RK;
+  d.nK = (d.r + RK - 1) / RK;
+  d.RV = 32;
+  d.nslices = 2;
+  d.stages = d.nK + d.nbt * d.nslices;
+}
+
+__device__ __forceinline__ void tc_load_sub(SubItem& d, const dq_attn_args& a, int w) {
+  load_sub<4>(d, a, w);
+  tc_geometry(d);
+}
+
+struct TcSmem {
+  alignas(1024) unsigned char ring[kTcStages][kStageBytes];
+  alignas(16) uint4 w[2 * kMaxR * 8];     // W limbs, chunk (limb * r + rr) * 8 + a (path-1 image)
+  alignas(16) float4 g0v[8 * kMaxR * 2];  // fp32 G0v [a][rr][c]
+  alignas(128) unsigned char pb[2][kTiles * 4 * 128];  // P limbs: K-major core matrices, chunk b/16
+  float red[kWarps][kD];
+  alignas(16) WMeta<1> wmeta;
+  SubItem sub[kSubRing];
+  uint64_t full[kTcStages], empty[kTcStages];
+  uint64_t wbar, g0bar, descfull[kSubRing];
+  uint64_t afull[2], afree[2], yfull[2], yfree[2], sfull, sfree, pfull;
+  unsigned pmax[8][kTiles];
+  int gamma[8][kTiles];
+  float rowmax[kWarps];
+  float lsum[kWarps];
+  uint32_t tmem;
+};
+
+// the W image (path-1 limb chunks + metadata) of an item's segment onto wbar (one thread)
+__device__ __forceinline__ void issue_wimg_tc(TcSmem& sm, const dq_attn_args& a, const SubItem& d) {
+  const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
+  const uint32_t wb = (uint32_t)(2 * d.r * 8 * 16);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  mbar_expect_tx(&sm.wbar, wb + (uint32_t)sizeof(WMeta<1>));
+  bulk_g2s(sm.w, img, wb, &sm.wbar);
+  bulk_g2s(&sm.wmeta, img + kWChunkBytes<1>, (uint32_t)sizeof(WMeta<1>), &sm.wbar);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_args args) {
+  constexpr int RB = 8;      // bytes per 16-code row at 4 bits
+  constexpr int X = kExcess<4>;
+  extern __shared__ __align__(1024) unsigned char smem_tc[];
+  TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_tc);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- prologue: barriers, TMEM ----------------------------------------------------------
+  if (tid == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kWarps);
+    }
+    for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.descfull[s], 1);
+    mbar_init(&sm.wbar, 1);
+    mbar_init(&sm.g0bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.afull[b], kWarps);
+      mbar_init(&sm.afree[b], 1);
+      mbar_init(&sm.yfull[b], 1);
+      mbar_init(&sm.yfree[b], kWarps);
+    }
+    mbar_init(&sm.sfull, 1);
+    mbar_init(&sm.sfree, kWarps);
+    mbar_init(&sm.pfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == kWarps + 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid < 8 * kTiles) {
+    (&sm.gamma[0][0])[tid] = 0;
+    (&sm.pmax[0][0])[tid] = 0u;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == kWarps) {
+    // ---- producer: descriptors and code stages of this CTA's items (as path 0) -------------
+    if (lane == 0) {
+      SubItem nd;
+      bool have = (int)blockIdx.x < args.nwork;
+      if (have) tc_load_sub(nd, args, blockIdx.x);
+      int g = 0;
+      for (int k = 0;; ++k) {
+        const int ds = k % kSubRing;
+        if (!have) {
+          sm.sub[ds].nbt = 0;
+          mbar_arrive(&sm.descfull[ds]);
+          break;
+        }
+        const SubItem d = nd;
+        sm.sub[ds] = d;
+        mbar_arrive(&sm.descfull[ds]);
+        bool nhave = false;
+        for (int ls = 0; ls < d.stages; ++ls, ++g) {
+          const int slot = g % kTcStages;
+          if (g >= kTcStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kTcStages - 1) & 1));
+          issue_stage<4>(d, ls, sm.ring[slot], &sm.full[slot]);
+          if (ls == min(2, d.stages - 1)) {
+            const int nxt = (int)gridDim.x + atomicAdd(args.sched, 1);
+            nhave = nxt < args.nwork;
+            if (nhave) tc_load_sub(nd, args, nxt);
+          }
+        }
+        have = nhave;
+      }
+      __threadfence();
+      if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
+        args.sched[0] = 0;
+        args.sched[1] = 0;
+      }
+    }
+    return;
+  }
+
+  if (warp == kWarps + 1) {
+    // ---- MMA warp: one elected lane issues every UMMA of the CTA ---------------------------
+    if (lane == 0) {
+      const uint32_t id_k_hi = tc_idesc(128, 8, 0, 1), id_k_lo = tc_idesc(128, 8, 0, 0);
+      const uint32_t id_v = tc_idesc(128, 8, 0, 0);
+      int na = 0, nv = 0;  // A-buffer uses, V stages (Y-buffer uses)
+      for (int j = 0;; ++j) {
+        mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+        const SubItem d = sm.sub[j % kSubRing];
+        if (d.nbt == 0) break;
+        const int nmb = (d.nbt + 1) / 2;
+        mbar_wait(&sm.wbar, (uint32_t)(j & 1));        // W image of this item's segment
+        if (j > 0) mbar_wait(&sm.sfree, (uint32_t)((j - 1) & 1));  // S of the previous item read
+        bool acc_s[2] = {false, false};  // per bond-row group: accumulate into S?
+        for (int ks = 0; ks < d.nK; ++ks, ++na) {
+          const int ab = na & 1;
+          mbar_wait(&sm.afull[ab], (uint32_t)((na >> 1) & 1));
+          tc_fence_after();
+          const int rk0 = ks * d.RK, nr = min(d.RK, d.r - rk0);
+          for (int kk = 0; kk < nr / 2; ++kk) {  // UMMA k-step = 32 bytes = 2 bond rows
+            const int rr = rk0 + 2 * kk;
+            const int grp = rr < kGroupR ? 0 : 1;
+            for (int limb = 0; limb < 2; ++limb) {
+              const uint64_t bdesc = tc_sdesc(&sm.w[(limb * d.r + rr) * 8], 128, 2 * d.r * 128);
+              for (int mb = 0; mb < nmb; ++mb) {
+                const uint32_t dcol = kColS + (uint32_t)(((grp * 2 + limb) * 2 + mb) * 8);
+                const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * d.RK * 4 + kk * 8);
+                tc_mma_ts(tmem + dcol, tmem + acol, bdesc, limb ? id_k_lo : id_k_hi, acc_s[grp] ? 1u : 0u);
+              }
+            }
+            acc_s[grp] = true;
+          }
+          tc_commit(&sm.afree[ab]);
+        }
+        tc_commit(&sm.sfull);
+        mbar_wait(&sm.pfull, (uint32_t)(j & 1));  // P limbs of this item in shared memory
+        tc_fence_after();
+        for (int t = 0; t < d.nbt; ++t)
+          for (int sl = 0; sl < 2; ++sl, ++na, ++nv) {
+            const int ab = na & 1, yb = nv & 1;
+            mbar_wait(&sm.afull[ab], (uint32_t)((na >> 1) & 1));
+            if (nv >= 2) mbar_wait(&sm.yfree[yb], (uint32_t)(((nv >> 1) - 1) & 1));
+            tc_fence_after();
+            for (int kk = 0; kk < 2; ++kk)      // 64 b = 2 k-steps
+              for (int limb = 0; limb < 2; ++limb) {
+                const uint64_t bdesc = tc_sdesc(&sm.pb[limb][(t * 4 + kk * 2) * 128], 128, 4 * kTiles * 128);
+                for (int mb = 0; mb < 4; ++mb) {
+                  const uint32_t dcol = kColY + (uint32_t)(yb * 64 + (mb * 2 + limb) * 8);
+                  const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * 16 + kk * 8);
+                  tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_v, kk ? 1u : 0u);
+                }
+              }
+            tc_commit(&sm.afree[ab]);
+            tc_commit(&sm.yfull[yb]);
+          }
+      }
+    }
+    // wait for the consumers' last TMEM reads, then free TMEM
+    __syncwarp();
+    named_sync2(kThreads + 32);
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    return;
+  }
+
+  // ---- consumer warps ----------------------------------------------------------------------
+  const int q = warp & 3;              // TMEM lane quarter of this warp
+  const int half = warp >> 2;          // K phase: M-block; V phase: M-blocks 2*half, 2*half+1
+  const int lane_in = 32 * q + lane;   // TMEM lane (row inside an M-block)
+  const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+  int st = 0, na = 0, nv = 0;
+  auto release = [&](int s) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s % kTcStages]);
+  };
+
+  if (tid == 0) {
+    mbar_wait(&sm.descfull[0], 0);
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // W images come from the prepare kernel
+    if (sm.sub[0].nbt > 0) issue_wimg_tc(sm, args, sm.sub[0]);
+  }
+
+  for (int j = 0;; ++j) {
+    mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+    const SubItem d = sm.sub[j % kSubRing];
+    if (d.nbt == 0) break;
+    const int wi = d.item, nbt = d.nbt, nmb = (nbt + 1) / 2, r = d.r;
+    auto stamp = [&](int k) {
+      if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + k] = global_ns();
+    };
+    stamp(0);
+    if (args.trace && tid == 0) {
+      args.trace[(size_t)wi * 8 + 6] = blockIdx.x;
+      args.trace[(size_t)wi * 8 + 7] = sm_id();
+    }
+    if (tid == 0) {  // G0v of this item (its buffer is free: the previous epilogue ended in a barrier)
+      const uint32_t gb = (uint32_t)(d.i1 * r * 32);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_expect_tx(&sm.g0bar, gb);
+      bulk_g2s(sm.g0v, d.vg0, gb, &sm.g0bar);
+    }
+
+    // ---- K phase: widen the K codes of each stage into TMEM (this thread = one b row) -------
+    const int jt = 2 * half + (q >> 1);           // tile of this thread's row
+    const int b_in = 32 * (q & 1) + lane;         // row inside the tile
+    const int swz = (16 / 4);                     // ktile swizzle unit at 4 bits: (rr & 3) * 4
+    for (int ks = 0; ks < d.nK; ++ks, ++st, ++na) {
+      const int slot = st % kTcStages, ab = na & 1;
+      mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
+      if (na >= 2) mbar_wait(&sm.afree[ab], (uint32_t)(((na >> 1) - 1) & 1));
+      const int rk0 = ks * d.RK, nr = min(d.RK, r - rk0);
+      if (half < nmb) {
+        const unsigned char* tile = sm.ring[slot] + jt * nr * kI2Pad * RB;
+        const bool live = jt < nbt;
+        for (int r4 = 0; r4 < nr; r4 += 4) {
+          uint32_t v[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rl = r4 + i, rr = rk0 + rl;
+            uint32_t o[4] = {0, 0, 0, 0};
+            if (live) {
+              const uint2 w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ ((rr & 3) * swz))) * RB);
+              o[0] = w2.x & 0x0F0F0F0Fu;
+              o[1] = (w2.x >> 4) & 0x0F0F0F0Fu;
+              o[2] = w2.y & 0x0F0F0F0Fu;
+              o[3] = (w2.y >> 4) & 0x0F0F0F0Fu;
+            }
+            v[4 * i] = o[0], v[4 * i + 1] = o[1], v[4 * i + 2] = o[2], v[4 * i + 3] = o[3];
+          }
+          tc_st16(tmem + lane_addr + kColA + (uint32_t)(ab * 64 + half * d.RK * 4 + r4 * 4), v);
+        }
+        tc_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.afull[ab]);
+      release(st);
+    }
+    stamp(1);
+
+    // ---- S from TMEM, softmax of the item -----------------------------------------------------
+    mbar_wait(&sm.wbar, (uint32_t)(j & 1));  // W metadata (beta, cs)
+    mbar_wait(&sm.sfull, (uint32_t)(j & 1));
+    tc_fence_after();
+    float s[8];
+    {
+      int acc[2][2][8];
+      if (half < nmb) {
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2)
+#pragma unroll
+          for (int limb = 0; limb < 2; ++limb)
+            tc_ld8(tmem + lane_addr + kColS + (uint32_t)(((g2 * 2 + limb) * 2 + half) * 8), acc[g2][limb]);
+        tc_wait_ld();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.sfree);
+      const float kscale = d.kscale * args.sm_scale * 1.4426950408889634f;
+      const bool row_ok = half < nmb && jt < nbt && d.wb0 + jt * kI2Pad + b_in < d.i2;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        float v = 0.f;
+#pragma unroll
+        for (int g2 = 0; g2 < (kGroupR < kMaxR ? 2 : 1); ++g2)
+          v += (float)(256 * acc[g2][0][a] + acc[g2][1][a] - sm.wmeta.beta[0][a][g2]) * (kscale * sm.wmeta.cs[0][a][g2]);
+        s[a] = (row_ok && a < d.i1) ? v : -INFINITY;
+      }
+    }
+    float m = s[0];
+#pragma unroll
+    for (int a = 1; a < 8; ++a) m = fmaxf(m, s[a]);
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) sm.rowmax[warp] = m;
+    named_sync(kThreads);
+    // every thread has combined its S with the W metadata, and every UMMA reading W
+    // completed before sfull: W(j+1) may replace W(j)
+    if (tid == 0) {
+      const int jn = j + 1;
+      mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
+      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg_tc(sm, args, sm.sub[jn % kSubRing]);
+    }
+    m = sm.rowmax[0];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) m = fmaxf(m, sm.rowmax[w]);
+    float p[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      p[a] = s[a] == -INFINITY ? 0.f : exp2f(s[a] - m);
+      float v = p[a];
+      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0 && jt < nbt && half < nmb) atomicMax(&sm.pmax[a][jt], __float_as_uint(v));
+    }
+    named_sync(kThreads);
+    float lsum = 0.f;
+    {
+      const int b_item = jt * kI2Pad + b_in;
+      const int pos = (b_item >> 4) * 128 + inv_ord16<4>(b_item & 15);
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const float pm = __uint_as_float(sm.pmax[a][min(jt, kTiles - 1)]);
+        const float pq = pow2_sub_exp(pm, kPBits<4>), pinv = pow2_exp_sub(pm, kPBits<4>);
+        const int pint = __float2int_rn(p[a] * pq);
+        lsum += (float)pint * pinv;
+        if (half < nmb) {
+          sm.pb[0][pos + a * 16] = (unsigned char)(pint >> 8);
+          sm.pb[1][pos + a * 16] = (unsigned char)(pint & 0xFF);
+        }
+        int gs = pint;
+        for (int o = 16; o; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+        if (X && lane == 0 && jt < nbt && half < nmb) atomicAdd(&sm.gamma[a][jt], X * gs);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P read by the tensor cores
+    named_sync(kThreads);
+    if (tid == 0) mbar_arrive(&sm.pfull);
+    stamp(2);
+
+    // ---- V phase: widen V codes into TMEM, fold each stage's Y into fp32 registers ---------
+    // thread rows: (slice sl, M-block 2*half + i): (r, e) = (32 sl + 8 (2 half + i) + lane_in / 16, lane_in % 16)
+    float accv[2][2][8];
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int a = 0; a < 8; ++a) accv[sl][i][a] = 0.f;
+    auto fold = [&](int t, int sl, int yb, int nvs) {
+      mbar_wait(&sm.yfull[yb], (uint32_t)((nvs >> 1) & 1));
+      tc_fence_after();
+      int y[2][2][8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int limb = 0; limb < 2; ++limb)
+          tc_ld8(tmem + lane_addr + kColY + (uint32_t)(yb * 64 + ((2 * half + i) * 2 + limb) * 8), y[i][limb]);
+      tc_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.yfree[yb]);
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const float pinv = pow2_exp_sub(__uint_as_float(sm.pmax[a][t]), kPBits<4>);
+        const int gam = sm.gamma[a][t];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          accv[sl][i][a] = fmaf((float)(256 * y[i][0][a] + y[i][1][a] - gam), pinv, accv[sl][i][a]);
+      }
+    };
+    int pend_t = -1, pend_sl = 0, pend_yb = 0, pend_nv = 0;
+    for (int t = 0; t < nbt; ++t)
+      for (int sl = 0; sl < 2; ++sl, ++st, ++na, ++nv) {
+        const int slot = st % kTcStages, ab = na & 1;
+        mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
+        if (na >= 2) mbar_wait(&sm.afree[ab], (uint32_t)(((na >> 1) - 1) & 1));
+        const unsigned char* buf = sm.ring[slot];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int rho = (2 * half + i) * 128 + lane_in;  // row (r_local * 16 + e) of the stage
+          const uint4 c0 = *reinterpret_cast<const uint4*>(buf + rho * 32);
+          const uint4 c1 = *reinterpret_cast<const uint4*>(buf + rho * 32 + 16);
+          const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+          uint32_t v[16];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[2 * k] = wv[k] & 0x0F0F0F0Fu;
+            v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
+          }
+          tc_st16(tmem + lane_addr + kColA + (uint32_t)(ab * 64 + (2 * half + i) * 16), v);
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.afull[ab]);
+        release(st);
+        if (pend_t >= 0) fold(pend_t, pend_sl, pend_yb, pend_nv);
+        pend_t = t, pend_sl = sl, pend_yb = nv & 1, pend_nv = nv;
+      }
+    fold(pend_t, pend_sl, pend_yb, pend_nv);
+    stamp(3);
+
+    // ---- epilogue: O[c, e] = scale_v * sum_{a, r} G0v[a, c, r] Y[(r, e), a] ---------------------
+    mbar_wait(&sm.g0bar, (uint32_t)(j & 1));
+    float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // [c] for e = lane_in % 16
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int rr = 32 * sl + 8 * (2 * half + i) + lane_in / 16;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          const float4 g_lo = sm.g0v[2 * (a * r + rr)], g_hi = sm.g0v[2 * (a * r + rr) + 1];
+          const float y = accv[sl][i][a];
+          ffma2(part[0], part[1], g_lo.x, g_lo.y, y, y);
+          ffma2(part[2], part[3], g_lo.z, g_lo.w, y, y);
+          ffma2(part[4], part[5], g_hi.x, g_hi.y, y, y);
+          ffma2(part[6], part[7], g_hi.z, g_hi.w, y, y);
+        }
+      }
+    // lanes l and l + 16 hold the same e
+#pragma unroll
+    for (int c = 0; c < 8; ++c) part[c] += __shfl_xor_sync(0xffffffffu, part[c], 16);
+    for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if (lane < 16) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) sm.red[warp][c * 16 + lane] = part[c];
+    }
+    if (lane == 0) sm.lsum[warp] = lsum;
+    named_sync(kThreads);
+    if (tid < 8 * kTiles) {  // ready for the next item's softmax
+      (&sm.gamma[0][0])[tid] = 0;
+      (&sm.pmax[0][0])[tid] = 0u;
+    }
+    if (tid < kD) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) v += sm.red[w][tid];
+      args.part_o[(size_t)d.part * kD + tid] = v * d.vscale;
+    }
+    if (tid == 0) {
+      float l = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) l += sm.lsum[w];
+      args.part_ml[(size_t)d.part * 2 + 0] = m;  // log2 domain
+      args.part_ml[(size_t)d.part * 2 + 1] = l;
+    }
+    named_sync(kThreads);  // red / lsum / g0v / pmax reusable
+    stamp(5);
+  }
+  tc_fence_before();
+  named_sync2(kThreads + 32);  // with the MMA warp: TMEM may be freed
+}
+
+}  // namespace attn
+}  // namespace dq

@@ -74,16 +74,21 @@ def _oracle_attend(k, v, q, bits, segs_T, tail):
     (8, 1, 1023, 1),
 ])
 @pytest.mark.parametrize("ctas", [None, 0, 3])  # persistent grid / one CTA per item / 3 CTAs
-def test_decode_attention_prefill_only(dq, bits, g, T, units, ctas):
+@pytest.mark.parametrize("tc", [False, True])    # mma.sync / tcgen05 split kernel (where eligible)
+def test_decode_attention_prefill_only(dq, bits, g, T, units, ctas, tc):
     from paper_2405_12591_b200.attention import DecodeKvCache
 
     rng = np.random.default_rng(T + 7 * g + bits)
     k = rng.standard_normal((units, T, 128)).astype(np.float16)
     v = rng.standard_normal((units, T, 128)).astype(np.float16)
     q = rng.standard_normal((units, g, 128)).astype(np.float16)
-    cache = DecodeKvCache(layers=1, units=units, g=g, bits=bits, ctas=ctas)
+    eligible = bits == 4 and g == 1 and T >= 512 and T % 8 == 0
+    if tc and not eligible:
+        pytest.skip("tcgen05 path: 4-bit codes, g = 1, full plans only")
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=bits, ctas=ctas, tc=tc)
     cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    assert cache._layers[0].args.path == (1 if tc else 0)
     for u in range(units):
         ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), bits,
                              [T], 0)
@@ -92,7 +97,8 @@ def test_decode_attention_prefill_only(dq, bits, g, T, units, ctas):
 
 @pytest.mark.parametrize("scale,bits", [(20.0, 4), (50.0, 4), (20.0, 2), (20.0, 8)])
 @pytest.mark.parametrize("ctas", [None, 0])  # persistent grid / one CTA per item
-def test_decode_attention_outlier_channels(dq, scale, bits, ctas):
+@pytest.mark.parametrize("tc", [False, True])
+def test_decode_attention_outlier_channels(dq, scale, bits, ctas, tc):
     """Outlier key channels (LLM-like) make the softmax peaky: tolerance must still hold."""
     from paper_2405_12591_b200.attention import DecodeKvCache
 
@@ -103,7 +109,9 @@ def test_decode_attention_outlier_channels(dq, scale, bits, ctas):
     k = k.astype(np.float16)
     v = rng.standard_normal((units, T, 128)).astype(np.float16)
     q = rng.standard_normal((units, 1, 128)).astype(np.float16)
-    cache = DecodeKvCache(layers=1, units=units, g=1, bits=bits, ctas=ctas)
+    if tc and bits != 4:
+        pytest.skip("tcgen05 path: 4-bit codes")
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=bits, ctas=ctas, tc=tc)
     cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
     out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
     for u in range(units):
