@@ -89,15 +89,19 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 4 : 2) attn_prepar
   if (live) atomicMax(&wmax[h][a][grp], __float_as_uint(m));
   __syncthreads();
   if (live) {
-    const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a][grp]), kWBits<BITS>);
+    // path 1 splits both limbs signed: one bit of headroom keeps the hi limb in s8
+    const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a][grp]), kWBits<BITS> - args.path);
     uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
     int wsum = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int wint = __float2int_rn(wv[i] * wq);
       wsum += wint;
-      hi[i >> 2] |= (uint32_t)((wint >> 8) & 0xFF) << (8 * (i & 3));
-      lo[i >> 2] |= (uint32_t)(wint & 0xFF) << (8 * (i & 3));
+      // path 0: hi signed, lo unsigned; path 1: both signed (lo in [-128, 127]) so one
+      // s8 UMMA of N = 16 takes both limbs; wint = 256 * hi + lo either way
+      const int whi = args.path ? (wint + 128) >> 8 : wint >> 8;
+      hi[i >> 2] |= (uint32_t)(whi & 0xFF) << (8 * (i & 3));
+      lo[i >> 2] |= (uint32_t)((wint - 256 * whi) & 0xFF) << (8 * (i & 3));
     }
     unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
     uint4* wout = reinterpret_cast<uint4*>(img);
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 4 : 2) attn_prepar
 
     int* mout = reinterpret_cast<int*>(static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride +
                                        kWChunkBytes<G>);
-    const float cs = pow2_exp_sub(__uint_as_float((&wmax[0][0][0])[tid]), kWBits<BITS>);
+    const float cs = pow2_exp_sub(__uint_as_float((&wmax[0][0][0])[tid]), kWBits<BITS> - args.path);
     mout[tid] = (&meta.beta[0][0][0])[tid];                               // beta[G][8][2]
     mout[G * 16 + tid] = __float_as_int(cs);                               // cs[G][8][2]
   }

@@ -29,8 +29,9 @@ constexpr int kTcStages = 10;                        // 10 x 16 KB ring, one CTA
 constexpr int kTcWarps = kWarps + 2;                 // + producer (8) + MMA (9)
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTmemCols = 512;
-// TMEM column map: A buffers [0, 128), S [128, 192), Y buffers [192, 320)
-constexpr uint32_t kColA = 0, kColS = 128, kColY = 192;
+// TMEM column map: kNumA A buffers of 64 columns, then S (64), then 2 Y buffers (64 each)
+constexpr int kNumA = 4;
+constexpr uint32_t kColA = 0, kColS = 64 * kNumA, kColY = kColS + 64;
 
 __device__ __forceinline__ uint32_t tc_idesc(int M, int N, int a_signed, int b_signed) {
   return (2u << 4) | ((uint32_t)a_signed << 7) | ((uint32_t)b_signed << 10) | ((uint32_t)(N >> 3) << 17) |
@@ -112,7 +113,7 @@ struct TcSmem {
   SubItem sub[kSubRing];
   uint64_t full[kTcStages], empty[kTcStages];
   uint64_t wbar, g0bar, descfull[kSubRing];
-  uint64_t afull[2], afree[2], yfull[2], yfree[2], sfull, sfree, pfull;
+  uint64_t afull[kNumA], afree[kNumA], yfull[2], yfree[2], sfull, sfree, pfull;
   unsigned pmax[8][kTiles];
   int gamma[8][kTiles];
   float rowmax[kWarps];
@@ -146,9 +147,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.descfull[s], 1);
     mbar_init(&sm.wbar, 1);
     mbar_init(&sm.g0bar, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNumA; ++b) {
       mbar_init(&sm.afull[b], kWarps);
       mbar_init(&sm.afree[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.yfull[b], 1);
       mbar_init(&sm.yfree[b], kWarps);
     }
@@ -213,8 +216,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
   if (warp == kWarps + 1) {
     // ---- MMA warp: one elected lane issues every UMMA of the CTA ---------------------------
     if (lane == 0) {
-      const uint32_t id_k_hi = tc_idesc(128, 8, 0, 1), id_k_lo = tc_idesc(128, 8, 0, 0);
-      const uint32_t id_v = tc_idesc(128, 8, 0, 0);
+      // both limbs of a B operand in one UMMA: N = 16 rows (hi limb a = 0..7, lo limb a = 0..7)
+      const uint32_t id_k = tc_idesc(128, 16, 0, 1);  // codes u8 x W limbs s8
+      const uint32_t id_v = tc_idesc(128, 16, 0, 0);  // codes u8 x P limbs u8
       int na = 0, nv = 0;  // A-buffer uses, V stages (Y-buffer uses)
       for (int j = 0;; ++j) {
         mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
@@ -223,45 +227,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
         const int nmb = (d.nbt + 1) / 2;
         mbar_wait(&sm.wbar, (uint32_t)(j & 1));        // W image of this item's segment
         if (j > 0) mbar_wait(&sm.sfree, (uint32_t)((j - 1) & 1));  // S of the previous item read
+        if (args.trace) args.trace[(size_t)d.item * 8 + 7] = global_ns();  // MMA warp: K issue starts
         bool acc_s[2] = {false, false};  // per bond-row group: accumulate into S?
         for (int ks = 0; ks < d.nK; ++ks, ++na) {
-          const int ab = na & 1;
-          mbar_wait(&sm.afull[ab], (uint32_t)((na >> 1) & 1));
+          const int ab = na % kNumA;
+          mbar_wait(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
           tc_fence_after();
           const int rk0 = ks * d.RK, nr = min(d.RK, d.r - rk0);
           for (int kk = 0; kk < nr / 2; ++kk) {  // UMMA k-step = 32 bytes = 2 bond rows
             const int rr = rk0 + 2 * kk;
             const int grp = rr < kGroupR ? 0 : 1;
-            for (int limb = 0; limb < 2; ++limb) {
-              const uint64_t bdesc = tc_sdesc(&sm.w[(limb * d.r + rr) * 8], 128, 2 * d.r * 128);
-              for (int mb = 0; mb < nmb; ++mb) {
-                const uint32_t dcol = kColS + (uint32_t)(((grp * 2 + limb) * 2 + mb) * 8);
-                const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * d.RK * 4 + kk * 8);
-                tc_mma_ts(tmem + dcol, tmem + acol, bdesc, limb ? id_k_lo : id_k_hi, acc_s[grp] ? 1u : 0u);
-              }
+            // rows 0-7: hi limb chunk of bond row rr, rows 8-15: lo limb (d.r * 128 bytes further)
+            const uint64_t bdesc = tc_sdesc(&sm.w[rr * 8], 128, d.r * 128);
+            for (int mb = 0; mb < nmb; ++mb) {
+              const uint32_t dcol = kColS + (uint32_t)((grp * 2 + mb) * 16);
+              const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * d.RK * 4 + kk * 8);
+              tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_k, acc_s[grp] ? 1u : 0u);
             }
             acc_s[grp] = true;
           }
           tc_commit(&sm.afree[ab]);
         }
         tc_commit(&sm.sfull);
+        if (args.trace) args.trace[(size_t)d.item * 8 + 4] = global_ns();  // MMA warp: K issue done
         mbar_wait(&sm.pfull, (uint32_t)(j & 1));  // P limbs of this item in shared memory
         tc_fence_after();
         for (int t = 0; t < d.nbt; ++t)
           for (int sl = 0; sl < 2; ++sl, ++na, ++nv) {
-            const int ab = na & 1, yb = nv & 1;
-            mbar_wait(&sm.afull[ab], (uint32_t)((na >> 1) & 1));
+            const int ab = na % kNumA, yb = nv & 1;
+            mbar_wait(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
             if (nv >= 2) mbar_wait(&sm.yfree[yb], (uint32_t)(((nv >> 1) - 1) & 1));
             tc_fence_after();
-            for (int kk = 0; kk < 2; ++kk)      // 64 b = 2 k-steps
-              for (int limb = 0; limb < 2; ++limb) {
-                const uint64_t bdesc = tc_sdesc(&sm.pb[limb][(t * 4 + kk * 2) * 128], 128, 4 * kTiles * 128);
-                for (int mb = 0; mb < 4; ++mb) {
-                  const uint32_t dcol = kColY + (uint32_t)(yb * 64 + (mb * 2 + limb) * 8);
-                  const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * 16 + kk * 8);
-                  tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_v, kk ? 1u : 0u);
-                }
+            for (int kk = 0; kk < 2; ++kk) {  // 64 b = 2 k-steps
+              // rows 0-7: P hi limb, rows 8-15: P lo limb (the next limb buffer)
+              const uint64_t bdesc = tc_sdesc(&sm.pb[0][(t * 4 + kk * 2) * 128], 128, sizeof(sm.pb[0]));
+              for (int mb = 0; mb < 4; ++mb) {
+                const uint32_t dcol = kColY + (uint32_t)(yb * 64 + mb * 16);
+                const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * 16 + kk * 8);
+                tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_v, kk ? 1u : 0u);
               }
+            }
             tc_commit(&sm.afree[ab]);
             tc_commit(&sm.yfull[yb]);
           }
@@ -301,10 +306,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
       if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + k] = global_ns();
     };
     stamp(0);
-    if (args.trace && tid == 0) {
-      args.trace[(size_t)wi * 8 + 6] = blockIdx.x;
-      args.trace[(size_t)wi * 8 + 7] = sm_id();
-    }
+    if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + 6] = blockIdx.x;
     if (tid == 0) {  // G0v of this item (its buffer is free: the previous epilogue ended in a barrier)
       const uint32_t gb = (uint32_t)(d.i1 * r * 32);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -317,9 +319,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     const int b_in = 32 * (q & 1) + lane;         // row inside the tile
     const int swz = (16 / 4);                     // ktile swizzle unit at 4 bits: (rr & 3) * 4
     for (int ks = 0; ks < d.nK; ++ks, ++st, ++na) {
-      const int slot = st % kTcStages, ab = na & 1;
+      const int slot = st % kTcStages, ab = na % kNumA;
       mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
-      if (na >= 2) mbar_wait(&sm.afree[ab], (uint32_t)(((na >> 1) - 1) & 1));
+      if (na >= kNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kNumA - 1) & 1));
       const int rk0 = ks * d.RK, nr = min(d.RK, r - rk0);
       if (half < nmb) {
         const unsigned char* tile = sm.ring[slot] + jt * nr * kI2Pad * RB;
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
         for (int g2 = 0; g2 < 2; ++g2)
 #pragma unroll
           for (int limb = 0; limb < 2; ++limb)
-            tc_ld8(tmem + lane_addr + kColS + (uint32_t)(((g2 * 2 + limb) * 2 + half) * 8), acc[g2][limb]);
+            tc_ld8(tmem + lane_addr + kColS + (uint32_t)((g2 * 2 + half) * 16 + limb * 8), acc[g2][limb]);
         tc_wait_ld();
       }
       tc_fence_before();
@@ -462,9 +464,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     int pend_t = -1, pend_sl = 0, pend_yb = 0, pend_nv = 0;
     for (int t = 0; t < nbt; ++t)
       for (int sl = 0; sl < 2; ++sl, ++st, ++na, ++nv) {
-        const int slot = st % kTcStages, ab = na & 1;
+        const int slot = st % kTcStages, ab = na % kNumA;
         mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
-        if (na >= 2) mbar_wait(&sm.afree[ab], (uint32_t)(((na >> 1) - 1) & 1));
+        if (na >= kNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kNumA - 1) & 1));
         const unsigned char* buf = sm.ring[slot];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {

@@ -13,7 +13,8 @@ from paper_2405_12591_b200.attention import DecodeKvCache  # noqa: E402
 
 units, T = int(os.environ.get("UNITS", 512)), int(os.environ.get("T", 4096))
 ctas = os.environ.get("CTAS")
-cache = DecodeKvCache(layers=1, units=units, g=1, bits=4, ctas=None if ctas is None else int(ctas))
+cache = DecodeKvCache(layers=1, units=units, g=1, bits=4, ctas=None if ctas is None else int(ctas),
+                      tc=bool(int(os.environ.get("TC", "0"))))
 k = torch.randn((units, T, 128), device="cuda").half()
 cache.prefill(0, k, k)
 del k
@@ -31,7 +32,8 @@ if os.environ.get("SAVE"):
     np.savez(os.environ["SAVE"], trace=trace.cpu().numpy(), work=cache._layers[0].keep[1].cpu().numpy())
 t0 = t[:, 0].min()
 ph = np.diff(t[:, :6], axis=1) / 1e3  # us
-names = ["prologue+W", "K stages", "softmax", "V stages", "epilogue"]
+names = (["K stages", "softmax", "V stages", "(unused)", "epilogue"] if cache._layers[0].args.path == 1 else
+         ["prologue+W", "K stages", "softmax", "V stages", "epilogue"])
 print(f"ctas {a.nctas}, items {a.nwork}, kernel span {(t[:, 5].max() - t0) / 1e3:.1f} us")
 for i, n in enumerate(names):
     print(f"  {n:11s} mean {ph[:, i].mean():6.2f} us  p50 {np.median(ph[:, i]):6.2f}  p90 {np.percentile(ph[:, i], 90):6.2f}")
@@ -46,9 +48,13 @@ grid = np.linspace(0, ends[-1], 40)
 conc = [int(((t[:, 0] - t0) / 1e3 <= x).sum() - ((t[:, 5] - t0) / 1e3 <= x).sum()) for x in grid]
 print("  resident items over time:", conc)
 # per-CTA finish times (stamp 6 = blockIdx, 7 = SM)
-cta = t[:, 6].astype(int)
+cta = t[:, 6].astype(int)  # (path 1: no SM ids)
 ncta = cta.max() + 1
 cta_end = np.array([(t[cta == c, 5].max() - t0) / 1e3 for c in range(ncta) if (cta == c).any()])
 cta_items = np.bincount(cta)
 print(f"  CTAs {ncta}: items per CTA min {cta_items.min()} max {cta_items.max()}")
 print("  CTA end quantiles (us):   ", np.round(np.percentile(cta_end, [0, 10, 50, 90, 100]), 1))
+if cache._layers[0].args.path == 1:  # stamps 7 / 4: the MMA warp's K-issue start / end
+    print(f"  MMA K issue: start-after-item-start {((t[:, 7] - t[:, 0]) / 1e3).mean():.2f} us, "
+          f"duration {((t[:, 4] - t[:, 7]) / 1e3).mean():.2f} us, ends {((t[:, 4] - t[:, 0]) / 1e3).mean():.2f} us "
+          f"into the item; consumers end K at {((t[:, 1] - t[:, 0]) / 1e3).mean():.2f} us")
