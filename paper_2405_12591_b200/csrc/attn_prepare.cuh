@@ -36,13 +36,14 @@ __device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a, in
   return ((h * 2 + limb) * r + rr) * 8 + (path ? a : (a ^ (2 * (rr & 3))));
 }
 
-// one CTA per segment, one thread per (h, a, rr) of W (threads beyond i1 / r idle): a
+// two CTAs per segment (blockIdx.y: a in [4y, 4y+4): the W scales are per column, so the
+// halves are independent), one thread per (h, a, rr) of W (threads beyond i1 / r idle): a
 // single wave of short-lived CTAs (the kernel is pure latency: ~16 KB in, ~16 KB out)
 template <int G>
-constexpr int kPrepThreadsOf = G * 8 * kMaxRW;
+constexpr int kPrepThreadsOf = G * 4 * kMaxRW;
 
 template <int BITS, int G>
-__global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 4 : 2) attn_prepare_kernel(dq_attn_args args) {
+__global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 8 : 4) attn_prepare_kernel(dq_attn_args args) {
   constexpr int X = kExcess<BITS>;
   __shared__ float q[G][128];
   __shared__ unsigned wmax[G][8][2];
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 4 : 2) attn_prepar
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int s = blockIdx.x;
   const int tid = threadIdx.x;
-  const int h = G == 1 ? 0 : tid / (8 * kMaxRW), a = (tid / kMaxRW) % 8, rr = tid % kMaxRW;
+  const int h = G == 1 ? 0 : tid / (4 * kMaxRW), a = 4 * blockIdx.y + (tid / kMaxRW) % 4, rr = tid % kMaxRW;
   const dq_segment& seg = args.segs[s];
   const int r = seg.r, i1 = seg.i1;
   const bool live = a < i1 && rr < r;
@@ -110,8 +111,7 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 4 : 2) attn_prepar
     if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
   }
   __syncthreads();
-  if (tid < G * 16) {
-
+  if (tid < G * 16 && ((tid >> 1) & 7) / 4 == (int)blockIdx.y) {  // this half's columns (h, a, grp)
     int* mout = reinterpret_cast<int*>(static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride +
                                        kWChunkBytes<G>);
     const float cs = pow2_exp_sub(__uint_as_float((&wmax[0][0][0])[tid]), kWBits<BITS> - args.path);
