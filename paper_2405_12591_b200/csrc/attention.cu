@@ -162,7 +162,7 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     if (!a.wimg || a.wimg_stride < kWImageBytes<G>) return fail(DQ_ERR_INVALID_ARG, "W image workspace too small");
   }
   if (a.nseg > 0 && a.nwork > 0 && (phases & 4)) {
-    attn_prepare_kernel<BITS, G><<<dim3(a.nseg, 2), kPrepThreadsOf<G>, 0, s>>>(a);
+    attn_prepare_kernel<BITS, G><<<dim3(a.nseg, kPrepSplit), kPrepThreadsOf<G>, 0, s>>>(a);
     DQ_LAUNCH_CHECK();
   }
   if (a.path == 1 && a.nwork > 0 && (phases & 1)) {

@@ -36,14 +36,15 @@ __device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a, in
   return ((h * 2 + limb) * r + rr) * 8 + (path ? a : (a ^ (2 * (rr & 3))));
 }
 
-// two CTAs per segment (blockIdx.y: a in [4y, 4y+4): the W scales are per column, so the
-// halves are independent), one thread per (h, a, rr) of W (threads beyond i1 / r idle): a
+// kPrepSplit CTAs per segment (blockIdx.y: a block of columns a; the W scales are per
+// column, so the blocks are independent), one thread per (h, a, rr) of W (threads beyond i1 / r idle): a
 // single wave of short-lived CTAs (the kernel is pure latency: ~16 KB in, ~16 KB out)
+constexpr int kPrepSplit = 4;  // CTAs per segment, each 8 / kPrepSplit columns a
 template <int G>
-constexpr int kPrepThreadsOf = G * 4 * kMaxRW;
+constexpr int kPrepThreadsOf = G * (8 / kPrepSplit) * kMaxRW;
 
 template <int BITS, int G>
-__global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 8 : 4) attn_prepare_kernel(dq_attn_args args) {
+__global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) attn_prepare_kernel(dq_attn_args args) {
   constexpr int X = kExcess<BITS>;
   __shared__ float q[G][128];
   __shared__ unsigned wmax[G][8][2];
@@ -52,7 +53,8 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 8 : 4) attn_prepar
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int s = blockIdx.x;
   const int tid = threadIdx.x;
-  const int h = G == 1 ? 0 : tid / (4 * kMaxRW), a = 4 * blockIdx.y + (tid / kMaxRW) % 4, rr = tid % kMaxRW;
+  constexpr int kA = 8 / kPrepSplit;
+  const int h = G == 1 ? 0 : tid / (kA * kMaxRW), a = kA * blockIdx.y + (tid / kMaxRW) % kA, rr = tid % kMaxRW;
   const dq_segment& seg = args.segs[s];
   const int r = seg.r, i1 = seg.i1;
   const bool live = a < i1 && rr < r;
@@ -63,9 +65,9 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 8 : 4) attn_prepar
     g_lo = g0k[2 * (a * r + rr)];
     g_hi = g0k[2 * (a * r + rr) + 1];
   }
-  if (tid < G * 128) {
+  for (int i = tid; i < G * 128; i += kPrepThreadsOf<G>) {
     const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)seg.unit * G * 128;
-    q[tid / 128][tid % 128] = __half2float(qh[tid]);
+    q[i / 128][i % 128] = __half2float(qh[i]);
   }
   if (tid < G * 16) {
     (&meta.beta[0][0][0])[tid] = 0;
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, G == 1 ? 8 : 4) attn_prepar
     if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
   }
   __syncthreads();
-  if (tid < G * 16 && ((tid >> 1) & 7) / 4 == (int)blockIdx.y) {  // this half's columns (h, a, grp)
+  if (tid < G * 16 && ((tid >> 1) & 7) / (8 / kPrepSplit) == (int)blockIdx.y) {  // this CTA's columns
     int* mout = reinterpret_cast<int*>(static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride +
                                        kWChunkBytes<G>);
     const float cs = pow2_exp_sub(__uint_as_float((&wmax[0][0][0])[tid]), kWBits<BITS> - args.path);
