@@ -26,6 +26,7 @@
 // index is permuted identically on both operands, which is free.  Full-precision K/V
 // never exist anywhere.
 #include "attn_tc.cuh"
+#include "attn_combine.cuh"
 
 #include <algorithm>
 #include <vector>
@@ -36,82 +37,16 @@ namespace {
 
 using namespace attn;
 
-// ---- combine: merge work-item partials with the dense fp16 tail ------------------
-// one CTA (128 threads) per kv head unit u (all head_groups virtual units of it: they
-// share the tail, and the fused append must happen once, after every head has read it);
-// thread d owns output dim d.
+// ---- combine: one CTA (128 threads) per kv head unit; see attn_combine.cuh -----------
 template <int G>
 __global__ void __launch_bounds__(128) combine_kernel(dq_attn_args args) {
   extern __shared__ float tail_s[];  // [tail_cap]
   __shared__ float red[4];
-  const int hg = args.head_groups > 1 ? args.head_groups : 1;
-  const int u = blockIdx.x;
-  const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
-  const int tl = args.tail_len ? args.tail_len[u] : 0;
-  const float l2e = 1.4426950408889634f;
-  for (int hh = 0; hh < G * hg; ++hh) {
-    const int v = u * hg + hh / G, h = hh % G;  // virtual unit, head inside it
-    const int p0 = args.unit_part0[v], np = args.unit_nparts[v];
-    // dense tail scores (log2 domain)
-    float tm = -INFINITY;
-    if (tl > 0) {
-      const __half* qh = reinterpret_cast<const __half*>(args.q) + ((size_t)v * G + h) * kD;
-      const uint2 qv = reinterpret_cast<const uint2*>(qh)[lane];
-      const __half2* q2 = reinterpret_cast<const __half2*>(&qv);
-      const float2 qa = __half22float2(q2[0]), qb = __half22float2(q2[1]);
-      const __half* tk = reinterpret_cast<const __half*>(args.tail_k) + (size_t)u * args.tail_cap * kD;
-      for (int t = warp; t < tl; t += 4) {
-        const uint2 kv = reinterpret_cast<const uint2*>(tk + (size_t)t * kD)[lane];
-        const __half2* k2 = reinterpret_cast<const __half2*>(&kv);
-        const float2 ka = __half22float2(k2[0]), kb = __half22float2(k2[1]);
-        float dot = qa.x * ka.x + qa.y * ka.y + qb.x * kb.x + qb.y * kb.y;
-        for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (lane == 0) tail_s[t] = dot * args.sm_scale * l2e;
-      }
-      __syncthreads();
-      for (int t = d; t < tl; t += 128) tm = fmaxf(tm, tail_s[t]);
-      for (int o = 16; o; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-      if (lane == 0) red[warp] = tm;
-      __syncthreads();
-      tm = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-      __syncthreads();
-    }
-    float M = tm;
-    for (int i = 0; i < np; ++i) M = fmaxf(M, args.part_ml[((size_t)(p0 + i) * G + h) * 2]);
-    float L = 0.f, O = 0.f;
-    for (int i = 0; i < np; ++i) {
-      const size_t s = (size_t)(p0 + i) * G + h;
-      const float m = args.part_ml[s * 2];
-      if (m == -INFINITY) continue;
-      const float f = exp2f(m - M);
-      L += f * args.part_ml[s * 2 + 1];
-      O += f * args.part_o[s * kD + d];
-    }
-    if (tl > 0) {
-      const __half* tv = reinterpret_cast<const __half*>(args.tail_v) + (size_t)u * args.tail_cap * kD;
-      float lt = 0.f, ot = 0.f;
-      for (int t = 0; t < tl; ++t) {
-        const float p = exp2f(tail_s[t] - M);
-        lt += p;
-        ot = fmaf(p, __half2float(tv[(size_t)t * kD + d]), ot);
-      }
-      L += lt;
-      O += ot;
-      __syncthreads();
-    }
-    __half* out = reinterpret_cast<__half*>(args.out) + ((size_t)v * G + h) * kD;
-    out[d] = __float2half_rn(L > 0.f ? O / L : 0.f);
-  }
-  if (args.app_k) {
-    // fused dq_tail_append: the new token joins the tail after this step's attention
-    __syncthreads();  // every thread has read tail_len[u]
-    if (tl < args.tail_cap) {
-      const size_t dst = ((size_t)u * args.tail_cap + tl) * kD + d;
-      reinterpret_cast<__half*>(args.tail_k)[dst] = reinterpret_cast<const __half*>(args.app_k)[(size_t)u * kD + d];
-      reinterpret_cast<__half*>(args.tail_v)[dst] = reinterpret_cast<const __half*>(args.app_v)[(size_t)u * kD + d];
-    }
-    if (d == 0) args.tail_len[u] = tl + 1;
-  }
+  // programmatic dependent launch: this grid was scheduled while the split kernel ran;
+  // wait for its partials, and let the next kernel (the next layer's prepare) get scheduled
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  combine_unit<G>(args, blockIdx.x, threadIdx.x, tail_s, red, [] { __syncthreads(); });
 }
 
 __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __half* __restrict__ v_rows,
@@ -162,8 +97,16 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     if (!a.wimg || a.wimg_stride < kWImageBytes<G>) return fail(DQ_ERR_INVALID_ARG, "W image workspace too small");
   }
   if (a.nseg > 0 && a.nwork > 0 && (phases & 4)) {
-    attn_prepare_kernel<BITS, G><<<dim3(a.nseg, kPrepSplit), kPrepThreadsOf<G>, 0, s>>>(a);
-    DQ_LAUNCH_CHECK();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.nseg, kPrepSplit);
+    cfg.blockDim = dim3(kPrepThreadsOf<G>);
+    cfg.stream = s;
+    cudaLaunchAttribute attr_pdl[1];
+    attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr_pdl;
+    cfg.numAttrs = 1;
+    DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_prepare_kernel<BITS, G>, a));
   }
   if (a.path == 1 && a.nwork > 0 && (phases & 1)) {
     if constexpr (BITS == 4 && G == 1) {
@@ -208,8 +151,17 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
   if (phases & 2) {
     const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1);
     const int hg = a.head_groups > 1 ? a.head_groups : 1;
-    combine_kernel<G><<<a.units / hg, 128, csmem, s>>>(a);
-    DQ_LAUNCH_CHECK();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.units / hg));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = csmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_pdl[1];
+    attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr_pdl;
+    cfg.numAttrs = 1;
+    DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, combine_kernel<G>, a));
   }
   return DQ_OK;
 }

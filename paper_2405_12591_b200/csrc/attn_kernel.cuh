@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     // programmatic dependent launch: everything above overlapped the prepare kernel; its
     // output (the per-segment W images) is read from here on
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
     if (sm.sub[0].nbt > 0) issue_wimg<G>(sm, args, sm.sub[0]);
   }
 

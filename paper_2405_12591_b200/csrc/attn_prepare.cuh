@@ -49,8 +49,11 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
   __shared__ float q[G][128];
   __shared__ unsigned wmax[G][8][2];
   __shared__ WMeta<G> meta;
-  // the dependent split kernel may start its prologue (barriers, code copies) right away
+  // the dependent split kernel may start its prologue (barriers, code copies) right away;
+  // q may come from the previous kernel in the stream (launched with programmatic
+  // serialization, this grid can be scheduled before that kernel finished)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int s = blockIdx.x;
   const int tid = threadIdx.x;
   constexpr int kA = 8 / kPrepSplit;

@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
 
   if (tid == 0) {
     mbar_wait(&sm.descfull[0], 0);
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // W images come from the prepare kernel
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
     if (sm.sub[0].nbt > 0) issue_wimg_tc(sm, args, sm.sub[0]);
   }
 
