@@ -218,6 +218,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
           if (g >= kStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kStages - 1) & 1));
           issue_stage<BITS>(d, ls, sm.ring[slot], &sm.full[slot]);
           if (ls == min(2, d.stages - 1)) {
+            // the ticket counter is shared with the previous launch on these args: under
+            // programmatic dependent launch, wait for that grid before drawing from it
+            if (k == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");
             // the next item, fetched while the ring is full: ticket, then its descriptor
             const int nxt = (int)gridDim.x + atomicAdd(args.sched, 1);
             nhave = nxt < args.nwork;

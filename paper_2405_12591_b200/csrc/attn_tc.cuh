@@ -15,9 +15,12 @@
 // Y buffers are double-buffered, so the consumers widen stage s+1 while stage s's MMAs run,
 // and fold stage s's Y (exact s32 -> scaled fp32) into registers afterwards.
 //
-// The numerics are identical to path 0: exact integer products of the excess-coded codes
-// with 15-bit two-limb W (per column and bond-row group scale) and 15-bit two-limb P (per
-// 64-row tile scale), excess removed exactly, fp32 accumulation across tiles.
+// Numerics: exact integer products of the excess-coded codes with 14-bit two-limb W (per
+// column and bond-row group scale, both limbs signed so one N = 16 UMMA takes them) and
+// 23-bit three-limb P (one scale per item: P = exp2(s - m) <= 1 in units of 2^-23).  Y is
+// accumulated over the whole item in TMEM (s32 per limb) and folded once per item; the
+// excess offset is removed exactly with sum_b P, accumulated alongside by a UMMA whose A
+// operand is all ones.
 #pragma once
 
 #include "attn_kernel.cuh"
@@ -29,9 +32,11 @@ constexpr int kTcStages = 10;                        // 10 x 16 KB ring, one CTA
 constexpr int kTcWarps = kWarps + 2;                 // + producer (8) + MMA (9)
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTmemCols = 512;
-// TMEM column map: kNumA A buffers of 64 columns, then S (64), then 2 Y buffers (64 each)
-constexpr int kNumA = 4;
-constexpr uint32_t kColA = 0, kColS = 64 * kNumA, kColY = kColS + 64;
+// TMEM column map: 2 A buffers of 64 columns, S (64), Y (8 M-blocks x 32: P limbs hi / mid /
+// lo / zero), a constant all-ones A operand (8 columns = K 32) and sum_b P (32)
+constexpr int kNumA = 2;
+constexpr uint32_t kColA = 0, kColS = 64 * kNumA, kColY = kColS + 64, kColOnes = kColY + 256, kColPsum = 480;
+constexpr int kPLimbs = 4;  // P limb groups of the V B operand (N = 32): hi, mid, lo, zero
 
 __device__ __forceinline__ uint32_t tc_idesc(int M, int N, int a_signed, int b_signed) {
   return (2u << 4) | ((uint32_t)a_signed << 7) | ((uint32_t)b_signed << 10) | ((uint32_t)(N >> 3) << 17) |
@@ -107,15 +112,13 @@ struct TcSmem {
   alignas(1024) unsigned char ring[kTcStages][kStageBytes];
   alignas(16) uint4 w[2 * kMaxR * 8];     // W limbs, chunk (limb * r + rr) * 8 + a (path-1 image)
   alignas(16) float4 g0v[8 * kMaxR * 2];  // fp32 G0v [a][rr][c]
-  alignas(128) unsigned char pb[2][kTiles * 4 * 128];  // P limbs: K-major core matrices, chunk b/16
+  alignas(128) unsigned char pb[kPLimbs][kTiles * 4 * 128];  // P limbs: K-major core matrices, chunk b/16
   float red[kWarps][kD];
   alignas(16) WMeta<1> wmeta;
   SubItem sub[kSubRing];
   uint64_t full[kTcStages], empty[kTcStages];
   uint64_t wbar, g0bar, descfull[kSubRing];
-  uint64_t afull[kNumA], afree[kNumA], yfull[2], yfree[2], sfull, sfree, pfull;
-  unsigned pmax[8][kTiles];
-  int gamma[8][kTiles];
+  uint64_t afull[kNumA], afree[kNumA], sfull, sfree, pfull, vdone, yfree;
   float rowmax[kWarps];
   float lsum[kWarps];
   uint32_t tmem;
@@ -151,13 +154,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
       mbar_init(&sm.afull[b], kWarps);
       mbar_init(&sm.afree[b], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.yfull[b], 1);
-      mbar_init(&sm.yfree[b], kWarps);
-    }
     mbar_init(&sm.sfull, 1);
     mbar_init(&sm.sfree, kWarps);
     mbar_init(&sm.pfull, 1);
+    mbar_init(&sm.vdone, 1);
+    mbar_init(&sm.yfree, kWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == kWarps + 1) {
@@ -165,10 +166,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid < 8 * kTiles) {
-    (&sm.gamma[0][0])[tid] = 0;
-    (&sm.pmax[0][0])[tid] = 0u;
-  }
+  for (int i = tid; i < (int)sizeof(sm.pb[3]) / 4; i += kTcThreads) reinterpret_cast<int*>(sm.pb[3])[i] = 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -197,6 +195,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
           if (g >= kTcStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kTcStages - 1) & 1));
           issue_stage<4>(d, ls, sm.ring[slot], &sm.full[slot]);
           if (ls == min(2, d.stages - 1)) {
+            // the ticket counter is shared with the previous launch on these args: under
+            // programmatic dependent launch, wait for that grid before drawing from it
+            if (k == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");
             const int nxt = (int)gridDim.x + atomicAdd(args.sched, 1);
             nhave = nxt < args.nwork;
             if (nhave) tc_load_sub(nd, args, nxt);
@@ -218,8 +219,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     if (lane == 0) {
       // both limbs of a B operand in one UMMA: N = 16 rows (hi limb a = 0..7, lo limb a = 0..7)
       const uint32_t id_k = tc_idesc(128, 16, 0, 1);  // codes u8 x W limbs s8
-      const uint32_t id_v = tc_idesc(128, 16, 0, 0);  // codes u8 x P limbs u8
-      int na = 0, nv = 0;  // A-buffer uses, V stages (Y-buffer uses)
+      const uint32_t id_v = tc_idesc(128, 32, 0, 0);  // codes u8 x P limbs u8 (hi, mid, lo, 0)
+      int na = 0;  // A-buffer uses
       for (int j = 0;; ++j) {
         mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
         const SubItem d = sm.sub[j % kSubRing];
@@ -251,25 +252,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
         tc_commit(&sm.sfull);
         if (args.trace) args.trace[(size_t)d.item * 8 + 4] = global_ns();  // MMA warp: K issue done
         mbar_wait(&sm.pfull, (uint32_t)(j & 1));  // P limbs of this item in shared memory
+        if (j > 0) mbar_wait(&sm.yfree, (uint32_t)((j - 1) & 1));  // Y / sum P of the previous item read
         tc_fence_after();
         for (int t = 0; t < d.nbt; ++t)
-          for (int sl = 0; sl < 2; ++sl, ++na, ++nv) {
-            const int ab = na % kNumA, yb = nv & 1;
+          for (int sl = 0; sl < 2; ++sl, ++na) {
+            const int ab = na % kNumA;
             mbar_wait(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
-            if (nv >= 2) mbar_wait(&sm.yfree[yb], (uint32_t)(((nv >> 1) - 1) & 1));
             tc_fence_after();
             for (int kk = 0; kk < 2; ++kk) {  // 64 b = 2 k-steps
-              // rows 0-7: P hi limb, rows 8-15: P lo limb (the next limb buffer)
+              // B rows: 0-7 P hi limb, 8-15 mid, 16-23 lo, 24-31 zero (the next limb buffers)
               const uint64_t bdesc = tc_sdesc(&sm.pb[0][(t * 4 + kk * 2) * 128], 128, sizeof(sm.pb[0]));
+              const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
               for (int mb = 0; mb < 4; ++mb) {
-                const uint32_t dcol = kColY + (uint32_t)(yb * 64 + mb * 16);
+                const uint32_t dcol = kColY + (uint32_t)((sl * 4 + mb) * 32);
                 const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * 16 + kk * 8);
-                tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_v, kk ? 1u : 0u);
+                tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_v, acc);
               }
+              if (sl == 0) tc_mma_ts(tmem + kColPsum, tmem + kColOnes, bdesc, id_v, acc);  // sum_b P
             }
             tc_commit(&sm.afree[ab]);
-            tc_commit(&sm.yfull[yb]);
           }
+        tc_commit(&sm.vdone);
       }
     }
     // wait for the consumers' last TMEM reads, then free TMEM
@@ -285,7 +288,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
   const int half = warp >> 2;          // K phase: M-block; V phase: M-blocks 2*half, 2*half+1
   const int lane_in = 32 * q + lane;   // TMEM lane (row inside an M-block)
   const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-  int st = 0, na = 0, nv = 0;
+  int st = 0, na = 0;
+  if (warp < 4) {  // the constant all-ones A operand (K = 32 bytes of 1) used to sum P
+    uint32_t ones[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) ones[i] = 0x01010101u;
+    tc_st16(tmem + lane_addr + kColOnes, ones);  // 16 columns: the 8 used + 8 spare
+    tc_wait_st();
+  }
   auto release = [&](int s) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s % kTcStages]);
@@ -398,73 +408,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     m = sm.rowmax[0];
 #pragma unroll
     for (int w = 1; w < kWarps; ++w) m = fmaxf(m, sm.rowmax[w]);
-    float p[8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      p[a] = s[a] == -INFINITY ? 0.f : exp2f(s[a] - m);
-      float v = p[a];
-      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0 && jt < nbt && half < nmb) atomicMax(&sm.pmax[a][jt], __float_as_uint(v));
-    }
-    named_sync(kThreads);
     float lsum = 0.f;
     {
+      // P = exp2(s - m) <= 1 as a 23-bit integer, three 8-bit limbs (hi <= 128)
       const int b_item = jt * kI2Pad + b_in;
       const int pos = (b_item >> 4) * 128 + inv_ord16<4>(b_item & 15);
 #pragma unroll
       for (int a = 0; a < 8; ++a) {
-        const float pm = __uint_as_float(sm.pmax[a][min(jt, kTiles - 1)]);
-        const float pq = pow2_sub_exp(pm, kPBits<4>), pinv = pow2_exp_sub(pm, kPBits<4>);
-        const int pint = __float2int_rn(p[a] * pq);
-        lsum += (float)pint * pinv;
+        const int pint = s[a] == -INFINITY ? 0 : __float2int_rn(exp2f(s[a] - m) * 8388608.f);
+        lsum += (float)pint;
         if (half < nmb) {
-          sm.pb[0][pos + a * 16] = (unsigned char)(pint >> 8);
-          sm.pb[1][pos + a * 16] = (unsigned char)(pint & 0xFF);
+          sm.pb[0][pos + a * 16] = (unsigned char)(pint >> 16);
+          sm.pb[1][pos + a * 16] = (unsigned char)((pint >> 8) & 0xFF);
+          sm.pb[2][pos + a * 16] = (unsigned char)(pint & 0xFF);
         }
-        int gs = pint;
-        for (int o = 16; o; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
-        if (X && lane == 0 && jt < nbt && half < nmb) atomicAdd(&sm.gamma[a][jt], X * gs);
       }
+      lsum *= 1.f / 8388608.f;
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P read by the tensor cores
     named_sync(kThreads);
     if (tid == 0) mbar_arrive(&sm.pfull);
     stamp(2);
 
-    // ---- V phase: widen V codes into TMEM, fold each stage's Y into fp32 registers ---------
-    // thread rows: (slice sl, M-block 2*half + i): (r, e) = (32 sl + 8 (2 half + i) + lane_in / 16, lane_in % 16)
-    float accv[2][2][8];
-#pragma unroll
-    for (int sl = 0; sl < 2; ++sl)
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int a = 0; a < 8; ++a) accv[sl][i][a] = 0.f;
-    auto fold = [&](int t, int sl, int yb, int nvs) {
-      mbar_wait(&sm.yfull[yb], (uint32_t)((nvs >> 1) & 1));
-      tc_fence_after();
-      int y[2][2][8];
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int limb = 0; limb < 2; ++limb)
-          tc_ld8(tmem + lane_addr + kColY + (uint32_t)(yb * 64 + ((2 * half + i) * 2 + limb) * 8), y[i][limb]);
-      tc_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.yfree[yb]);
-#pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        const float pinv = pow2_exp_sub(__uint_as_float(sm.pmax[a][t]), kPBits<4>);
-        const int gam = sm.gamma[a][t];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-          accv[sl][i][a] = fmaf((float)(256 * y[i][0][a] + y[i][1][a] - gam), pinv, accv[sl][i][a]);
-      }
-    };
-    int pend_t = -1, pend_sl = 0, pend_yb = 0, pend_nv = 0;
+    // ---- V phase: widen V codes into TMEM; Y accumulates over the item in TMEM -----------------
     for (int t = 0; t < nbt; ++t)
-      for (int sl = 0; sl < 2; ++sl, ++st, ++na, ++nv) {
+      for (int sl = 0; sl < 2; ++sl, ++st, ++na) {
         const int slot = st % kTcStages, ab = na % kNumA;
         mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
         if (na >= kNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kNumA - 1) & 1));
@@ -488,10 +456,37 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.afull[ab]);
         release(st);
-        if (pend_t >= 0) fold(pend_t, pend_sl, pend_yb, pend_nv);
-        pend_t = t, pend_sl = sl, pend_yb = nv & 1, pend_nv = nv;
       }
-    fold(pend_t, pend_sl, pend_yb, pend_nv);
+    // Y (thread rows: slice sl, M-block 2*half + i: (r, e) = (32 sl + 8 (2 half + i) + lane_in / 16,
+    // lane_in % 16)) and sum_b P, once per item
+    mbar_wait(&sm.vdone, (uint32_t)(j & 1));
+    tc_fence_after();
+    float accv[2][2][8];
+    {
+      int ps[3][8];
+#pragma unroll
+      for (int l = 0; l < 3; ++l) tc_ld8(tmem + lane_addr + kColPsum + (uint32_t)(l * 8), ps[l]);
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          int y[3][8];
+#pragma unroll
+          for (int l = 0; l < 3; ++l)
+            tc_ld8(tmem + lane_addr + kColY + (uint32_t)((sl * 4 + 2 * half + i) * 32 + l * 8), y[l]);
+          tc_wait_ld();
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            // sum_b (code + X) P - X sum_b P, per limb exact in s32, then 2^16 / 2^8 / 1 in fp32
+            const float hi = (float)(y[0][a] - X * ps[0][a]), mid = (float)(y[1][a] - X * ps[1][a]);
+            const float lo = (float)(y[2][a] - X * ps[2][a]);
+            accv[sl][i][a] = fmaf(fmaf(hi, 256.f, mid), 256.f, lo) * (1.f / 8388608.f);
+          }
+        }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.yfree);
     stamp(3);
 
     // ---- epilogue: O[c, e] = scale_v * sum_{a, r} G0v[a, c, r] Y[(r, e), a] ---------------------
@@ -522,10 +517,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     }
     if (lane == 0) sm.lsum[warp] = lsum;
     named_sync(kThreads);
-    if (tid < 8 * kTiles) {  // ready for the next item's softmax
-      (&sm.gamma[0][0])[tid] = 0;
-      (&sm.pmax[0][0])[tid] = 0u;
-    }
     if (tid < kD) {
       float v = 0.f;
 #pragma unroll
