@@ -222,17 +222,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
       const uint32_t id_v = tc_idesc(128, 32, 0, 0);  // codes u8 x P limbs u8 (hi, mid, lo, 0)
       int na = 0;  // A-buffer uses
       for (int j = 0;; ++j) {
-        mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+        mbar_wait_spin(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
         const SubItem d = sm.sub[j % kSubRing];
         if (d.nbt == 0) break;
         const int nmb = (d.nbt + 1) / 2;
-        mbar_wait(&sm.wbar, (uint32_t)(j & 1));        // W image of this item's segment
-        if (j > 0) mbar_wait(&sm.sfree, (uint32_t)((j - 1) & 1));  // S of the previous item read
+        mbar_wait_spin(&sm.wbar, (uint32_t)(j & 1));        // W image of this item's segment
+        if (j > 0) mbar_wait_spin(&sm.sfree, (uint32_t)((j - 1) & 1));  // S of the previous item read
         if (args.trace) args.trace[(size_t)d.item * 8 + 7] = global_ns();  // MMA warp: K issue starts
         bool acc_s[2] = {false, false};  // per bond-row group: accumulate into S?
+        int64_t wait_ns = 0;
         for (int ks = 0; ks < d.nK; ++ks, ++na) {
           const int ab = na % kNumA;
-          mbar_wait(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
+          const int64_t w0 = args.trace ? global_ns() : 0;
+          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
+          if (args.trace) wait_ns += global_ns() - w0;
           tc_fence_after();
           const int rk0 = ks * d.RK, nr = min(d.RK, d.r - rk0);
           for (int kk = 0; kk < nr / 2; ++kk) {  // UMMA k-step = 32 bytes = 2 bond rows
@@ -251,13 +254,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
         }
         tc_commit(&sm.sfull);
         if (args.trace) args.trace[(size_t)d.item * 8 + 4] = global_ns();  // MMA warp: K issue done
-        mbar_wait(&sm.pfull, (uint32_t)(j & 1));  // P limbs of this item in shared memory
-        if (j > 0) mbar_wait(&sm.yfree, (uint32_t)((j - 1) & 1));  // Y / sum P of the previous item read
+        if (args.trace) args.trace[(size_t)d.item * 8 + 6] = wait_ns;      // MMA warp: K waits on A
+        mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs of this item in shared memory
+        if (j > 0) mbar_wait_spin(&sm.yfree, (uint32_t)((j - 1) & 1));  // Y / sum P of the previous item read
         tc_fence_after();
         for (int t = 0; t < d.nbt; ++t)
           for (int sl = 0; sl < 2; ++sl, ++na) {
             const int ab = na % kNumA;
-            mbar_wait(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
+            mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
             tc_fence_after();
             for (int kk = 0; kk < 2; ++kk) {  // 64 b = 2 k-steps
               // B rows: 0-7 P hi limb, 8-15 mid, 16-23 lo, 24-31 zero (the next limb buffers)
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
       if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + k] = global_ns();
     };
     stamp(0);
-    if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + 6] = blockIdx.x;
+
     if (tid == 0) {  // G0v of this item (its buffer is free: the previous epilogue ended in a barrier)
       const uint32_t gb = (uint32_t)(d.i1 * r * 32);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -47,14 +47,17 @@ print("  end-time quantiles (us):  ", np.round(np.percentile(ends, [0, 25, 50, 7
 grid = np.linspace(0, ends[-1], 40)
 conc = [int(((t[:, 0] - t0) / 1e3 <= x).sum() - ((t[:, 5] - t0) / 1e3 <= x).sum()) for x in grid]
 print("  resident items over time:", conc)
-# per-CTA finish times (stamp 6 = blockIdx, 7 = SM)
+if cache._layers[0].args.path == 1:  # stamps 7 / 4: the MMA warp's K-issue start / end
+    print(f"  MMA K issue: start-after-item-start {((t[:, 7] - t[:, 0]) / 1e3).mean():.2f} us, "
+          f"duration {((t[:, 4] - t[:, 7]) / 1e3).mean():.2f} us, ends {((t[:, 4] - t[:, 0]) / 1e3).mean():.2f} us "
+          f"into the item; consumers end K at {((t[:, 1] - t[:, 0]) / 1e3).mean():.2f} us; "
+          f"MMA waited {(t[:, 6] / 1e3).mean():.2f} us of it on A buffers")
+# per-CTA finish times (stamp 6 = blockIdx, 7 = SM; path 1 reuses them)
+if cache._layers[0].args.path == 1:
+    t[:, 6] = 0
 cta = t[:, 6].astype(int)  # (path 1: no SM ids)
 ncta = cta.max() + 1
 cta_end = np.array([(t[cta == c, 5].max() - t0) / 1e3 for c in range(ncta) if (cta == c).any()])
 cta_items = np.bincount(cta)
 print(f"  CTAs {ncta}: items per CTA min {cta_items.min()} max {cta_items.max()}")
 print("  CTA end quantiles (us):   ", np.round(np.percentile(cta_end, [0, 10, 50, 90, 100]), 1))
-if cache._layers[0].args.path == 1:  # stamps 7 / 4: the MMA warp's K-issue start / end
-    print(f"  MMA K issue: start-after-item-start {((t[:, 7] - t[:, 0]) / 1e3).mean():.2f} us, "
-          f"duration {((t[:, 4] - t[:, 7]) / 1e3).mean():.2f} us, ends {((t[:, 4] - t[:, 0]) / 1e3).mean():.2f} us "
-          f"into the item; consumers end K at {((t[:, 1] - t[:, 0]) / 1e3).mean():.2f} us")

@@ -10,15 +10,15 @@ __device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo, uint32_t 
 }
 __host__ __device__ constexpr uint32_t idesc(int M, int N) { return (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24); }
 
-template <int N, bool TS, int ND>
+template <int N, bool TS, int ND, bool BUSY = false, bool VARY = false>
 __global__ void rate(long long* out, int iters) {
-  __shared__ __align__(1024) uint8_t sa[128 * 32];
-  __shared__ __align__(1024) uint8_t sb[256 * 32];
+  __shared__ __align__(1024) uint8_t sa[128 * 32 * 2];
+  __shared__ __align__(1024) uint8_t sb[256 * 32 * 2];
   __shared__ uint32_t tbase;
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < 128 * 32; i += blockDim.x) sa[i] = i & 7;
-  for (int i = tid; i < 256 * 32; i += blockDim.x) sb[i] = i & 3;
+  for (int i = tid; i < 128 * 32 * 2; i += blockDim.x) sa[i] = i & 7;
+  for (int i = tid; i < 256 * 32 * 2; i += blockDim.x) sb[i] = i & 3;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -32,49 +32,61 @@ __global__ void rate(long long* out, int iters) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tbase;
+  __shared__ volatile int stop;
+  if (tid == 0) stop = 0;
+  __syncthreads();
+  if (BUSY && warp >= 1) {  // other warps keep writing TMEM (like the consumers widening codes)
+    uint32_t v[16];
+    for (int i = 0; i < 16; ++i) v[i] = 0x01010101u * (i + tid);
+    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + 64;
+    while (!stop) {
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+                   "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+                   "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+    }
+  }
   if (tid == 0) {
     const uint64_t b = sdesc(sb, 128, (32 / 16) * 128), a = sdesc(sa, 128, (32 / 16) * 128);
     const uint32_t id = idesc(128, N);
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
       if (TS)
-        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem + 256 + (i % ND) * N), "r"(tmem), "l"(b), "r"(id), "r"((uint32_t)(i >= ND)));
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem + 256 + (i % ND) * N), "r"(tmem + (VARY ? (i % 8) * 8 : 0)), "l"(VARY ? b + (uint64_t)((i % 8) * 16) : b), "r"(id), "r"((uint32_t)(i >= ND)));
       else
-        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + 256 + (i % ND) * N), "l"(a), "l"(b), "r"(id), "r"((uint32_t)(i >= ND)));
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + 256 + (i % ND) * N), "l"(VARY ? a + (uint64_t)((i % 8) * 16) : a), "l"(VARY ? b + (uint64_t)((i % 8) * 16) : b), "r"(id), "r"((uint32_t)(i >= ND)));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}" ::"r"(smem_u32(&bar)));
     out[0] = clock64() - t0;
+    stop = 1;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int N, bool TS, int ND = 1>
+template <int N, bool TS, int ND = 1, bool BUSY = false, bool VARY = false>
 void run() {
   long long* d;
   cudaMalloc(&d, 8);
   long long c1 = 0, c2 = 0;
-  rate<N, TS, ND><<<1, 128>>>(d, 64);
+  rate<N, TS, ND, BUSY, VARY><<<1, 128>>>(d, 64);
   cudaDeviceSynchronize();
-  rate<N, TS, ND><<<1, 128>>>(d, 64);
+  rate<N, TS, ND, BUSY, VARY><<<1, 128>>>(d, 64);
   cudaMemcpy(&c1, d, 8, cudaMemcpyDeviceToHost);
-  rate<N, TS, ND><<<1, 128>>>(d, 1024);
+  rate<N, TS, ND, BUSY, VARY><<<1, 128>>>(d, 1024);
   cudaMemcpy(&c2, d, 8, cudaMemcpyDeviceToHost);
-  printf("ND=%d N=%3d A=%s: %.1f cycles per UMMA (M128 K32), first 64 took %lld cycles, %s\n", ND, N,
+  printf("VARY=%d BUSY=%d ND=%d N=%3d A=%s: %.1f cycles per UMMA (M128 K32), first 64 took %lld cycles, %s\n", (int)VARY, (int)BUSY, ND, N,
          TS ? "TMEM" : "SMEM", (double)(c2 - c1) / (1024 - 64), c1, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
 int main() {
-  run<8, true, 1>();
-  run<8, true, 4>();
   run<16, true, 4>();
-  run<16, true, 8>();
-  run<64, true, 2>();
-  run<64, true, 4>();
-  run<8, false, 4>();
-  run<16, false, 8>();
+  run<16, true, 4, false, true>();
+  run<16, true, 1, false, true>();
+  run<16, false, 4, false, true>();
+  run<16, true, 4, true, true>();
   return 0;
 }
