@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     for (int ks = 0; ks < d.nK; ++ks, ++st) {
       const int slot = st % kStages;
       mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
+#ifdef DQ_ATTN_NULL_CONSUMER  // measurement only: the memory pipeline without the contractions
+      release(st);
+      continue;
+#endif
       const int rk0 = ks * d.RK;
       const int nr = min(d.RK, r - rk0);
       if (jt < nbt) {
@@ -355,6 +359,19 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       release(st);
     }
     if (r > kGroupR) flush_group(1);
+#ifdef DQ_ATTN_NULL_STREAM  // measurement only: the producer / ring / scheduler alone
+    for (int vs = 0; vs < nbt * d.nslices; ++vs, ++st) {
+      mbar_wait(&sm.full[st % kStages], (uint32_t)((st / kStages) & 1));
+      release(st);
+    }
+    named_sync(kThreads);
+    if (tid == 0) {
+      const int jn = j + 1;
+      mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
+      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G>(sm, args, sm.sub[jn % kSubRing]);
+    }
+    continue;
+#endif
 
     stamp(2);
     // ---- phase 2: softmax of the sub-item straight from the accumulators --------------
@@ -470,6 +487,11 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     for (int vs = 0, btl = 0, sl = 0; vs < nV; ++vs, ++st) {
       const int slot = st % kStages;
       mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
+#ifdef DQ_ATTN_NULL_CONSUMER
+      if (++sl == d.nslices) sl = 0, ++btl;
+      release(st);
+      continue;
+#endif
       if (sl == my_slice) {
         uint4 ph[G], pl_[G];
         int gam[G][2];
