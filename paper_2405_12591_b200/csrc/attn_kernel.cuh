@@ -20,7 +20,10 @@
 namespace dq {
 namespace attn {
 
-constexpr int kWarps = 8;                   // consumer warps
+#ifndef DQ_ATTN_WARPS
+#define DQ_ATTN_WARPS 8
+#endif
+constexpr int kWarps = DQ_ATTN_WARPS;       // consumer warps (8, or 16 with one CTA per SM)
 constexpr int kThreads = kWarps * 32;       // consumer threads
 constexpr int kCtaThreads = kThreads + 32;  // + the producer warp
 constexpr int kD = 128;
@@ -273,9 +276,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 
     stamp(1);
     // ---- phase 1: S = W . codes_k on the int8 tensor pipe ------------------------------
-    constexpr int MT = 2;                   // 16-row m-tiles per warp (32 b rows)
-    const int jt = warp >> 1;               // tile of this warp inside the sub-item
-    const int bl_base = 32 * (warp & 1);    // first row of this warp inside the tile
+    constexpr int kWpt = kWarps / kTiles;   // warps per 64-row tile
+    constexpr int MT = 4 / kWpt;            // 16-row m-tiles per warp
+    const int jt = warp / kWpt;             // tile of this warp inside the sub-item
+    const int bl_base = 16 * MT * (warp % kWpt);  // first row of this warp inside the tile
     int acc_hi[MT][G][4], acc_lo[MT][G][4];
     float sacc[MT][G][4];  // scores in the log2 domain, accumulated per bond-row group
 #pragma unroll
@@ -476,9 +480,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     const int kslice = kWarps / d.nslices;
     const int my_slice = warp / kslice;
     const int rbase_in_slice = (warp % kslice) * rw;
-    float accv[8][G][4];
+    constexpr int kRw = kMaxR / kWarps;  // bond rows per warp at r = 64
+    float accv[kRw][G][4];
 #pragma unroll
-    for (int t = 0; t < 8; ++t)
+    for (int t = 0; t < kRw; ++t)
 #pragma unroll
       for (int h = 0; h < G; ++h)
 #pragma unroll
@@ -508,7 +513,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         }
         const unsigned char* buf = sm.ring[slot];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < kRw; ++t) {
           if (t < rw) {
             const int rl = rbase_in_slice + t;
             uint32_t x0[4], x1[4];
@@ -545,7 +550,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     mbar_wait(&sm.g0bar, (uint32_t)(j & 1));  // fp32 G0v [a][rr][c] (normalised), in the W buffer
     const float4* g0v = sm.wg.g0v;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < kRw; ++t) {
       if (t < rw) {
         const int rr = warp * rw + t;
 #pragma unroll

@@ -1,0 +1,76 @@
+"""Quantisation-error statistics of the paper's tables on the device path vs the reference's
+own sweeps (tests/golden/golden_analysis.json, made by make_golden_analysis.py)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(os.path.join(HERE, "golden", "golden_analysis.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def suite():
+    from paper_2405_12591_b200.analysis import default_suite
+
+    return default_suite()
+
+
+def _by_key(records):
+    return {(r["method"] if isinstance(r, dict) else r.method, r["bits"] if isinstance(r, dict) else r.bits,
+             r["seed"] if isinstance(r, dict) else r.seed): r for r in records}
+
+
+def test_strategy_sweep_matches_reference(golden, suite):
+    """matrix RTN / DecoQuant large core / both cores at 2, 4, 8 bits on 20 outlier matrices:
+    every record within 1e-3 relative of the reference, medians within 2e-4, and the paper's
+    ordering (DecoQuant below matrix RTN at every bit width)."""
+    from paper_2405_12591_b200.analysis import median_by, strategy_sweep
+
+    got = strategy_sweep(suite)
+    ref = _by_key(golden["strategy"])
+    assert len(got) == len(ref) == 180
+    for r in got:
+        g = ref[(r.method, r.bits, r.seed)]
+        assert r.param_overhead == pytest.approx(g["param_overhead"], rel=1e-12)
+        assert r.frobenius_error == pytest.approx(g["frobenius_error"], rel=1e-3), (r, g)
+    med = median_by(got)
+    for (method, bits), v in med.items():
+        assert v == pytest.approx(golden["strategy_median"][f"{method}/{bits}"], rel=2e-4)
+    for bits in (2, 4, 8):
+        assert med[("deco-tl-only", bits)] < med[("matrix-rtn", bits)]
+
+
+def test_decomposition_comparison_matches_reference(golden, suite):
+    from paper_2405_12591_b200.analysis import decomposition_comparison, median_by
+
+    got = decomposition_comparison(suite)
+    med = median_by(got)
+    for (method, bits), v in med.items():
+        assert v == pytest.approx(golden["decomposition_median"][f"{method}/{bits}"], rel=2e-3), method
+    assert med[("deco-tl-only", 4)] < med[("svd-quant", 4)] < med[("qr-quant", 4)]
+
+
+def test_migration_report_matches_reference(golden, suite):
+    """The large core's IQR collapses, the small core keeps the outliers (IQR statistics of the
+    device factorisation against the reference's LAPACK one)."""
+    from paper_2405_12591_b200.analysis import migration_report
+
+    mat, large, small = migration_report(suite[0])
+    g = golden["migration"]
+    assert (mat.q1, mat.q3, mat.outlier_count) == (g["matrix"]["q1"], g["matrix"]["q3"], g["matrix"]["outlier_count"])
+    # the cores are compared sign-invariantly: a bond row's sign is a convention
+    # (ours: largest entry positive, LAPACK's: arbitrary), and it shifts quartiles slightly
+    for st, k in ((large, "large"), (small, "small")):
+        assert st.total_count == g[k]["total"]
+        assert st.iqr == pytest.approx(g[k]["iqr"], rel=2e-2)
+        assert abs(st.outlier_count - g[k]["outlier_count"]) <= 0.02 * g[k]["total"]
+    assert large.iqr < 0.05 * mat.iqr  # the outliers migrate out of the large core
