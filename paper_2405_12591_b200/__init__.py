@@ -7,8 +7,9 @@ DecoQuant protocol and the KV cache.  Compute runs in ``libdquant_b200.so``
 (hand-written CUDA, C ABI in include/dquant_b200.h); there is no CPU fallback.
 The batched decode hot path is ``DecodeKvCache`` (attention.py).
 
-Out of scope for this build: the analysis sweeps, the
-DQT1/DQZ1 file formats, the CLI and the dense tensor primitives.
+Also here: the quantisation-error sweeps of the paper's tables on the device path
+(``analysis``) and the DQT1 / DQZ1 interchange files (``formats``).  Out of scope
+(SURVEY.md 2 / 8f): the CLI and the dense tensor primitives.
 """
 
 from .compress import (
