@@ -1,0 +1,160 @@
+"""LLaMA-shaped decoder with a DecoQuant KV cache: the end-to-end decode harness.
+
+Random-init weights (std 0.02, bf16) of the named shapes; one decode step per call:
+
+    RMSNorm -> QKV projection -> RoPE -> fused DecoQuant attention (+ KV append) -> O projection
+    -> residual -> RMSNorm -> SwiGLU MLP -> residual        (x layers), RMSNorm -> LM head -> argmax
+
+The attention of every layer is ``DecodeKvCache.attend(layer, q, append=(k, v))``: the new
+token's K/V join the fp16 tail and the compressed segments are read by the fused kernels.
+Dense projections are cuBLAS GEMMs through torch (library code, as the task allows); the step
+is capturable in one CUDA graph (``capture()`` / ``replay()``).  Tensor parallelism across
+GPUs shards the KV heads (``sharding.py``); this harness runs the single-GPU shard.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from .attention import DecodeKvCache
+from .errors import ShapeMismatch
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    layers: int
+    hidden: int
+    heads: int
+    kv_heads: int
+    ffn: int
+    vocab: int = 32000
+    head_dim: int = 128
+
+    @property
+    def g(self) -> int:
+        return self.heads // self.kv_heads
+
+
+LLAMA2_7B = ModelShape(layers=32, hidden=4096, heads=32, kv_heads=32, ffn=11008)
+LLAMA2_13B = ModelShape(layers=40, hidden=5120, heads=40, kv_heads=40, ffn=13824)
+LLAMA2_70B = ModelShape(layers=80, hidden=8192, heads=64, kv_heads=8, ffn=28672)
+
+
+def _rms(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-5) -> torch.Tensor:
+    xf = x.float()
+    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)).to(x.dtype) * w
+
+
+def _rope(x: torch.Tensor, pos: torch.Tensor, theta: float = 10000.0) -> torch.Tensor:
+    """Rotary embedding of (..., head_dim) at one position (a device scalar, so the step is
+    graph-capturable), half-split convention."""
+    d = x.shape[-1]
+    inv = theta ** (-torch.arange(0, d, 2, device=x.device, dtype=torch.float32) / d)
+    ang = pos.float() * inv
+    cos, sin = torch.cos(ang), torch.sin(ang)
+    x1, x2 = x[..., : d // 2].float(), x[..., d // 2:].float()
+    return torch.cat([x1 * cos - x2 * sin, x1 * sin + x2 * cos], -1).to(x.dtype)
+
+
+class DecoQuantLM:
+    """Decoder of ``shape`` for ``batch`` sequences whose KV cache is DecoQuant-compressed."""
+
+    def __init__(self, shape: ModelShape, batch: int, bits: int = 4, chunk_len: int = 1024, seed: int = 0,
+                 device="cuda"):
+        if shape.head_dim != 128 or shape.heads % shape.kv_heads:
+            raise ShapeMismatch("head_dim must be 128 and heads a multiple of kv_heads")
+        self.shape, self.batch = shape, batch
+        self.dev = torch.device(device)
+        gen = torch.Generator(device=self.dev).manual_seed(seed)
+        s, hd = shape, shape.head_dim
+
+        def w(*dims):
+            return (torch.randn(dims, generator=gen, device=self.dev, dtype=torch.float32) * 0.02).to(torch.bfloat16)
+
+        self.embed = w(s.vocab, s.hidden)
+        self.lm_head = w(s.hidden, s.vocab)
+        self.norm = torch.ones(s.hidden, device=self.dev, dtype=torch.bfloat16)
+        self.layers = []
+        for _ in range(s.layers):
+            self.layers.append({
+                "ln1": torch.ones(s.hidden, device=self.dev, dtype=torch.bfloat16),
+                "ln2": torch.ones(s.hidden, device=self.dev, dtype=torch.bfloat16),
+                "qkv": w(s.hidden, (s.heads + 2 * s.kv_heads) * hd),
+                "o": w(s.heads * hd, s.hidden),
+                "gate_up": w(s.hidden, 2 * s.ffn),
+                "down": w(s.ffn, s.hidden),
+            })
+        self.cache = DecodeKvCache(layers=s.layers, units=batch * s.kv_heads, g=s.g, bits=bits,
+                                   chunk_len=chunk_len)
+        self.pos = torch.zeros((), dtype=torch.int64, device=self.dev)  # decode position (device)
+        self.graph = None
+        self._tok = self._next = None
+
+    def prefill_random(self, tokens: int, seed: int = 1):
+        """Fill every layer's cache with `tokens` positions of synthetic K/V (N(0,1) fp16),
+        compressed by the K3 write path (one segment per (sequence, kv head))."""
+        gen = torch.Generator(device=self.dev).manual_seed(seed)
+        units = self.batch * self.shape.kv_heads
+        for layer in range(self.shape.layers):
+            k = torch.randn((units, tokens, 128), generator=gen, device=self.dev).to(torch.float16)
+            v = torch.randn((units, tokens, 128), generator=gen, device=self.dev).to(torch.float16)
+            self.cache.prefill(layer, k, v)
+        self.pos.fill_(tokens)
+
+    def _layer(self, i: int, x: torch.Tensor) -> torch.Tensor:
+        s, L, B = self.shape, self.layers[i], self.batch
+        h = _rms(x, L["ln1"])
+        qkv = h @ L["qkv"]
+        q, k, v = qkv.split([s.heads * 128, s.kv_heads * 128, s.kv_heads * 128], dim=-1)
+        q = _rope(q.view(B, s.heads, 128), self.pos)
+        k = _rope(k.view(B, s.kv_heads, 128), self.pos)
+        # units = (sequence, kv head); query heads kv * g .. kv * g + g - 1 share a kv head
+        att = self.cache.attend(i, q.reshape(B * s.kv_heads, s.g, 128).to(torch.float16),
+                                append=(k.reshape(B * s.kv_heads, 128).to(torch.float16),
+                                        v.reshape(B * s.kv_heads, 128).to(torch.float16)))
+        x = x + att.reshape(B, s.heads * 128).to(torch.bfloat16) @ L["o"]
+        h = _rms(x, L["ln2"])
+        gate, up = (h @ L["gate_up"]).chunk(2, dim=-1)
+        return x + (torch.nn.functional.silu(gate) * up) @ L["down"]
+
+    def step(self, tokens: torch.Tensor) -> torch.Tensor:
+        """One decode step: tokens (batch,) int64 -> next tokens (batch,) (greedy)."""
+        x = self.embed[tokens]
+        for i in range(self.shape.layers):
+            x = self._layer(i, x)
+        logits = _rms(x, self.norm) @ self.lm_head
+        self.pos.add_(1)
+        return logits.argmax(-1)
+
+    def capture(self, tokens: torch.Tensor | None = None) -> torch.Tensor:
+        """Run one eager decode step on `tokens` (zeros by default) and record the step as a CUDA
+        graph (replay() runs it; the cache's host-side token counters advance per replay).
+        Returns the eager step's next tokens.  Refused when a tail chunk would seal inside."""
+        if any(lay.tail_len + 2 >= self.cache.chunk_len for lay in self.cache._layers):
+            raise ShapeMismatch("a tail chunk seals within the next steps: decode them eagerly first")
+        self._tok = torch.zeros(self.batch, dtype=torch.int64, device=self.dev)
+        if tokens is not None:
+            self._tok.copy_(tokens)
+        first = self.step(self._tok).clone()  # eager step: builds every layer's segment table
+        torch.cuda.synchronize()
+        tails = [lay.tail_len for lay in self.cache._layers]
+        pos = self.pos.clone()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._next = self.step(self._tok)
+        for lay, t in zip(self.cache._layers, tails):  # the capture ran no device work
+            lay.tail_len = t
+        self.pos.copy_(pos)
+        return first
+
+    def replay(self, tokens: torch.Tensor) -> torch.Tensor:
+        if any(lay.tail_len + 1 >= self.cache.chunk_len for lay in self.cache._layers):
+            raise ShapeMismatch("a tail chunk seals on this token: decode it eagerly, then capture() again")
+        self._tok.copy_(tokens)
+        self.graph.replay()
+        for layer in range(self.shape.layers):
+            self.cache._after_append(layer)
+        return self._next
