@@ -264,9 +264,17 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     const int wi = d.item;
     const int r = d.r, i1 = d.i1, i2 = d.i2, wb0 = d.wb0;
     const int nbt = d.nbt;
+#ifdef DQ_ATTN_WARP_TRACE  // profiling build: trace = [nwork][kWarps][8] per-warp stamps
+    auto stamp = [&](int) {};
+    auto wstamp = [&](int k) {
+      if (args.trace && lane == 0) args.trace[((size_t)wi * kWarps + warp) * 8 + k] = global_ns();
+    };
+#else
     auto stamp = [&](int k) {  // optional per-sub-item phase timestamps (profiling only)
       if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + k] = global_ns();
     };
+    auto wstamp = [&](int) {};
+#endif
     stamp(0);
     if (args.trace && tid == 0) {
       args.trace[(size_t)wi * 8 + 6] = blockIdx.x;
@@ -275,6 +283,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     mbar_wait(&sm.wbar, (uint32_t)(j & 1));
 
     stamp(1);
+    wstamp(0);
     // ---- phase 1: S = W . codes_k on the int8 tensor pipe ------------------------------
     constexpr int kWpt = kWarps / kTiles;   // warps per 64-row tile
     constexpr int MT = 4 / kWpt;            // 16-row m-tiles per warp
@@ -378,6 +387,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 #endif
 
     stamp(2);
+    wstamp(1);
     // ---- phase 2: softmax of the sub-item straight from the accumulators --------------
     float sv[MT][G][4];
     float mh[G];
@@ -398,6 +408,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       if (lane == 0) sm.rowmax[h][warp] = m;
     }
     named_sync(kThreads);  // every warp is past phase 1: the W buffer is dead
+    wstamp(2);
     if (tid == 0) {   // prefetch the fp32 G0v for the epilogue into it
       const uint32_t gb = (uint32_t)(i1 * r * 32);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -433,6 +444,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       }
     }
     named_sync(kThreads);  // per-tile probability maxima complete
+    wstamp(3);
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float lsum = 0.f;
@@ -472,6 +484,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       if (lane == 0) sm.lsum[h][warp] = lsum;
     }
     named_sync(kThreads);  // P limbs, gamma and lsum complete
+    wstamp(4);
 
     stamp(3);
     // ---- phase 3: Y = codes_v . P^T on the int8 tensor pipe ----------------------------
@@ -540,6 +553,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     }
 
     stamp(4);
+    wstamp(5);
     // ---- phase 4: O = scale_v * G0v . Y on CUDA cores, reduce, write the partial -------
     // accv[t][h]: rows e = gid (k 0,1) / gid+8 (k 2,3); cols a = 2*tid4 + (k & 1)
     float part[G][16];  // [h][c*2 + (e == gid+8)]
@@ -578,6 +592,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         part[h][k] = v;
       }
     named_sync(kThreads);  // every warp is past the V stages and G0v: P and W/G0v buffers are free
+    wstamp(6);
     if (tid == 0) {
       const int jn = j + 1;
       mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
@@ -618,6 +633,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       args.part_ml[((size_t)d.part * G + tid) * 2 + 1] = l;
     }
     stamp(5);
+    wstamp(7);
   }
 }
 
