@@ -120,20 +120,22 @@ def test_decode_attention_outlier_channels(dq, scale, bits, ctas, tc):
         assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
 
 
-def test_decode_attention_segments_and_tail(dq):
-    """prefill 1500 + 2 sealed chunks of 256 + tail 77, g=2, int4, outlier columns."""
+@pytest.mark.parametrize("g,tc", [(2, False), (1, True)])
+def test_decode_attention_segments_and_tail(dq, g, tc):
+    """prefill 1500 + 2 sealed chunks of 512 + tail 77, int4, outlier columns; g = 1 also on
+    the tcgen05 split kernel (prefill 1504 keeps every segment on the full i1 = 8 plan)."""
     from paper_2405_12591_b200.attention import DecodeKvCache
 
-    units, g, chunk = 3, 2, 256
+    units, chunk = 3, 512
     rng = np.random.default_rng(5)
-    P, steps = 1500, 2 * chunk + 77
+    P, steps = (1504 if tc else 1500), 2 * chunk + 77
     total = P + steps
     k = rng.standard_normal((units, total, 128)).astype(np.float32)
     k[:, :, [3, 77]] *= 15.0  # outlier channels
     k = k.astype(np.float16)
     v = rng.standard_normal((units, total, 128)).astype(np.float16)
     q = rng.standard_normal((units, g, 128)).astype(np.float16)
-    cache = DecodeKvCache(layers=2, units=units, g=g, bits=4, chunk_len=chunk)
+    cache = DecodeKvCache(layers=2, units=units, g=g, bits=4, chunk_len=chunk, tc=tc)
     kd, vd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
     cache.prefill(1, kd[:, :P], vd[:, :P])
     for t in range(P, total):
