@@ -414,12 +414,14 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
                    "kv_bits": bits, "layers": layers, "kv_heads": kv_heads, "g": g,
                    "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": cache._layers[0].args.chunk_b,
-                   "split_ctas": cache.ctas, "kernel_g": cache.kernel_g, "head_groups": cache.head_groups,
-                   "split_path": "tcgen05" if cache._layers[0].args.path == 1 else "mma.sync",
+                   "split_ctas": cache.split_ctas, "kernel_g": cache._layers[0].kernel_g,
+                   "head_groups": g // cache._layers[0].kernel_g,
+                   "split_path": {0: "mma.sync", 1: "tcgen05", 2: "tcgen05-gqa"}[cache._layers[0].args.path],
                    "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB streamed per step per GPU"},
         "hbm_gbs_step": step_bytes / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "traffic_source": traffic_src, "kernel": "decode_attn_kernel",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "kernel": {0: "decode_attn_kernel", 1: "decode_attn_tc_kernel", 2: "decode_attn_gqa_kernel"}[cache._layers[0].args.path],
                      "bytes_per_launch": kern_bytes,
                      "launch_ms": kern_ms, "peak_kind": peak_kind},
         "memory_per_token_vs_fp16": actual_bytes / fp16_bytes,

@@ -35,7 +35,8 @@ from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_
 
 HEAD_DIM = 128
 DEFAULT_CHUNK_B = 256
-KERNEL_G = (1, 2)   # query heads per kv head the split kernel is instantiated for
+KERNEL_G = (1, 2, 8)  # query heads per kv head the split kernels are instantiated for (8: tcgen05 only)
+GQA_G = 8             # heads of the tcgen05 GQA kernel (path 2)
 MAX_G = 16          # wider GQA groups run as g / kernel_g head groups over the same codes
 MAX_BLOCKS_PER_CALL = 512  # bounds the K3 fp32 core1 scratch
 
@@ -76,6 +77,7 @@ class _Layer:
         self.tokens_sealed = 0
         self.tail_len = 0  # host mirror (all units append in lock step)
         self.args = None   # cached AttnArgs
+        self.kernel_g = None  # heads per split-kernel instance used for this layer
         self.keep = []     # tensors referenced by args
 
 
@@ -150,17 +152,25 @@ class DecodeKvCache:
             raise ShapeMismatch("layers, units and chunk_len must be >= 1")
         self.device = _lib.require_cuda()
         self.layers, self.units, self.g, self.bits = layers, units, g, bits
-        # the split kernel runs kernel_g heads at a time; g > 2 becomes head_groups virtual
-        # units per kv head that share its segments (their re-reads of the codes are L2 hits:
-        # the work list puts a tile range's head groups next to each other)
-        self.kernel_g = kernel_g if kernel_g is not None else (2 if g % 2 == 0 else 1)
+        # the split kernel runs kernel_g heads at a time; g > kernel_g becomes head_groups
+        # virtual units per kv head that share its segments (their re-reads of the codes are L2
+        # hits: the work list puts a tile range's head groups next to each other).
+        # kernel_g = 8 is the tcgen05 GQA kernel (path 2: 4-bit codes, full plans i1 = 8,
+        # r = 64); a layer whose segments do not qualify falls back to mma.sync heads of 2.
+        if kernel_g is None:
+            kernel_g = GQA_G if (g % GQA_G == 0 and bits == 4 and tc is not False) else (2 if g % 2 == 0 else 1)
+        self.kernel_g = kernel_g
         if self.kernel_g not in KERNEL_G or g % self.kernel_g:
             raise Unsupported(f"kernel_g must be in {KERNEL_G} and divide g")
+        if self.kernel_g == GQA_G and (bits != 4 or tc is False):
+            raise Unsupported("kernel_g = 8 is the tcgen05 GQA kernel: 4-bit codes, tc not False")
         self.head_groups = g // self.kernel_g
-        # split kernel: tcgen05 (path 1) for 4-bit codes, one head per kernel and the full plan
-        # (i1 = 8, r = 64 -- any segment of >= 512 tokens with 8 | T); mma.sync (path 0) otherwise.
-        # True = tcgen05 (required), None / False = mma.sync (path 1 is correct but not yet faster).
+        # split kernel for kernel_g = 1: tcgen05 (path 1) for 4-bit codes and the full plan
+        # (i1 = 8, r = 64 -- any segment of >= 512 tokens with 8 | T), mma.sync (path 0)
+        # otherwise.  True = tcgen05 (required), None / False = mma.sync (path 1 is correct but
+        # not yet faster).  kernel_g = 8 always runs tcgen05 (path 2).
         self.tc = tc
+        self.split_ctas = None
         self.chunk_len, self.dim, self.chunk_b = chunk_len, dim, chunk_b
         # split-kernel grid: None = persistent (resident CTAs of this device), 0 = one CTA
         # per work item, k > 0 = k persistent CTAs
@@ -235,7 +245,15 @@ class DecodeKvCache:
         segs = []
         # the kernel sees g0h = core0 / norm, so the per-segment scale carries the norm back
         scales = [((grp.k_scale * grp.k_norm).cpu(), (grp.v_scale * grp.v_norm).cpu()) for grp in lay.groups]
-        hg, gk, vunits = self.head_groups, self.kernel_g, self.units * self.head_groups
+        full_plans = all(grp.plan.i1 == 8 and grp.plan.r == 64 for grp in lay.groups)
+        gk = self.kernel_g
+        if gk == GQA_G and not full_plans:
+            if self.tc:
+                raise Unsupported("the tcgen05 GQA path needs i1 = 8, r = 64 plans (8 | T, T >= 512)")
+            gk = 2  # mma.sync fallback for this layer
+        hg = self.g // gk
+        vunits = self.units * hg
+        lay.kernel_g = gk
         for grp, (ks, vs) in zip(lay.groups, scales):
             p = grp.plan
             kb, vb = grp.k_payload.shape[1], grp.v_payload.shape[1]
@@ -256,10 +274,12 @@ class DecodeKvCache:
         nseg = len(segs)
         seg_arr = (_lib.Segment * max(nseg, 1))(*segs)
         # work plan (host) -> device tables
-        if self.ctas is None:
+        ctas = self.ctas
+        if ctas is None:
             c = ctypes.c_int32()
             check(lib().dq_attention_ctas(gk, self.bits, ctypes.byref(c)), "attention_ctas")
-            self.ctas = c.value
+            ctas = c.value
+        self.split_ctas = ctas
         # the largest items: the per-item cost (W image, softmax, epilogue) is fixed, and
         # smaller items measured slower even where they shorten the scheduler's last round
         chunk_b = self.chunk_b or DEFAULT_CHUNK_B
@@ -290,11 +310,14 @@ class DecodeKvCache:
         a.units = vunits
         a.g = gk
         a.head_groups = hg
-        eligible = self.bits == 4 and gk == 1
-        eligible = eligible and all(grp.plan.i1 == 8 and grp.plan.r == 64 for grp in lay.groups)
-        if self.tc and not eligible:
-            raise Unsupported("the tcgen05 path needs 4-bit codes, one head per kernel and i1 = 8, r = 64 plans")
-        a.path = 1 if (eligible and self.tc) else 0
+        if gk == GQA_G:
+            a.path = 2
+        else:
+            eligible = self.bits == 4 and gk == 1 and full_plans
+            if self.tc and not eligible:
+                raise Unsupported("the tcgen05 path needs 4-bit codes, one head (or 8) per kernel and i1 = 8, "
+                                  "r = 64 plans")
+            a.path = 1 if (eligible and self.tc) else 0
         a.bits = self.bits
         a.tail_k = self.tail_k[layer].data_ptr()
         a.tail_v = self.tail_v[layer].data_ptr()
@@ -305,7 +328,7 @@ class DecodeKvCache:
         a.work = work_dev.data_ptr() if nwork else None
         a.nwork = nwork
         a.sched = sched.data_ptr()
-        a.nctas = self.ctas
+        a.nctas = ctas
         a.max_parts = tp
         a.unit_part0 = p0_dev.data_ptr()
         a.work_part = wpart_dev.data_ptr() if nwork else None

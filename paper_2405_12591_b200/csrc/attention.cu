@@ -25,7 +25,7 @@
 // accumulation); the excess-code offset is removed exactly in integers.  The reduction
 // index is permuted identically on both operands, which is free.  Full-precision K/V
 // never exist anywhere.
-#include "attn_tc.cuh"
+#include "attn_gqa.cuh"
 #include "attn_combine.cuh"
 
 #include <algorithm>
@@ -85,12 +85,33 @@ int occupancy(int* per_sm) {
   return DQ_OK;
 }
 
+// one CTA per SM: the tcgen05 kernels allocate all 512 TMEM columns
+template <class Kernel>
+int launch_tc(Kernel kernel, size_t smem, int threads, const dq_attn_args& a, cudaStream_t s) {
+  int sms = 0, dev = 0;
+  DQ_CUDA_TRY(cudaGetDevice(&dev));
+  DQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.nwork < sms ? a.nwork : sms));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, a));
+  return DQ_OK;
+}
+
 template <int BITS, int G>
 int launch_attn(const dq_attn_args& a, cudaStream_t s) {
-  const size_t smem = sizeof(AttnSmem<G>);
-  {
+  if constexpr (G <= 2) {
     const int rc = set_attrs<BITS, G>();
     if (rc != DQ_OK) return rc;
+  } else {
+    if (a.path != 2 || BITS != 4) return fail(DQ_ERR_UNSUPPORTED, "g = %d runs on the tcgen05 GQA path (4-bit codes)", G);
   }
   const int phases = a.phases ? a.phases : 7;
   if (a.nwork > 0 && (phases & 5)) {
@@ -116,37 +137,40 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
                                          (int)sizeof(TcSmem)));
         tc_attr = true;
       }
-      int sms = 0, dev = 0;
-      DQ_CUDA_TRY(cudaGetDevice(&dev));
-      DQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const int rc = launch_tc(decode_attn_tc_kernel, sizeof(TcSmem), kTcThreads, a, s);
+      if (rc != DQ_OK) return rc;
+    } else {
+      return fail(DQ_ERR_UNSUPPORTED, "the tcgen05 path 1 covers 4-bit codes with g = 1");
+    }
+  } else if (a.path == 2 && a.nwork > 0 && (phases & 1)) {
+    if constexpr (BITS == 4 && G == kGqG) {
+      static bool gq_attr = false;
+      if (!gq_attr) {
+        DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_gqa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(GqSmem)));
+        gq_attr = true;
+      }
+      const int rc = launch_tc(decode_attn_gqa_kernel, sizeof(GqSmem), kGqThreads, a, s);
+      if (rc != DQ_OK) return rc;
+    } else {
+      return fail(DQ_ERR_UNSUPPORTED, "the tcgen05 GQA path covers 4-bit codes with g = 8");
+    }
+  } else if (a.nwork > 0 && (phases & 1)) {
+    if constexpr (G <= 2) {
+      // programmatic dependent launch: the split kernel's prologue and first code copies
+      // overlap the prepare kernel; it waits (griddepcontrol.wait) only for the W images
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(a.nwork < sms ? a.nwork : sms));  // one CTA per SM (TMEM: 512 columns)
-      cfg.blockDim = dim3(kTcThreads);
-      cfg.dynamicSmemBytes = sizeof(TcSmem);
+      cfg.gridDim = dim3((unsigned)(a.nctas > 0 && a.nctas < a.nwork ? a.nctas : a.nwork));
+      cfg.blockDim = dim3(kCtaThreads);
+      cfg.dynamicSmemBytes = sizeof(AttnSmem<G>);
       cfg.stream = s;
       cudaLaunchAttribute attr_pdl[1];
       attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr_pdl;
       cfg.numAttrs = 1;
-      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_tc_kernel, a));
-    } else {
-      return fail(DQ_ERR_UNSUPPORTED, "the tcgen05 path covers 4-bit codes with g = 1");
+      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G>, a));
     }
-  } else if (a.nwork > 0 && (phases & 1)) {
-    // programmatic dependent launch: the split kernel's prologue and first code copies
-    // overlap the prepare kernel; it waits (griddepcontrol.wait) only for the W images
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(a.nctas > 0 && a.nctas < a.nwork ? a.nctas : a.nwork));
-    cfg.blockDim = dim3(kCtaThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr_pdl[1];
-    attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr_pdl;
-    cfg.numAttrs = 1;
-    DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G>, a));
   }
   if (phases & 2) {
     const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1);
@@ -174,8 +198,9 @@ int dispatch_g(const dq_attn_args& a, cudaStream_t s) {
   switch (a.g) {
     case 1: return launch_attn<BITS, 1>(a, s);
     case 2: return launch_attn<BITS, 2>(a, s);
+    case kGqG: return launch_attn<BITS, kGqG>(a, s);
   }
-  return fail(DQ_ERR_UNSUPPORTED, "g must be 1 or 2 in this build (got %d)", a.g);
+  return fail(DQ_ERR_UNSUPPORTED, "g must be 1, 2 or %d in this build (got %d)", kGqG, a.g);
 }
 
 }  // namespace
@@ -241,6 +266,7 @@ extern "C" int dq_attention_ctas(int32_t g, int32_t bits, int32_t* ctas) {
     case 4 * 16 + 2: rc = occupancy<4, 2>(&per_sm); break;
     case 8 * 16 + 1: rc = occupancy<8, 1>(&per_sm); break;
     case 8 * 16 + 2: rc = occupancy<8, 2>(&per_sm); break;
+    case 4 * 16 + kGqG: per_sm = 1; break;  // the tcgen05 GQA kernel: one CTA per SM
     default: return fail(DQ_ERR_UNSUPPORTED, "no split kernel for bits %d, g %d", bits, g);
   }
   if (rc != DQ_OK) return rc;
@@ -252,7 +278,8 @@ extern "C" int dq_attention_wimg_bytes(int32_t g, int64_t* bytes) {
   if (!bytes) return fail(DQ_ERR_INVALID_ARG, "null output");
   if (g == 1) *bytes = kWImageBytes<1>;
   else if (g == 2) *bytes = kWImageBytes<2>;
-  else return fail(DQ_ERR_UNSUPPORTED, "g must be 1 or 2 in this build (got %d)", g);
+  else if (g == kGqG) *bytes = kWImageBytes<kGqG>;
+  else return fail(DQ_ERR_UNSUPPORTED, "g must be 1, 2 or %d in this build (got %d)", kGqG, g);
   return DQ_OK;
 }
 

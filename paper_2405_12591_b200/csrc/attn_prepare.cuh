@@ -78,7 +78,9 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
   }
   __syncthreads();
   const float gk[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
-  const int grp = rr < kGroupR ? 0 : 1;
+  // path 2 keeps one scale per column: its S accumulators have no room for a second group
+  const int grp = (rr < kGroupR || args.path == 2) ? 0 : 1;
+  const int headroom = args.path ? 1 : 0;
   // W[h][a][rr][e] in fp32 (e in ord16 order), then one fixed-point scale 2^(kWBits - e2)
   // per (h, a, bond-row group) from the exact group maximum
   float wv[16];
@@ -95,16 +97,16 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
   if (live) atomicMax(&wmax[h][a][grp], __float_as_uint(m));
   __syncthreads();
   if (live) {
-    // path 1 splits both limbs signed: one bit of headroom keeps the hi limb in s8
-    const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a][grp]), kWBits<BITS> - args.path);
+    // the tcgen05 paths split both limbs signed: one bit of headroom keeps the hi limb in s8
+    const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a][grp]), kWBits<BITS> - headroom);
     uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
     int wsum = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int wint = __float2int_rn(wv[i] * wq);
       wsum += wint;
-      // path 0: hi signed, lo unsigned; path 1: both signed (lo in [-128, 127]) so one
-      // s8 UMMA of N = 16 takes both limbs; wint = 256 * hi + lo either way
+      // path 0: hi signed, lo unsigned; paths 1 / 2: both signed (lo in [-128, 127]) so one
+      // s8 UMMA takes both limbs; wint = 256 * hi + lo either way
       const int whi = args.path ? (wint + 128) >> 8 : wint >> 8;
       hi[i >> 2] |= (uint32_t)(whi & 0xFF) << (8 * (i & 3));
       lo[i >> 2] |= (uint32_t)((wint - 256 * whi) & 0xFF) << (8 * (i & 3));
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
   if (tid < G * 16 && ((tid >> 1) & 7) / (8 / kPrepSplit) == (int)blockIdx.y) {  // this CTA's columns
     int* mout = reinterpret_cast<int*>(static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride +
                                        kWChunkBytes<G>);
-    const float cs = pow2_exp_sub(__uint_as_float((&wmax[0][0][0])[tid]), kWBits<BITS> - args.path);
+    const float cs = pow2_exp_sub(__uint_as_float((&wmax[0][0][0])[tid]), kWBits<BITS> - (args.path ? 1 : 0));
     mout[tid] = (&meta.beta[0][0][0])[tid];                               // beta[G][8][2]
     mout[G * 16 + tid] = __float_as_int(cs);                               // cs[G][8][2]
   }

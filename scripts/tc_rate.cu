@@ -88,5 +88,10 @@ int main() {
   run<16, true, 1, false, true>();
   run<16, false, 4, false, true>();
   run<16, true, 4, true, true>();
+  run<64, true, 2, false, true>();
+  run<128, true, 1, false, true>();
+  run<128, false, 1, false, true>();
+  run<256, true, 1, false, true>();
+  run<256, false, 1, false, true>();
   return 0;
 }

@@ -199,6 +199,57 @@ def test_gqa_head_groups(dq, g, kernel_g):
         assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
 
 
+@pytest.mark.parametrize("g,T,units,scale", [
+    (8, 4096, 3, 1.0), (8, 1024, 2, 1.0), (8, 2240, 2, 1.0), (8, 600, 2, 1.0), (8, 4096, 2, 20.0),
+    (8, 8192, 1, 50.0), (16, 2048, 2, 12.0),
+])
+def test_gqa_tcgen05(dq, g, T, units, scale):
+    """The tcgen05 GQA split kernel (path 2: 8 heads x 2 limbs x 8 columns per N = 128 UMMA),
+    items of 1..4 tiles (T = 2240: 35 tiles; T = 600: a partial last tile), outlier key
+    channels, g = 16 as two head groups of 8."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(T + g + int(scale))
+    k = rng.standard_normal((units, T, 128)).astype(np.float32)
+    k[:, :, [3, 77]] *= scale
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = rng.standard_normal((units, g, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=4)
+    assert cache.kernel_g == 8
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    assert cache._layers[0].args.path == 2
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), 4, [T], 0)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
+def test_gqa_tcgen05_segments_tail_append(dq):
+    """Path 2 over prefill + sealed chunks + fp16 tail with the fused append, step by step."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    units, g, chunk, P, steps = 2, 8, 512, 1504, 530
+    rng = np.random.default_rng(77)
+    k = rng.standard_normal((units, P + steps, 128)).astype(np.float32)
+    k[:, :, [5, 90]] *= 10.0
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, P + steps, 128)).astype(np.float16)
+    q = rng.standard_normal((units, g, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=4, chunk_len=chunk)
+    kd, vd, qd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    cache.prefill(0, kd[:, :P], vd[:, :P])
+    for t in range(P, P + steps):
+        cache.attend(0, qd, append=(kd[:, t], vd[:, t]))
+    assert len(cache._layers[0].groups) == 2 and cache._layers[0].tail_len == steps - chunk
+    out = cache.attend(0, qd).float().cpu().numpy()
+    assert cache._layers[0].args.path == 2
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), 4,
+                             [P, chunk], steps - chunk)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
 def test_fused_append_matches_attend_then_append(dq):
     """attend(append=(k, v)) == attend + append_token, step by step, across a tail seal."""
     from paper_2405_12591_b200.attention import DecodeKvCache
