@@ -16,7 +16,8 @@ import torch
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdquant_b200.so")
+# DQ_LIB: an alternative build of the same library (profiling variants); the in-tree one by default
+LIB_PATH = os.environ.get("DQ_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdquant_b200.so")
 
 DQ_OK = 0
 DQ_F32, DQ_F16 = 0, 1

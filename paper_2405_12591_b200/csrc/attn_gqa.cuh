@@ -7,15 +7,20 @@
 //   Y[(r,e), (h,l,a)]  = sum_b code_v[(r,e), b] . P_l[b, (h,a)]          M = 128 (r,e), N = 128, K = b
 //
 // A operands (the codes) are widened from the shared-memory ring into tensor memory by the
-// consumer warps (tcgen05.st: lane = row, 4 K-bytes per column); B operands (W image, P)
-// sit in shared memory as K-major core matrices.  One elected lane of the MMA warp issues
-// every UMMA (kind::i8, s32 accumulators in TMEM) and signals through tcgen05.commit.
+// consumer warps (tcgen05.st: lane = row, 4 K-bytes per column); B operands sit in shared
+// memory as K-major core matrices: the W image streams through the ring in 16 KB slices of
+// 8 bond rows next to the K codes of the same bond rows (so no 128 KB W buffer: the ring is
+// 5 x 32 KB deep), P is written by the softmax.  One elected lane of the MMA warp issues
+// every UMMA (kind::i8, s32 accumulators in TMEM) and signals through tcgen05.commit; its
+// commit is also the ring slot's last release (the UMMAs read W from the slot).
 //
-// Per work item (<= 256 rows b = 2 M-blocks): 8 K stages (8 bond rows x all tiles) -> S in
-// TMEM (2 x 128 columns) -> softmax from TMEM -> P limbs in shared memory -> 8 V stages (one
-// M-block of 8 bond rows x all tiles each) -> Y per stage (128 columns, double-buffered in
-// the S columns) -> the epilogue folds Y with G0v on CUDA cores while the next stage's
-// UMMAs run.  TMEM: A buffers [0, 128), S / Y [128, 384).
+// Per work item (<= 256 rows b = 2 M-blocks): 8 K stages (8 bond rows x all tiles + W slice)
+// -> S in TMEM (2 x 128 columns) -> softmax from TMEM -> P limbs in shared memory -> 8 V
+// stages (one M-block of 8 bond rows x all tiles each) -> Y per stage (128 columns, double-
+// buffered in the S columns) -> the epilogue folds Y with G0v on CUDA cores while the next
+// stage's UMMAs run.  TMEM: 4 A buffers [0, 256), S / Y [256, 512).  16 consumer warps (4
+// warpgroups: a warp reaches TMEM lanes 32 (warp % 4) ..): K widening by (M-block, bond-row
+// half), softmax by (M-block, head half), V widening by tile, the Y fold by head pair.
 //
 // Numerics (exact integer products, as path 0): codes excess-coded u8; W = two signed 8-bit
 // limbs of a 14-bit fixed point with one scale per (h, a) column; P = exp2(s - m_h) as a
@@ -29,59 +34,68 @@ namespace dq {
 namespace attn {
 
 constexpr int kGqG = 8;                            // query heads per kernel instance
-constexpr int kGqStages = 3;                       // ring: 3 x 16 KB (W image 128 KB + P 32 KB)
-constexpr int kGqWarps = 8;                        // consumer warps: 2 warpgroups
+constexpr int kGqStages = 5;                       // ring: 5 x 32 KB
+constexpr int kGqSlot = 32768;                     // K stage: codes [0, 16 KB) + W slice [16 KB, 32 KB)
+constexpr int kGqWSlice = 16 * 8 * 8 * 16;         // W slice: 16 (h, limb) x 8 bond rows x 8 a x 16 e = 16 KB
+constexpr int kGqWarps = 16;                       // consumer warps: 4 warpgroups
 constexpr int kGqCons = kGqWarps * 32;
 constexpr int kGqThreads = kGqCons + 64;           // + producer (8) + MMA (9)
-constexpr uint32_t kGqColA = 0, kGqColSY = 128;    // A: 2 x 64 columns; S / Y: 2 x 128 columns
+constexpr int kGqNumA = 4;                         // TMEM A buffers (64 columns each)
+constexpr uint32_t kGqColA = 0, kGqColSY = 256;    // A: 4 x 64 columns; S / Y: 2 x 128 columns
 constexpr int kGqPBits = 15;
 constexpr int kGqVTileBytes = 8 * 16 * kI2Pad / 2;  // V stage per tile: 8 bond rows x 16 e x 64 b
 
 struct GqSmem {
-  alignas(1024) unsigned char ring[kGqStages][kStageBytes];
-  alignas(128) uint4 w[kGqG * 2 * kMaxR * 8];      // W limbs: chunk ((h*2 + limb)*r + rr)*8 + a
-  alignas(16) WMeta<kGqG> wmeta;                   // beta, cs per (h, a) (group 0)
+  alignas(128) unsigned char ring[kGqStages][kGqSlot];
   // P limbs as core matrices [(h*2 + limb)][b / 16][a][16 b]; the epilogue's cross-warp
   // reduction reuses the buffer once every V UMMA of the item has completed
   union alignas(128) {
     unsigned char pb[kGqG * 2 * (kCB / 16) * 128];
-    float red[4][kGqG][kD];
+    float red[4][kGqG][kD];  // [warp quarter][head][c * 16 + e]
   } pr;
   alignas(16) float4 g0v[8 * kMaxR * 2];           // fp32 G0v [a][rr][c]
-  alignas(16) float pinv[kGqG][8];                 // 2^(e - 15) of the P column maxima
-  unsigned pmax[kGqG][8];
-  int gsum[kGqG][8];
-  float rowmax[kGqG][kGqWarps];
+  alignas(16) WMeta<kGqG> wmeta[2];                // beta, cs per (h, a) (group 0), by item parity
+  alignas(16) float pinv[kGqG * 8];                // 2^(e - 15) of the P column maxima
+  alignas(16) float xoff[kGqG * 8];                // -X * gsum * pinv: the excess offset of Y per column
+  alignas(16) int gsum[kGqG * 8];                  // sum_b Pint per column
+  unsigned pmax[kGqG * 8];
+  float rowmax[2][8][4];                           // [head half][M-block * 4 + warp quarter][head]
   SubItem sub[kSubRing];
   uint64_t full[kGqStages], empty[kGqStages];
-  uint64_t wbar, wfree, g0bar, descfull[kSubRing];
-  uint64_t afull[2], afree[2], sfull, pfull, yfull[2], yfree[2];
+  uint64_t g0bar, descfull[kSubRing];
+  uint64_t afull[kGqNumA], afree[kGqNumA], sfull, pfull, yfull[2], yfree[2];
   uint32_t tmem;
 };
 static_assert(sizeof(GqSmem) <= 232448, "path-2 shared memory exceeds the 227 KB opt-in limit");
 
-// stage geometry of path 2: K stages as path 1 (RK bond rows x all tiles); V stages of 8 bond
-// rows (one M-block of (r, e)) x all tiles
+// stage geometry of path 2: K stages of 8 bond rows x all tiles (codes <= 16 KB, + the W
+// slice of those bond rows); V stages of 8 bond rows (one M-block of (r, e)) x all tiles
 __device__ __forceinline__ void gq_load_sub(SubItem& d, const dq_attn_args& a, int w) {
   load_sub<4>(d, a, w);
-  const int nmb = (d.nbt + 1) / 2;
-  int RK = (kStageBytes / (d.nbt * kI2Pad * 8)) & ~3;
-  RK = min(RK, nmb == 2 ? 8 : 16);
-  d.RK = RK;
-  d.nK = (d.r + RK - 1) / RK;
+  d.RK = 8;
+  d.nK = d.r / 8;
   d.RV = 8;
   d.nslices = d.r / 8;
   d.stages = d.nK + d.nslices;
 }
 
-__device__ __forceinline__ void gq_issue_stage(const SubItem& d, int st, unsigned char* buf, uint64_t* bar) {
+// stage `st` of item `d` (the k-th item of this CTA) into ring slot `buf` (one thread)
+__device__ __forceinline__ void gq_issue_stage(GqSmem& sm, const dq_attn_args& a, const SubItem& d, int k, int st,
+                                               unsigned char* buf, uint64_t* bar) {
+  const int bt0 = d.wb0 / kI2Pad;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (st < d.nK) {
-    issue_stage<4>(d, st, buf, bar);
+    constexpr uint32_t chunk = 8 * kI2Pad * 8;  // 8 bond rows x 64 b x 8 bytes per tile
+    const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
+    const uint32_t meta = st == 0 ? (uint32_t)sizeof(WMeta<kGqG>) : 0u;
+    mbar_expect_tx(bar, chunk * d.nbt + kGqWSlice + meta);
+    const unsigned char* src = d.kc + ((size_t)bt0 * d.r + 8 * st) * kI2Pad * 8;
+    for (int j = 0; j < d.nbt; ++j) bulk_g2s(buf + j * chunk, src + (size_t)j * d.r * kI2Pad * 8, chunk, bar);
+    bulk_g2s(buf + 16384, img + (size_t)st * kGqWSlice, kGqWSlice, bar);
+    if (meta) bulk_g2s(&sm.wmeta[k & 1], img + kWChunkBytes<kGqG>, meta, bar);
     return;
   }
   const int mbv = st - d.nK;
-  const int bt0 = d.wb0 / kI2Pad;
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   mbar_expect_tx(bar, (uint32_t)(kGqVTileBytes * d.nbt));
   for (int t = 0; t < d.nbt; ++t) {
     const unsigned char* src = d.vc + ((size_t)(bt0 + t) * d.r + 8 * mbv) * 16 * kI2Pad / 2;
@@ -89,12 +103,19 @@ __device__ __forceinline__ void gq_issue_stage(const SubItem& d, int st, unsigne
   }
 }
 
-__device__ __forceinline__ void gq_issue_wimg(GqSmem& sm, const dq_attn_args& a, const SubItem& d) {
-  const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  mbar_expect_tx(&sm.wbar, (uint32_t)(kWChunkBytes<kGqG> + sizeof(WMeta<kGqG>)));
-  bulk_g2s(sm.w, img, (uint32_t)kWChunkBytes<kGqG>, &sm.wbar);
-  bulk_g2s(&sm.wmeta, img + kWChunkBytes<kGqG>, (uint32_t)sizeof(WMeta<kGqG>), &sm.wbar);
+// 2^x on the SFU (ex2.approx.ftz: -inf -> +0, relative error ~2^-22)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^(k - e) for x = m * 2^e (m in [0.5, 1)), x >= 0 clamped below to 2^-100, as float bits
+// (3 integer ops; pow2_sub_exp with the exponent field kept in place)
+template <int K>
+__device__ __forceinline__ float pow2_sub_exp3(unsigned xbits) {
+  const unsigned e = max(xbits & 0x7F800000u, 27u << 23);
+  return __uint_as_float(((unsigned)(K + 253) << 23) - e);
 }
 
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, int (&r)[16]) {
@@ -106,15 +127,21 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, int (&r)[16]) {
       : "memory");
 }
 
-__device__ __forceinline__ unsigned redux_max(unsigned v) {
-  unsigned r;
-  asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
-  return r;
-}
-__device__ __forceinline__ int redux_add(int v) {
-  int r;
-  asm volatile("redux.sync.add.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
-  return r;
+// warp reduce-scatter of N values per lane: afterwards lane l holds, in v[0 .. N/32), the
+// reduction over the 32 lanes of columns (N / 32) * l + i.  Five exchange steps of N/2,
+// N/4, ... independent shuffles (no serial chain through a reduction unit).
+template <int N, class T, class Op>
+__device__ __forceinline__ void warp_reduce_scatter(T (&v)[N], int lane, Op op) {
+#pragma unroll
+  for (int o = 16, n = N; o >= 1; o >>= 1, n >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const T send = up ? v[i] : v[n / 2 + i];
+      const T keep = up ? v[n / 2 + i] : v[i];
+      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_args args) {
@@ -128,15 +155,15 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   if (tid == 0) {
     for (int s = 0; s < kGqStages; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kGqWarps);
+      mbar_init(&sm.empty[s], kGqWarps + 1);  // the consumer warps + the MMA warp's commit
     }
     for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.descfull[s], 1);
-    mbar_init(&sm.wbar, 1);
-    mbar_init(&sm.wfree, 1);
     mbar_init(&sm.g0bar, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kGqNumA; ++b) {
       mbar_init(&sm.afull[b], kGqWarps);
       mbar_init(&sm.afree[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.yfull[b], 1);
       mbar_init(&sm.yfree[b], kGqWarps);
     }
@@ -145,8 +172,8 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (tid < kGqG * 8) {
-    (&sm.pmax[0][0])[tid] = 0u;
-    (&sm.gsum[0][0])[tid] = 0;
+    sm.pmax[tid] = 0u;
+    sm.gsum[tid] = 0;
   }
   if (warp == kGqWarps + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem)),
@@ -159,8 +186,11 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   const uint32_t tmem = sm.tmem;
 
   if (warp == kGqWarps) {
-    // ---- producer: descriptors and code stages of this CTA's items (as paths 0 / 1) ---------
+    // ---- producer: descriptors and stages of this CTA's items, in order --------------------
     if (lane == 0) {
+      // the W images come from the prepare kernel, and the ticket counter is shared with the
+      // previous launch on these args: wait for both grids before the first copy
+      asm volatile("griddepcontrol.wait;\n" ::: "memory");
       SubItem nd;
       bool have = (int)blockIdx.x < args.nwork;
       if (have) gq_load_sub(nd, args, blockIdx.x);
@@ -175,22 +205,12 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
         const SubItem d = nd;
         sm.sub[ds] = d;
         mbar_arrive(&sm.descfull[ds]);
-        // W image of item k >= 1 once item k - 1 is done with its own (its K UMMAs completed
-        // and the consumers read its metadata): by now the consumers are deep in item k - 1's
-        // V phase, so the wait is short (item 0's image comes from consumer thread 0)
-        if (k > 0) {
-          mbar_wait(&sm.wfree, (uint32_t)((k - 1) & 1));
-          gq_issue_wimg(sm, args, d);
-        }
         bool nhave = false;
         for (int ls = 0; ls < d.stages; ++ls, ++g) {
           const int slot = g % kGqStages;
           if (g >= kGqStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kGqStages - 1) & 1));
-          gq_issue_stage(d, ls, sm.ring[slot], &sm.full[slot]);
+          gq_issue_stage(sm, args, d, k, ls, sm.ring[slot], &sm.full[slot]);
           if (ls == min(2, d.stages - 1)) {
-            // the ticket counter is shared with the previous launch on these args: under
-            // programmatic dependent launch, wait for that grid before drawing from it
-            if (k == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");
             const int nxt = (int)gridDim.x + atomicAdd(args.sched, 1);
             nhave = nxt < args.nwork;
             if (nhave) gq_load_sub(nd, args, nxt);
@@ -212,51 +232,95 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     if (lane == 0) {
       const uint32_t id_k = tc_idesc(128, 128, 0, 1);  // codes u8 x W limbs s8
       const uint32_t id_v = tc_idesc(128, 128, 0, 0);  // codes u8 x P limbs u8
-      int na = 0;              // A-buffer uses
+      const uint64_t pdesc = tc_sdesc(sm.pr.pb, 128, (kCB / 16) * 128);  // P: b chunks 128 B, (h, limb) groups 2 KB
+      int na = 0;              // A-buffer uses = ring stages consumed
       int uy[2] = {0, 0};      // Y-buffer uses
       for (int j = 0;; ++j) {
         mbar_wait_spin(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
         const SubItem d = sm.sub[j % kSubRing];
         if (d.nbt == 0) break;
         const int nmb = (d.nbt + 1) / 2;
-        mbar_wait_spin(&sm.wbar, (uint32_t)(j & 1));  // W image of this item's segment
         // S occupies the Y columns: the previous item's epilogue must have read both buffers
         for (int b = 0; b < 2; ++b)
           if (uy[b] > 0) mbar_wait_spin(&sm.yfree[b], (uint32_t)((uy[b] - 1) & 1));
         tc_fence_after();
+#ifndef DQ_GQ_SMTRACE
+        if (args.trace) args.trace[(size_t)d.item * 8 + 7] = global_ns();  // MMA warp: K issue starts
+#endif
+#ifdef DQ_GQ_MMAWAIT  // measurement only: time the MMA warp waits for A buffers (K: slot 6, V: slot 4)
+        int64_t wk = 0, wv = 0;
+#endif
         for (int ks = 0; ks < d.nK; ++ks, ++na) {
-          const int ab = na & 1;
-          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na >> 1) & 1));
+          const int ab = na % kGqNumA;
+#ifdef DQ_GQ_MMAWAIT
+          const int64_t w0 = global_ns();
+          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
+          wk += global_ns() - w0;
+#else
+          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
+#endif
           tc_fence_after();
-          const int rk0 = ks * d.RK, nr = min(d.RK, d.r - rk0);
-          for (int kk = 0; kk < nr / 2; ++kk) {  // UMMA k-step = 32 bytes = 2 bond rows
-            const int rr = rk0 + 2 * kk;
-            // N rows (h*2 + limb)*8 + a: 16 core-matrix groups r*128 bytes apart
-            const uint64_t bdesc = tc_sdesc(&sm.w[rr * 8], 128, d.r * 128);
-            for (int mb = 0; mb < nmb; ++mb)
-              tc_mma_ts(tmem + kGqColSY + (uint32_t)(mb * 128),
-                        tmem + kGqColA + (uint32_t)(ab * 64 + mb * d.RK * 4 + kk * 8), bdesc, id_k,
-                        (ks | kk) ? 1u : 0u);
+          // this stage's W slice: N rows (h*2 + limb)*8 + a in 16 core-matrix groups 1 KB apart,
+          // bond rows 128 B apart; k-step kk (2 bond rows) = +256 B = +16 in the address field
+          const uint64_t bdesc = tc_sdesc(sm.ring[na % kGqStages] + 16384, 128, 1024);
+          const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64);
+          const uint32_t acc0 = ks ? 1u : 0u;
+#ifndef DQ_GQ_NULL_MMA  // measurement only: no UMMAs (the commits still signal)
+          if (nmb == 2) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              tc_mma_ts(tmem + kGqColSY, a0 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
+              tc_mma_ts(tmem + kGqColSY + 128, a0 + 32 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) tc_mma_ts(tmem + kGqColSY, a0 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
           }
+#else
+          if (bdesc == 0) args.trace[1] = a0 + acc0;
+#endif
           tc_commit(&sm.afree[ab]);
+          tc_commit(&sm.empty[na % kGqStages]);  // the W slice has been read
         }
         tc_commit(&sm.sfull);
+#if !defined(DQ_GQ_SMTRACE) && !defined(DQ_GQ_MMAWAIT)
+        if (args.trace) args.trace[(size_t)d.item * 8 + 4] = global_ns();  // MMA warp: K issue done
+#endif
         mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs in shared memory, S read
         tc_fence_after();
         for (int vs = 0; vs < d.nslices; ++vs, ++na) {
-          const int ab = na & 1, yb = vs & 1;
-          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na >> 1) & 1));
+          const int ab = na % kGqNumA, yb = vs & 1;
+#ifdef DQ_GQ_MMAWAIT
+          const int64_t w0 = global_ns();
+          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
+          if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
+          wv += global_ns() - w0;
+#else
+          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
+#endif
           if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
           tc_fence_after();
-          for (int kk = 0; kk < 2 * d.nbt; ++kk) {  // 32 rows b per k-step
-            const uint64_t bdesc = tc_sdesc(&sm.pr.pb[kk * 2 * 128], 128, (kCB / 16) * 128);
-            tc_mma_ts(tmem + kGqColSY + (uint32_t)(yb * 128), tmem + kGqColA + (uint32_t)(ab * 64 + kk * 8), bdesc,
-                      id_v, kk ? 1u : 0u);
-          }
+          const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64), d0 = tmem + kGqColSY + (uint32_t)(yb * 128);
+#ifndef DQ_GQ_NULL_MMA
+          // 32 rows b per k-step: +256 B of P = +16 in the address field
+          tc_mma_ts(d0, a0, pdesc, id_v, 0u);
+          for (int kk = 1; kk < 2 * d.nbt; ++kk) tc_mma_ts(d0, a0 + kk * 8, pdesc + kk * 16, id_v, 1u);
+#else
+          if (pdesc == 0) args.trace[1] = a0 + d0;
+#endif
           tc_commit(&sm.afree[ab]);
+          tc_commit(&sm.empty[na % kGqStages]);
           tc_commit(&sm.yfull[yb]);
           ++uy[yb];
         }
+#ifdef DQ_GQ_MMAWAIT
+        if (args.trace) {
+          args.trace[(size_t)d.item * 8 + 6] = wk;
+          args.trace[(size_t)d.item * 8 + 4] = wv;
+        }
+#elif !defined(DQ_GQ_SMTRACE)
+        if (args.trace) args.trace[(size_t)d.item * 8 + 6] = global_ns();  // MMA warp: V issue done
+#endif
       }
     }
     __syncwarp();
@@ -267,8 +331,14 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   }
 
   // ---- consumer warps ----------------------------------------------------------------------
+#ifdef DQ_GQ_SPIN  // measurement: consumers spin on their barriers instead of suspending
+  auto cwait = [](uint64_t* bar, uint32_t parity) { mbar_wait_spin(bar, parity); };
+#else
+  auto cwait = [](uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); };
+#endif
   const int q = warp & 3;                // TMEM lane quarter of this warp
-  const int wg = warp >> 2;              // warpgroup: K / softmax M-block; V tiles 2wg, 2wg+1; heads 4wg..4wg+3
+  const int wg = warp >> 2;              // warpgroup 0..3
+  const int mbk = wg & 1, hh = wg >> 1;  // K / softmax: M-block (rows b) and half (bond rows / heads 4hh..4hh+3)
   const int lane_in = 32 * q + lane;     // TMEM lane
   const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
   int st = 0, na = 0;
@@ -277,16 +347,10 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s % kGqStages]);
   };
-
-  if (tid == 0) {
-    mbar_wait(&sm.descfull[0], 0);
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
-    if (sm.sub[0].nbt > 0) gq_issue_wimg(sm, args, sm.sub[0]);
-  }
+  if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
 
   for (int j = 0;; ++j) {
-    mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+    cwait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
     const SubItem d = sm.sub[j % kSubRing];
     if (d.nbt == 0) break;
     const int wi = d.item, nbt = d.nbt, nmb = (nbt + 1) / 2;
@@ -302,30 +366,31 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     }
 
     // ---- K phase: widen this thread's row b of each stage into TMEM --------------------------
-    const int jt = 2 * wg + (q >> 1);        // tile of this thread's row
+    const int jt = 2 * mbk + (q >> 1);       // tile of this thread's row
     const int b_in = 32 * (q & 1) + lane;    // row inside the tile
     for (int ks = 0; ks < d.nK; ++ks, ++st, ++na) {
-      const int slot = st % kGqStages, ab = na & 1;
-      mbar_wait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
-      if (na >= 2) mbar_wait(&sm.afree[ab], (uint32_t)(((na >> 1) - 1) & 1));
-      const int rk0 = ks * d.RK, nr = min(d.RK, d.r - rk0);
-      if (wg < nmb) {
-        const unsigned char* tile = sm.ring[slot] + jt * nr * kI2Pad * RB;
+      const int slot = st % kGqStages, ab = na % kGqNumA;
+      cwait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
+      if (na >= kGqNumA) cwait(&sm.afree[ab], (uint32_t)((na / kGqNumA - 1) & 1));
+      if (mbk < nmb) {  // bond rows 4hh .. 4hh+3 of the stage for this thread's row
+        const unsigned char* tile = sm.ring[slot] + jt * 8 * kI2Pad * RB;
         const bool live = jt < nbt;
-        for (int r4 = 0; r4 < nr; r4 += 4) {
-          uint32_t v[16];
+        uint32_t v[16];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int rl = r4 + i, rr = rk0 + rl;
-            uint2 w2 = make_uint2(0u, 0u);
-            if (live) w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ ((rr & 3) * 4))) * RB);
-            v[4 * i] = w2.x & 0x0F0F0F0Fu;
-            v[4 * i + 1] = (w2.x >> 4) & 0x0F0F0F0Fu;
-            v[4 * i + 2] = w2.y & 0x0F0F0F0Fu;
-            v[4 * i + 3] = (w2.y >> 4) & 0x0F0F0F0Fu;
-          }
-          tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + wg * d.RK * 4 + r4 * 4), v);
+        for (int i = 0; i < 4; ++i) {
+          const int rl = 4 * hh + i;  // rr & 3 = i (stages start at multiples of 8)
+          uint2 w2 = make_uint2(0u, 0u);
+          if (live) w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ (i * 4))) * RB);
+          v[4 * i] = w2.x & 0x0F0F0F0Fu;
+          v[4 * i + 1] = (w2.x >> 4) & 0x0F0F0F0Fu;
+          v[4 * i + 2] = w2.y & 0x0F0F0F0Fu;
+          v[4 * i + 3] = (w2.y >> 4) & 0x0F0F0F0Fu;
         }
+#ifndef DQ_GQ_NULL_WIDEN  // measurement only: no TMEM stores from the consumers
+        tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + mbk * 32 + hh * 16), v);
+#else
+        if (v[0] == 0x12345678u) args.trace[0] = v[1];
+#endif
         tc_wait_st();
       }
       tc_fence_before();
@@ -336,104 +401,126 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     stamp(1);
 
     // ---- softmax of the item straight from S in TMEM (this thread = row b) -----------------
-    mbar_wait(&sm.wbar, (uint32_t)(j & 1));  // W metadata
-    mbar_wait(&sm.sfull, (uint32_t)(j & 1));
+    cwait(&sm.sfull, (uint32_t)(j & 1));  // all K UMMAs done (the W metadata landed with stage 0)
     tc_fence_after();
-    const bool row_ok = wg < nmb && jt < nbt && d.wb0 + jt * kI2Pad + b_in < d.i2;
+#ifdef DQ_GQ_SMTRACE  // profiling build: softmax sub-phases in the MMA warp's trace slots
+    stamp(7);
+#endif
+    const WMeta<kGqG>& wm = sm.wmeta[j & 1];
+    // this thread: row b of M-block mbk, heads 4hh .. 4hh+3 (columns 32hh .. 32hh+31)
+    const bool row_ok = mbk < nmb && jt < nbt && d.wb0 + jt * kI2Pad + b_in < d.i2;
     const float kscale = d.kscale * args.sm_scale * 1.4426950408889634f;
-    float s[kGqG][8];
-    if (wg < nmb) {
+    float s[32];  // [hl * 8 + a], log2 domain
+    if (mbk < nmb) {
+      int acc[4][16];
 #pragma unroll
-      for (int h0 = 0; h0 < kGqG; h0 += 4) {
-        int acc[4][16];
+      for (int hl = 0; hl < 4; ++hl)
+        tc_ld16(tmem + lane_addr + kGqColSY + (uint32_t)(mbk * 128 + (4 * hh + hl) * 16), acc[hl]);
+      tc_wait_ld();
 #pragma unroll
-        for (int hh = 0; hh < 4; ++hh)
-          tc_ld16(tmem + lane_addr + kGqColSY + (uint32_t)(wg * 128 + (h0 + hh) * 16), acc[hh]);
-        tc_wait_ld();
+      for (int hl = 0; hl < 4; ++hl)
 #pragma unroll
-        for (int hh = 0; hh < 4; ++hh)
-#pragma unroll
-          for (int a = 0; a < 8; ++a) {
-            const int h = h0 + hh;
-            const float v = (float)(256 * acc[hh][a] + acc[hh][8 + a] - sm.wmeta.beta[h][a][0]) *
-                            (kscale * sm.wmeta.cs[h][a][0]);
-            s[h][a] = row_ok ? v : -INFINITY;
-          }
-      }
+        for (int a = 0; a < 8; ++a) {
+          const int h = 4 * hh + hl;
+          const float v = (float)(256 * acc[hl][a] + acc[hl][8 + a] - wm.beta[h][a][0]) * (kscale * wm.cs[h][a][0]);
+          s[hl * 8 + a] = row_ok ? v : -INFINITY;
+        }
     } else {
 #pragma unroll
-      for (int h = 0; h < kGqG; ++h)
-#pragma unroll
-        for (int a = 0; a < 8; ++a) s[h][a] = -INFINITY;
+      for (int i = 0; i < 32; ++i) s[i] = -INFINITY;
     }
     tc_fence_before();
+    {  // row maxima per head over (a, b): per-thread over a, then a reduce-scatter (lane & 3 = head)
+      float m4[4];
 #pragma unroll
-    for (int h = 0; h < kGqG; ++h) {
-      float m = s[h][0];
+      for (int hl = 0; hl < 4; ++hl) {
+        float m = s[hl * 8];
 #pragma unroll
-      for (int a = 1; a < 8; ++a) m = fmaxf(m, s[h][a]);
-      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) sm.rowmax[h][warp] = m;
+        for (int a = 1; a < 8; ++a) m = fmaxf(m, s[hl * 8 + a]);
+        m4[hl] = m;
+      }
+#pragma unroll
+      for (int o = 2, n = 4; o >= 1; o >>= 1, n >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+          const float send = up ? m4[i] : m4[n / 2 + i];
+          const float keep = up ? m4[n / 2 + i] : m4[i];
+          m4[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
+        }
+      }
+      float m = m4[0];
+#pragma unroll
+      for (int o = 4; o <= 16; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane < 4) sm.rowmax[hh][mbk * 4 + q][lane] = m;  // lane = head - 4hh
     }
     named_sync(kGqCons);
-    // every K UMMA completed before sfull and every W-metadata read is done: W(j+1) may land
-    if (tid == 0) mbar_arrive(&sm.wfree);
-    float mh[kGqG];
+#ifdef DQ_GQ_SMTRACE
+    stamp(4);
+#endif
+    float mh[4];
 #pragma unroll
-    for (int h = 0; h < kGqG; ++h) {
-      float m = sm.rowmax[h][0];
+    for (int hl = 0; hl < 4; ++hl) {
+      float m = sm.rowmax[hh][0][hl];
 #pragma unroll
-      for (int w = 1; w < kGqWarps; ++w) m = fmaxf(m, sm.rowmax[h][w]);
-      mh[h] = m;
+      for (int w = 1; w < 8; ++w) m = fmaxf(m, sm.rowmax[hh][w][hl]);
+      mh[hl] = m;
     }
     // P = exp2(s - m_h) and the per-column maxima over the item's rows
 #pragma unroll
-    for (int h = 0; h < kGqG; ++h)
+    for (int i = 0; i < 32; ++i) s[i] = ex2(s[i] - mh[i / 8]);  // masked rows: ex2(-inf) = 0
+    {
+      unsigned t[32];  // P >= 0: float order = unsigned order of the bits
 #pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        const float p = s[h][a] == -INFINITY ? 0.f : exp2f(s[h][a] - mh[h]);
-        s[h][a] = p;
-        const unsigned mx = redux_max(__float_as_uint(p));
-        if (lane == ((h * 8 + a) & 31)) atomicMax(&sm.pmax[h][a], mx);
-      }
+      for (int i = 0; i < 32; ++i) t[i] = __float_as_uint(s[i]);
+      warp_reduce_scatter(t, lane, [](unsigned x, unsigned y) { return max(x, y); });
+      atomicMax(&sm.pmax[32 * hh + lane], t[0]);
+    }
     named_sync(kGqCons);
+#ifdef DQ_GQ_SMTRACE
+    stamp(6);
+#endif
     // 15-bit fixed point per column; limbs hi (<= 128) and lo into the B operand of the V UMMAs
     {
-      const int b_item = jt * kI2Pad + b_in;
-      unsigned char* pcol = sm.pr.pb + (b_item >> 4) * 128 + inv_ord16<4>(b_item & 15);
-      const bool write = wg < nmb && jt < nbt;
+      int pint[32];
 #pragma unroll
-      for (int h = 0; h < kGqG; ++h)
+      for (int i = 0; i < 32; ++i)
+        pint[i] = __float2int_rn(s[i] * pow2_sub_exp3<kGqPBits>(sm.pmax[32 * hh + i]));
+      if (mbk < nmb && jt < nbt) {
+        const int b_item = jt * kI2Pad + b_in;
+        unsigned char* pcol = sm.pr.pb + (b_item >> 4) * 128 + inv_ord16<4>(b_item & 15);
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          const int pint = __float2int_rn(s[h][a] * pow2_sub_exp(__uint_as_float(sm.pmax[h][a]), kGqPBits));
-          const int gs = redux_add(pint);
-          if (lane == ((h * 8 + a) & 31)) atomicAdd(&sm.gsum[h][a], gs);
-          if (write) {
-            pcol[((h * 2 + 0) * (kCB / 16)) * 128 + a * 16] = (unsigned char)(pint >> 8);
-            pcol[((h * 2 + 1) * (kCB / 16)) * 128 + a * 16] = (unsigned char)(pint & 0xFF);
+        for (int hl = 0; hl < 4; ++hl)
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            const int h = 4 * hh + hl;
+            pcol[((h * 2 + 0) * (kCB / 16)) * 128 + a * 16] = (unsigned char)(pint[hl * 8 + a] >> 8);
+            pcol[((h * 2 + 1) * (kCB / 16)) * 128 + a * 16] = (unsigned char)(pint[hl * 8 + a] & 0xFF);
           }
-        }
+      }
+      warp_reduce_scatter(pint, lane, [](int x, int y) { return x + y; });
+      atomicAdd(&sm.gsum[32 * hh + lane], pint[0]);
     }
-    if (tid < kGqG * 8) (&sm.pinv[0][0])[tid] = pow2_exp_sub(__uint_as_float((&sm.pmax[0][0])[tid]), kGqPBits);
+    if (tid < kGqG * 8) sm.pinv[tid] = pow2_exp_sub(__uint_as_float(sm.pmax[tid]), kGqPBits);
+    named_sync(kGqCons);  // gsum complete
+    if (tid < kGqG * 8) sm.xoff[tid] = -(float)(X * sm.gsum[tid]) * sm.pinv[tid];
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P read by the tensor cores
     named_sync(kGqCons);
     if (tid == 0) mbar_arrive(&sm.pfull);
     stamp(2);
 
     // ---- V phase: widen stage vs, fold Y of stage vs - 1 while its UMMAs run ------------------
-    float o[4][8];  // [head 4wg + hl][c] for e = lane_in & 15, summed over this thread's bond rows
+    float o[2][8];  // [head 2wg + hl][c] for e = lane_in & 15, summed over this thread's bond rows
 #pragma unroll
-    for (int hl = 0; hl < 4; ++hl)
+    for (int hl = 0; hl < 2; ++hl)
 #pragma unroll
       for (int c = 0; c < 8; ++c) o[hl][c] = 0.f;
     auto widen_v = [&]() {
-      const int slot = st % kGqStages, ab = na & 1;
-      mbar_wait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
-      if (na >= 2) mbar_wait(&sm.afree[ab], (uint32_t)(((na >> 1) - 1) & 1));
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int t = 2 * wg + i;
+      const int slot = st % kGqStages, ab = na % kGqNumA;
+      cwait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
+      if (na >= kGqNumA) cwait(&sm.afree[ab], (uint32_t)((na / kGqNumA - 1) & 1));
+      {
+        const int t = wg;  // this warpgroup's tile
         if (t < nbt) {
           const unsigned char* src = sm.ring[slot] + t * kGqVTileBytes + lane_in * 32;
           const uint4 c0 = *reinterpret_cast<const uint4*>(src);
@@ -445,7 +532,11 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
             v[2 * k] = wv[k] & 0x0F0F0F0Fu;
             v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
           }
+#ifndef DQ_GQ_NULL_WIDEN
           tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + t * 16), v);
+#else
+          if (v[0] == 0x12345678u) args.trace[0] = v[1];
+#endif
         }
       }
       tc_wait_st();
@@ -458,40 +549,44 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     };
     auto fold_y = [&](int vs) {
       const int yb = vs & 1;
-      mbar_wait(&sm.yfull[yb], (uint32_t)(uyc[yb] & 1));
+      cwait(&sm.yfull[yb], (uint32_t)(uyc[yb] & 1));
       ++uyc[yb];
       tc_fence_after();
-      float yf[4][8];
+      float yf[2][8];
       {
-        int y[4][16];
+        int y[2][16];
 #pragma unroll
-        for (int hl = 0; hl < 4; ++hl)
-          tc_ld16(tmem + lane_addr + kGqColSY + (uint32_t)(yb * 128 + (4 * wg + hl) * 16), y[hl]);
+        for (int hl = 0; hl < 2; ++hl)
+          tc_ld16(tmem + lane_addr + kGqColSY + (uint32_t)(yb * 128 + (2 * wg + hl) * 16), y[hl]);
         tc_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.yfree[yb]);
 #pragma unroll
-        for (int hl = 0; hl < 4; ++hl) {
-          const int h = 4 * wg + hl;
-          const float4 pi0 = *reinterpret_cast<const float4*>(&sm.pinv[h][0]);
-          const float4 pi1 = *reinterpret_cast<const float4*>(&sm.pinv[h][4]);
-          const int4 gs0 = *reinterpret_cast<const int4*>(&sm.gsum[h][0]);
-          const int4 gs1 = *reinterpret_cast<const int4*>(&sm.gsum[h][4]);
+        for (int hl = 0; hl < 2; ++hl) {
+          const int h = 2 * wg + hl;
+          const float4 pi0 = *reinterpret_cast<const float4*>(&sm.pinv[h * 8]);
+          const float4 pi1 = *reinterpret_cast<const float4*>(&sm.pinv[h * 8 + 4]);
+          const float4 xo0 = *reinterpret_cast<const float4*>(&sm.xoff[h * 8]);
+          const float4 xo1 = *reinterpret_cast<const float4*>(&sm.xoff[h * 8 + 4]);
           const float pi[8] = {pi0.x, pi0.y, pi0.z, pi0.w, pi1.x, pi1.y, pi1.z, pi1.w};
-          const int gs[8] = {gs0.x, gs0.y, gs0.z, gs0.w, gs1.x, gs1.y, gs1.z, gs1.w};
+          const float xo[8] = {xo0.x, xo0.y, xo0.z, xo0.w, xo1.x, xo1.y, xo1.z, xo1.w};
+          // (sum_b (code + X) Pint - X sum_b Pint) * 2^(e - 15): both limbs in one exact s32
 #pragma unroll
-          for (int a = 0; a < 8; ++a)
-            yf[hl][a] = (float)(256 * y[hl][a] + y[hl][8 + a] - X * gs[a]) * pi[a];
+          for (int a = 0; a < 8; ++a) yf[hl][a] = fmaf((float)(256 * y[hl][a] + y[hl][8 + a]), pi[a], xo[a]);
         }
       }
+#ifdef DQ_GQ_NULL_FOLD  // measurement only: no G0v contraction
+      o[0][0] += yf[0][0] + yf[1][7];
+      return;
+#endif
       // O[h, c, e] += sum_a G0v[a, c, r] Y[h, a, (r, e)] for this thread's (r, e)
       const int rr = 8 * vs + (lane_in >> 4);
 #pragma unroll
       for (int a = 0; a < 8; ++a) {
         const float4 g_lo = sm.g0v[2 * (a * kMaxR + rr)], g_hi = sm.g0v[2 * (a * kMaxR + rr) + 1];
 #pragma unroll
-        for (int hl = 0; hl < 4; ++hl) {
+        for (int hl = 0; hl < 2; ++hl) {
           const float y = yf[hl][a];
           ffma2(o[hl][0], o[hl][1], g_lo.x, g_lo.y, y, y);
           ffma2(o[hl][2], o[hl][3], g_lo.z, g_lo.w, y, y);
@@ -500,7 +595,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
         }
       }
     };
-    mbar_wait(&sm.g0bar, (uint32_t)(j & 1));
+    cwait(&sm.g0bar, (uint32_t)(j & 1));
     for (int vs = 0; vs < d.nslices; ++vs) {
       widen_v();
       if (vs > 0) fold_y(vs - 1);
@@ -510,15 +605,15 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
 
     // ---- reduce over bond rows: lanes l / l ^ 16, then the 4 warps of the warpgroup ----------
 #pragma unroll
-    for (int hl = 0; hl < 4; ++hl)
+    for (int hl = 0; hl < 2; ++hl)
 #pragma unroll
       for (int c = 0; c < 8; ++c) o[hl][c] += __shfl_xor_sync(0xffffffffu, o[hl][c], 16);
     named_sync(kGqCons);  // every V UMMA has completed (yfull): P is dead
     if (lane < 16) {
 #pragma unroll
-      for (int hl = 0; hl < 4; ++hl)
+      for (int hl = 0; hl < 2; ++hl)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) sm.pr.red[q][4 * wg + hl][c * 16 + lane] = o[hl][c];
+        for (int c = 0; c < 8; ++c) sm.pr.red[q][2 * wg + hl][c * 16 + lane] = o[hl][c];
     }
     named_sync(kGqCons);
     for (int i = tid; i < kGqG * kD; i += kGqCons) {
@@ -526,17 +621,19 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       const float v = sm.pr.red[0][h][dd] + sm.pr.red[1][h][dd] + sm.pr.red[2][h][dd] + sm.pr.red[3][h][dd];
       args.part_o[((size_t)d.part * kGqG + h) * kD + dd] = v * d.vscale;
     }
-    if (tid < kGqG) {
+    if (q == 0 && mbk == 0 && lane < 4) {  // warps 0 / 8: heads 4hh .. 4hh+3
+      const int h = 4 * hh + lane;
       float l = 0.f;
 #pragma unroll
-      for (int a = 0; a < 8; ++a) l += (float)sm.gsum[tid][a] * sm.pinv[tid][a];
-      args.part_ml[((size_t)d.part * kGqG + tid) * 2 + 0] = mh[tid];  // log2 domain
-      args.part_ml[((size_t)d.part * kGqG + tid) * 2 + 1] = l;
+      for (int a = 0; a < 8; ++a) l += (float)sm.gsum[h * 8 + a] * sm.pinv[h * 8 + a];
+      const float mv = lane == 0 ? mh[0] : lane == 1 ? mh[1] : lane == 2 ? mh[2] : mh[3];
+      args.part_ml[((size_t)d.part * kGqG + h) * 2 + 0] = mv;  // log2 domain
+      args.part_ml[((size_t)d.part * kGqG + h) * 2 + 1] = l;
     }
     named_sync(kGqCons);  // red, pmax, gsum, pinv, g0v reusable
     if (tid < kGqG * 8) {
-      (&sm.pmax[0][0])[tid] = 0u;
-      (&sm.gsum[0][0])[tid] = 0;
+      sm.pmax[tid] = 0u;
+      sm.gsum[tid] = 0;
     }
     stamp(5);
   }

@@ -33,6 +33,8 @@ constexpr int kWImageBytes = kWChunkBytes<G> + (int)sizeof(WMeta<G>);
 // the mma.sync fragments (path 0), or plain for tcgen05 (path 1: rows a of one bond row
 // form a K-major core matrix, 8 rows x 16 bytes, the next bond row 128 bytes further)
 __device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a, int path = 0) {
+  if (path == 2)  // GQA path (8 heads, r = 64): slices of 8 bond rows [rr / 8][h*2 + limb][rr % 8][a], 16 KB each
+    return (((rr >> 3) * 16 + h * 2 + limb) * 8 + (rr & 7)) * 8 + a;
   return ((h * 2 + limb) * r + rr) * 8 + (path ? a : (a ^ (2 * (rr & 3))));
 }
 

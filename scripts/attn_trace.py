@@ -12,13 +12,14 @@ from paper_2405_12591_b200 import _lib  # noqa: E402
 from paper_2405_12591_b200.attention import DecodeKvCache  # noqa: E402
 
 units, T = int(os.environ.get("UNITS", 512)), int(os.environ.get("T", 4096))
+G = int(os.environ.get("G", 1))  # G=8: the tcgen05 GQA kernel (path 2)
 ctas = os.environ.get("CTAS")
-cache = DecodeKvCache(layers=1, units=units, g=1, bits=4, ctas=None if ctas is None else int(ctas),
-                      tc=bool(int(os.environ.get("TC", "0"))))
+cache = DecodeKvCache(layers=1, units=units, g=G, bits=4, ctas=None if ctas is None else int(ctas),
+                      tc=None if G == 8 else bool(int(os.environ.get("TC", "0"))))
 k = torch.randn((units, T, 128), device="cuda").half()
 cache.prefill(0, k, k)
 del k
-q = torch.randn((units, 1, 128), device="cuda").half()
+q = torch.randn((units, G, 128), device="cuda").half()
 out = torch.empty_like(q)
 cache.attend(0, q, out)
 a = cache._layers[0].args
@@ -31,8 +32,18 @@ t = trace.cpu().numpy().astype(np.float64)
 if os.environ.get("SAVE"):
     np.savez(os.environ["SAVE"], trace=trace.cpu().numpy(), work=cache._layers[0].keep[1].cpu().numpy())
 t0 = t[:, 0].min()
+path = cache._layers[0].args.path
+if path == 2:  # stamps 0 start, 1 K done, 2 softmax done, 3 V done, 5 end; MMA warp 7 / 4 / 6
+    rel = lambda c: ((t[:, c] - t[:, 0]) / 1e3).mean()  # noqa: E731
+    print(f"MMA warp: K issue {rel(7):.2f} -> {rel(4):.2f} us, V issue done {rel(6):.2f} us; consumers: K done "
+          f"{rel(1):.2f}, softmax done {rel(2):.2f}, V done {rel(3):.2f}, end {rel(5):.2f} us (item-relative means)")
+    if os.environ.get("MMAWAIT"):  # build with -DDQ_GQ_MMAWAIT: slot 6 / 4 = MMA warp waits (K / V), ns
+        print(f"MMA warp waits: K phase {(t[:, 6] / 1e3).mean():.2f} us, V phase {(t[:, 4] / 1e3).mean():.2f} us")
+    if os.environ.get("SMTRACE"):  # build with -DDQ_GQ_SMTRACE: 7 S ready, 4 row max, 6 column max
+        print(f"softmax: S ready {rel(7):.2f}, row max {rel(4):.2f}, column max {rel(6):.2f}, P written {rel(2):.2f}")
+    t[:, 4] = t[:, 3]
 ph = np.diff(t[:, :6], axis=1) / 1e3  # us
-names = (["K stages", "softmax", "V stages", "(unused)", "epilogue"] if cache._layers[0].args.path == 1 else
+names = (["K stages", "softmax", "V stages", "(unused)", "epilogue"] if path in (1, 2) else
          ["prologue+W", "K stages", "softmax", "V stages", "epilogue"])
 print(f"ctas {a.nctas}, items {a.nwork}, kernel span {(t[:, 5].max() - t0) / 1e3:.1f} us")
 for i, n in enumerate(names):
@@ -53,7 +64,7 @@ if cache._layers[0].args.path == 1:  # stamps 7 / 4: the MMA warp's K-issue star
           f"into the item; consumers end K at {((t[:, 1] - t[:, 0]) / 1e3).mean():.2f} us; "
           f"MMA waited {(t[:, 6] / 1e3).mean():.2f} us of it on A buffers")
 # per-CTA finish times (stamp 6 = blockIdx, 7 = SM; path 1 reuses them)
-if cache._layers[0].args.path == 1:
+if path in (1, 2):
     t[:, 6] = 0
 cta = t[:, 6].astype(int)  # (path 1: no SM ids)
 ncta = cta.max() + 1
