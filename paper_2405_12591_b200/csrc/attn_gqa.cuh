@@ -118,6 +118,14 @@ __device__ __forceinline__ float pow2_sub_exp3(unsigned xbits) {
   return __uint_as_float(((unsigned)(K + 253) << 23) - e);
 }
 
+// one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n.reg .pred P;\n.reg .b32 r;\nelect.sync r|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}" : "=r"(p));
+  return p != 0;
+}
+
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, int (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -228,99 +236,68 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   }
 
   if (warp == kGqWarps + 1) {
-    // ---- MMA warp: one elected lane issues every UMMA of the CTA ---------------------------
-    if (lane == 0) {
-      const uint32_t id_k = tc_idesc(128, 128, 0, 1);  // codes u8 x W limbs s8
-      const uint32_t id_v = tc_idesc(128, 128, 0, 0);  // codes u8 x P limbs u8
-      const uint64_t pdesc = tc_sdesc(sm.pr.pb, 128, (kCB / 16) * 128);  // P: b chunks 128 B, (h, limb) groups 2 KB
-      int na = 0;              // A-buffer uses = ring stages consumed
-      int uy[2] = {0, 0};      // Y-buffer uses
-      for (int j = 0;; ++j) {
-        mbar_wait_spin(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
-        const SubItem d = sm.sub[j % kSubRing];
-        if (d.nbt == 0) break;
-        const int nmb = (d.nbt + 1) / 2;
-        // S occupies the Y columns: the previous item's epilogue must have read both buffers
-        for (int b = 0; b < 2; ++b)
-          if (uy[b] > 0) mbar_wait_spin(&sm.yfree[b], (uint32_t)((uy[b] - 1) & 1));
+    // ---- MMA warp: the whole (converged) warp runs the schedule with warp-uniform operands,
+    // one elected lane issues each UMMA / commit (operands stay in uniform registers: no
+    // per-UMMA register-to-uniform moves on the issue path)
+    const bool leader = elect_one();
+    const uint32_t id_k = tc_idesc(128, 128, 0, 1);  // codes u8 x W limbs s8
+    const uint32_t id_v = tc_idesc(128, 128, 0, 0);  // codes u8 x P limbs u8
+    const uint64_t pdesc = tc_sdesc(sm.pr.pb, 128, (kCB / 16) * 128);  // P: b chunks 128 B, (h, limb) groups 2 KB
+    int na = 0;              // A-buffer uses = ring stages consumed
+    int uy[2] = {0, 0};      // Y-buffer uses
+    for (int j = 0;; ++j) {
+      mbar_wait_spin(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+      const int nbt = sm.sub[j % kSubRing].nbt, nK = sm.sub[j % kSubRing].nK, nV = sm.sub[j % kSubRing].nslices;
+      if (nbt == 0) break;
+      // S occupies the Y columns: the previous item's epilogue must have read both buffers
+      for (int b = 0; b < 2; ++b)
+        if (uy[b] > 0) mbar_wait_spin(&sm.yfree[b], (uint32_t)((uy[b] - 1) & 1));
+      tc_fence_after();
+      for (int ks = 0; ks < nK; ++ks, ++na) {
+        const int ab = na % kGqNumA;
+        mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
         tc_fence_after();
-#ifndef DQ_GQ_SMTRACE
-        if (args.trace) args.trace[(size_t)d.item * 8 + 7] = global_ns();  // MMA warp: K issue starts
-#endif
-#ifdef DQ_GQ_MMAWAIT  // measurement only: time the MMA warp waits for A buffers (K: slot 6, V: slot 4)
-        int64_t wk = 0, wv = 0;
-#endif
-        for (int ks = 0; ks < d.nK; ++ks, ++na) {
-          const int ab = na % kGqNumA;
-#ifdef DQ_GQ_MMAWAIT
-          const int64_t w0 = global_ns();
-          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
-          wk += global_ns() - w0;
-#else
-          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
-#endif
-          tc_fence_after();
-          // this stage's W slice: N rows (h*2 + limb)*8 + a in 16 core-matrix groups 1 KB apart,
-          // bond rows 128 B apart; k-step kk (2 bond rows) = +256 B = +16 in the address field
-          const uint64_t bdesc = tc_sdesc(sm.ring[na % kGqStages] + 16384, 128, 1024);
-          const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64);
-          const uint32_t acc0 = ks ? 1u : 0u;
+        // this stage's W slice: N rows (h*2 + limb)*8 + a in 16 core-matrix groups 1 KB apart,
+        // bond rows 128 B apart; k-step kk (2 bond rows) = +256 B = +16 in the address field
+        const uint64_t bdesc = tc_sdesc(sm.ring[na % kGqStages] + 16384, 128, 1024);
+        const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64);
+        const uint32_t acc0 = ks ? 1u : 0u;
+        if (leader) {
 #ifndef DQ_GQ_NULL_MMA  // measurement only: no UMMAs (the commits still signal)
-          if (nmb == 2) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              tc_mma_ts(tmem + kGqColSY, a0 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
-              tc_mma_ts(tmem + kGqColSY + 128, a0 + 32 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
-            }
-          } else {
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) tc_mma_ts(tmem + kGqColSY, a0 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
+          for (int kk = 0; kk < 4; ++kk) {
+            tc_mma_ts(tmem + kGqColSY, a0 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
+            if (nbt > 2) tc_mma_ts(tmem + kGqColSY + 128, a0 + 32 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
           }
-#else
-          if (bdesc == 0) args.trace[1] = a0 + acc0;
 #endif
           tc_commit(&sm.afree[ab]);
           tc_commit(&sm.empty[na % kGqStages]);  // the W slice has been read
         }
-        tc_commit(&sm.sfull);
-#if !defined(DQ_GQ_SMTRACE) && !defined(DQ_GQ_MMAWAIT)
-        if (args.trace) args.trace[(size_t)d.item * 8 + 4] = global_ns();  // MMA warp: K issue done
-#endif
-        mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs in shared memory, S read
+        __syncwarp();
+      }
+      if (leader) tc_commit(&sm.sfull);
+      __syncwarp();
+      mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs in shared memory, S read
+      tc_fence_after();
+      for (int vs = 0; vs < nV; ++vs, ++na) {
+        const int ab = na % kGqNumA, yb = vs & 1;
+        mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
+        if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
         tc_fence_after();
-        for (int vs = 0; vs < d.nslices; ++vs, ++na) {
-          const int ab = na % kGqNumA, yb = vs & 1;
-#ifdef DQ_GQ_MMAWAIT
-          const int64_t w0 = global_ns();
-          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
-          if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
-          wv += global_ns() - w0;
-#else
-          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
-#endif
-          if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
-          tc_fence_after();
-          const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64), d0 = tmem + kGqColSY + (uint32_t)(yb * 128);
+        const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64), d0 = tmem + kGqColSY + (uint32_t)(yb * 128);
+        if (leader) {
 #ifndef DQ_GQ_NULL_MMA
           // 32 rows b per k-step: +256 B of P = +16 in the address field
-          tc_mma_ts(d0, a0, pdesc, id_v, 0u);
-          for (int kk = 1; kk < 2 * d.nbt; ++kk) tc_mma_ts(d0, a0 + kk * 8, pdesc + kk * 16, id_v, 1u);
-#else
-          if (pdesc == 0) args.trace[1] = a0 + d0;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            if (kk < 2 * nbt) tc_mma_ts(d0, a0 + kk * 8, pdesc + kk * 16, id_v, kk ? 1u : 0u);
 #endif
           tc_commit(&sm.afree[ab]);
           tc_commit(&sm.empty[na % kGqStages]);
           tc_commit(&sm.yfull[yb]);
-          ++uy[yb];
         }
-#ifdef DQ_GQ_MMAWAIT
-        if (args.trace) {
-          args.trace[(size_t)d.item * 8 + 6] = wk;
-          args.trace[(size_t)d.item * 8 + 4] = wv;
-        }
-#elif !defined(DQ_GQ_SMTRACE)
-        if (args.trace) args.trace[(size_t)d.item * 8 + 6] = global_ns();  // MMA warp: V issue done
-#endif
+        __syncwarp();
+        ++uy[yb];
       }
     }
     __syncwarp();
@@ -555,10 +532,17 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       float yf[2][8];
       {
         int y[2][16];
+#ifndef DQ_GQ_NULL_YLD  // measurement only: no Y reads from TMEM
 #pragma unroll
         for (int hl = 0; hl < 2; ++hl)
           tc_ld16(tmem + lane_addr + kGqColSY + (uint32_t)(yb * 128 + (2 * wg + hl) * 16), y[hl]);
         tc_wait_ld();
+#else
+#pragma unroll
+        for (int hl = 0; hl < 2; ++hl)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) y[hl][k] = lane + k;
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.yfree[yb]);
@@ -596,10 +580,14 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       }
     };
     cwait(&sm.g0bar, (uint32_t)(j & 1));
+    // the fold lags the widening by two stages: stage vs's UMMAs have two widen + fold
+    // rounds to complete before their Y is read (Y is double-buffered, so the UMMAs of vs wait
+    // only for the fold of vs - 2, which comes right before)
     for (int vs = 0; vs < d.nslices; ++vs) {
       widen_v();
-      if (vs > 0) fold_y(vs - 1);
+      if (vs > 1) fold_y(vs - 2);
     }
+    fold_y(d.nslices - 2);
     fold_y(d.nslices - 1);
     stamp(3);
 
