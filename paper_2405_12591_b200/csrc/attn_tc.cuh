@@ -215,69 +215,77 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
   }
 
   if (warp == kWarps + 1) {
-    // ---- MMA warp: one elected lane issues every UMMA of the CTA ---------------------------
-    if (lane == 0) {
-      // both limbs of a B operand in one UMMA: N = 16 rows (hi limb a = 0..7, lo limb a = 0..7)
-      const uint32_t id_k = tc_idesc(128, 16, 0, 1);  // codes u8 x W limbs s8
-      const uint32_t id_v = tc_idesc(128, 32, 0, 0);  // codes u8 x P limbs u8 (hi, mid, lo, 0)
-      int na = 0;  // A-buffer uses
-      for (int j = 0;; ++j) {
-        mbar_wait_spin(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
-        const SubItem d = sm.sub[j % kSubRing];
-        if (d.nbt == 0) break;
-        const int nmb = (d.nbt + 1) / 2;
-        mbar_wait_spin(&sm.wbar, (uint32_t)(j & 1));        // W image of this item's segment
-        if (j > 0) mbar_wait_spin(&sm.sfree, (uint32_t)((j - 1) & 1));  // S of the previous item read
-        if (args.trace) args.trace[(size_t)d.item * 8 + 7] = global_ns();  // MMA warp: K issue starts
-        bool acc_s[2] = {false, false};  // per bond-row group: accumulate into S?
-        int64_t wait_ns = 0;
-        for (int ks = 0; ks < d.nK; ++ks, ++na) {
-          const int ab = na % kNumA;
-          const int64_t w0 = args.trace ? global_ns() : 0;
-          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
-          if (args.trace) wait_ns += global_ns() - w0;
-          tc_fence_after();
-          const int rk0 = ks * d.RK, nr = min(d.RK, d.r - rk0);
-          for (int kk = 0; kk < nr / 2; ++kk) {  // UMMA k-step = 32 bytes = 2 bond rows
-            const int rr = rk0 + 2 * kk;
-            const int grp = rr < kGroupR ? 0 : 1;
-            // rows 0-7: hi limb chunk of bond row rr, rows 8-15: lo limb (d.r * 128 bytes further)
-            const uint64_t bdesc = tc_sdesc(&sm.w[rr * 8], 128, d.r * 128);
-            for (int mb = 0; mb < nmb; ++mb) {
-              const uint32_t dcol = kColS + (uint32_t)((grp * 2 + mb) * 16);
-              const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * d.RK * 4 + kk * 8);
-              tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_k, acc_s[grp] ? 1u : 0u);
+    // ---- MMA warp: the whole (converged) warp runs the schedule with warp-uniform operands;
+    // one elected lane issues each UMMA / commit (operands stay in uniform registers)
+    uint32_t lead;
+    asm volatile("{\n.reg .pred P;\n.reg .b32 r;\nelect.sync r|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}" : "=r"(lead));
+    const bool leader = lead != 0;
+    // both limbs of a B operand in one UMMA: N = 16 rows (hi limb a = 0..7, lo limb a = 0..7)
+    const uint32_t id_k = tc_idesc(128, 16, 0, 1);  // codes u8 x W limbs s8
+    const uint32_t id_v = tc_idesc(128, 32, 0, 0);  // codes u8 x P limbs u8 (hi, mid, lo, 0)
+    int na = 0;  // A-buffer uses
+    for (int j = 0;; ++j) {
+      mbar_wait_spin(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+      const int nbt = sm.sub[j % kSubRing].nbt, nK = sm.sub[j % kSubRing].nK, RK = sm.sub[j % kSubRing].RK;
+      const int r = sm.sub[j % kSubRing].r;
+      if (nbt == 0) break;
+      const int nmb = (nbt + 1) / 2;
+      mbar_wait_spin(&sm.wbar, (uint32_t)(j & 1));        // W image of this item's segment
+      if (j > 0) mbar_wait_spin(&sm.sfree, (uint32_t)((j - 1) & 1));  // S of the previous item read
+      for (int ks = 0; ks < nK; ++ks, ++na) {
+        const int ab = na % kNumA;
+        mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
+        tc_fence_after();
+        const int rk0 = ks * RK, nr = min(RK, r - rk0);
+        // rows 0-7: hi limb chunk of bond row rr, rows 8-15: lo limb (r * 128 bytes further);
+        // k-step kk (2 bond rows) = +256 B = +16 in the address field
+        const uint64_t bdesc = tc_sdesc(&sm.w[rk0 * 8], 128, r * 128);
+        const uint32_t acol = tmem + kColA + (uint32_t)(ab * 64);
+        if (leader) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {  // UMMA k-step = 32 bytes = 2 bond rows
+            if (kk < nr / 2) {
+              const int rr = rk0 + 2 * kk;
+              const uint32_t grp = rr < kGroupR ? 0u : 1u;
+              const uint32_t acc = (rr != 0 && rr != kGroupR) ? 1u : 0u;  // each group's first bond rows reset S
+              tc_mma_ts(tmem + kColS + grp * 32, acol + kk * 8, bdesc + kk * 16, id_k, acc);
+              if (nmb == 2) tc_mma_ts(tmem + kColS + grp * 32 + 16, acol + RK * 4 + kk * 8, bdesc + kk * 16, id_k, acc);
             }
-            acc_s[grp] = true;
           }
           tc_commit(&sm.afree[ab]);
         }
-        tc_commit(&sm.sfull);
-        if (args.trace) args.trace[(size_t)d.item * 8 + 4] = global_ns();  // MMA warp: K issue done
-        if (args.trace) args.trace[(size_t)d.item * 8 + 6] = wait_ns;      // MMA warp: K waits on A
-        mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs of this item in shared memory
-        if (j > 0) mbar_wait_spin(&sm.yfree, (uint32_t)((j - 1) & 1));  // Y / sum P of the previous item read
-        tc_fence_after();
-        for (int t = 0; t < d.nbt; ++t)
-          for (int sl = 0; sl < 2; ++sl, ++na) {
-            const int ab = na % kNumA;
-            mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
-            tc_fence_after();
+        __syncwarp();
+      }
+      if (leader) tc_commit(&sm.sfull);
+      __syncwarp();
+      mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs of this item in shared memory
+      if (j > 0) mbar_wait_spin(&sm.yfree, (uint32_t)((j - 1) & 1));  // Y / sum P of the previous item read
+      tc_fence_after();
+      const uint64_t pdesc = tc_sdesc(&sm.pb[0][0], 128, sizeof(sm.pb[0]));
+      for (int t = 0; t < nbt; ++t)
+        for (int sl = 0; sl < 2; ++sl, ++na) {
+          const int ab = na % kNumA;
+          mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kNumA) & 1));
+          tc_fence_after();
+          if (leader) {
+#pragma unroll
             for (int kk = 0; kk < 2; ++kk) {  // 64 b = 2 k-steps
-              // B rows: 0-7 P hi limb, 8-15 mid, 16-23 lo, 24-31 zero (the next limb buffers)
-              const uint64_t bdesc = tc_sdesc(&sm.pb[0][(t * 4 + kk * 2) * 128], 128, sizeof(sm.pb[0]));
+              // B rows: 0-7 P hi limb, 8-15 mid, 16-23 lo, 24-31 zero (the next limb buffers);
+              // +256 B per k-step = +16 in the address field
+              const uint64_t bdesc = pdesc + (uint64_t)((t * 4 + kk * 2) * 8);
               const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-              for (int mb = 0; mb < 4; ++mb) {
-                const uint32_t dcol = kColY + (uint32_t)((sl * 4 + mb) * 32);
-                const uint32_t acol = kColA + (uint32_t)(ab * 64 + mb * 16 + kk * 8);
-                tc_mma_ts(tmem + dcol, tmem + acol, bdesc, id_v, acc);
-              }
+#pragma unroll
+              for (int mb = 0; mb < 4; ++mb)
+                tc_mma_ts(tmem + kColY + (uint32_t)((sl * 4 + mb) * 32), tmem + kColA + (uint32_t)(ab * 64 + mb * 16 + kk * 8),
+                          bdesc, id_v, acc);
               if (sl == 0) tc_mma_ts(tmem + kColPsum, tmem + kColOnes, bdesc, id_v, acc);  // sum_b P
             }
             tc_commit(&sm.afree[ab]);
           }
-        tc_commit(&sm.vdone);
-      }
+          __syncwarp();
+        }
+      if (leader) tc_commit(&sm.vdone);
+      __syncwarp();
     }
     // wait for the consumers' last TMEM reads, then free TMEM
     __syncwarp();
