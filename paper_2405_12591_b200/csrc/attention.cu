@@ -49,6 +49,26 @@ __global__ void __launch_bounds__(128) combine_kernel(dq_attn_args args) {
   combine_unit<G>(args, blockIdx.x, threadIdx.x, tail_s, red, [] { __syncthreads(); });
 }
 
+// combine for the GQA kernel's 8 heads: one 128-thread group per head (named barrier 1 + group),
+// then the fused append once every group has read the tail
+__global__ void __launch_bounds__(kGqG * 128) combine_gqa_kernel(dq_attn_args args) {
+  extern __shared__ float tail_sg[];  // [kGqG][tail_cap]
+  __shared__ float red[kGqG][4];
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const int u = blockIdx.x, grp = threadIdx.x >> 7, d = threadIdx.x & 127;
+  const int hg = args.head_groups > 1 ? args.head_groups : 1;
+  const int tl = args.tail_len ? args.tail_len[u] : 0;
+  const int cap = args.tail_cap > 0 ? args.tail_cap : 1;
+  for (int vv = 0; vv < hg; ++vv)
+    combine_head<kGqG>(args, u, u * hg + vv, grp, d, tl, tail_sg + (size_t)grp * cap, red[grp],
+                       [grp] { asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory"); });
+  if (args.app_k) {
+    __syncthreads();  // every group has read tail_len[u] and the tail
+    if (grp == 0) combine_append(args, u, d, tl);
+  }
+}
+
 __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __half* __restrict__ v_rows,
                                    __half* __restrict__ tail_k, __half* __restrict__ tail_v, int32_t* tail_len,
                                    int tail_cap) {
@@ -117,7 +137,20 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
   if (a.nwork > 0 && (phases & 5)) {
     if (!a.wimg || a.wimg_stride < kWImageBytes<G>) return fail(DQ_ERR_INVALID_ARG, "W image workspace too small");
   }
-  if (a.nseg > 0 && a.nwork > 0 && (phases & 4)) {
+  if (a.nseg > 0 && a.nwork > 0 && (phases & 4) && a.path == 2) {
+    if constexpr (BITS == 4 && G == kGqG) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)a.nseg);
+      cfg.blockDim = dim3(kPrepGqThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute attr_pdl[1];
+      attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr_pdl;
+      cfg.numAttrs = 1;
+      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_prepare_gqa_kernel, a));
+    }
+  } else if (a.nseg > 0 && a.nwork > 0 && (phases & 4)) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)a.nseg, kPrepSplit);
     cfg.blockDim = dim3(kPrepThreadsOf<G>);
@@ -173,11 +206,20 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     }
   }
   if (phases & 2) {
-    const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1);
+    const bool gq = G == kGqG;  // one 128-thread group per head
+    const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1) * (gq ? kGqG : 1);
     const int hg = a.head_groups > 1 ? a.head_groups : 1;
+    if (gq && csmem > 48 * 1024) {
+      static bool cg_attr = false;
+      if (!cg_attr) {
+        DQ_CUDA_TRY(cudaFuncSetAttribute(combine_gqa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        cg_attr = true;
+      }
+      if (csmem > 160 * 1024) return fail(DQ_ERR_UNSUPPORTED, "tail capacity %d too large for the GQA combine", a.tail_cap);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units / hg));
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(gq ? kGqG * 128 : 128);
     cfg.dynamicSmemBytes = csmem;
     cfg.stream = s;
     cudaLaunchAttribute attr_pdl[1];
@@ -185,7 +227,11 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr_pdl;
     cfg.numAttrs = 1;
-    DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, combine_kernel<G>, a));
+    if (gq) {
+      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, combine_gqa_kernel, a));
+    } else {
+      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, combine_kernel<G>, a));
+    }
   }
   return DQ_OK;
 }

@@ -274,12 +274,13 @@ def test_fused_append_matches_attend_then_append(dq):
     assert torch.equal(a.tail_k[0, :, :steps - chunk], b.tail_k[0, :, :steps - chunk])
 
 
-def test_decode_step_graph_matches_eager(dq):
+@pytest.mark.parametrize("g,P", [(2, 700), (8, 704)])  # mma.sync split kernel / tcgen05 GQA kernel (path 2)
+def test_decode_step_graph_matches_eager(dq, g, P):
     """DecodeStepGraph (captured multi-layer step, host I/O) == eager attend(append=...) per layer."""
     from paper_2405_12591_b200.attention import DecodeKvCache
     from paper_2405_12591_b200.decode_step import DecodeStepGraph
 
-    L, U, g, P, steps = 3, 4, 2, 700, 5
+    L, U, steps = 3, 4, 5
     rng = np.random.default_rng(21)
     kv = torch.from_numpy(rng.standard_normal((L, 2, U, P, 128)).astype(np.float16)).cuda()
     caches = [DecodeKvCache(layers=L, units=U, g=g, bits=4, chunk_len=64) for _ in range(2)]
@@ -304,6 +305,7 @@ def test_decode_step_graph_matches_eager(dq):
 
     fill(0)
     stepper = DecodeStepGraph(graphed, q_h, k_h, v_h, out_h)  # runs step 0 eagerly, then captures
+    assert graphed._layers[0].args.path == (2 if g == 8 else 0)
     ref = eager_step()
     torch.cuda.synchronize()
     assert torch.equal(out_h, ref)
