@@ -35,6 +35,7 @@ from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_
 
 HEAD_DIM = 128
 DEFAULT_CHUNK_B = 256
+MAX_CHUNK_B = 512  # > 256: 8-tile items, mma.sync split kernel with g = 1 and 2- / 4-bit codes
 KERNEL_G = (1, 2, 8)  # query heads per kv head the split kernels are instantiated for (8: tcgen05 only)
 GQA_G = 8             # heads of the tcgen05 GQA kernel (path 2)
 MAX_G = 16          # wider GQA groups run as g / kernel_g head groups over the same codes
@@ -144,8 +145,8 @@ class DecodeKvCache:
             raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
         if not 1 <= g <= MAX_G:
             raise Unsupported(f"GQA groups of 1..{MAX_G} query heads per kv head are supported (got {g})")
-        if chunk_b is not None and (chunk_b % 64 or not 64 <= chunk_b <= DEFAULT_CHUNK_B):
-            raise Unsupported(f"work items must be 64..{DEFAULT_CHUNK_B} rows, a multiple of 64")
+        if chunk_b is not None and (chunk_b % 64 or not 64 <= chunk_b <= MAX_CHUNK_B):
+            raise Unsupported(f"work items must be 64..{MAX_CHUNK_B} rows, a multiple of 64")
         if bits not in SUPPORTED_BITS:
             raise UnsupportedBits(f"bits must be in {SUPPORTED_BITS}")
         if layers < 1 or units < 1 or chunk_len < 1:
@@ -281,8 +282,10 @@ class DecodeKvCache:
             ctas = c.value
         self.split_ctas = ctas
         # the largest items: the per-item cost (W image, softmax, epilogue) is fixed, and
-        # smaller items measured slower even where they shorten the scheduler's last round
-        chunk_b = self.chunk_b or DEFAULT_CHUNK_B
+        # smaller items measured slower even where they shorten the scheduler's last round.
+        # 2-bit codes carry half the bytes per row, so their items are 512 rows (C3: 0.387 ->
+        # 0.453 of HBM); at 4 bits 512-row items measured slower (0.630 -> 0.597)
+        chunk_b = self.chunk_b or (MAX_CHUNK_B if self.bits == 2 and gk == 1 else DEFAULT_CHUNK_B)
         wp = plan_work(seg_arr, nseg, vunits, chunk_b)
         if hg > 1:  # a tile range's head groups back to back in the ticket order (L2 reuse)
             order = sorted(range(wp.nwork), key=lambda i: (wp.work[3 * i] // hg, wp.work[3 * i + 1],

@@ -83,13 +83,13 @@ __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __ha
 }
 
 
-template <int BITS, int G>
+template <int BITS, int G, int NT = kTiles>
 int set_attrs() {
   static bool attr = false;
   if (!attr) {
-    const int smem = (int)sizeof(AttnSmem<G>);
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    const int smem = (int)sizeof(AttnSmem<G, NT>);
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      100));
     attr = true;
   }
@@ -195,14 +195,25 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(a.nctas > 0 && a.nctas < a.nwork ? a.nctas : a.nwork));
       cfg.blockDim = dim3(kCtaThreads);
-      cfg.dynamicSmemBytes = sizeof(AttnSmem<G>);
       cfg.stream = s;
       cudaLaunchAttribute attr_pdl[1];
       attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr_pdl;
       cfg.numAttrs = 1;
-      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G>, a));
+      if (a.chunk_b > kCB) {  // 8-tile work items (g = 1, 2- and 4-bit codes)
+        if constexpr (G == 1 && BITS <= 4) {
+          const int rc = set_attrs<BITS, G, 2 * kTiles>();
+          if (rc != DQ_OK) return rc;
+          cfg.dynamicSmemBytes = sizeof(AttnSmem<G, 2 * kTiles>);
+          DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, 2 * kTiles>, a));
+        } else {
+          return fail(DQ_ERR_UNSUPPORTED, "work items of more than %d rows need g = 1 and 2- or 4-bit codes", kCB);
+        }
+      } else {
+        cfg.dynamicSmemBytes = sizeof(AttnSmem<G>);
+        DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G>, a));
+      }
     }
   }
   if (phases & 2) {
@@ -238,9 +249,9 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
 
 template <int BITS>
 int dispatch_g(const dq_attn_args& a, cudaStream_t s) {
-  if (a.chunk_b <= 0 || a.chunk_b > kCB || a.chunk_b % kI2Pad)
-    return fail(DQ_ERR_UNSUPPORTED, "chunk_b must be a multiple of %d in %d..%d (got %d)", kI2Pad, kI2Pad, kCB,
-                a.chunk_b);
+  if (a.chunk_b <= 0 || a.chunk_b > 2 * kCB || a.chunk_b % kI2Pad || (a.chunk_b > kCB && a.path != 0))
+    return fail(DQ_ERR_UNSUPPORTED, "chunk_b must be a multiple of %d in %d..%d (%d off path 0; got %d)", kI2Pad, kI2Pad,
+                2 * kCB, kCB, a.chunk_b);
   switch (a.g) {
     case 1: return launch_attn<BITS, 1>(a, s);
     case 2: return launch_attn<BITS, 2>(a, s);

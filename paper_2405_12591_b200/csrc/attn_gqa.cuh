@@ -279,10 +279,23 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       __syncwarp();
       mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs in shared memory, S read
       tc_fence_after();
+#ifdef DQ_GQ_MMAWAIT  // measurement only: V phase of the MMA warp: span (slot 4) and A / Y waits (slot 6, 7)
+      const int64_t v0 = global_ns();
+      int64_t wa = 0, wy = 0;
+#endif
       for (int vs = 0; vs < nV; ++vs, ++na) {
         const int ab = na % kGqNumA, yb = vs & 1;
+#ifdef DQ_GQ_MMAWAIT
+        int64_t w0 = global_ns();
+        mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
+        wa += global_ns() - w0;
+        w0 = global_ns();
+        if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
+        wy += global_ns() - w0;
+#else
         mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
         if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
+#endif
         tc_fence_after();
         const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64), d0 = tmem + kGqColSY + (uint32_t)(yb * 128);
         if (leader) {
@@ -299,6 +312,14 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
         __syncwarp();
         ++uy[yb];
       }
+#ifdef DQ_GQ_MMAWAIT
+      if (leader && args.trace) {
+        const int it = sm.sub[j % kSubRing].item;
+        args.trace[(size_t)it * 8 + 4] = global_ns() - v0;
+        args.trace[(size_t)it * 8 + 6] = wa;
+        args.trace[(size_t)it * 8 + 7] = wy;
+      }
+#endif
     }
     __syncwarp();
     named_sync2(kGqCons + 32);  // the consumers' last TMEM reads are done

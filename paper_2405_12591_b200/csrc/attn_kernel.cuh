@@ -63,7 +63,8 @@ struct SubItem {
   int stages, pad_[3];      // nbt == 0: end of this CTA's items
 };
 
-template <int G>
+// NT: 64-row tiles per work item (4, or 8 for g = 1: twice the bytes per fixed per-item cost)
+template <int G, int NT = kTiles>
 struct AttnSmem {
   static constexpr int kStages = kStagesOf<G>;
   alignas(128) unsigned char ring[kStages][kStageBytes];
@@ -74,19 +75,19 @@ struct AttnSmem {
   uint64_t descfull[kSubRing];      // descriptor j written (producer arrival), phase j / kSubRing
   SubItem sub[kSubRing];            // descriptor ring: the CTA's j-th item lives in slot j % kSubRing
   alignas(16) WMeta<G> wmeta;  // per-column W scales and excess corrections (TMA target)
-  int gamma[G][8][kTiles]; // excess correction of Y per 64-row tile: kExcess * sum_b Pint[a][b]
+  int gamma[G][8][NT];     // excess correction of Y per 64-row tile: kExcess * sum_b Pint[a][b]
   float lsum[G][kWarps];   // probability mass per warp
-  unsigned pmax[G][8][kTiles];  // largest probability per (h, a, tile), float bits
+  unsigned pmax[G][8][NT];  // largest probability per (h, a, tile), float bits
   // K phase: W limbs, 16-byte chunks [((h*2 + limb)*r + rr)*8 + (a ^ 2*(rr&3))];
   // V phase + epilogue (aliased, W is dead): fp32 G0v [a][rr][c] by TMA
   union {
     uint4 w[G * 2 * kMaxR * 8];
     float4 g0v[8 * kMaxR * 2];
   } wg;
-  // V phase: P limbs [((h*2 + limb)*8 + a)*kNG + (bg ^ 4*(a&1))];
+  // V phase: P limbs [((h*2 + limb)*8 + a)*(4 NT) + (bg ^ 4*(a&1))];
   // epilogue (aliased, P is dead): cross-warp reduction of the O partial
   union {
-    uint4 p[G * 2 * 8 * kNG];
+    uint4 p[G * 2 * 8 * 4 * NT];
     float red[kWarps][G][kD];
   } pr;
   float rowmax[G][kWarps];
@@ -154,8 +155,8 @@ __device__ __forceinline__ void issue_stage(const SubItem& d, int st, unsigned c
 }
 
 // the W image (limb chunks + metadata) of a sub-item's segment onto wbar (one thread)
-template <int G>
-__device__ __forceinline__ void issue_wimg(AttnSmem<G>& sm, const dq_attn_args& a, const SubItem& d) {
+template <int G, int NT>
+__device__ __forceinline__ void issue_wimg(AttnSmem<G, NT>& sm, const dq_attn_args& a, const SubItem& d) {
   const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
   const uint32_t wb = (uint32_t)(G * 2 * d.r * 8 * 16);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -164,18 +165,19 @@ __device__ __forceinline__ void issue_wimg(AttnSmem<G>& sm, const dq_attn_args& 
   bulk_g2s(&sm.wmeta, img + kWChunkBytes<G>, (uint32_t)sizeof(WMeta<G>), &sm.wbar);
 }
 
+template <int NT>
 __device__ __forceinline__ int p_chunk(int h, int limb, int a, int bg) {
-  return ((h * 2 + limb) * 8 + a) * kNG + (bg ^ (4 * (a & 1)));
+  return ((h * 2 + limb) * 8 + a) * (4 * NT) + (bg ^ (4 * (a & 1)));
 }
 
-template <int BITS, int G>
+template <int BITS, int G, int NT = kTiles>
 __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel(dq_attn_args args) {
   constexpr int kStages = kStagesOf<G>;
   constexpr int RB = 2 * BITS;
   constexpr int X = kExcess<BITS>;
   constexpr bool SA = BITS == 8;  // A operand (codes) signed
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  AttnSmem<G>& sm = *reinterpret_cast<AttnSmem<G>*>(smem_raw);
+  AttnSmem<G, NT>& sm = *reinterpret_cast<AttnSmem<G, NT>*>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tid4 = lane & 3;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     mbar_init(&sm.g0bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (tid < G * 8 * kTiles) {
+  if (tid < G * 8 * NT) {
     (&sm.gamma[0][0][0])[tid] = 0;
     (&sm.pmax[0][0][0])[tid] = 0u;
   }
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     // output (the per-segment W images) is read from here on
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
-    if (sm.sub[0].nbt > 0) issue_wimg<G>(sm, args, sm.sub[0]);
+    if (sm.sub[0].nbt > 0) issue_wimg<G, NT>(sm, args, sm.sub[0]);
   }
 
   int st = 0;  // running global stage index (identical in every consumer thread)
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     stamp(1);
     wstamp(0);
     // ---- phase 1: S = W . codes_k on the int8 tensor pipe ------------------------------
-    constexpr int kWpt = kWarps / kTiles;   // warps per 64-row tile
+    constexpr int kWpt = kWarps / NT;       // warps per 64-row tile
     constexpr int MT = 4 / kWpt;            // 16-row m-tiles per warp
     const int jt = warp / kWpt;             // tile of this warp inside the sub-item
     const int bl_base = 16 * MT * (warp % kWpt);  // first row of this warp inside the tile
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     if (tid == 0) {
       const int jn = j + 1;
       mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G>(sm, args, sm.sub[jn % kSubRing]);
+      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT>(sm, args, sm.sub[jn % kSubRing]);
     }
     continue;
 #endif
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       float pq[2], pinv[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const float pm = __uint_as_float(sm.pmax[h][2 * tid4 + q][min(jt, kTiles - 1)]);
+        const float pm = __uint_as_float(sm.pmax[h][2 * tid4 + q][min(jt, NT - 1)]);
         pq[q] = pow2_sub_exp(pm, kPBits<BITS>);
         pinv[q] = pow2_exp_sub(pm, kPBits<BITS>);
       }
@@ -467,8 +469,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
           gsum[k & 1] += pint;
           if (jt < nbt) {
             const int pos = inv_ord16<BITS>(bl & 15);
-            pb[p_chunk(h, 0, a, bl >> 4) * 16 + pos] = (unsigned char)(pint >> 8);
-            pb[p_chunk(h, 1, a, bl >> 4) * 16 + pos] = (unsigned char)(pint & 0xFF);
+            pb[p_chunk<NT>(h, 0, a, bl >> 4) * 16 + pos] = (unsigned char)(pint >> 8);
+            pb[p_chunk<NT>(h, 1, a, bl >> 4) * 16 + pos] = (unsigned char)(pint & 0xFF);
           }
         }
       // per (a, tile) sums: reduce over the 8 gid lanes sharing tid4 (same a, same tile)
@@ -516,8 +518,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         float pinv[G][2];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          ph[h] = sm.pr.p[p_chunk(h, 0, gid, btl * 4 + tid4)];
-          pl_[h] = sm.pr.p[p_chunk(h, 1, gid, btl * 4 + tid4)];
+          ph[h] = sm.pr.p[p_chunk<NT>(h, 0, gid, btl * 4 + tid4)];
+          pl_[h] = sm.pr.p[p_chunk<NT>(h, 1, gid, btl * 4 + tid4)];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             gam[h][q] = sm.gamma[h][2 * tid4 + q][btl];
@@ -596,9 +598,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     if (tid == 0) {
       const int jn = j + 1;
       mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G>(sm, args, sm.sub[jn % kSubRing]);
+      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT>(sm, args, sm.sub[jn % kSubRing]);
     }
-    if (tid < G * 8 * kTiles) {
+    if (tid < G * 8 * NT) {
       (&sm.gamma[0][0][0])[tid] = 0;
       (&sm.pmax[0][0][0])[tid] = 0u;
     }

@@ -95,6 +95,27 @@ def test_decode_attention_prefill_only(dq, bits, g, T, units, ctas, tc):
         assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
 
 
+@pytest.mark.parametrize("bits,T,units,scale", [(4, 4096, 3, 1.0), (2, 8192, 2, 1.0), (4, 1009, 2, 1.0),
+                                                (4, 2240, 2, 20.0), (2, 600, 2, 20.0), (4, 100, 2, 1.0)])
+def test_decode_attention_512_row_items(dq, bits, T, units, scale):
+    """8-tile work items (chunk_b = 512, mma.sync split kernel, g = 1): ragged last items, outlier keys."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(T + bits + int(scale))
+    k = rng.standard_normal((units, T, 128)).astype(np.float32)
+    k[:, :, [3, 77]] *= scale
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = rng.standard_normal((units, 1, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=bits, chunk_b=512)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    assert cache._layers[0].args.chunk_b == 512 and cache._layers[0].args.path == 0
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), bits, [T], 0)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
 @pytest.mark.parametrize("scale,bits", [(20.0, 4), (50.0, 4), (20.0, 2), (20.0, 8)])
 @pytest.mark.parametrize("ctas", [None, 0])  # persistent grid / one CTA per item
 @pytest.mark.parametrize("tc", [False, True])
