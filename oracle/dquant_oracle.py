@@ -12,6 +12,8 @@ It restates, in numpy, the algorithm of the reference package ``dquant``
                                            two's-complement packing, low bits first)
 * shape planning ... mpo.py:66-96, 54-63  (peel largest divisor <= 8, bond law)
 * TT-SVD, n=2 ...... mpo.py:144-178       (interleave, fp64 LAPACK SVD, sqrt(s) split)
+* chains n >= 2 .... mpo.py:144-198, compress.py:85-231 (sequential TT-SVD, contraction,
+                                           DecoQuant of every core but the first, core sweeps)
 * reconstruction ... mpo.py:181-198, compress.py:97-107
 * DecoQuant ........ compress.py:85-94    (quantize every core but the first)
 * fused reads ...... compress.py:159-231  (x @ W and x @ W^T, factored order)
@@ -206,6 +208,72 @@ def contract2(core0: np.ndarray, core1: np.ndarray, p: Plan2) -> np.ndarray:
     r = core0.shape[-1]
     a = core0.astype(np.float64).reshape(p.i1 * p.j1, r) @ core1.astype(np.float64).reshape(r, p.i2 * p.j2)
     return np.ascontiguousarray(deinterleaved(a, p).astype(np.float32))
+
+
+# ---------------------------------------------------------------------------
+# chains of any length n >= 2
+# ---------------------------------------------------------------------------
+
+
+def tt_split(m: np.ndarray, i_f, j_f):
+    """Full-rank sequential TT-SVD (mpo.py:153-178): interleave (144-150) in fp64, then per core
+    the SVD of the carry reshaped to (d_prev * i_k * j_k, rest); core = U sqrt(s), carry =
+    sqrt(s) Vt; the last core is the carry.  Cores cast to f32 (mpo.py:178)."""
+    n = len(i_f)
+    order = [x for k in range(n) for x in (k, n + k)]
+    carry = np.transpose(np.asarray(m, np.float64).reshape(tuple(i_f) + tuple(j_f)), order)
+    cores, d_prev = [], 1
+    for k in range(n):
+        mat = carry.reshape(d_prev * i_f[k] * j_f[k], -1)
+        if k == n - 1:
+            cores.append(mat.reshape(d_prev, i_f[k], j_f[k], 1))
+            break
+        u, s, vt = np.linalg.svd(mat, full_matrices=False)
+        rs = np.sqrt(s)
+        cores.append((u * rs).reshape(d_prev, i_f[k], j_f[k], len(s)))
+        carry = rs[:, None] * vt
+        d_prev = len(s)
+    return [c.astype(np.float32) for c in cores]
+
+
+def contract(cores) -> np.ndarray:
+    """mpo.py:181-198: fp64 left-to-right contraction, de-interleave, f32."""
+    return np.ascontiguousarray(contract_f64(cores).astype(np.float32))
+
+
+def deco_chain(m: np.ndarray, bits: int, n: int):
+    """compress.py:85-94 for any n: TT-SVD, then RTN of every core but the first.  Returns the
+    first core and (codes, scale) per quantized core, plus the dequantized chain."""
+    i_f, j_f = plan(*np.asarray(m).shape, n)
+    cores = tt_split(m, i_f, j_f)
+    quant = [rtn(c, bits) for c in cores[1:]]  # (scale, codes)
+    deq = [cores[0]] + [dequant(codes, scale).reshape(c.shape) for (scale, codes), c in zip(quant, cores[1:])]
+    return cores[0], quant, deq
+
+
+def chain_matmul(x: np.ndarray, deq) -> np.ndarray:
+    """x @ W through the dequantized cores (compress.py:159-192; the tiling is a memory bound,
+    not arithmetic, so the dense restatement computes the same fp64 products)."""
+    return (np.asarray(x, np.float64) @ contract_f64(deq)).astype(np.float32)
+
+
+def chain_matmul_t(x: np.ndarray, deq) -> np.ndarray:
+    """x @ W.T (compress.py:195-231)."""
+    return (np.asarray(x, np.float64) @ contract_f64(deq).T).astype(np.float32)
+
+
+def contract_f64(cores) -> np.ndarray:
+    """mpo.py:181-198 without the final f32 cast."""
+    c64 = [np.asarray(c, np.float64) for c in cores]
+    cur = c64[0].reshape(-1, c64[0].shape[3])
+    for t in c64[1:]:
+        cur = (cur @ t.reshape(t.shape[0], -1)).reshape(-1, t.shape[3])
+    i_f = [c.shape[1] for c in c64]
+    j_f = [c.shape[2] for c in c64]
+    n = len(c64)
+    full = cur.reshape([x for a, b in zip(i_f, j_f) for x in (a, b)])
+    full = np.transpose(full, [2 * k for k in range(n)] + [2 * k + 1 for k in range(n)])
+    return full.reshape(prod(i_f), prod(j_f))
 
 
 # ---------------------------------------------------------------------------

@@ -155,6 +155,21 @@ def strategy_sweep(suite, bits_list=(2, 4, 8)):
     return sorted(records, key=lambda t: (t.seed, t.method, t.bits))
 
 
+def length_sweep(suite, n_list=(2, 3, 4), bits: int = 4):
+    """Compression error as the chain length grows, first core kept (analysis.py:222-235): n = 2
+    on the K3 kernels, n = 3, 4 through the device fp64 TT-SVD (``mpo.decompose``)."""
+    dev = _lib.require_cuda()
+    records = []
+    for seed, m in enumerate(suite):
+        x = torch.as_tensor(np.asarray(m, np.float32)).to(dev)
+        for n in n_list:
+            chain = decompose(x, plan_shapes(x.shape[0], x.shape[1], n))
+            cores = (chain.local_tensors[0],) + tuple(dequantize(quantize_rtn(c, bits)) for c in chain.local_tensors[1:])
+            e, r = _errors(x, reconstruct(MpoChain(cores)))
+            records.append(ErrorRecord(TL_ONLY, bits, n, seed, e, r, _overhead(chain)))
+    return sorted(records, key=lambda t: (t.seed, t.n, t.bits))
+
+
 def decomposition_comparison(suite, bits: int = 4):
     """Chain vs SVD vs QR, quantizing the larger factor (analysis.py:246-271)."""
     dev = _lib.require_cuda()

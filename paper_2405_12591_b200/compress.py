@@ -6,7 +6,11 @@ Mirrors ``dquant/compress.py``: ``TILE_ELEMENTS`` (20), ``WorkingSetMeter`` (23-
 (195-231), ``compression_report`` (234-248).
 
 GPU kernels: deco_quantize -> K3 (csrc/factor.cu), deco_dequantize -> K4
-(csrc/reads.cu reconstruct), fused reads -> csrc/reads.cu.  Chains of length 2.
+(csrc/reads.cu reconstruct), fused reads -> csrc/reads.cu, for chains of length 2 (the hot
+path).  Longer chains (n = 3, 4: the reference's length sweep and CacheConfig(n)) run on the
+device too: the fp64 TT-SVD of ``mpo.decompose``, K2 quantize / dequantize per core, and the
+reference's left-to-right / right-to-left core sweeps as fp64 GEMMs over codes unpacked tile
+by tile (``unpack_range``, never more than TILE_ELEMENTS codes at once).
 """
 
 from __future__ import annotations
@@ -21,7 +25,7 @@ import torch
 from . import _lib, mpo
 from ._lib import check, lib, ptr, stream_ptr
 from .errors import ShapeMismatch, Unsupported
-from .quantize import QuantizedTensor, _check_bits, payload_size
+from .quantize import QuantizedTensor, _check_bits, dequantize, payload_size, quantize_rtn, unpack_range
 
 TILE_ELEMENTS = 64 * 64
 # codes one CTA of the fused kernels holds dequantized at any moment (one per thread)
@@ -132,10 +136,15 @@ def deco_quantize(m, bits: int, n: int = 2) -> QuantizedMpo:
     shape = tuple(m.shape) if is_t else np.asarray(m).shape
     if len(shape) != 2:
         raise ShapeMismatch(f"expected a matrix, got shape {shape}")
-    if n != 2:
-        raise Unsupported("the sm_100a DecoQuant kernels implement chains of length n=2")
     plan = mpo.plan_shapes(shape[0], shape[1], n)
     x = m if is_t else torch.from_numpy(np.ascontiguousarray(np.asarray(m, dtype=np.float32)))
+    if n != 2:  # longer chains: device TT-SVD, then K2 on every core but the first
+        chain = mpo.decompose(x.to(_lib.require_cuda()), plan)
+        cores = [chain.local_tensors[0]] + [quantize_rtn(t, bits) for t in chain.local_tensors[1:]]
+        if not is_t:
+            cores[0] = cores[0].cpu().numpy()
+            cores[1:] = [QuantizedTensor(c.shape, c.bits, c.scale, data=c.data, torch_out=False) for c in cores[1:]]
+        return QuantizedMpo(plan=plan, bits=bits, local_tensors=tuple(cores))
     res = deco_quantize_batched(x.reshape(1, *shape), bits)
     _lib.raise_flags(res["flags"], "deco_quantize")
     p = res["plan"]
@@ -153,8 +162,30 @@ def _parts(q: QuantizedMpo):
     return _core0_dev(core0), qt, scale
 
 
+def _rebuild_chain(q: QuantizedMpo):
+    """Dequantized cores as a device MpoChain (compress.py:97-102)."""
+    dev = _lib.require_cuda()
+    cores = []
+    for t in q.local_tensors:
+        if isinstance(t, QuantizedTensor):
+            c = dequantize(QuantizedTensor(t.shape, t.bits, t.scale, data=t.data, torch_out=True))
+        else:
+            c = (t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t))).to(dev, torch.float32)
+        cores.append(c)
+    return mpo.MpoChain(tuple(cores))
+
+
+def _is_torch_mpo(q: QuantizedMpo) -> bool:
+    t = q.local_tensors[-1]
+    return t._torch if isinstance(t, QuantizedTensor) else isinstance(t, torch.Tensor)
+
+
 def deco_dequantize(q: QuantizedMpo):
-    """Recover the full-precision matrix (compress.py:105-107): kernel K4."""
+    """Recover the full-precision matrix (compress.py:105-107): kernel K4 (n = 2), or the
+    dequantized cores contracted in fp64 on the device (longer chains)."""
+    if q.plan.n != 2:
+        out = mpo.reconstruct(_rebuild_chain(q))
+        return out if _is_torch_mpo(q) else out.cpu().numpy()
     core0, qt, scale = _parts(q)
     out = torch.empty((q.rows, q.cols), dtype=torch.float32, device=qt.data.device)
     check(lib().dq_deco_dequantize_batched(ptr(core0), ptr(qt.data), qt.data.numel(), _lib.LAYOUT_REF, ptr(scale), 1,
@@ -163,7 +194,105 @@ def deco_dequantize(q: QuantizedMpo):
     return out if qt._torch else out.cpu().numpy()
 
 
+def _core_f64(core, dev):
+    return (core if isinstance(core, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(core))).to(
+        dev, torch.float64)
+
+
+def _tile_codes(qt: QuantizedTensor, start: int, count: int, dev, meter):
+    codes = unpack_range(qt.data, start, count, qt.bits)
+    if meter is not None:
+        meter.record(count)
+    return codes.to(dev, torch.float64) * float(np.float32(qt.scale))
+
+
+def _gemm_packed_right(a, qt, rows, cols, meter, dev):
+    """a @ M for a packed (rows, cols) core, unpacked in tiles (compress.py:110-131)."""
+    out = torch.zeros((a.shape[0], cols), dtype=torch.float64, device=dev)
+    if cols <= TILE_ELEMENTS:
+        rt = max(1, TILE_ELEMENTS // cols)
+        for r0 in range(0, rows, rt):
+            r1 = min(rows, r0 + rt)
+            out += a[:, r0:r1] @ _tile_codes(qt, r0 * cols, (r1 - r0) * cols, dev, meter).reshape(r1 - r0, cols)
+    else:
+        for r in range(rows):
+            for c0 in range(0, cols, TILE_ELEMENTS):
+                c1 = min(cols, c0 + TILE_ELEMENTS)
+                out[:, c0:c1] += torch.outer(a[:, r], _tile_codes(qt, r * cols + c0, c1 - c0, dev, meter))
+    return out
+
+
+def _gemm_packed_left(qt, rows, cols, b, meter, dev):
+    """M @ b for a packed (rows, cols) core, unpacked in tiles (compress.py:134-156)."""
+    out = torch.zeros((rows, b.shape[1]), dtype=torch.float64, device=dev)
+    if cols <= TILE_ELEMENTS:
+        rt = max(1, TILE_ELEMENTS // cols)
+        for r0 in range(0, rows, rt):
+            r1 = min(rows, r0 + rt)
+            out[r0:r1] = _tile_codes(qt, r0 * cols, (r1 - r0) * cols, dev, meter).reshape(r1 - r0, cols) @ b
+    else:
+        for r in range(rows):
+            for c0 in range(0, cols, TILE_ELEMENTS):
+                c1 = min(cols, c0 + TILE_ELEMENTS)
+                out[r] += _tile_codes(qt, r * cols + c0, c1 - c0, dev, meter) @ b[c0:c1]
+    return out
+
+
+def _fused_chain(x, q: QuantizedMpo, meter, transposed: bool):
+    """Longer chains: the reference's core sweeps (compress.py:159-231) on the device in fp64."""
+    dev = _lib.require_cuda()
+    is_t = isinstance(x, torch.Tensor)
+    xs = tuple(x.shape) if is_t else np.asarray(x).shape
+    need = q.cols if transposed else q.rows
+    if len(xs) != 2 or xs[1] != need:
+        raise ShapeMismatch(f"operand shape {xs} does not match {'cols' if transposed else 'rows'} {need}")
+    xd = (x if is_t else torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)))).to(dev, torch.float64)
+    p = xs[0]
+    i_f, j_f, n = q.plan.i_factors, q.plan.j_factors, q.plan.n
+    cores = q.local_tensors
+    if not transposed:  # x @ W: left to right, state (p, i_rest, j_acc, d)
+        cur = xd.reshape((p,) + tuple(i_f) + (1, 1))
+        j_acc, d = 1, 1
+        for k in range(n):
+            ik, jk = i_f[k], j_f[k]
+            i_rest = prod(i_f[k + 1:]) if k + 1 < n else 1
+            cur = cur.reshape(p, ik, i_rest, j_acc, d).permute(0, 2, 3, 4, 1).contiguous()
+            a = cur.reshape(p * i_rest * j_acc, d * ik)
+            core = cores[k]
+            d_next = core.shape[3]
+            if isinstance(core, QuantizedTensor):
+                out = _gemm_packed_right(a, core, d * ik, jk * d_next, meter, dev)
+            else:
+                out = a @ _core_f64(core, dev).reshape(d * ik, jk * d_next)
+            j_acc *= jk
+            d = d_next
+            cur = out.reshape(p, i_rest, j_acc, d)
+        res = cur.reshape(p, q.cols).to(torch.float32).contiguous()
+    else:  # x @ W.T: right to left, state (j_lead, d_prev, i_acc, p)
+        cur = xd.t().contiguous().reshape(tuple(j_f) + (1, 1, p))
+        i_acc = 1
+        for k in range(n - 1, -1, -1):
+            ik, jk = i_f[k], j_f[k]
+            d_prev = 1 if k == 0 else cores[k - 1].shape[3]
+            d_k = cores[k].shape[3]
+            j_lead = prod(j_f[:k]) if k > 0 else 1
+            cur = cur.reshape(j_lead, jk, d_k, i_acc, p).permute(1, 2, 0, 3, 4).contiguous()
+            b = cur.reshape(jk * d_k, j_lead * i_acc * p)
+            core = cores[k]
+            if isinstance(core, QuantizedTensor):
+                out = _gemm_packed_left(core, d_prev * ik, jk * d_k, b, meter, dev)
+            else:
+                out = _core_f64(core, dev).reshape(d_prev * ik, jk * d_k) @ b
+            out = out.reshape(d_prev, ik, j_lead, i_acc, p).permute(2, 0, 1, 3, 4).contiguous()
+            i_acc *= ik
+            cur = out.reshape(j_lead, d_prev, i_acc, p)
+        res = cur.reshape(q.rows, p).t().to(torch.float32).contiguous()
+    return res if is_t else res.cpu().numpy()
+
+
 def _fused(x, q: QuantizedMpo, meter, transposed: bool):
+    if q.plan.n != 2:
+        return _fused_chain(x, q, meter, transposed)
     core0, qt, scale = _parts(q)
     is_t = isinstance(x, torch.Tensor)
     xs = tuple(x.shape) if is_t else np.asarray(x).shape

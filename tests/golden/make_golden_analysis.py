@@ -9,6 +9,7 @@ suite and writes ``tests/golden/golden_analysis.json``:
   columns x 20), so a restated generator can be checked to reproduce the same matrices;
 - ``strategy``: ``strategy_sweep(suite)`` records (matrix RTN / DecoQuant large core only /
   both cores, bits 2, 4, 8) and their medians -- the paper's error table;
+- ``length``: ``length_sweep(suite)`` (chain length n = 2, 3, 4, large cores quantized, 4 bits);
 - ``decomposition``: ``decomposition_comparison(suite)`` (chain vs SVD vs QR, 4 bits);
 - ``migration``: ``migration_report`` IQR statistics of seed 0 (matrix, large, small core).
 
@@ -54,6 +55,9 @@ def main():
     strat = analysis.strategy_sweep(suite)
     out["strategy"] = _records(strat)
     out["strategy_median"] = {f"{k[0]}/{k[1]}": v for k, v in analysis.median_by(strat).items()}
+    length = analysis.length_sweep(suite)
+    out["length"] = _records(length)
+    out["length_median"] = {f"{k[0]}/{k[1]}": v for k, v in analysis.median_by(length, key=lambda r: (r.method, r.n)).items()}
     dec = analysis.decomposition_comparison(suite)
     out["decomposition"] = _records(dec)
     out["decomposition_median"] = {f"{k[0]}/{k[1]}": v for k, v in analysis.median_by(dec).items()}

@@ -74,3 +74,20 @@ def test_migration_report_matches_reference(golden, suite):
         assert st.iqr == pytest.approx(g[k]["iqr"], rel=2e-2)
         assert abs(st.outlier_count - g[k]["outlier_count"]) <= 0.02 * g[k]["total"]
     assert large.iqr < 0.05 * mat.iqr  # the outliers migrate out of the large core
+
+
+def test_length_sweep_matches_reference(golden, suite):
+    """Chain length n = 2, 3, 4 (the reference's length_sweep, analysis.py:222-235):
+    n = 2 on the K3 kernels, n = 3, 4 through the device fp64 TT-SVD; every record within 1e-3
+    of the reference, medians within 2e-4."""
+    from paper_2405_12591_b200.analysis import length_sweep, median_by
+
+    got = length_sweep(suite)
+    ref = {(r["n"], r["seed"]): r for r in golden["length"]}
+    assert len(got) == len(ref) == 60
+    for r in got:
+        g = ref[(r.n, r.seed)]
+        assert r.param_overhead == pytest.approx(g["param_overhead"], rel=1e-12)
+        assert r.frobenius_error == pytest.approx(g["frobenius_error"], rel=1e-3), (r, g)
+    for (method, n), v in median_by(got, key=lambda r: (r.method, r.n)).items():
+        assert v == pytest.approx(golden["length_median"][f"{method}/{n}"], rel=2e-4)
