@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--kernel-g", type=int, default=None, help="query heads per split-kernel head group (1 or 2)")
     ap.add_argument("--tc", type=int, default=None, choices=[0, 1],
                     help="split kernel: 1 = tcgen05, 0 = mma.sync, default: tcgen05 where eligible")
+    ap.add_argument("--asym", type=int, default=0, choices=[0, 1],
+                    help="1: the opt-in per-channel asymmetric quantizer (not the reference scheme)")
     ap.add_argument("--ctas", type=int, default=None,
                     help="split-kernel grid: default persistent (resident CTAs), 0 = one CTA per 256-row slice")
     ap.add_argument("--layers", type=int, default=None, help="override layer count (debug only)")
@@ -286,7 +288,7 @@ def run_ours(args, cfg):
 
     cache = DecodeKvCache(layers=layers, units=units, g=g, bits=bits, chunk_len=chunk_len, chunk_b=args.chunk_b,
                           ctas=args.ctas, kernel_g=args.kernel_g,
-                          tc=None if args.tc is None else bool(args.tc))
+                          tc=None if args.tc is None else bool(args.tc), asym=bool(args.asym))
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
 
@@ -412,7 +414,8 @@ def run_ours(args, cfg):
         "dtype": "f16",
         "data": "synthetic: per-layer K/V ~ N(0,1) fp16 compressed by the K3 write path; q/k/v rows ~ N(0,1) fp16",
         "config": {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
-                   "kv_bits": bits, "layers": layers, "kv_heads": kv_heads, "g": g,
+                   "kv_bits": bits, "quantizer": "per-channel asymmetric (opt-in)" if args.asym else "per-tensor symmetric (reference)",
+                   "layers": layers, "kv_heads": kv_heads, "g": g,
                    "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": cache._layers[0].args.chunk_b,
                    "split_ctas": cache.split_ctas, "kernel_g": cache._layers[0].kernel_g,
                    "head_groups": g // cache._layers[0].kernel_g,

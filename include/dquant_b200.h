@@ -22,6 +22,8 @@
  *   dq_dequantize .................. quantize.dequantize        quantize.py:154-157
  *   dq_decompose_batched ........... mpo.decompose (n=2)        mpo.py:153-178
  *   dq_deco_quantize_batched ....... compress.deco_quantize     compress.py:85-94
+ *   dq_deco_quantize_asym_batched .. (opt-in per-channel asymmetric mode of north_star; no
+ *                                    reference counterpart, parity against the oracle only)
  *   dq_deco_dequantize_batched ..... compress.deco_dequantize + mpo.reconstruct
  *                                                              compress.py:105-107, mpo.py:181-198
  *   dq_fused_matmul_t .............. compress.fused_matmul_t    compress.py:195-231
@@ -122,6 +124,17 @@ int dq_decompose_plan_batched(const void* blocks, int32_t in_dtype, int64_t nblk
 int dq_deco_quantize_batched(const void* blocks, int32_t in_dtype, int64_t nblk, int64_t rows, int64_t cols,
                              int32_t bits, int32_t layout, float* core0, uint8_t* payload, int64_t payload_stride,
                              float* scale, int32_t* flags, void* workspace, size_t workspace_bytes, void* stream);
+/* Opt-in per-channel ASYMMETRIC quantisation of core1 (north_star; not in the reference, whose
+ * quantizer is per-tensor symmetric, quantize.py:123-151 -- parity unpinned, checked against the
+ * oracle's restatement only).  Channel = (r, e) over b, bits in {2, 4}, qmu = 2^bits - 1:
+ *   s = f32((max - min) / qmu)   (|max| or 1 for a constant channel)
+ *   z = clip(floor(-min / s + 0.5), 0, qmu),  u = clip(floor(v / s + 0.5) + z, 0, qmu)   (fp64)
+ *   value = s * (u - z);  the raw codes u are packed in `layout` (KTILE / VTILE / REF).
+ * channels: nblk x [2][r][j2] f32 (the scales s, then the zero points z as floats). */
+int dq_deco_quantize_asym_batched(const void* blocks, int32_t in_dtype, int64_t nblk, int64_t rows, int64_t cols,
+                                  int32_t bits, int32_t layout, float* core0, uint8_t* payload,
+                                  int64_t payload_stride, float* channels, int32_t* flags, void* workspace,
+                                  size_t workspace_bytes, void* stream);
 /* copy of core0 (fp16 or fp32) in the attention-friendly layout out[a][r][c] (i1 x r x j1),
  * normalised by a power of two per block so that max|out| is in [0.5, 1); norm[blk] receives
  * that factor (core0 = out * norm).  norm may be null (then no normalisation). */
@@ -163,6 +176,10 @@ typedef struct dq_segment {
   int32_t unit;       /* owning unit */
   int32_t token0;     /* first token index of the segment inside its unit */
   int32_t pad_;
+  const float* k_ch;  /* asymmetric mode: [2][r][16] per-channel scales and zero points (see
+                         dq_deco_quantize_asym_batched); k_scale / v_scale then carry only the G0
+                         normalisation.  Null: the reference's symmetric per-tensor codes */
+  const float* v_ch;
 } dq_segment;
 
 typedef struct dq_attn_args {
@@ -200,7 +217,10 @@ typedef struct dq_attn_args {
                              query heads run as head_groups "virtual units" u * head_groups + k (each g
                              heads, same codes; segs/q/out/partials indexed by virtual unit, the tail and
                              the combine grid by kv head u).  0 or 1: none */
-  int32_t path;           /* split kernel: 0 = mma.sync (all plans), 1 = tcgen05 (int4, g = 1, r = 64, i1 = 8) */
+  int32_t path;           /* split kernel: 0 = mma.sync (all plans), 1 = tcgen05 (int4, g = 1, r = 64, i1 = 8),
+                             2 = tcgen05 GQA (int4, g = 8, r = 64, i1 = 8) */
+  int32_t asym;           /* 1: every segment is in the asymmetric per-channel mode (path 0, 2- / 4-bit) */
+  int32_t pad2_;
 } dq_attn_args;
 
 /* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */

@@ -289,7 +289,9 @@ class Encoded:
     bits: int
     core0: np.ndarray  # (1, i1, j1, r) float32
     scale: np.float32
-    codes: np.ndarray  # (r, i2, j2) int8, reference payload order
+    codes: np.ndarray  # (r, i2, j2) int8, reference payload order (unsigned codes in the asymmetric mode)
+    ch_scale: np.ndarray | None = None  # asymmetric mode: (r, j2) f32 channel scales
+    ch_zero: np.ndarray | None = None   # asymmetric mode: (r, j2) zero points
 
     @property
     def r(self) -> int:
@@ -299,8 +301,16 @@ class Encoded:
     def payload(self) -> bytes:
         return pack_codes(self.codes.reshape(-1), self.bits).tobytes()
 
+    def g1(self) -> np.ndarray:
+        """Dequantized core1 (r, i2, j2) in fp64."""
+        if self.ch_scale is None:
+            return self.codes.astype(np.float64) * np.float64(self.scale)
+        return (self.codes.astype(np.float64) - self.ch_zero[:, None, :]) * self.ch_scale.astype(np.float64)[:, None, :]
+
     def core1_deq(self) -> np.ndarray:
-        return dequant(self.codes, self.scale).reshape(self.r, self.plan.i2, self.plan.j2, 1)
+        if self.ch_scale is None:
+            return dequant(self.codes, self.scale).reshape(self.r, self.plan.i2, self.plan.j2, 1)
+        return self.g1().astype(np.float32).reshape(self.r, self.plan.i2, self.plan.j2, 1)
 
 
 def encode(m: np.ndarray, bits: int) -> Encoded:
@@ -312,6 +322,34 @@ def encode(m: np.ndarray, bits: int) -> Encoded:
     core0, core1, _ = tt_split2(m, p)
     scale, codes = rtn(core1, bits)
     return Encoded(p, bits, core0, scale, codes.reshape(core1.shape[0], p.i2, p.j2))
+
+
+def rtn_asym(core1, bits: int):
+    """OPT-IN per-channel asymmetric quantizer (north_star's "per-channel asymmetric int4/int2";
+    NOT in the reference, whose quantizer is per-tensor symmetric -- this restates the build's own
+    K3 mode, include/dquant_b200.h dq_deco_quantize_asym_batched, so its parity is unpinned).
+    Channel (r, e) of core1 (r, i2, j2) over b, qmu = 2^bits - 1, fp64 arithmetic:
+    s = f32((max - min) / qmu) (|max| or 1 for a constant channel), z = clip(floor(-min/s + .5)),
+    u = clip(floor(v/s + .5) + z, 0, qmu).  Returns (s (r, j2) f32, z (r, j2) int32, u uint8)."""
+    c = np.asarray(core1, np.float32)
+    qmu = (1 << bits) - 1
+    mn, mx = c.min(axis=1), c.max(axis=1)
+    rng = mx.astype(np.float64) - mn.astype(np.float64)
+    s = np.where(rng > 0, rng / qmu, np.where(mx != 0, np.abs(mx).astype(np.float64), 1.0)).astype(np.float32)
+    s64 = s.astype(np.float64)
+    z = np.clip(np.floor(-mn.astype(np.float64) / s64 + 0.5), 0, qmu)
+    u = np.clip(np.floor(c.astype(np.float64) / s64[:, None, :] + 0.5) + z[:, None, :], 0, qmu)
+    return s, z.astype(np.int32), u.astype(np.uint8)
+
+
+def encode_asym(m: np.ndarray, bits: int) -> Encoded:
+    """``encode`` with the opt-in asymmetric per-channel quantizer (``rtn_asym``) on core1."""
+    m = np.asarray(m, dtype=np.float32)
+    p = Plan2.of(*m.shape)
+    core0, core1, _ = tt_split2(m, p)
+    c1 = core1.reshape(core1.shape[0], p.i2, p.j2)
+    s, z, u = rtn_asym(c1, bits)
+    return Encoded(p, bits, core0, np.float32(1.0), u, s, z)
 
 
 def decode(e: Encoded) -> np.ndarray:
@@ -326,7 +364,7 @@ def matmul_t(x: np.ndarray, e: Encoded) -> np.ndarray:
     """
     pl = e.plan
     x64 = np.asarray(x, dtype=np.float64).reshape(-1, pl.j1, pl.j2)
-    g1 = e.codes.astype(np.float64) * np.float64(e.scale)  # (r, i2, j2)
+    g1 = e.g1()  # (r, i2, j2)
     h = np.einsum("rbe,pce->prbc", g1, x64)
     g0 = e.core0.astype(np.float64).reshape(pl.i1, pl.j1, e.r)
     out = np.einsum("acr,prbc->pab", g0, h)
@@ -342,7 +380,7 @@ def matmul(x: np.ndarray, e: Encoded) -> np.ndarray:
     x64 = np.asarray(x, dtype=np.float64).reshape(-1, pl.i1, pl.i2)
     g0 = e.core0.astype(np.float64).reshape(pl.i1, pl.j1, e.r)
     y = np.einsum("pab,acr->pbcr", x64, g0)
-    g1 = e.codes.astype(np.float64) * np.float64(e.scale)
+    g1 = e.g1()
     out = np.einsum("pbcr,rbe->pce", y, g1)
     return np.ascontiguousarray(out.reshape(x64.shape[0], pl.j1 * pl.j2).astype(np.float32))
 
@@ -373,10 +411,13 @@ class LayerOracle:
     rows: list = field(default_factory=list)
     tail_k: list = field(default_factory=list)
     tail_v: list = field(default_factory=list)
+    asym: bool = False  # the build's opt-in per-channel asymmetric mode (encode_asym)
 
     def _seal(self, block):
         block = np.ascontiguousarray(block, dtype=np.float32)
-        return block if self.bits is None else encode(block, self.bits)
+        if self.bits is None:
+            return block
+        return encode_asym(block, self.bits) if self.asym else encode(block, self.bits)
 
     def prefill(self, k, v):
         """kvcache.py:99-114: the whole prompt becomes ONE segment."""

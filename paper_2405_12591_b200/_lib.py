@@ -59,6 +59,8 @@ class Segment(ctypes.Structure):
         ("unit", c_int32),
         ("token0", c_int32),
         ("pad_", c_int32),
+        ("k_ch", c_void_p),
+        ("v_ch", c_void_p),
     ]
 
 
@@ -97,6 +99,8 @@ class AttnArgs(ctypes.Structure):
         ("app_v", c_void_p),
         ("head_groups", c_int32),
         ("path", c_int32),
+        ("asym", c_int32),
+        ("pad2_", c_int32),
     ]
 
 
@@ -120,6 +124,9 @@ SIGNATURES = {
                                             c_void_p, c_size_t, c_void_p]),
     "dq_deco_quantize_batched": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p,
                                            c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "dq_deco_quantize_asym_batched": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int32, c_int32,
+                                                c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_size_t,
+                                                c_void_p]),
     "dq_core0_relayout": (c_int32, [c_void_p, c_int64, POINTER(Plan2), c_void_p, c_int32, c_void_p, c_void_p]),
     "dq_deco_dequantize_batched": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int64,
                                              c_int64, c_int32, c_void_p, c_int32, c_void_p]),

@@ -28,7 +28,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib, ptr, stream_ptr
-from .compress import QuantizedMpo, deco_quantize_batched
+from .compress import QuantizedMpo, deco_quantize_asym_batched, deco_quantize_batched
 from .errors import AlreadyPrefilled, DimMismatch, LayerOutOfRange, ShapeMismatch, Unsupported
 from .mpo import plan_shapes
 from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_size
@@ -60,16 +60,23 @@ class SegmentGroup:
     k_norm: torch.Tensor     # (units,) f32 power-of-two G0 normalisation
     v_norm: torch.Tensor
     token0: int
+    k_ch: torch.Tensor | None = None  # asymmetric mode: (units, 2, r, 16) f32 channel scales, zero points
+    v_ch: torch.Tensor | None = None
 
     def reference_bytes(self, bits: int) -> int:
-        """compression_report().bytes_compressed of one unit's K (or V) block (compress.py:234-248)."""
+        """compression_report().bytes_compressed of one unit's K (or V) block (compress.py:234-248);
+        the asymmetric mode stores a 16-bit scale and zero point per (r, e) channel instead of
+        one scale."""
         p = self.plan
-        return payload_size(p.r * p.i2 * p.j2, bits) + 2 + 2 * (p.i1 * p.j1 * p.r)
+        scales = 2 * 2 * p.r * p.j2 if self.k_ch is not None else 2
+        return payload_size(p.r * p.i2 * p.j2, bits) + scales + 2 * (p.i1 * p.j1 * p.r)
 
     def stream_bytes(self) -> int:
-        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k and G0v, scales."""
+        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k and G0v, scales
+        (the channel tables in the asymmetric mode)."""
+        ch = 2 * self.k_ch[0].numel() * 4 if self.k_ch is not None else 0
         return (self.k_payload.shape[1] + self.v_payload.shape[1] + self.k_g0h.element_size() * self.k_g0h.shape[1]
-                + self.v_g0h.element_size() * self.v_g0h.shape[1] + 8)
+                + self.v_g0h.element_size() * self.v_g0h.shape[1] + 8 + ch)
 
 
 class _Layer:
@@ -82,26 +89,34 @@ class _Layer:
         self.keep = []     # tensors referenced by args
 
 
-def compress_blocks(blocks: torch.Tensor, bits: int, layout: int, g0_dtype=torch.float16):
+def compress_blocks(blocks: torch.Tensor, bits: int, layout: int, g0_dtype=torch.float16, asym: bool = False):
     """K3 over (nblk, T, 128) fp16/fp32 CUDA blocks in slices of MAX_BLOCKS_PER_CALL.
 
-    Returns (payload (nblk, bytes), core0 f32, g0 [a][r][c] normalised in g0_dtype, norm f32, scale f32, plan).
+    Returns (payload (nblk, bytes), core0 f32, g0 [a][r][c] normalised in g0_dtype, norm f32, scale f32, plan);
+    with ``asym`` the scale is 1 and the per-channel tables come back as a 7th item (nblk, 2, r, 16).
     """
     nblk = blocks.shape[0]
     outs = []
     for s in range(0, nblk, MAX_BLOCKS_PER_CALL):
-        res = deco_quantize_batched(blocks[s:s + MAX_BLOCKS_PER_CALL], bits, layout)
+        fn = deco_quantize_asym_batched if asym else deco_quantize_batched
+        res = fn(blocks[s:s + MAX_BLOCKS_PER_CALL], bits, layout)
         _lib.raise_flags(res["flags"], "deco_quantize")
         outs.append(res)
     p = outs[0]["plan"]
     payload = torch.cat([o["payload"] for o in outs]) if len(outs) > 1 else outs[0]["payload"]
     core0 = torch.cat([o["core0"] for o in outs]) if len(outs) > 1 else outs[0]["core0"]
-    scale = torch.cat([o["scale"] for o in outs]) if len(outs) > 1 else outs[0]["scale"]
+    if asym:
+        chans = torch.cat([o["channels"] for o in outs]) if len(outs) > 1 else outs[0]["channels"]
+        scale = torch.ones(nblk, dtype=torch.float32, device=blocks.device)
+    else:
+        scale = torch.cat([o["scale"] for o in outs]) if len(outs) > 1 else outs[0]["scale"]
     g0 = torch.empty((nblk, p.i1 * p.r * p.j1), dtype=g0_dtype, device=blocks.device)
     norm = torch.empty(nblk, dtype=torch.float32, device=blocks.device)
     code = _lib.DQ_F16 if g0_dtype == torch.float16 else _lib.DQ_F32
     check(lib().dq_core0_relayout(ptr(core0), nblk, ctypes.byref(p), ptr(g0), code, ptr(norm), stream_ptr()),
           "core0_relayout")
+    if asym:
+        return payload, core0, g0, norm, scale, p, chans
     return payload, core0, g0, norm, scale, p
 
 
@@ -140,7 +155,7 @@ class DecodeKvCache:
 
     def __init__(self, layers: int, units: int, g: int = 1, bits: int = 4, chunk_len: int = 1024,
                  dim: int = HEAD_DIM, chunk_b: int | None = None, sm_scale: float | None = None,
-                 ctas: int | None = None, kernel_g: int | None = None, tc: bool | None = None):
+                 ctas: int | None = None, kernel_g: int | None = None, tc: bool | None = None, asym: bool = False):
         if dim != HEAD_DIM:
             raise Unsupported("the fused decode kernel is specialised for head_dim 128 (j = (8, 16))")
         if not 1 <= g <= MAX_G:
@@ -158,8 +173,14 @@ class DecodeKvCache:
         # hits: the work list puts a tile range's head groups next to each other).
         # kernel_g = 8 is the tcgen05 GQA kernel (path 2: 4-bit codes, full plans i1 = 8,
         # r = 64); a layer whose segments do not qualify falls back to mma.sync heads of 2.
+        # asym: the opt-in per-channel asymmetric quantizer (north_star; the reference's own scheme,
+        # per-tensor symmetric, is the default and the parity mode).  2- / 4-bit, mma.sync kernel.
+        self.asym = bool(asym)
+        if self.asym and (bits not in (2, 4) or tc or (kernel_g or 1) > 2):
+            raise Unsupported("the asymmetric mode covers 2- / 4-bit codes on the mma.sync split kernel (g <= 2)")
         if kernel_g is None:
-            kernel_g = GQA_G if (g % GQA_G == 0 and bits == 4 and tc is not False) else (2 if g % 2 == 0 else 1)
+            kernel_g = (GQA_G if (g % GQA_G == 0 and bits == 4 and tc is not False and not self.asym)
+                        else (2 if g % 2 == 0 else 1))
         self.kernel_g = kernel_g
         if self.kernel_g not in KERNEL_G or g % self.kernel_g:
             raise Unsupported(f"kernel_g must be in {KERNEL_G} and divide g")
@@ -199,10 +220,14 @@ class DecodeKvCache:
         T = keys.shape[1]
         # fp32 G0 on the score side: scores of outlier-heavy keys are large, and the fp16
         # rounding of G0k (2^-11) would show up as absolute logit error
-        kp, kc0, kg, kn, ks, p = compress_blocks(keys, self.bits, _lib.LAYOUT_KTILE, torch.float32)
-        vp, vc0, vg, vn, vs, _ = compress_blocks(values, self.bits, _lib.LAYOUT_VTILE, torch.float32)
+        kres = compress_blocks(keys, self.bits, _lib.LAYOUT_KTILE, torch.float32, self.asym)
+        vres = compress_blocks(values, self.bits, _lib.LAYOUT_VTILE, torch.float32, self.asym)
+        kp, kc0, kg, kn, ks, p = kres[:6]
+        vp, vc0, vg, vn, vs, _ = vres[:6]
+        kch, vch = (kres[6], vres[6]) if self.asym else (None, None)
         i2p = -(-p.i2 // _lib.I2_PAD) * _lib.I2_PAD
-        lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, kn, vn, lay.tokens_sealed))
+        lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, kn, vn, lay.tokens_sealed,
+                                       kch, vch))
         lay.tokens_sealed += T
         lay.args = None
 
@@ -271,6 +296,9 @@ class DecodeKvCache:
                     s.v_scale = float(vs[u])
                     s.T, s.i1, s.i2, s.r, s.i2p = grp.T, p.i1, p.i2, p.r, grp.i2p
                     s.unit, s.token0 = u * hg + hk, grp.token0
+                    if grp.k_ch is not None:
+                        s.k_ch = grp.k_ch[u].data_ptr()
+                        s.v_ch = grp.v_ch[u].data_ptr()
                     segs.append(s)
         nseg = len(segs)
         seg_arr = (_lib.Segment * max(nseg, 1))(*segs)
@@ -322,6 +350,7 @@ class DecodeKvCache:
                                   "r = 64 plans")
             a.path = 1 if (eligible and self.tc) else 0
         a.bits = self.bits
+        a.asym = 1 if self.asym else 0
         a.tail_k = self.tail_k[layer].data_ptr()
         a.tail_v = self.tail_v[layer].data_ptr()
         a.tail_len = self.tail_len[layer].data_ptr()
@@ -424,6 +453,8 @@ class DecodeKvCache:
     def export_segment(self, layer: int, index: int, unit: int, which: str = "k") -> QuantizedMpo:
         """Segment ``index`` of ``unit`` as a reference-form QuantizedMpo (wire-order payload)."""
         grp = self._layer(layer).groups[index]
+        if grp.k_ch is not None:
+            raise Unsupported("asymmetric segments have no reference (symmetric per-tensor) form")
         p = grp.plan
         src = grp.k_payload if which == "k" else grp.v_payload
         layout = _lib.LAYOUT_KTILE if which == "k" else _lib.LAYOUT_VTILE

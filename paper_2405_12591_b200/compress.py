@@ -129,6 +129,40 @@ def deco_quantize_batched(blocks: torch.Tensor, bits: int, layout: int = _lib.LA
             "bytes": nbytes}
 
 
+def deco_quantize_asym_batched(blocks: torch.Tensor, bits: int, layout: int = _lib.LAYOUT_REF,
+                               stride: int | None = None):
+    """K3 with the opt-in per-channel ASYMMETRIC quantizer (north_star; not in the reference,
+    parity against the oracle's ``rtn_asym`` only): channel (r, e) of core1 over b, 2 or 4 bits.
+
+    Returns dict(core0, payload (raw codes u in `layout`), channels (nblk, 2, r, 16) f32 = scales
+    then zero points, plan, flags); value = scale * (u - zero).
+    """
+    if bits not in (2, 4):
+        from .quantize import UnsupportedBits
+        raise UnsupportedBits("the asymmetric mode covers 2- and 4-bit codes")
+    dev = _lib.require_cuda()
+    if blocks.ndim != 3:
+        raise ShapeMismatch("expected (nblk, rows, cols)")
+    dtype = _lib.DQ_F16 if blocks.dtype == torch.float16 else _lib.DQ_F32
+    x = blocks.to(device=dev, dtype=torch.float16 if dtype == _lib.DQ_F16 else torch.float32).contiguous()
+    nblk, rows, cols = x.shape
+    p = _lib.plan2(rows, cols)
+    nbytes = _lib.layout_bytes(p, bits, layout)
+    stride = stride or nbytes
+    core0 = torch.empty((nblk, 1, p.i1, p.j1, p.r), dtype=torch.float32, device=dev)
+    payload = torch.empty((nblk, stride), dtype=torch.uint8, device=dev)
+    channels = torch.empty((nblk, 2, p.r, p.j2), dtype=torch.float32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    size = ctypes.c_size_t()
+    check(lib().dq_decompose_workspace_size(nblk, rows, cols, ctypes.byref(size)), "workspace")
+    ws = torch.empty(max(size.value, 256), dtype=torch.uint8, device=dev)
+    check(lib().dq_deco_quantize_asym_batched(ptr(x), dtype, nblk, rows, cols, bits, layout, ptr(core0), ptr(payload),
+                                              stride, ptr(channels), ptr(flags), ptr(ws), ws.numel(), stream_ptr()),
+          "deco_quantize_asym")
+    return {"core0": core0, "payload": payload, "channels": channels, "plan": p, "flags": flags, "layout": layout,
+            "bytes": nbytes}
+
+
 def deco_quantize(m, bits: int, n: int = 2) -> QuantizedMpo:
     """Factorize and quantize every core except the first (compress.py:85-94)."""
     _check_bits(bits)
@@ -339,5 +373,6 @@ def compression_report(q: QuantizedMpo) -> CompressionReport:
 
 __all__ = [
     "TILE_ELEMENTS", "WorkingSetMeter", "QuantizedMpo", "CompressionReport", "deco_quantize", "deco_dequantize",
-    "fused_matmul", "fused_matmul_t", "compression_report", "deco_quantize_batched", "prod",
+    "fused_matmul", "fused_matmul_t", "compression_report", "deco_quantize_batched", "deco_quantize_asym_batched",
+    "prod",
 ]

@@ -83,13 +83,14 @@ __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __ha
 }
 
 
-template <int BITS, int G, int NT = kTiles>
+template <int BITS, int G, int NT = kTiles, bool ASYM = false>
 int set_attrs() {
   static bool attr = false;
   if (!attr) {
-    const int smem = (int)sizeof(AttnSmem<G, NT>);
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    const int smem = (int)sizeof(AttnSmem<G, NT, ASYM>);
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT, ASYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT, ASYM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      100));
     attr = true;
   }
@@ -160,7 +161,11 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr_pdl;
     cfg.numAttrs = 1;
-    DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_prepare_kernel<BITS, G>, a));
+    if (a.asym) {
+      if constexpr (BITS <= 4 && G <= 2) DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_prepare_kernel<BITS, G, true>, a));
+    } else {
+      DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_prepare_kernel<BITS, G>, a));
+    }
   }
   if (a.path == 1 && a.nwork > 0 && (phases & 1)) {
     if constexpr (BITS == 4 && G == 1) {
@@ -201,14 +206,29 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
       attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr_pdl;
       cfg.numAttrs = 1;
+      if (a.asym && BITS == 8) return fail(DQ_ERR_UNSUPPORTED, "the asymmetric mode covers 2- and 4-bit codes");
       if (a.chunk_b > kCB) {  // 8-tile work items (g = 1, 2- and 4-bit codes)
         if constexpr (G == 1 && BITS <= 4) {
-          const int rc = set_attrs<BITS, G, 2 * kTiles>();
-          if (rc != DQ_OK) return rc;
-          cfg.dynamicSmemBytes = sizeof(AttnSmem<G, 2 * kTiles>);
-          DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, 2 * kTiles>, a));
+          if (a.asym) {
+            const int rc = set_attrs<BITS, G, 2 * kTiles, true>();
+            if (rc != DQ_OK) return rc;
+            cfg.dynamicSmemBytes = sizeof(AttnSmem<G, 2 * kTiles, true>);
+            DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, 2 * kTiles, true>, a));
+          } else {
+            const int rc = set_attrs<BITS, G, 2 * kTiles>();
+            if (rc != DQ_OK) return rc;
+            cfg.dynamicSmemBytes = sizeof(AttnSmem<G, 2 * kTiles>);
+            DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, 2 * kTiles>, a));
+          }
         } else {
           return fail(DQ_ERR_UNSUPPORTED, "work items of more than %d rows need g = 1 and 2- or 4-bit codes", kCB);
+        }
+      } else if (a.asym) {
+        if constexpr (BITS <= 4) {
+          const int rc = set_attrs<BITS, G, kTiles, true>();
+          if (rc != DQ_OK) return rc;
+          cfg.dynamicSmemBytes = sizeof(AttnSmem<G, kTiles, true>);
+          DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, kTiles, true>, a));
         }
       } else {
         cfg.dynamicSmemBytes = sizeof(AttnSmem<G>);
@@ -249,6 +269,7 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
 
 template <int BITS>
 int dispatch_g(const dq_attn_args& a, cudaStream_t s) {
+  if (a.asym && a.path != 0) return fail(DQ_ERR_UNSUPPORTED, "the asymmetric mode runs on the mma.sync split kernel");
   if (a.chunk_b <= 0 || a.chunk_b > 2 * kCB || a.chunk_b % kI2Pad || (a.chunk_b > kCB && a.path != 0))
     return fail(DQ_ERR_UNSUPPORTED, "chunk_b must be a multiple of %d in %d..%d (%d off path 0; got %d)", kI2Pad, kI2Pad,
                 2 * kCB, kCB, a.chunk_b);

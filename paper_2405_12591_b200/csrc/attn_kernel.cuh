@@ -64,9 +64,10 @@ struct SubItem {
 };
 
 // NT: 64-row tiles per work item (4, or 8 for g = 1: twice the bytes per fixed per-item cost)
-template <int G, int NT = kTiles>
+template <int G, int NT = kTiles, bool ASYM = false>
 struct AttnSmem {
-  static constexpr int kStages = kStagesOf<G>;
+  // 8-tile items with the asymmetric channel table: one stage less keeps 2 CTAs per SM
+  static constexpr int kStages = (ASYM && NT > kTiles) ? kStagesOf<G> - 1 : kStagesOf<G>;
   alignas(128) unsigned char ring[kStages][kStageBytes];
   uint64_t full[kStages];
   uint64_t empty[kStages];
@@ -91,6 +92,8 @@ struct AttnSmem {
     float red[kWarps][G][kD];
   } pr;
   float rowmax[G][kWarps];
+  // asymmetric mode: the segment's V channel table [2][r][16] (scales, zero points; r <= kMaxR)
+  alignas(16) float vch[ASYM ? 2 * kMaxR * 16 : 4];
 };
 
 // stage geometry of a sub-item with r bond rows and nbt tiles
@@ -155,8 +158,8 @@ __device__ __forceinline__ void issue_stage(const SubItem& d, int st, unsigned c
 }
 
 // the W image (limb chunks + metadata) of a sub-item's segment onto wbar (one thread)
-template <int G, int NT>
-__device__ __forceinline__ void issue_wimg(AttnSmem<G, NT>& sm, const dq_attn_args& a, const SubItem& d) {
+template <int G, int NT, bool ASYM>
+__device__ __forceinline__ void issue_wimg(AttnSmem<G, NT, ASYM>& sm, const dq_attn_args& a, const SubItem& d) {
   const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
   const uint32_t wb = (uint32_t)(G * 2 * d.r * 8 * 16);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -170,14 +173,14 @@ __device__ __forceinline__ int p_chunk(int h, int limb, int a, int bg) {
   return ((h * 2 + limb) * 8 + a) * (4 * NT) + (bg ^ (4 * (a & 1)));
 }
 
-template <int BITS, int G, int NT = kTiles>
+template <int BITS, int G, int NT = kTiles, bool ASYM = false>
 __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel(dq_attn_args args) {
-  constexpr int kStages = kStagesOf<G>;
+  constexpr int kStages = AttnSmem<G, NT, ASYM>::kStages;
   constexpr int RB = 2 * BITS;
   constexpr int X = kExcess<BITS>;
   constexpr bool SA = BITS == 8;  // A operand (codes) signed
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  AttnSmem<G, NT>& sm = *reinterpret_cast<AttnSmem<G, NT>*>(smem_raw);
+  AttnSmem<G, NT, ASYM>& sm = *reinterpret_cast<AttnSmem<G, NT, ASYM>*>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tid4 = lane & 3;
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     // output (the per-segment W images) is read from here on
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
-    if (sm.sub[0].nbt > 0) issue_wimg<G, NT>(sm, args, sm.sub[0]);
+    if (sm.sub[0].nbt > 0) issue_wimg<G, NT, ASYM>(sm, args, sm.sub[0]);
   }
 
   int st = 0;  // running global stage index (identical in every consumer thread)
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     if (tid == 0) {
       const int jn = j + 1;
       mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT>(sm, args, sm.sub[jn % kSubRing]);
+      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(sm, args, sm.sub[jn % kSubRing]);
     }
     continue;
 #endif
@@ -411,11 +414,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     }
     named_sync(kThreads);  // every warp is past phase 1: the W buffer is dead
     wstamp(2);
-    if (tid == 0) {   // prefetch the fp32 G0v for the epilogue into it
+    if (tid == 0) {   // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
       const uint32_t gb = (uint32_t)(i1 * r * 32);
+      const uint32_t cb = ASYM ? (uint32_t)(2 * r * 16 * 4) : 0u;
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_expect_tx(&sm.g0bar, gb);
+      mbar_expect_tx(&sm.g0bar, gb + cb);
       bulk_g2s(sm.wg.g0v, d.vg0, gb, &sm.g0bar);
+      if (ASYM) bulk_g2s(sm.vch, args.segs[d.seg].v_ch, cb, &sm.g0bar);
     }
     unsigned char* pb = reinterpret_cast<unsigned char*>(sm.pr.p);
     // P = exp2(s - m) in fixed point with one scale per (h, a, 64-row tile), set by that
@@ -480,7 +485,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         v += __shfl_xor_sync(0xffffffffu, v, 4);
         v += __shfl_xor_sync(0xffffffffu, v, 8);
         v += __shfl_xor_sync(0xffffffffu, v, 16);
-        if (X && gid == 0 && jt < nbt) atomicAdd(&sm.gamma[h][2 * tid4 + q][jt], X * v);
+        // gamma = X sum_b Pint (symmetric), sum_b Pint (asymmetric: the zero point is per channel)
+        if (X && gid == 0 && jt < nbt) atomicAdd(&sm.gamma[h][2 * tid4 + q][jt], ASYM ? v : X * v);
       }
       for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
       if (lane == 0) sm.lsum[h][warp] = lsum;
@@ -504,6 +510,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 #pragma unroll
         for (int k = 0; k < 4; ++k) accv[t][h][k] = 0.f;
     const int nV = nbt * d.nslices;
+    if (ASYM) mbar_wait(&sm.g0bar, (uint32_t)(j & 1));  // the V zero points seed the accumulators
     for (int vs = 0, btl = 0, sl = 0; vs < nV; ++vs, ++st) {
       const int slot = st % kStages;
       mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
@@ -534,10 +541,17 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
             uint32_t x0[4], x1[4];
             row_bytes<BITS>(lds_row<BITS>(buf + (rl * 16 + gid) * 8 * BITS + RB * tid4), x0);
             row_bytes<BITS>(lds_row<BITS>(buf + (rl * 16 + gid + 8) * 8 * BITS + RB * tid4), x1);
+            int z0 = 1, z1 = 1;  // asymmetric: zero points of (bond row, e = gid / gid + 8)
+            if (ASYM) {
+              const int rr = warp * rw + t;
+              z0 = (int)sm.vch[r * 16 + rr * 16 + gid];  // zero points follow the scales
+              z1 = (int)sm.vch[r * 16 + rr * 16 + gid + 8];
+            }
 #pragma unroll
             for (int h = 0; h < G; ++h) {
-              // the excess correction seeds the low-limb accumulator
-              int yh[4] = {0, 0, 0, 0}, yl[4] = {-gam[h][0], -gam[h][1], -gam[h][0], -gam[h][1]};
+              // the excess (or zero-point) correction seeds the low-limb accumulator
+              int yh[4] = {0, 0, 0, 0};
+              int yl[4] = {-z0 * gam[h][0], -z0 * gam[h][1], -z1 * gam[h][0], -z1 * gam[h][1]};
               imma<SA, false>(yh, x0[0], x1[0], x0[1], x1[1], ph[h].x, ph[h].y);
               imma<SA, false>(yl, x0[0], x1[0], x0[1], x1[1], pl_[h].x, pl_[h].y);
               imma<SA, false>(yh, x0[2], x1[2], x0[3], x1[3], ph[h].z, ph[h].w);
@@ -569,6 +583,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     for (int t = 0; t < kRw; ++t) {
       if (t < rw) {
         const int rr = warp * rw + t;
+        // asymmetric: the per-(bond row, e) channel scales of V
+        const float s0 = ASYM ? sm.vch[rr * 16 + gid] : 1.f, s1 = ASYM ? sm.vch[rr * 16 + gid + 8] : 1.f;
 #pragma unroll
         for (int aa = 0; aa < 2; ++aa) {
           const int a = 2 * tid4 + aa;
@@ -576,10 +592,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
             const float4 g_lo = g0v[2 * (a * r + rr)], g_hi = g0v[2 * (a * r + rr) + 1];
             const float gc[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
 #pragma unroll
-            for (int h = 0; h < G; ++h)
+            for (int h = 0; h < G; ++h) {
+              const float y0 = ASYM ? accv[t][h][aa] * s0 : accv[t][h][aa];
+              const float y1 = ASYM ? accv[t][h][2 + aa] * s1 : accv[t][h][2 + aa];
 #pragma unroll
-              for (int c = 0; c < 8; ++c)
-                ffma2(part[h][2 * c], part[h][2 * c + 1], gc[c], gc[c], accv[t][h][aa], accv[t][h][2 + aa]);
+              for (int c = 0; c < 8; ++c) ffma2(part[h][2 * c], part[h][2 * c + 1], gc[c], gc[c], y0, y1);
+            }
           }
         }
       }
@@ -598,7 +616,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     if (tid == 0) {
       const int jn = j + 1;
       mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT>(sm, args, sm.sub[jn % kSubRing]);
+      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(sm, args, sm.sub[jn % kSubRing]);
     }
     if (tid < G * 8 * NT) {
       (&sm.gamma[0][0][0])[tid] = 0;

@@ -45,8 +45,12 @@ constexpr int kPrepSplit = 4;  // CTAs per segment, each 8 / kPrepSplit columns 
 template <int G>
 constexpr int kPrepThreadsOf = G * (8 / kPrepSplit) * kMaxRW;
 
-template <int BITS, int G>
-__global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) attn_prepare_kernel(dq_attn_args args) {
+// ASYM: the segments carry per-(rr, e) channel tables (asymmetric mode): their scales fold
+// into W and their zero points into beta (instantiated separately so the symmetric kernel
+// keeps its register budget)
+template <int BITS, int G, bool ASYM = false>
+__global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPrepThreadsOf<G>)
+    attn_prepare_kernel(dq_attn_args args) {
   constexpr int X = kExcess<BITS>;
   __shared__ float q[G][128];
   __shared__ unsigned wmax[G][8][2];
@@ -80,6 +84,19 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
   }
   __syncthreads();
   const float gk[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
+  // asymmetric mode: the per-(rr, e) channel scales fold into W, the zero points into beta
+  const float* kch = (ASYM && live) ? seg.k_ch : nullptr;
+  float chs[ASYM ? 16 : 1], chz[ASYM ? 16 : 1];
+  if (ASYM && kch) {
+    const float4* s4 = reinterpret_cast<const float4*>(kch + rr * 16);
+    const float4* z4 = reinterpret_cast<const float4*>(kch + r * 16 + rr * 16);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 a4 = s4[k], b4 = z4[k];
+      chs[4 * k] = a4.x, chs[4 * k + 1] = a4.y, chs[4 * k + 2] = a4.z, chs[4 * k + 3] = a4.w;
+      chz[4 * k] = b4.x, chz[4 * k + 1] = b4.y, chz[4 * k + 2] = b4.z, chz[4 * k + 3] = b4.w;
+    }
+  }
   // path 2 keeps one scale per column: its S accumulators have no room for a second group
   const int grp = (rr < kGroupR || args.path == 2) ? 0 : 1;
   const int headroom = args.path ? 1 : 0;
@@ -93,6 +110,7 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
     float acc = 0.f;
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc = fmaf(q[h][c * 16 + e], gk[c], acc);
+    if constexpr (ASYM) acc *= chs[e];
     wv[i] = acc;
     m = fmaxf(m, fabsf(acc));
   }
@@ -106,7 +124,9 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int wint = __float2int_rn(wv[i] * wq);
-      wsum += wint;
+      // symmetric: sum of Wint (times the excess X below); asymmetric: sum of Wint * zero point
+      if constexpr (ASYM) wsum += wint * (int)chz[ord16<BITS>(i)];
+      else wsum += wint;
       // path 0: hi signed, lo unsigned; paths 1 / 2: both signed (lo in [-128, 127]) so one
       // s8 UMMA takes both limbs; wint = 256 * hi + lo either way
       const int whi = args.path ? (wint + 128) >> 8 : wint >> 8;
@@ -117,7 +137,8 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, 2048 / kPrepThreadsOf<G>) a
     uint4* wout = reinterpret_cast<uint4*>(img);
     wout[w_chunk(h, 0, r, rr, a, args.path)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     wout[w_chunk(h, 1, r, rr, a, args.path)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
+    if (ASYM) atomicAdd(&meta.beta[h][a][grp], wsum);
+    else if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
   }
   __syncthreads();
   if (tid < G * 16 && ((tid >> 1) & 7) / (8 / kPrepSplit) == (int)blockIdx.y) {  // this CTA's columns

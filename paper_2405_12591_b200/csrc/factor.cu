@@ -414,6 +414,60 @@ __global__ void quantize_core_kernel(const float* __restrict__ core1, int64_t co
   }
 }
 
+// ---- opt-in per-channel asymmetric quantisation (dq_deco_quantize_asym_batched) ----------
+// channel (rr, e) of core1 [r][i2][j2] over b: scale, zero point (fp64 arithmetic, f32 scale)
+__global__ void asym_channels_kernel(const float* __restrict__ core1, int64_t core_elems, int r, int i2, int j2,
+                                     int bits, float* __restrict__ channels) {
+  const int64_t blk = blockIdx.y;
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;  // rr * j2 + e
+  if (ch >= r * j2) return;
+  const int rr = ch / j2, e = ch % j2;
+  const float* src = core1 + blk * core_elems + (int64_t)rr * i2 * j2 + e;
+  float mn = src[0], mx = src[0];
+  for (int b = 1; b < i2; ++b) {
+    const float v = src[(int64_t)b * j2];
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+  }
+  const int qmu = (1 << bits) - 1;
+  const double range = __dadd_rn((double)mx, -(double)mn);
+  const float s = range > 0.0 ? (float)__ddiv_rn(range, (double)qmu) : (mx != 0.f ? fabsf(mx) : 1.f);
+  double z = floor(__dadd_rn(__ddiv_rn(-(double)mn, (double)s), 0.5));
+  z = z < 0.0 ? 0.0 : (z > qmu ? (double)qmu : z);
+  float* out = channels + blk * (int64_t)2 * r * j2;
+  out[ch] = s;
+  out[r * j2 + ch] = (float)z;
+}
+
+__global__ void quantize_core_asym_kernel(const float* __restrict__ core1, int64_t core_elems, CoreGeom geom,
+                                          int64_t out_bytes, const float* __restrict__ channels,
+                                          uint8_t* __restrict__ payload, int64_t payload_stride) {
+  const int64_t blk = blockIdx.y;
+  const int bits = geom.bits, per = 8 / bits, qmu = (1 << bits) - 1;
+  const float* src = core1 + blk * core_elems;
+  const float* chs = channels + blk * (int64_t)2 * geom.r * geom.j2;
+  const float* chz = chs + geom.r * geom.j2;
+  uint8_t* dst = payload + blk * payload_stride;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < out_bytes; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned v = 0;
+    for (int k = 0; k < per; ++k) {
+      const int64_t slot = i * per + k;
+      if (slot >= geom_slots(geom)) break;
+      int rr, b, e;
+      unsigned code = 0;  // padding slots hold 0
+      if (geom_coords(geom, slot, rr, b, e)) {
+        const int ch = rr * geom.j2 + e;
+        double u = __dadd_rn(floor(__dadd_rn(__ddiv_rn((double)src[((int64_t)rr * geom.i2 + b) * geom.j2 + e],
+                                                      (double)chs[ch]), 0.5)), (double)chz[ch]);
+        u = u < 0.0 ? 0.0 : (u > qmu ? (double)qmu : u);
+        code = (unsigned)u;
+      }
+      v |= (code & ((1u << bits) - 1u)) << (k * bits);
+    }
+    dst[i] = (uint8_t)v;
+  }
+}
+
 struct Workspace {
   double* G;
   double* U;
@@ -550,6 +604,39 @@ extern "C" int dq_deco_quantize_batched(const void* blocks, int32_t dtype, int64
   if (gx > 64) gx = 64;
   quantize_core_kernel<<<dim3((unsigned)gx, (unsigned)nblk), kThreads, 0, s>>>(
       w.core1, (int64_t)d.r * d.n, g, out_bytes, w.amax, payload, payload_stride, scale, flags);
+  DQ_LAUNCH_CHECK();
+  return DQ_OK;
+}
+
+extern "C" int dq_deco_quantize_asym_batched(const void* blocks, int32_t dtype, int64_t nblk, int64_t rows,
+                                             int64_t cols, int32_t bits, int32_t layout, float* core0,
+                                             uint8_t* payload, int64_t payload_stride, float* channels,
+                                             int32_t* flags, void* ws, size_t wsb, void* stream) {
+  if (bits != 2 && bits != 4) return fail(DQ_ERR_UNSUPPORTED_BITS, "asymmetric mode: bits must be 2 or 4, got %d", bits);
+  int st = check_args(blocks, dtype, nblk, rows, cols);
+  if (st) return st;
+  if (nblk == 0) return DQ_OK;
+  dq_plan2 p = make_plan2(rows, cols);
+  Dims d = make_dims(p, rows, cols, dtype);
+  int64_t out_bytes;
+  st = dq_layout_bytes(&p, bits, layout, &out_bytes);
+  if (st) return st;
+  if (payload_stride < out_bytes) return fail(DQ_ERR_INVALID_ARG, "payload_stride smaller than one core");
+  if (!core0 || !payload || !channels || !ws || wsb < ws_bytes(nblk, d, true))
+    return fail(DQ_ERR_INVALID_ARG, "dq_deco_quantize_asym_batched: missing output or workspace too small");
+  Workspace w = carve(ws, nblk, d, true);
+  cudaStream_t s = (cudaStream_t)stream;
+  st = factor_core(blocks, d, nblk, core0, w.core1, w, flags, s);
+  if (st) return st;
+  const int nch = (int)(p.r * p.j2);
+  asym_channels_kernel<<<dim3((unsigned)ceil_div(nch, 128), (unsigned)nblk), 128, 0, s>>>(
+      w.core1, (int64_t)d.r * d.n, (int)p.r, (int)p.i2, (int)p.j2, bits, channels);
+  DQ_LAUNCH_CHECK();
+  CoreGeom g = make_geom(p, bits, layout);
+  int64_t gx = ceil_div(out_bytes, kThreads);
+  if (gx > 64) gx = 64;
+  quantize_core_asym_kernel<<<dim3((unsigned)gx, (unsigned)nblk), kThreads, 0, s>>>(
+      w.core1, (int64_t)d.r * d.n, g, out_bytes, channels, payload, payload_stride);
   DQ_LAUNCH_CHECK();
   return DQ_OK;
 }

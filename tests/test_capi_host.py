@@ -115,7 +115,7 @@ def test_attention_work_plan(L, chunk_b):
 def test_struct_layouts(L):
     # sizes must match the C structs in include/dquant_b200.h
     assert ctypes.sizeof(L.Plan2) == 40
-    assert ctypes.sizeof(L.Segment) == 4 * 8 + 2 * 4 + 8 * 4
+    assert ctypes.sizeof(L.Segment) == 6 * 8 + 2 * 4 + 8 * 4  # 4 + 2 (asymmetric channel tables) pointers
     assert L.AttnArgs.work.offset % 8 == 0
 
 
