@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--kernel-g", type=int, default=None, help="query heads per split-kernel head group (1 or 2)")
     ap.add_argument("--tc", type=int, default=None, choices=[0, 1],
                     help="split kernel: 1 = tcgen05, 0 = mma.sync, default: tcgen05 where eligible")
+    ap.add_argument("--tail", type=int, default=0,
+                    help="fp16 tail tokens per unit before the timed region (steady state: e.g. 512)")
     ap.add_argument("--asym", type=int, default=0, choices=[0, 1],
                     help="1: the opt-in per-channel asymmetric quantizer (not the reference scheme)")
     ap.add_argument("--ctas", type=int, default=None,
@@ -331,7 +333,12 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    appended = args.warmup + args.steps + 1 + max(3, args.warmup // 2) + max(3, args.steps // 2)
+    # steady state: a partly filled fp16 tail, appended through the public API
+    for layer in range(layers):
+        for _ in range(args.tail):
+            cache.append_token(layer, kn[layer], vn[layer])
+    torch.cuda.synchronize()
+    appended = args.tail + args.warmup + args.steps + 1 + max(3, args.warmup // 2) + max(3, args.steps // 2)
     if appended + 1 >= chunk_len:
         raise SystemExit("steps too large: the tail would seal a chunk inside the timed region")
 
@@ -414,7 +421,7 @@ def run_ours(args, cfg):
         "dtype": "f16",
         "data": "synthetic: per-layer K/V ~ N(0,1) fp16 compressed by the K3 write path; q/k/v rows ~ N(0,1) fp16",
         "config": {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
-                   "kv_bits": bits, "quantizer": "per-channel asymmetric (opt-in)" if args.asym else "per-tensor symmetric (reference)",
+                   "kv_bits": bits, "tail_tokens": args.tail, "quantizer": "per-channel asymmetric (opt-in)" if args.asym else "per-tensor symmetric (reference)",
                    "layers": layers, "kv_heads": kv_heads, "g": g,
                    "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": cache._layers[0].args.chunk_b,
                    "split_ctas": cache.split_ctas, "kernel_g": cache._layers[0].kernel_g,

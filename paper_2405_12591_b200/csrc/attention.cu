@@ -37,32 +37,63 @@ namespace {
 
 using namespace attn;
 
-// ---- combine: one CTA (128 threads) per kv head unit; see attn_combine.cuh -----------
+// ---- combine: one CTA per kv head unit; see attn_combine.cuh --------------------------
+// Launched with programmatic dependent launch behind the split kernel.  Everything before
+// griddepcontrol.wait overlaps the split kernel: this grid is scheduled only once the split
+// kernel has passed its own wait, so the prepare kernel, the producers of q and every earlier
+// step have completed; the dense fp16 tail (written by earlier steps) is read here, the split
+// kernel's partials only after the wait.
+constexpr int kCombineThreads = 256;
+
 template <int G>
-__global__ void __launch_bounds__(128) combine_kernel(dq_attn_args args) {
+__global__ void __launch_bounds__(kCombineThreads) combine_kernel(dq_attn_args args) {
   extern __shared__ float tail_s[];  // [tail_cap]
-  __shared__ float red[4];
-  // programmatic dependent launch: this grid was scheduled while the split kernel ran;
-  // wait for its partials, and let the next kernel (the next layer's prepare) get scheduled
+  __shared__ __align__(16) float red[(kCombineThreads / 32) * 130];
+  const int u = blockIdx.x, d = threadIdx.x;
+  const int hg = args.head_groups > 1 ? args.head_groups : 1;
+  auto sync = [] { __syncthreads(); };
+  if (G == 1 && hg == 1) {  // tail partial first (overlapping the split kernel), then the merge
+    const int tl = args.tail_len ? args.tail_len[u] : 0;
+    float Mt = -INFINITY, Lt = 0.f, Ot = 0.f;
+    if (tl > 0) tail_partial<1>(args, u, u, 0, d, kCombineThreads, tl, tail_s, red, sync, Mt, Lt, Ot);
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    merge_head<1>(args, u, 0, d, Mt, Lt, Ot);
+    if (args.app_k) {
+      sync();
+      combine_append(args, u, d, tl);
+    }
+    return;
+  }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  combine_unit<G>(args, blockIdx.x, threadIdx.x, tail_s, red, [] { __syncthreads(); });
+  combine_unit<G>(args, u, d, kCombineThreads, tail_s, red, sync);
 }
 
-// combine for the GQA kernel's 8 heads: one 128-thread group per head (named barrier 1 + group),
-// then the fused append once every group has read the tail
+// combine for the GQA kernel's 8 heads: one 128-thread group per head (named barrier 1 + group);
+// the tail partials overlap the split kernel (see combine_kernel), the merges follow its wait
+// and the fused append comes once every group has read the tail
 __global__ void __launch_bounds__(kGqG * 128) combine_gqa_kernel(dq_attn_args args) {
   extern __shared__ float tail_sg[];  // [kGqG][tail_cap]
-  __shared__ float red[kGqG][4];
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  __shared__ __align__(16) float red[kGqG][4 * 130];
   const int u = blockIdx.x, grp = threadIdx.x >> 7, d = threadIdx.x & 127;
   const int hg = args.head_groups > 1 ? args.head_groups : 1;
   const int tl = args.tail_len ? args.tail_len[u] : 0;
   const int cap = args.tail_cap > 0 ? args.tail_cap : 1;
-  for (int vv = 0; vv < hg; ++vv)
-    combine_head<kGqG>(args, u, u * hg + vv, grp, d, tl, tail_sg + (size_t)grp * cap, red[grp],
-                       [grp] { asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory"); });
+  auto gsync = [grp] { asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory"); };
+  if (hg == 1) {
+    float Mt = -INFINITY, Lt = 0.f, Ot = 0.f;
+    if (tl > 0)
+      tail_partial<kGqG>(args, u, u, grp, d, 128, tl, tail_sg + (size_t)grp * cap, red[grp], gsync, Mt, Lt, Ot);
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    merge_head<kGqG>(args, u, grp, d, Mt, Lt, Ot);
+  } else {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    for (int vv = 0; vv < hg; ++vv)
+      combine_head<kGqG>(args, u, u * hg + vv, grp, d, 128, tl, tail_sg + (size_t)grp * cap, red[grp], gsync);
+  }
   if (args.app_k) {
     __syncthreads();  // every group has read tail_len[u] and the tail
     if (grp == 0) combine_append(args, u, d, tl);
@@ -240,7 +271,7 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     const bool gq = G == kGqG;  // one 128-thread group per head
     const size_t csmem = sizeof(float) * (a.tail_cap > 0 ? a.tail_cap : 1) * (gq ? kGqG : 1);
     const int hg = a.head_groups > 1 ? a.head_groups : 1;
-    if (gq && csmem > 48 * 1024) {
+    if (gq) {  // static reduction buffers + 8 tail buffers exceed the default 48 KB
       static bool cg_attr = false;
       if (!cg_attr) {
         DQ_CUDA_TRY(cudaFuncSetAttribute(combine_gqa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -250,7 +281,7 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units / hg));
-    cfg.blockDim = dim3(gq ? kGqG * 128 : 128);
+    cfg.blockDim = dim3(gq ? kGqG * 128 : kCombineThreads);
     cfg.dynamicSmemBytes = csmem;
     cfg.stream = s;
     cudaLaunchAttribute attr_pdl[1];

@@ -12,65 +12,116 @@ namespace attn {
 // d < 128 owns output dim d; threads d >= 128 of the calling group only join `sync`, a
 // barrier over the whole group.  All head_groups virtual units of u run here: they share
 // the tail, and the append must come after every head has read it.
-// One head h of virtual unit v (of kv head unit u): merge the v's work-item partials with the
-// dense fp16 tail and write the fp16 output row.  Thread d < 128 owns output dim d; `sync` is
-// a barrier over the calling group (128 threads, or more threads that only join it).
+// Dense fp16 tail attention of head h of virtual unit v (kv head unit u): the tail is one more
+// flash-decoding partial (Mt, Lt, Ot) -- it does not depend on the split kernel, so the PDL
+// combine computes it before waiting for the split kernel's partials.  nthr threads (a
+// multiple of 128) of the calling group: scores warp-parallel over tokens (4 tokens in flight
+// per warp), P.V warp-parallel over tokens with each lane owning 4 dims, then a cross-warp
+// reduction; thread d < 128 returns Ot for dim d.  tail_s holds tl floats, red 5 * nthr / 32
+// floats... (red: [nw][128] O partials + [nw] sums + [nw] maxima).
 template <int G, class Sync>
-__device__ __forceinline__ void combine_head(const dq_attn_args& args, int u, int v, int h, int d, int tl,
-                                             float* tail_s, float* red, Sync sync) {
-  const int lane = d & 31, warp = d >> 5;
-  const bool act = d < 128;
+__device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, int v, int h, int tid, int nthr, int tl,
+                                             float* tail_s, float* red, Sync sync, float& Mt, float& Lt, float& Ot) {
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
   const float l2e = 1.4426950408889634f;
-  const int p0 = args.unit_part0[v], np = args.unit_nparts[v];
-  // dense tail scores (log2 domain)
-  float tm = -INFINITY;
-  if (tl > 0) {
-    const __half* qh = reinterpret_cast<const __half*>(args.q) + ((size_t)v * G + h) * 128;
-    const uint2 qv = reinterpret_cast<const uint2*>(qh)[lane];
-    const __half2* q2 = reinterpret_cast<const __half2*>(&qv);
-    const float2 qa = __half22float2(q2[0]), qb = __half22float2(q2[1]);
-    const __half* tk = reinterpret_cast<const __half*>(args.tail_k) + (size_t)u * args.tail_cap * 128;
-    for (int t = warp; act && t < tl; t += 4) {
-      const uint2 kv = reinterpret_cast<const uint2*>(tk + (size_t)t * 128)[lane];
-      const __half2* k2 = reinterpret_cast<const __half2*>(&kv);
-      const float2 ka = __half22float2(k2[0]), kb = __half22float2(k2[1]);
-      float dot = qa.x * ka.x + qa.y * ka.y + qb.x * kb.x + qb.y * kb.y;
-      for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (lane == 0) tail_s[t] = dot * args.sm_scale * l2e;
+  const __half* qh = reinterpret_cast<const __half*>(args.q) + ((size_t)v * G + h) * 128;
+  const uint2 qv = reinterpret_cast<const uint2*>(qh)[lane];
+  const __half2* q2 = reinterpret_cast<const __half2*>(&qv);
+  const float2 qa = __half22float2(q2[0]), qb = __half22float2(q2[1]);
+  const __half* tk = reinterpret_cast<const __half*>(args.tail_k) + (size_t)u * args.tail_cap * 128;
+  const __half* tv = reinterpret_cast<const __half*>(args.tail_v) + (size_t)u * args.tail_cap * 128;
+  for (int t0 = warp; t0 < tl; t0 += 4 * nw) {
+    float dot[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int t = t0 + i * nw;
+      dot[i] = 0.f;
+      if (t < tl) {
+        const uint2 kv = reinterpret_cast<const uint2*>(tk + (size_t)t * 128)[lane];
+        const __half2* k2 = reinterpret_cast<const __half2*>(&kv);
+        const float2 ka = __half22float2(k2[0]), kb = __half22float2(k2[1]);
+        dot[i] = qa.x * ka.x + qa.y * ka.y + qb.x * kb.x + qb.y * kb.y;
+      }
     }
-    sync();
-    for (int t = d; act && t < tl; t += 128) tm = fmaxf(tm, tail_s[t]);
-    for (int o = 16; o; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-    if (act && lane == 0) red[warp] = tm;
-    sync();
-    tm = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-    sync();
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (t0 + i * nw < tl) tail_s[t0 + i * nw] = dot[i] * args.sm_scale * l2e;  // log2 domain
+    }
   }
-  float M = tm;
+  sync();
+  float m = -INFINITY;
+  for (int t = tid; t < tl; t += nthr) m = fmaxf(m, tail_s[t]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float* red_o = red;             // [nw][128]
+  float* red_l = red + nw * 128;  // [nw]
+  float* red_m = red_l + nw;      // [nw]
+  if (lane == 0) red_m[warp] = m;
+  sync();
+  m = red_m[0];
+  for (int w = 1; w < nw; ++w) m = fmaxf(m, red_m[w]);
+  float o4[4] = {0.f, 0.f, 0.f, 0.f}, l = 0.f;
+  for (int t = warp; t < tl; t += nw) {
+    const float p = exp2f(tail_s[t] - m);
+    l += p;
+    const uint2 vv = reinterpret_cast<const uint2*>(tv + (size_t)t * 128)[lane];
+    const __half2* v2 = reinterpret_cast<const __half2*>(&vv);
+    const float2 va = __half22float2(v2[0]), vb = __half22float2(v2[1]);
+    o4[0] = fmaf(p, va.x, o4[0]);
+    o4[1] = fmaf(p, va.y, o4[1]);
+    o4[2] = fmaf(p, vb.x, o4[2]);
+    o4[3] = fmaf(p, vb.y, o4[3]);
+  }
+  *reinterpret_cast<float4*>(red_o + warp * 128 + 4 * lane) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+  if (lane == 0) red_l[warp] = l;
+  sync();
+  Mt = m;
+  Lt = 0.f;
+  Ot = 0.f;
+  for (int w = 0; w < nw; ++w) {
+    Lt += red_l[w];
+    if (tid < 128) Ot += red_o[w * 128 + tid];
+  }
+  sync();  // red and tail_s reusable
+}
+
+// Merge of head h of virtual unit v: its work-item partials plus the tail partial (Mt, Lt, Ot;
+// Mt = -inf without a tail), fp16 output row.  Thread d < 128 owns dim d.
+template <int G>
+__device__ __forceinline__ void merge_head(const dq_attn_args& args, int v, int h, int d, float Mt, float Lt, float Ot) {
+  if (d >= 128) return;
+  const int p0 = args.unit_part0[v], np = args.unit_nparts[v];
+  float M = Mt;
   for (int i = 0; i < np; ++i) M = fmaxf(M, args.part_ml[((size_t)(p0 + i) * G + h) * 2]);
   float L = 0.f, O = 0.f;
+  if (Mt != -INFINITY) {
+    const float f = exp2f(Mt - M);
+    L = f * Lt;
+    O = f * Ot;
+  }
   for (int i = 0; i < np; ++i) {
     const size_t s = (size_t)(p0 + i) * G + h;
     const float m = args.part_ml[s * 2];
     if (m == -INFINITY) continue;
     const float f = exp2f(m - M);
     L += f * args.part_ml[s * 2 + 1];
-    O += f * args.part_o[s * 128 + (d & (128 - 1))];
-  }
-  if (tl > 0) {
-    const __half* tv = reinterpret_cast<const __half*>(args.tail_v) + (size_t)u * args.tail_cap * 128;
-    float lt = 0.f, ot = 0.f;
-    for (int t = 0; act && t < tl; ++t) {
-      const float p = exp2f(tail_s[t] - M);
-      lt += p;
-      ot = fmaf(p, __half2float(tv[(size_t)t * 128 + d]), ot);
-    }
-    L += lt;
-    O += ot;
-    sync();
+    O += f * args.part_o[s * 128 + d];
   }
   __half* out = reinterpret_cast<__half*>(args.out) + ((size_t)v * G + h) * 128;
-  if (act) out[d] = __float2half_rn(L > 0.f ? O / L : 0.f);
+  out[d] = __float2half_rn(L > 0.f ? O / L : 0.f);
+}
+
+// One head: tail partial then merge (callers that have already waited for the split kernel)
+template <int G, class Sync>
+__device__ __forceinline__ void combine_head(const dq_attn_args& args, int u, int v, int h, int d, int nthr, int tl,
+                                             float* tail_s, float* red, Sync sync) {
+  float Mt = -INFINITY, Lt = 0.f, Ot = 0.f;
+  if (tl > 0) tail_partial<G>(args, u, v, h, d, nthr, tl, tail_s, red, sync, Mt, Lt, Ot);
+  merge_head<G>(args, v, h, d, Mt, Lt, Ot);
 }
 
 // fused dq_tail_append: the new token joins unit u's tail after this step's attention (the
@@ -89,11 +140,12 @@ __device__ __forceinline__ void combine_append(const dq_attn_args& args, int u, 
 // head_groups virtual units of u run here, head after head: they share the tail, and the
 // append must come after every head has read it.
 template <int G, class Sync>
-__device__ __forceinline__ void combine_unit(const dq_attn_args& args, int u, int d, float* tail_s, float* red,
+__device__ __forceinline__ void combine_unit(const dq_attn_args& args, int u, int d, int nthr, float* tail_s, float* red,
                                              Sync sync) {
   const int hg = args.head_groups > 1 ? args.head_groups : 1;
   const int tl = args.tail_len ? args.tail_len[u] : 0;
-  for (int hh = 0; hh < G * hg; ++hh) combine_head<G>(args, u, u * hg + hh / G, hh % G, d, tl, tail_s, red, sync);
+  for (int hh = 0; hh < G * hg; ++hh)
+    combine_head<G>(args, u, u * hg + hh / G, hh % G, d, nthr, tl, tail_s, red, sync);
   if (args.app_k) {
     sync();  // every thread has read tail_len[u]
     combine_append(args, u, d, tl);

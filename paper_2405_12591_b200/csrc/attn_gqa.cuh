@@ -345,7 +345,12 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s % kGqStages]);
   };
-  if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
+  if (tid == 0) {
+    // the combine may be scheduled once this grid's prerequisites (prepare kernel, producers of
+    // q) have completed: it reads q and the tail before waiting for this grid
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  }
 
   for (int j = 0;; ++j) {
     cwait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
