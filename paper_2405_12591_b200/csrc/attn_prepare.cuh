@@ -52,7 +52,7 @@ template <int BITS, int G, bool ASYM = false>
 __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPrepThreadsOf<G>)
     attn_prepare_kernel(dq_attn_args args) {
   constexpr int X = kExcess<BITS>;
-  __shared__ float q[G][128];
+  __shared__ __align__(16) float q[G][128];
   __shared__ unsigned wmax[G][8][2];
   __shared__ WMeta<G> meta;
   // the dependent split kernel may start its prologue (barriers, code copies) right away;
@@ -105,14 +105,19 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
   float wv[16];
   float m = 0.f;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int e = ord16<BITS>(i);
-    float acc = 0.f;
+  for (int i = 0; i < 16; ++i) wv[i] = 0.f;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc = fmaf(q[h][c * 16 + e], gk[c], acc);
-    if constexpr (ASYM) acc *= chs[e];
-    wv[i] = acc;
-    m = fmaxf(m, fabsf(acc));
+  for (int c = 0; c < 8; ++c) {  // q[h][c*16 .. c*16+15] as four broadcast 128-bit loads
+    const float4* q4 = reinterpret_cast<const float4*>(&q[h][c * 16]);
+    const float4 x0 = q4[0], x1 = q4[1], x2 = q4[2], x3 = q4[3];
+    const float qc[16] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x, x3.y, x3.z, x3.w};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) wv[i] = fmaf(qc[ord16<BITS>(i)], gk[c], wv[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if constexpr (ASYM) wv[i] *= chs[ord16<BITS>(i)];
+    m = fmaxf(m, fabsf(wv[i]));
   }
   if (live) atomicMax(&wmax[h][a][grp], __float_as_uint(m));
   __syncthreads();

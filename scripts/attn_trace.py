@@ -14,7 +14,9 @@ from paper_2405_12591_b200.attention import DecodeKvCache  # noqa: E402
 units, T = int(os.environ.get("UNITS", 512)), int(os.environ.get("T", 4096))
 G = int(os.environ.get("G", 1))  # G=8: the tcgen05 GQA kernel (path 2)
 ctas = os.environ.get("CTAS")
-cache = DecodeKvCache(layers=1, units=units, g=G, bits=4, ctas=None if ctas is None else int(ctas),
+cache = DecodeKvCache(layers=1, units=units, g=G, bits=int(os.environ.get("BITS", 4)),
+                      chunk_b=int(os.environ["CHUNK_B"]) if os.environ.get("CHUNK_B") else None,
+                      ctas=None if ctas is None else int(ctas),
                       tc=None if G == 8 else bool(int(os.environ.get("TC", "0"))))
 k = torch.randn((units, T, 128), device="cuda").half()
 cache.prefill(0, k, k)
@@ -33,12 +35,13 @@ if os.environ.get("SAVE"):
     np.savez(os.environ["SAVE"], trace=trace.cpu().numpy(), work=cache._layers[0].keep[1].cpu().numpy())
 t0 = t[:, 0].min()
 path = cache._layers[0].args.path
-if path == 2:  # stamps 0 start, 1 K done, 2 softmax done, 3 V done, 5 end; MMA warp 7 / 4 / 6
+if path == 2:  # stamps 0 start, 1 K done, 2 softmax done, 3 V done, 5 end (slots 4, 6, 7: profiling builds)
     rel = lambda c: ((t[:, c] - t[:, 0]) / 1e3).mean()  # noqa: E731
-    print(f"MMA warp: K issue {rel(7):.2f} -> {rel(4):.2f} us, V issue done {rel(6):.2f} us; consumers: K done "
-          f"{rel(1):.2f}, softmax done {rel(2):.2f}, V done {rel(3):.2f}, end {rel(5):.2f} us (item-relative means)")
-    if os.environ.get("MMAWAIT"):  # build with -DDQ_GQ_MMAWAIT: slot 6 / 4 = MMA warp waits (K / V), ns
-        print(f"MMA warp waits: K phase {(t[:, 6] / 1e3).mean():.2f} us, V phase {(t[:, 4] / 1e3).mean():.2f} us")
+    print(f"consumers: K done {rel(1):.2f}, softmax done {rel(2):.2f}, V done {rel(3):.2f}, end {rel(5):.2f} us "
+          f"(item-relative means)")
+    if os.environ.get("MMAWAIT"):  # build with -DDQ_GQ_MMAWAIT: MMA warp V phase span / A waits / Y waits, ns
+        print(f"MMA warp V phase: span {(t[:, 4] / 1e3).mean():.2f} us, waiting for A {(t[:, 6] / 1e3).mean():.2f} us, "
+              f"for Y {(t[:, 7] / 1e3).mean():.2f} us")
     if os.environ.get("SMTRACE"):  # build with -DDQ_GQ_SMTRACE: 7 S ready, 4 row max, 6 column max
         print(f"softmax: S ready {rel(7):.2f}, row max {rel(4):.2f}, column max {rel(6):.2f}, P written {rel(2):.2f}")
     t[:, 4] = t[:, 3]
@@ -58,11 +61,6 @@ print("  end-time quantiles (us):  ", np.round(np.percentile(ends, [0, 25, 50, 7
 grid = np.linspace(0, ends[-1], 40)
 conc = [int(((t[:, 0] - t0) / 1e3 <= x).sum() - ((t[:, 5] - t0) / 1e3 <= x).sum()) for x in grid]
 print("  resident items over time:", conc)
-if cache._layers[0].args.path == 1:  # stamps 7 / 4: the MMA warp's K-issue start / end
-    print(f"  MMA K issue: start-after-item-start {((t[:, 7] - t[:, 0]) / 1e3).mean():.2f} us, "
-          f"duration {((t[:, 4] - t[:, 7]) / 1e3).mean():.2f} us, ends {((t[:, 4] - t[:, 0]) / 1e3).mean():.2f} us "
-          f"into the item; consumers end K at {((t[:, 1] - t[:, 0]) / 1e3).mean():.2f} us; "
-          f"MMA waited {(t[:, 6] / 1e3).mean():.2f} us of it on A buffers")
 # per-CTA finish times (stamp 6 = blockIdx, 7 = SM; path 1 reuses them)
 if path in (1, 2):
     t[:, 6] = 0
