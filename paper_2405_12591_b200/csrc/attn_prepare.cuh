@@ -156,30 +156,13 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
 }
 
 // Prepare kernel of the tcgen05 GQA path (path 2: 8 heads, 4-bit codes, r = 64): one CTA per
-// segment (one wave at 512 segments), one thread per (bond row rr, column pair a, a + 1)
-// looping over the 8 heads: each broadcast load of q feeds both columns, and a warp's W
-// stores cover 8 bond rows x 8 columns of one slice (1 KB, in two 512-byte halves).  Two
-// passes over W (recomputed): the per-(h, a) maxima set the scales, then the limbs.
-constexpr int kPrepGqThreads = 4 * kMaxRW;
+// segment (512 threads, one per (bond row rr, column a)), heads in turn.  A head's 16 W values
+// per thread stay in registers across its column-maximum reduction (warp shuffles + one shared
+// atomic per column and warp, one barrier per head), so W is computed once.  A warp covers 4
+// bond rows x 8 columns of one 8-row slice: each of its W stores is 512 contiguous bytes.
+constexpr int kPrepGqThreads = 8 * kMaxRW;
 
-// W[h][a][rr][16 e] (e in ord16 order) for two columns, from q[h] in shared memory
-__device__ __forceinline__ void gq_w32(const float* qh, const float (&gk)[2][8], float (&wv)[2][16]) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) wv[0][i] = wv[1][i] = 0.f;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float4* q4 = reinterpret_cast<const float4*>(qh + c * 16);
-    const float4 x0 = q4[0], x1 = q4[1], x2 = q4[2], x3 = q4[3];
-    const float qc[16] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x, x3.y, x3.z, x3.w};
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      wv[0][i] = fmaf(qc[ord16<4>(i)], gk[0][c], wv[0][i]);
-      wv[1][i] = fmaf(qc[ord16<4>(i)], gk[1][c], wv[1][i]);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kPrepGqThreads, 4) attn_prepare_gqa_kernel(dq_attn_args args) {
+__global__ void __launch_bounds__(kPrepGqThreads, 2) attn_prepare_gqa_kernel(dq_attn_args args) {
   constexpr int G = 8, X = kExcess<4>, WB = kWBits<4> - 1;  // both limbs signed: one bit of headroom
   __shared__ __align__(16) float q[G][128];
   __shared__ unsigned wmax[G][8];
@@ -187,7 +170,7 @@ __global__ void __launch_bounds__(kPrepGqThreads, 4) attn_prepare_gqa_kernel(dq_
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-  const int rr = tid >> 2, a0 = 2 * (tid & 3);
+  const int rr = tid >> 3, a = tid & 7;
   const dq_segment& seg = args.segs[s];
   const int r = seg.r;
   const bool live = rr < r;
@@ -197,66 +180,56 @@ __global__ void __launch_bounds__(kPrepGqThreads, 4) attn_prepare_gqa_kernel(dq_
     (&wmax[0][0])[tid] = 0u;
     (&bsum[0][0])[tid] = 0;
   }
-  float gk[2][8];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    float4 g_lo = make_float4(0.f, 0.f, 0.f, 0.f), g_hi = g_lo;
-    if (live) {
-      const float4* g0k = reinterpret_cast<const float4*>(seg.k_g0);  // fp32 [a][rr][c], normalised
-      g_lo = g0k[2 * ((a0 + k) * r + rr)];
-      g_hi = g0k[2 * ((a0 + k) * r + rr) + 1];
-    }
-    gk[k][0] = g_lo.x, gk[k][1] = g_lo.y, gk[k][2] = g_lo.z, gk[k][3] = g_lo.w;
-    gk[k][4] = g_hi.x, gk[k][5] = g_hi.y, gk[k][6] = g_hi.z, gk[k][7] = g_hi.w;
+  float gk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (live) {
+    const float4* g0k = reinterpret_cast<const float4*>(seg.k_g0);  // fp32 [a][rr][c], normalised
+    const float4 g_lo = g0k[2 * (a * r + rr)], g_hi = g0k[2 * (a * r + rr) + 1];
+    gk[0] = g_lo.x, gk[1] = g_lo.y, gk[2] = g_lo.z, gk[3] = g_lo.w;
+    gk[4] = g_hi.x, gk[5] = g_hi.y, gk[6] = g_hi.z, gk[7] = g_hi.w;
   }
   __syncthreads();
-  // pass 1: column maxima (the 8 lanes of a warp with these columns, then across warps)
-#pragma unroll 1
-  for (int h = 0; h < G; ++h) {
-    float wv[2][16];
-    gq_w32(q[h], gk, wv);
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      float m = 0.f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) m = fmaxf(m, fabsf(wv[k][i]));
-      unsigned mu = __float_as_uint(m);
-      mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, 4));
-      mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, 8));
-      mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, 16));
-      if (lane < 4) atomicMax(&wmax[h][a0 + k], mu);
-    }
-  }
-  __syncthreads();
-  // pass 2: two signed limbs per value, wint = 256 * hi + lo, |wint| < 2^WB
   unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
   uint4* wout = reinterpret_cast<uint4*>(img);
 #pragma unroll 1
   for (int h = 0; h < G; ++h) {
-    float wv[2][16];
-    gq_w32(q[h], gk, wv);
+    float wv[16];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a0 + k]), WB);
-      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-      int wsum = 0;
+    for (int i = 0; i < 16; ++i) wv[i] = 0.f;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int wint = __float2int_rn(wv[k][i] * wq);
-        wsum += wint;
-        const int whi = (wint + 128) >> 8;
-        hi[i >> 2] |= (uint32_t)(whi & 0xFF) << (8 * (i & 3));
-        lo[i >> 2] |= (uint32_t)((wint - 256 * whi) & 0xFF) << (8 * (i & 3));
-      }
-      if (live) {
-        wout[w_chunk(h, 0, r, rr, a0 + k, 2)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        wout[w_chunk(h, 1, r, rr, a0 + k, 2)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
-      wsum += __shfl_xor_sync(0xffffffffu, wsum, 4);
-      wsum += __shfl_xor_sync(0xffffffffu, wsum, 8);
-      wsum += __shfl_xor_sync(0xffffffffu, wsum, 16);
-      if (lane < 4) atomicAdd(&bsum[h][a0 + k], wsum);
+    for (int c = 0; c < 8; ++c) {
+      const float4* q4 = reinterpret_cast<const float4*>(&q[h][c * 16]);
+      const float4 x0 = q4[0], x1 = q4[1], x2 = q4[2], x3 = q4[3];
+      const float qc[16] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x, x3.y, x3.z, x3.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) wv[i] = fmaf(qc[ord16<4>(i)], gk[c], wv[i]);
     }
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m = fmaxf(m, fabsf(wv[i]));
+    unsigned mu = __float_as_uint(m);
+    mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, 8));
+    mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, 16));
+    if (lane < 8) atomicMax(&wmax[h][a], mu);
+    __syncthreads();
+    // two signed limbs per value, wint = 256 * hi + lo, |wint| < 2^WB
+    const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a]), WB);
+    uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    int wsum = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int wint = __float2int_rn(wv[i] * wq);
+      wsum += wint;
+      const int whi = (wint + 128) >> 8;
+      hi[i >> 2] |= (uint32_t)(whi & 0xFF) << (8 * (i & 3));
+      lo[i >> 2] |= (uint32_t)((wint - 256 * whi) & 0xFF) << (8 * (i & 3));
+    }
+    if (live) {
+      wout[w_chunk(h, 0, r, rr, a, 2)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      wout[w_chunk(h, 1, r, rr, a, 2)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    wsum += __shfl_xor_sync(0xffffffffu, wsum, 8);
+    wsum += __shfl_xor_sync(0xffffffffu, wsum, 16);
+    if (lane < 8) atomicAdd(&bsum[h][a], wsum);
   }
   __syncthreads();
   if (tid < G * 16) {  // metadata: beta[G][8][2], cs[G][8][2] (group 1 unused on this path)
