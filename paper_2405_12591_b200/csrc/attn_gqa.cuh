@@ -37,9 +37,13 @@ constexpr int kGqG = 8;                            // query heads per kernel ins
 constexpr int kGqStages = 5;                       // ring: 5 x 32 KB
 constexpr int kGqSlot = 32768;                     // K stage: codes [0, 16 KB) + W slice [16 KB, 32 KB)
 constexpr int kGqWSlice = 16 * 8 * 8 * 16;         // W slice: 16 (h, limb) x 8 bond rows x 8 a x 16 e = 16 KB
-constexpr int kGqWarps = 16;                       // consumer warps: 4 warpgroups
+constexpr int kGqWarps = 16;                       // math warps (softmax, Y fold, epilogue): 4 warpgroups
 constexpr int kGqCons = kGqWarps * 32;
-constexpr int kGqThreads = kGqCons + 64;           // + producer (8) + MMA (9)
+constexpr int kGqWide = 4;                         // widening warpgroup: codes ring -> TMEM A operands
+constexpr int kGqProducer = kGqWarps + kGqWide;    // producer warp (20), then the MMA warp (21)
+constexpr int kGqMma = kGqProducer + 1;
+constexpr int kGqThreads = kGqCons + kGqWide * 32 + 64;
+constexpr int kGqTmemUsers = kGqCons + kGqWide * 32 + 32;  // threads that touch TMEM (final barrier)
 constexpr int kGqNumA = 4;                         // TMEM A buffers (64 columns each)
 constexpr uint32_t kGqColA = 0, kGqColSY = 256;    // A: 4 x 64 columns; S / Y: 2 x 128 columns
 constexpr int kGqPBits = 15;
@@ -163,12 +167,12 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   if (tid == 0) {
     for (int s = 0; s < kGqStages; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kGqWarps + 1);  // the consumer warps + the MMA warp's commit
+      mbar_init(&sm.empty[s], kGqWide + 1);  // the widening warps + the MMA warp's commit
     }
     for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.descfull[s], 1);
     mbar_init(&sm.g0bar, 1);
     for (int b = 0; b < kGqNumA; ++b) {
-      mbar_init(&sm.afull[b], kGqWarps);
+      mbar_init(&sm.afull[b], kGqWide);
       mbar_init(&sm.afree[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     sm.pmax[tid] = 0u;
     sm.gsum[tid] = 0;
   }
-  if (warp == kGqWarps + 1) {
+  if (warp == kGqMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
 
-  if (warp == kGqWarps) {
+  if (warp == kGqProducer) {
     // ---- producer: descriptors and stages of this CTA's items, in order --------------------
     if (lane == 0) {
       // the W images come from the prepare kernel, and the ticket counter is shared with the
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     return;
   }
 
-  if (warp == kGqWarps + 1) {
+  if (warp == kGqMma) {
     // ---- MMA warp: the whole (converged) warp runs the schedule with warp-uniform operands,
     // one elected lane issues each UMMA / commit (operands stay in uniform registers: no
     // per-UMMA register-to-uniform moves on the issue path)
@@ -322,9 +326,76 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
 #endif
     }
     __syncwarp();
-    named_sync2(kGqCons + 32);  // the consumers' last TMEM reads are done
+    named_sync2(kGqTmemUsers);  // the other warps' last TMEM accesses are done
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    return;
+  }
+
+  if (warp >= kGqWarps) {
+    // ---- widening warpgroup: every K and V stage, in ring order, into the TMEM A buffers ----
+    // (warp & 3 = its TMEM lane quadrant); it runs ahead of the math warps by up to 4 A buffers,
+    // so the next item's first K stages are widened while the math warps fold this item's Y
+    const int q = warp & 3;
+    const int lane_in = 32 * q + lane;
+    const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+    int st = 0, na = 0;
+    for (int j = 0;; ++j) {
+      mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+      const SubItem d = sm.sub[j % kSubRing];
+      if (d.nbt == 0) break;
+      const int nbt = d.nbt, nmb = (nbt + 1) / 2;
+      for (int ks = 0; ks < d.nK + d.nslices; ++ks, ++st, ++na) {
+        const int slot = st % kGqStages, ab = na % kGqNumA;
+        mbar_wait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
+        if (na >= kGqNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kGqNumA - 1) & 1));
+        if (ks < d.nK) {  // K stage: 8 bond rows of rows b = 128 mb + lane_in, both M-blocks
+          for (int mb = 0; mb < nmb; ++mb) {
+            const int jt = 2 * mb + (q >> 1), b_in = 32 * (q & 1) + lane;
+            const unsigned char* tile = sm.ring[slot] + jt * 8 * kI2Pad * RB;
+            const bool live = jt < nbt;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              uint32_t v[16];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int rl = 4 * half + i;  // rr & 3 = i (stages start at multiples of 8)
+                uint2 w2 = make_uint2(0u, 0u);
+                if (live) w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ (i * 4))) * RB);
+                v[4 * i] = w2.x & 0x0F0F0F0Fu;
+                v[4 * i + 1] = (w2.x >> 4) & 0x0F0F0F0Fu;
+                v[4 * i + 2] = w2.y & 0x0F0F0F0Fu;
+                v[4 * i + 3] = (w2.y >> 4) & 0x0F0F0F0Fu;
+              }
+              tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + mb * 32 + half * 16), v);
+            }
+          }
+        } else {  // V stage: row (r_local, e) = lane_in of every tile
+          for (int t = 0; t < nbt; ++t) {
+            const unsigned char* src = sm.ring[slot] + t * kGqVTileBytes + lane_in * 32;
+            const uint4 c0 = *reinterpret_cast<const uint4*>(src);
+            const uint4 c1 = *reinterpret_cast<const uint4*>(src + 16);
+            const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            uint32_t v[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              v[2 * k] = wv[k] & 0x0F0F0F0Fu;
+              v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
+            }
+            tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + t * 16), v);
+          }
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&sm.afull[ab]);
+          mbar_arrive(&sm.empty[slot]);
+        }
+      }
+    }
+    tc_fence_before();
+    named_sync2(kGqTmemUsers);
     return;
   }
 
@@ -339,12 +410,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   const int mbk = wg & 1, hh = wg >> 1;  // K / softmax: M-block (rows b) and half (bond rows / heads 4hh..4hh+3)
   const int lane_in = 32 * q + lane;     // TMEM lane
   const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-  int st = 0, na = 0;
   int uyc[2] = {0, 0};
-  auto release = [&](int s) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[s % kGqStages]);
-  };
   if (tid == 0) {
     // the combine may be scheduled once this grid's prerequisites (prepare kernel, producers of
     // q) have completed: it reads q and the tail before waiting for this grid
@@ -368,39 +434,9 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       bulk_g2s(sm.g0v, d.vg0, gb, &sm.g0bar);
     }
 
-    // ---- K phase: widen this thread's row b of each stage into TMEM --------------------------
-    const int jt = 2 * mbk + (q >> 1);       // tile of this thread's row
-    const int b_in = 32 * (q & 1) + lane;    // row inside the tile
-    for (int ks = 0; ks < d.nK; ++ks, ++st, ++na) {
-      const int slot = st % kGqStages, ab = na % kGqNumA;
-      cwait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
-      if (na >= kGqNumA) cwait(&sm.afree[ab], (uint32_t)((na / kGqNumA - 1) & 1));
-      if (mbk < nmb) {  // bond rows 4hh .. 4hh+3 of the stage for this thread's row
-        const unsigned char* tile = sm.ring[slot] + jt * 8 * kI2Pad * RB;
-        const bool live = jt < nbt;
-        uint32_t v[16];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rl = 4 * hh + i;  // rr & 3 = i (stages start at multiples of 8)
-          uint2 w2 = make_uint2(0u, 0u);
-          if (live) w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ (i * 4))) * RB);
-          v[4 * i] = w2.x & 0x0F0F0F0Fu;
-          v[4 * i + 1] = (w2.x >> 4) & 0x0F0F0F0Fu;
-          v[4 * i + 2] = w2.y & 0x0F0F0F0Fu;
-          v[4 * i + 3] = (w2.y >> 4) & 0x0F0F0F0Fu;
-        }
-#ifndef DQ_GQ_NULL_WIDEN  // measurement only: no TMEM stores from the consumers
-        tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + mbk * 32 + hh * 16), v);
-#else
-        if (v[0] == 0x12345678u) args.trace[0] = v[1];
-#endif
-        tc_wait_st();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.afull[ab]);
-      release(st);
-    }
+    // this thread's row b for the softmax: tile jt, row b_in inside it
+    const int jt = 2 * mbk + (q >> 1);
+    const int b_in = 32 * (q & 1) + lane;
     stamp(1);
 
     // ---- softmax of the item straight from S in TMEM (this thread = row b) -----------------
@@ -518,38 +554,6 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     for (int hl = 0; hl < 2; ++hl)
 #pragma unroll
       for (int c = 0; c < 8; ++c) o[hl][c] = 0.f;
-    auto widen_v = [&]() {
-      const int slot = st % kGqStages, ab = na % kGqNumA;
-      cwait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
-      if (na >= kGqNumA) cwait(&sm.afree[ab], (uint32_t)((na / kGqNumA - 1) & 1));
-      {
-        const int t = wg;  // this warpgroup's tile
-        if (t < nbt) {
-          const unsigned char* src = sm.ring[slot] + t * kGqVTileBytes + lane_in * 32;
-          const uint4 c0 = *reinterpret_cast<const uint4*>(src);
-          const uint4 c1 = *reinterpret_cast<const uint4*>(src + 16);
-          const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          uint32_t v[16];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            v[2 * k] = wv[k] & 0x0F0F0F0Fu;
-            v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
-          }
-#ifndef DQ_GQ_NULL_WIDEN
-          tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + t * 16), v);
-#else
-          if (v[0] == 0x12345678u) args.trace[0] = v[1];
-#endif
-        }
-      }
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.afull[ab]);
-      release(st);
-      ++st;
-      ++na;
-    };
     auto fold_y = [&](int vs) {
       const int yb = vs & 1;
       cwait(&sm.yfull[yb], (uint32_t)(uyc[yb] & 1));
@@ -606,15 +610,9 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       }
     };
     cwait(&sm.g0bar, (uint32_t)(j & 1));
-    // the fold lags the widening by two stages: stage vs's UMMAs have two widen + fold
-    // rounds to complete before their Y is read (Y is double-buffered, so the UMMAs of vs wait
-    // only for the fold of vs - 2, which comes right before)
-    for (int vs = 0; vs < d.nslices; ++vs) {
-      widen_v();
-      if (vs > 1) fold_y(vs - 2);
-    }
-    fold_y(d.nslices - 2);
-    fold_y(d.nslices - 1);
+    // the widening warps feed the A buffers; Y is double-buffered, so stage vs + 1's UMMAs run
+    // while this stage is folded
+    for (int vs = 0; vs < d.nslices; ++vs) fold_y(vs);
     stamp(3);
 
     // ---- reduce over bond rows: lanes l / l ^ 16, then the 4 warps of the warpgroup ----------
@@ -652,7 +650,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     stamp(5);
   }
   tc_fence_before();
-  named_sync2(kGqCons + 32);  // with the MMA warp: TMEM may be freed
+  named_sync2(kGqTmemUsers);  // with the widening and MMA warps: TMEM may be freed
 }
 
 }  // namespace attn
