@@ -119,8 +119,18 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
     if constexpr (ASYM) wv[i] *= chs[ord16<BITS>(i)];
     m = fmaxf(m, fabsf(wv[i]));
   }
-  if (live) atomicMax(&wmax[h][a][grp], __float_as_uint(m));
+  {  // per-group column maxima: warp reductions (a warp = 32 bond rows of one column), then
+     // one shared atomic per warp and group instead of 32 contending ones
+    const unsigned mu = live ? __float_as_uint(m) : 0u;
+    const unsigned m0 = __reduce_max_sync(0xffffffffu, grp == 0 ? mu : 0u);
+    const unsigned m1 = __reduce_max_sync(0xffffffffu, grp == 1 ? mu : 0u);
+    if ((threadIdx.x & 31) == 0) {
+      if (m0) atomicMax(&wmax[h][a][0], m0);
+      if (m1) atomicMax(&wmax[h][a][1], m1);
+    }
+  }
   __syncthreads();
+  int wtot = 0;  // this thread's share of beta
   if (live) {
     // the tcgen05 paths split both limbs signed: one bit of headroom keeps the hi limb in s8
     const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a][grp]), kWBits<BITS> - headroom);
@@ -142,8 +152,15 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
     uint4* wout = reinterpret_cast<uint4*>(img);
     wout[w_chunk(h, 0, r, rr, a, args.path)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     wout[w_chunk(h, 1, r, rr, a, args.path)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    if (ASYM) atomicAdd(&meta.beta[h][a][grp], wsum);
-    else if (X) atomicAdd(&meta.beta[h][a][grp], X * wsum);
+    wtot = ASYM ? wsum : X * wsum;
+  }
+  if (ASYM || X) {  // beta per group: warp sums, one shared atomic per warp and group
+    const int b0 = __reduce_add_sync(0xffffffffu, grp == 0 ? wtot : 0);
+    const int b1 = __reduce_add_sync(0xffffffffu, grp == 1 ? wtot : 0);
+    if ((threadIdx.x & 31) == 0) {
+      if (b0) atomicAdd(&meta.beta[h][a][0], b0);
+      if (b1) atomicAdd(&meta.beta[h][a][1], b1);
+    }
   }
   __syncthreads();
   if (tid < G * 16 && ((tid >> 1) & 7) / (8 / kPrepSplit) == (int)blockIdx.y) {  // this CTA's columns
