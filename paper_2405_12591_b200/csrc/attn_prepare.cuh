@@ -57,9 +57,9 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
   __shared__ WMeta<G> meta;
   // the dependent split kernel may start its prologue (barriers, code copies) right away;
   // q may come from the previous kernel in the stream (launched with programmatic
-  // serialization, this grid can be scheduled before that kernel finished)
+  // serialization, this grid can be scheduled before that kernel finished): the segment
+  // table and G0k (written at prefill) are loaded before waiting for it, q after
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int s = blockIdx.x;
   const int tid = threadIdx.x;
   constexpr int kA = 8 / kPrepSplit;
@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
     g_lo = g0k[2 * (a * r + rr)];
     g_hi = g0k[2 * (a * r + rr) + 1];
   }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   for (int i = tid; i < G * 128; i += kPrepThreadsOf<G>) {
     const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)seg.unit * G * 128;
     q[i / 128][i % 128] = __half2float(qh[i]);
@@ -185,18 +186,16 @@ __global__ void __launch_bounds__(kPrepGqThreads, 2) attn_prepare_gqa_kernel(dq_
   __shared__ unsigned wmax[G][8];
   __shared__ int bsum[G][8];
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const int rr = tid >> 3, a = tid & 7;
   const dq_segment& seg = args.segs[s];
   const int r = seg.r;
   const bool live = rr < r;
-  const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)seg.unit * G * 128;
-  for (int i = tid; i < G * 128; i += kPrepGqThreads) q[i / 128][i % 128] = __half2float(qh[i]);
   if (tid < G * 8) {
     (&wmax[0][0])[tid] = 0u;
     (&bsum[0][0])[tid] = 0;
   }
+  // the segment table and G0k (written at prefill) before waiting for the previous kernel
   float gk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (live) {
     const float4* g0k = reinterpret_cast<const float4*>(seg.k_g0);  // fp32 [a][rr][c], normalised
@@ -204,6 +203,9 @@ __global__ void __launch_bounds__(kPrepGqThreads, 2) attn_prepare_gqa_kernel(dq_
     gk[0] = g_lo.x, gk[1] = g_lo.y, gk[2] = g_lo.z, gk[3] = g_lo.w;
     gk[4] = g_hi.x, gk[5] = g_hi.y, gk[6] = g_hi.z, gk[7] = g_hi.w;
   }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // q may come from the previous kernel
+  const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)seg.unit * G * 128;
+  for (int i = tid; i < G * 128; i += kPrepGqThreads) q[i / 128][i % 128] = __half2float(qh[i]);
   __syncthreads();
   unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
   uint4* wout = reinterpret_cast<uint4*>(img);
