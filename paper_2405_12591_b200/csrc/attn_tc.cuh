@@ -29,7 +29,11 @@ namespace dq {
 namespace attn {
 
 constexpr int kTcStages = 10;                        // 10 x 16 KB ring, one CTA per SM
-constexpr int kTcWarps = kWarps + 2;                 // + producer (8) + MMA (9)
+constexpr int kTcWide = 8;                           // widening warpgroups (warps 8 .. 15)
+constexpr int kTcProducer = kWarps + kTcWide;        // producer warp (12), then the MMA warp (13)
+constexpr int kTcMma = kTcProducer + 1;
+constexpr int kTcWarps = kWarps + kTcWide + 2;
+constexpr int kTcTmemUsers = (kWarps + kTcWide + 1) * 32;  // threads that touch TMEM (final barrier)
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTmemCols = 512;
 // TMEM column map: 2 A buffers of 64 columns, S (64), Y (8 M-blocks x 32: P limbs hi / mid /
@@ -145,13 +149,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kWarps);
+      mbar_init(&sm.empty[s], kTcWide);
     }
     for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.descfull[s], 1);
     mbar_init(&sm.wbar, 1);
     mbar_init(&sm.g0bar, 1);
     for (int b = 0; b < kNumA; ++b) {
-      mbar_init(&sm.afull[b], kWarps);
+      mbar_init(&sm.afull[b], kTcWide);
       mbar_init(&sm.afree[b], 1);
     }
     mbar_init(&sm.sfull, 1);
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     mbar_init(&sm.yfree, kWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == kWarps + 1) {
+  if (warp == kTcMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
 
-  if (warp == kWarps) {
+  if (warp == kTcProducer) {
     // ---- producer: descriptors and code stages of this CTA's items (as path 0) -------------
     if (lane == 0) {
       SubItem nd;
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     return;
   }
 
-  if (warp == kWarps + 1) {
+  if (warp == kTcMma) {
     // ---- MMA warp: the whole (converged) warp runs the schedule with warp-uniform operands;
     // one elected lane issues each UMMA / commit (operands stay in uniform registers)
     uint32_t lead;
@@ -287,11 +291,87 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
       if (leader) tc_commit(&sm.vdone);
       __syncwarp();
     }
-    // wait for the consumers' last TMEM reads, then free TMEM
+    // wait for the other warps' last TMEM accesses, then free TMEM
     __syncwarp();
-    named_sync2(kThreads + 32);
+    named_sync2(kTcTmemUsers);
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    return;
+  }
+
+  if (warp >= kWarps) {
+    // ---- widening warpgroup: every K and V stage, in ring order, into the TMEM A buffers ----
+    // (warp & 3 = its TMEM lane quadrant).  S and Y have their own TMEM columns, so it runs
+    // ahead into the next item's K stages while the consumer warps do this item's softmax and
+    // fold.
+    const int q = warp & 3;
+    const int wwg = (warp - kWarps) >> 2;  // K: M-block wwg; V: M-blocks 2 wwg, 2 wwg + 1
+    const int lane_in = 32 * q + lane;
+    const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+    const int swz = (16 / 4);  // ktile swizzle unit at 4 bits: (rr & 3) * 4
+    int st = 0, na = 0;
+    for (int j = 0;; ++j) {
+      mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+      const SubItem d = sm.sub[j % kSubRing];
+      if (d.nbt == 0) break;
+      const int nbt = d.nbt, nmb = (nbt + 1) / 2, r = d.r;
+      for (int ks = 0; ks < d.stages; ++ks, ++st, ++na) {
+        const int slot = st % kTcStages, ab = na % kNumA;
+        mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
+        if (na >= kNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kNumA - 1) & 1));
+        if (ks < d.nK) {  // K stage: RK bond rows of rows b = 128 mb + lane_in of each M-block
+          const int rk0 = ks * d.RK, nr = min(d.RK, r - rk0);
+          for (int mb = wwg; mb < nmb; mb += 2) {
+            const int jt = 2 * mb + (q >> 1), b_in = 32 * (q & 1) + lane;
+            const unsigned char* tile = sm.ring[slot] + jt * nr * kI2Pad * RB;
+            const bool live = jt < nbt;
+            for (int r4 = 0; r4 < nr; r4 += 4) {
+              uint32_t v[16];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int rl = r4 + i, rr = rk0 + rl;
+                uint32_t o[4] = {0, 0, 0, 0};
+                if (live) {
+                  const uint2 w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ ((rr & 3) * swz))) * RB);
+                  o[0] = w2.x & 0x0F0F0F0Fu;
+                  o[1] = (w2.x >> 4) & 0x0F0F0F0Fu;
+                  o[2] = w2.y & 0x0F0F0F0Fu;
+                  o[3] = (w2.y >> 4) & 0x0F0F0F0Fu;
+                }
+                v[4 * i] = o[0], v[4 * i + 1] = o[1], v[4 * i + 2] = o[2], v[4 * i + 3] = o[3];
+              }
+              tc_st16(tmem + lane_addr + kColA + (uint32_t)(ab * 64 + mb * d.RK * 4 + r4 * 4), v);
+            }
+          }
+        } else {  // V stage (tile, 32-bond-row slice): rows (r_local * 16 + e) = 128 mb4 + lane_in
+          const unsigned char* buf = sm.ring[slot];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int mb4 = 2 * wwg + i;
+            const int rho = mb4 * 128 + lane_in;
+            const uint4 c0 = *reinterpret_cast<const uint4*>(buf + rho * 32);
+            const uint4 c1 = *reinterpret_cast<const uint4*>(buf + rho * 32 + 16);
+            const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            uint32_t v[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              v[2 * k] = wv[k] & 0x0F0F0F0Fu;
+              v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
+            }
+            tc_st16(tmem + lane_addr + kColA + (uint32_t)(ab * 64 + mb4 * 16), v);
+          }
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&sm.afull[ab]);
+          mbar_arrive(&sm.empty[slot]);
+        }
+      }
+    }
+    tc_fence_before();
+    named_sync2(kTcTmemUsers);
     return;
   }
 
@@ -300,7 +380,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
   const int half = warp >> 2;          // K phase: M-block; V phase: M-blocks 2*half, 2*half+1
   const int lane_in = 32 * q + lane;   // TMEM lane (row inside an M-block)
   const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-  int st = 0, na = 0;
   if (warp < 4) {  // the constant all-ones A operand (K = 32 bytes of 1) used to sum P
     uint32_t ones[16];
 #pragma unroll
@@ -308,11 +387,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     tc_st16(tmem + lane_addr + kColOnes, ones);  // 16 columns: the 8 used + 8 spare
     tc_wait_st();
   }
-  auto release = [&](int s) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[s % kTcStages]);
-  };
-
   if (tid == 0) {
     mbar_wait(&sm.descfull[0], 0);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -337,42 +411,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
       bulk_g2s(sm.g0v, d.vg0, gb, &sm.g0bar);
     }
 
-    // ---- K phase: widen the K codes of each stage into TMEM (this thread = one b row) -------
-    const int jt = 2 * half + (q >> 1);           // tile of this thread's row
-    const int b_in = 32 * (q & 1) + lane;         // row inside the tile
-    const int swz = (16 / 4);                     // ktile swizzle unit at 4 bits: (rr & 3) * 4
-    for (int ks = 0; ks < d.nK; ++ks, ++st, ++na) {
-      const int slot = st % kTcStages, ab = na % kNumA;
-      mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
-      if (na >= kNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kNumA - 1) & 1));
-      const int rk0 = ks * d.RK, nr = min(d.RK, r - rk0);
-      if (half < nmb) {
-        const unsigned char* tile = sm.ring[slot] + jt * nr * kI2Pad * RB;
-        const bool live = jt < nbt;
-        for (int r4 = 0; r4 < nr; r4 += 4) {
-          uint32_t v[16];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int rl = r4 + i, rr = rk0 + rl;
-            uint32_t o[4] = {0, 0, 0, 0};
-            if (live) {
-              const uint2 w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ ((rr & 3) * swz))) * RB);
-              o[0] = w2.x & 0x0F0F0F0Fu;
-              o[1] = (w2.x >> 4) & 0x0F0F0F0Fu;
-              o[2] = w2.y & 0x0F0F0F0Fu;
-              o[3] = (w2.y >> 4) & 0x0F0F0F0Fu;
-            }
-            v[4 * i] = o[0], v[4 * i + 1] = o[1], v[4 * i + 2] = o[2], v[4 * i + 3] = o[3];
-          }
-          tc_st16(tmem + lane_addr + kColA + (uint32_t)(ab * 64 + half * d.RK * 4 + r4 * 4), v);
-        }
-        tc_wait_st();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.afull[ab]);
-      release(st);
-    }
+    // this thread's row b: tile jt, row b_in inside it (the widening warps fill the A buffers)
+    const int jt = 2 * half + (q >> 1);
+    const int b_in = 32 * (q & 1) + lane;
     stamp(1);
 
     // ---- S from TMEM, softmax of the item -----------------------------------------------------
@@ -442,33 +483,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     if (tid == 0) mbar_arrive(&sm.pfull);
     stamp(2);
 
-    // ---- V phase: widen V codes into TMEM; Y accumulates over the item in TMEM -----------------
-    for (int t = 0; t < nbt; ++t)
-      for (int sl = 0; sl < 2; ++sl, ++st, ++na) {
-        const int slot = st % kTcStages, ab = na % kNumA;
-        mbar_wait(&sm.full[slot], (uint32_t)((st / kTcStages) & 1));
-        if (na >= kNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kNumA - 1) & 1));
-        const unsigned char* buf = sm.ring[slot];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int rho = (2 * half + i) * 128 + lane_in;  // row (r_local * 16 + e) of the stage
-          const uint4 c0 = *reinterpret_cast<const uint4*>(buf + rho * 32);
-          const uint4 c1 = *reinterpret_cast<const uint4*>(buf + rho * 32 + 16);
-          const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          uint32_t v[16];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            v[2 * k] = wv[k] & 0x0F0F0F0Fu;
-            v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
-          }
-          tc_st16(tmem + lane_addr + kColA + (uint32_t)(ab * 64 + (2 * half + i) * 16), v);
-        }
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.afull[ab]);
-        release(st);
-      }
     // Y (thread rows: slice sl, M-block 2*half + i: (r, e) = (32 sl + 8 (2 half + i) + lane_in / 16,
     // lane_in % 16)) and sum_b P, once per item
     mbar_wait(&sm.vdone, (uint32_t)(j & 1));
@@ -546,7 +560,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
     stamp(5);
   }
   tc_fence_before();
-  named_sync2(kThreads + 32);  // with the MMA warp: TMEM may be freed
+  named_sync2(kTcTmemUsers);  // with the widening and MMA warps: TMEM may be freed
 }
 
 }  // namespace attn
