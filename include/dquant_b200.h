@@ -241,6 +241,20 @@ int dq_decode_attention(const dq_attn_args* h_args, void* stream);
 int dq_tail_append(const uint16_t* k_rows, const uint16_t* v_rows, int32_t units, uint16_t* tail_k,
                    uint16_t* tail_v, int32_t* tail_len, int32_t tail_cap, void* stream);
 
+/* ---- decode-harness kernels (no reference counterpart: the reference
+ * has no model, its toy analogue is kvcache.py:234-309).  The elementwise work around the
+ * cuBLAS projections of model.py's LLaMA-shaped decoder; all tensors bf16 (uint16_t) unless
+ * stated, row-major, device pointers. */
+/* x_out = x + y (skipped when y is NULL: x is the residual as is), h = RMSNorm(x_out) * w */
+int dq_model_add_rmsnorm(const uint16_t* x, const uint16_t* y, const uint16_t* w, uint16_t* x_out, uint16_t* h,
+                         int32_t rows, int32_t hidden, float eps, void* stream);
+/* fused QKV rows (batch, (heads + 2 kv_heads) * 128) -> rotary q (batch, heads, 128) fp16,
+ * rotary k and plain v (batch, kv_heads, 128) fp16, at decode position *pos (device int64) */
+int dq_model_qkv_rope(const uint16_t* qkv, int32_t batch, int32_t heads, int32_t kv_heads, const int64_t* pos,
+                      float theta, uint16_t* q, uint16_t* k, uint16_t* v, void* stream);
+/* SwiGLU: gate_up rows (rows, 2 ffn) = [gate | up] -> out (rows, ffn) = silu(gate) * up */
+int dq_model_silu_mul(const uint16_t* gate_up, int32_t rows, int32_t ffn, uint16_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -143,6 +143,11 @@ SIGNATURES = {
     "dq_decode_attention": (c_int32, [POINTER(AttnArgs), c_void_p]),
     "dq_attention_wimg_bytes": (c_int32, [c_int32, POINTER(c_int64)]),
     "dq_tail_append": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
+    "dq_model_add_rmsnorm": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_float,
+                                       c_void_p]),
+    "dq_model_qkv_rope": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_float, c_void_p, c_void_p,
+                                    c_void_p, c_void_p]),
+    "dq_model_silu_mul": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
 }
 
 _LIB = None

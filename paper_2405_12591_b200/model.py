@@ -7,7 +7,9 @@ Random-init weights (std 0.02, bf16) of the named shapes; one decode step per ca
 
 The attention of every layer is ``DecodeKvCache.attend(layer, q, append=(k, v))``: the new
 token's K/V join the fp16 tail and the compressed segments are read by the fused kernels.
-Dense projections are cuBLAS GEMMs through torch (library code, as the task allows); the step
+Dense projections are cuBLAS GEMMs through torch (library code, as the task allows); the
+elementwise work between them is three fused kernels of the C ABI (csrc/model.cu: residual
+add + RMSNorm, QKV split + RoPE + fp16 cast, SwiGLU), so a layer is ten launches; the step
 is capturable in one CUDA graph (``capture()`` / ``replay()``).  Tensor parallelism across
 GPUs shards the KV heads (``sharding.py``); this harness runs the single-GPU shard.
 """
@@ -19,6 +21,7 @@ from dataclasses import dataclass
 
 import torch
 
+from ._lib import check, lib, ptr, stream_ptr
 from .attention import DecodeKvCache
 from .errors import ShapeMismatch
 
@@ -104,28 +107,47 @@ class DecoQuantLM:
             self.cache.prefill(layer, k, v)
         self.pos.fill_(tokens)
 
-    def _layer(self, i: int, x: torch.Tensor) -> torch.Tensor:
+    # ---- fused harness kernels (csrc/model.cu); _rms / _rope above are their torch statements
+    def _norm(self, x: torch.Tensor, y: torch.Tensor | None, w: torch.Tensor) -> torch.Tensor:
+        """x += y in place (y None: x as is); returns RMSNorm(x) * w."""
+        h = torch.empty_like(x)
+        check(lib().dq_model_add_rmsnorm(x.data_ptr(), ptr(y), w.data_ptr(), x.data_ptr(), h.data_ptr(),
+                                         x.shape[0], x.shape[1], 1e-5, stream_ptr()), "add_rmsnorm")
+        return h
+
+    def _qkv_rope(self, qkv: torch.Tensor):
+        s, B = self.shape, self.batch
+        q = torch.empty((B * s.kv_heads, s.g, 128), dtype=torch.float16, device=self.dev)
+        k = torch.empty((B * s.kv_heads, 128), dtype=torch.float16, device=self.dev)
+        v = torch.empty_like(k)
+        check(lib().dq_model_qkv_rope(qkv.data_ptr(), B, s.heads, s.kv_heads, self.pos.data_ptr(), 10000.0,
+                                      q.data_ptr(), k.data_ptr(), v.data_ptr(), stream_ptr()), "qkv_rope")
+        return q, k, v
+
+    def _silu_mul(self, gu: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((gu.shape[0], gu.shape[1] // 2), dtype=gu.dtype, device=self.dev)
+        check(lib().dq_model_silu_mul(gu.data_ptr(), gu.shape[0], gu.shape[1] // 2, out.data_ptr(), stream_ptr()),
+              "silu_mul")
+        return out
+
+    def _layer(self, i: int, x: torch.Tensor, y: torch.Tensor | None) -> torch.Tensor:
+        """Layer i on the residual x (updated in place) whose previous layer's MLP output y has not
+        been added yet (it is fused into this layer's first norm); returns this layer's MLP output."""
         s, L, B = self.shape, self.layers[i], self.batch
-        h = _rms(x, L["ln1"])
-        qkv = h @ L["qkv"]
-        q, k, v = qkv.split([s.heads * 128, s.kv_heads * 128, s.kv_heads * 128], dim=-1)
-        q = _rope(q.view(B, s.heads, 128), self.pos)
-        k = _rope(k.view(B, s.kv_heads, 128), self.pos)
+        h = self._norm(x, y, L["ln1"])
+        q, k, v = self._qkv_rope(h @ L["qkv"])
         # units = (sequence, kv head); query heads kv * g .. kv * g + g - 1 share a kv head
-        att = self.cache.attend(i, q.reshape(B * s.kv_heads, s.g, 128).to(torch.float16),
-                                append=(k.reshape(B * s.kv_heads, 128).to(torch.float16),
-                                        v.reshape(B * s.kv_heads, 128).to(torch.float16)))
-        x = x + att.reshape(B, s.heads * 128).to(torch.bfloat16) @ L["o"]
-        h = _rms(x, L["ln2"])
-        gate, up = (h @ L["gate_up"]).chunk(2, dim=-1)
-        return x + (torch.nn.functional.silu(gate) * up) @ L["down"]
+        att = self.cache.attend(i, q, append=(k, v))
+        h = self._norm(x, att.view(B, s.heads * 128).to(torch.bfloat16) @ L["o"], L["ln2"])
+        return self._silu_mul(h @ L["gate_up"]) @ L["down"]
 
     def step(self, tokens: torch.Tensor) -> torch.Tensor:
         """One decode step: tokens (batch,) int64 -> next tokens (batch,) (greedy)."""
         x = self.embed[tokens]
+        y = None
         for i in range(self.shape.layers):
-            x = self._layer(i, x)
-        logits = _rms(x, self.norm) @ self.lm_head
+            y = self._layer(i, x, y)
+        logits = self._norm(x, y, self.norm) @ self.lm_head
         self.pos.add_(1)
         return logits.argmax(-1)
 

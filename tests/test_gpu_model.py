@@ -82,3 +82,78 @@ def test_captured_step_matches_eager():
         assert torch.equal(tok_e, tok_g)
     assert eager.cache.tokens(0) == graphed.cache.tokens(0) == 605
     assert torch.equal(eager.cache.tail_len, graphed.cache.tail_len)
+
+
+def _bf16_ulps(a: torch.Tensor, b: torch.Tensor) -> int:
+    """Largest distance in bf16 units in the last place (ordered-integer view)."""
+    ia, ib = (t.contiguous().view(torch.int16).to(torch.int32) for t in (a, b))
+    ia = torch.where(ia < 0, -32768 - ia, ia)
+    ib = torch.where(ib < 0, -32768 - ib, ib)
+    return int((ia - ib).abs().max())
+
+
+@pytest.mark.parametrize("hidden,with_y", [(4096, True), (5120, False), (8192, True), (256, True)])
+def test_add_rmsnorm_kernel_matches_torch(hidden, with_y):
+    """dq_model_add_rmsnorm vs model._rms(x + y): the residual sum is bit-exact, the normalised
+    row within one bf16 ulp (only the fp32 sum-of-squares order differs)."""
+    from paper_2405_12591_b200 import model as M
+
+    g = torch.Generator(device="cuda").manual_seed(hidden)
+    x = torch.randn((16, hidden), generator=g, device="cuda").to(torch.bfloat16)
+    y = torch.randn((16, hidden), generator=g, device="cuda").to(torch.bfloat16) if with_y else None
+    w = (1 + 0.1 * torch.randn(hidden, generator=g, device="cuda")).to(torch.bfloat16)
+    ref_x = x + y if with_y else x.clone()
+    ref_h = M._rms(ref_x, w)
+    lm = M.DecoQuantLM.__new__(M.DecoQuantLM)
+    h = M.DecoQuantLM._norm(lm, x, y, w)
+    assert torch.equal(x, ref_x)
+    assert _bf16_ulps(h, ref_h) <= 1
+
+
+@pytest.mark.parametrize("heads,kv_heads,pos", [(32, 32, 4096), (64, 8, 16384), (4, 2, 0)])
+def test_qkv_rope_kernel_matches_torch(heads, kv_heads, pos):
+    """dq_model_qkv_rope vs model._rope on the split QKV row: v bit-exact, q/k within one bf16
+    ulp (cos/sin/pow of the device libm vs torch's kernels)."""
+    from paper_2405_12591_b200 import model as M
+
+    B = 5
+    shape = M.ModelShape(layers=1, hidden=heads * 128, heads=heads, kv_heads=kv_heads, ffn=256)
+    g = torch.Generator(device="cuda").manual_seed(heads)
+    qkv = torch.randn((B, (heads + 2 * kv_heads) * 128), generator=g, device="cuda").to(torch.bfloat16)
+    p = torch.tensor(pos, dtype=torch.int64, device="cuda")
+    lm = M.DecoQuantLM.__new__(M.DecoQuantLM)
+    lm.shape, lm.batch, lm.dev, lm.pos = shape, B, torch.device("cuda"), p
+    q, k, v = lm._qkv_rope(qkv)
+    rq, rk, rv = qkv.split([heads * 128, kv_heads * 128, kv_heads * 128], dim=-1)
+    rq = M._rope(rq.reshape(B, heads, 128), p).reshape(B * kv_heads, heads // kv_heads, 128)
+    rk = M._rope(rk.reshape(B, kv_heads, 128), p).reshape(B * kv_heads, 128)
+    assert torch.equal(v, rv.reshape(B * kv_heads, 128).to(torch.float16))
+    assert _bf16_ulps(q.to(torch.bfloat16), rq) <= 1
+    assert _bf16_ulps(k.to(torch.bfloat16), rk) <= 1
+    assert q.dtype == k.dtype == torch.float16
+
+
+def test_silu_mul_kernel_matches_torch():
+    from paper_2405_12591_b200 import model as M
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    gu = (4 * torch.randn((16, 2 * 11008), generator=g, device="cuda")).to(torch.bfloat16)
+    lm = M.DecoQuantLM.__new__(M.DecoQuantLM)
+    lm.dev = torch.device("cuda")
+    out = lm._silu_mul(gu)
+    gate, up = gu.chunk(2, dim=-1)
+    assert _bf16_ulps(out, torch.nn.functional.silu(gate) * up) <= 1
+
+
+def test_harness_kernels_reject_bad_shapes():
+    from paper_2405_12591_b200._lib import lib
+    from paper_2405_12591_b200.errors import ShapeMismatch
+    from paper_2405_12591_b200._lib import check
+
+    x = torch.zeros((2, 12), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ShapeMismatch):
+        check(lib().dq_model_add_rmsnorm(x.data_ptr(), None, x.data_ptr(), x.data_ptr(), x.data_ptr(), 2, 12,
+                                         1e-5, None))
+    with pytest.raises(ShapeMismatch):
+        check(lib().dq_model_qkv_rope(x.data_ptr(), 1, 3, 2, x.data_ptr(), 1e4, x.data_ptr(), x.data_ptr(),
+                                      x.data_ptr(), None))
