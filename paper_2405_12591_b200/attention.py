@@ -312,9 +312,18 @@ class DecodeKvCache:
         # the largest items: the per-item cost (W image, softmax, epilogue) is fixed, and
         # smaller items measured slower even where they shorten the scheduler's last round.
         # 2-bit codes carry half the bytes per row, so their items are 512 rows (C3: 0.387 ->
-        # 0.453 of HBM); at 4 bits 512-row items measured slower (0.630 -> 0.597)
+        # 0.453 of HBM).  At 4 bits 512-row items win only where the 256-row plan needs 1.5 to 2
+        # rounds of the persistent grid, so that halving the item count fills one round
+        # (scripts/chunk_sweep.py: 32 units x 32K 45.7 -> 40.9 us, 256 x 4K 45.9 -> 43.1 us);
+        # with fewer items the grid idles (16 x 32K: 26.9 -> 37.7 us) and with more the
+        # fixed cost saved does not repay the coarser last round (512 x 4K: 74.3 -> 79.1 us)
+        path0 = gk == 1 and not (self.tc and self.bits == 4 and full_plans)
         chunk_b = self.chunk_b or (MAX_CHUNK_B if self.bits == 2 and gk == 1 else DEFAULT_CHUNK_B)
         wp = plan_work(seg_arr, nseg, vunits, chunk_b)
+        if (self.chunk_b is None and self.bits == 4 and path0 and not self.asym
+                and 1.5 * ctas <= wp.nwork <= 2 * ctas):
+            chunk_b = MAX_CHUNK_B
+            wp = plan_work(seg_arr, nseg, vunits, chunk_b)
         if hg > 1:  # a tile range's head groups back to back in the ticket order (L2 reuse)
             order = sorted(range(wp.nwork), key=lambda i: (wp.work[3 * i] // hg, wp.work[3 * i + 1],
                                                            wp.work[3 * i] % hg))
