@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Split-kernel work-item size sweep: mean attention time per layer (prepare + split + combine,
 CUDA events, layers cycled so the compressed cache exceeds L2) for each (units, T, bits) case
-and chunk_b in CHUNKS.
+and chunk_b in CHUNKS (0: the automatic plan).
 
     CASES="32x32768x4,16x32768x4,512x4096x4" CHUNKS=256,512 python scripts/chunk_sweep.py
 """
@@ -19,7 +19,7 @@ for units, T, bits in cases:
     per_layer = units * T * 128 * 2 * bits / 8
     layers = max(2, int(4 * 126e6 / per_layer) + 1)
     for cb in chunks:
-        cache = DecodeKvCache(layers=layers, units=units, g=1, bits=bits, chunk_len=1024, chunk_b=cb)
+        cache = DecodeKvCache(layers=layers, units=units, g=1, bits=bits, chunk_len=1024, chunk_b=cb or None)
         gen = torch.Generator(device="cuda").manual_seed(0)
         for layer in range(layers):
             k = torch.randn((units, T, 128), generator=gen, device="cuda").half()
