@@ -83,7 +83,7 @@ struct AttnSmem {
   // V phase + epilogue (aliased, W is dead): fp32 G0v [a][rr][c] by TMA
   union {
     uint4 w[G * 2 * kMaxR * 8];
-    float4 g0v[8 * kMaxR * 2];
+    float4 g0v[8 * (kMaxR * 2 + 1)];  // [a][rr][c] with a 16-byte pad per a (kG0vPad)
   } wg;
   // V phase: P limbs [((h*2 + limb)*8 + a)*(4 NT) + (bg ^ 4*(a&1))];
   // epilogue (aliased, P is dead): cross-warp reduction of the O partial
@@ -281,10 +281,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     auto wstamp = [&](int) {};
 #endif
     stamp(0);
+#ifndef DQ_ATTN_WARP_TRACE  // slots 6 and 7 of the per-item trace (the per-warp trace uses them)
     if (args.trace && tid == 0) {
       args.trace[(size_t)wi * 8 + 6] = blockIdx.x;
       args.trace[(size_t)wi * 8 + 7] = sm_id();
     }
+#endif
     mbar_wait(&sm.wbar, (uint32_t)(j & 1));
 
     stamp(1);
@@ -419,7 +421,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       const uint32_t cb = ASYM ? (uint32_t)(2 * r * 16 * 4) : 0u;
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_expect_tx(&sm.g0bar, gb + cb);
-      bulk_g2s(sm.wg.g0v, d.vg0, gb, &sm.g0bar);
+      // one copy per a into blocks of 2r + 1 float4s: the epilogue's lanes tid4 = 0..3 read
+      // a = 2 tid4 + aa, and the pad puts their blocks 32 bytes apart in the banks (an
+      // unpadded 2r-float4 stride maps all four onto the same banks: a 4-way conflict per load)
+      for (int a = 0; a < i1; ++a)
+        bulk_g2s(sm.wg.g0v + a * (2 * r + 1), reinterpret_cast<const float4*>(d.vg0) + a * 2 * r, (uint32_t)(r * 32),
+                 &sm.g0bar);
       if (ASYM) bulk_g2s(sm.vch, args.segs[d.seg].v_ch, cb, &sm.g0bar);
     }
     unsigned char* pb = reinterpret_cast<unsigned char*>(sm.pr.p);
@@ -579,6 +586,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
     mbar_wait(&sm.g0bar, (uint32_t)(j & 1));  // fp32 G0v [a][rr][c] (normalised), in the W buffer
     const float4* g0v = sm.wg.g0v;
+#ifdef DQ_ATTN_NULL_FOLD  // measurement only: no G0v fold (wrong results), Y still consumed
+#pragma unroll
+    for (int t = 0; t < kRw; ++t)
+#pragma unroll
+      for (int h = 0; h < G; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) part[h][(t * 4 + k) & 15] += accv[t][h][k];
+    if (tid < 0)
+#endif
 #pragma unroll
     for (int t = 0; t < kRw; ++t) {
       if (t < rw) {
@@ -589,7 +605,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         for (int aa = 0; aa < 2; ++aa) {
           const int a = 2 * tid4 + aa;
           if (a < i1) {
-            const float4 g_lo = g0v[2 * (a * r + rr)], g_hi = g0v[2 * (a * r + rr) + 1];
+            const float4 g_lo = g0v[a * (2 * r + 1) + 2 * rr], g_hi = g0v[a * (2 * r + 1) + 2 * rr + 1];
             const float gc[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
 #pragma unroll
             for (int h = 0; h < G; ++h) {
