@@ -416,18 +416,20 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     }
     named_sync(kThreads);  // every warp is past phase 1: the W buffer is dead
     wstamp(2);
-    if (tid == 0) {   // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
-      const uint32_t gb = (uint32_t)(i1 * r * 32);
+    if (lane == 0 && warp < i1) {  // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
+      // one copy per a, issued by warp a, into blocks of 2r + 1 float4s: the epilogue's lanes
+      // tid4 = 0..3 read a = 2 tid4 + aa, and the pad puts their blocks 32 bytes apart in the
+      // banks (an unpadded 2r-float4 stride maps all four onto the same banks: a 4-way
+      // conflict per load, 10 us of a C2 layer).  A copy completing before warp 0's expect_tx
+      // only takes the transaction count negative; the phase needs that arrival.
       const uint32_t cb = ASYM ? (uint32_t)(2 * r * 16 * 4) : 0u;
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_expect_tx(&sm.g0bar, gb + cb);
-      // one copy per a into blocks of 2r + 1 float4s: the epilogue's lanes tid4 = 0..3 read
-      // a = 2 tid4 + aa, and the pad puts their blocks 32 bytes apart in the banks (an
-      // unpadded 2r-float4 stride maps all four onto the same banks: a 4-way conflict per load)
-      for (int a = 0; a < i1; ++a)
-        bulk_g2s(sm.wg.g0v + a * (2 * r + 1), reinterpret_cast<const float4*>(d.vg0) + a * 2 * r, (uint32_t)(r * 32),
-                 &sm.g0bar);
-      if (ASYM) bulk_g2s(sm.vch, args.segs[d.seg].v_ch, cb, &sm.g0bar);
+      if (warp == 0) {
+        mbar_expect_tx(&sm.g0bar, (uint32_t)(i1 * r * 32) + cb);
+        if (ASYM) bulk_g2s(sm.vch, args.segs[d.seg].v_ch, cb, &sm.g0bar);
+      }
+      bulk_g2s(sm.wg.g0v + warp * (2 * r + 1), reinterpret_cast<const float4*>(d.vg0) + warp * 2 * r,
+               (uint32_t)(r * 32), &sm.g0bar);
     }
     unsigned char* pb = reinterpret_cast<unsigned char*>(sm.pr.p);
     // P = exp2(s - m) in fixed point with one scale per (h, a, 64-row tile), set by that
