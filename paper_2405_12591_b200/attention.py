@@ -35,6 +35,7 @@ from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_
 
 HEAD_DIM = 128
 DEFAULT_CHUNK_B = 256
+TAIL_SPLIT = 0.2  # fraction of the persistent grid whose last 512-row items are halved (split_tail)
 MAX_CHUNK_B = 512  # > 256: 8-tile items, mma.sync split kernel with g = 1 and 2- / 4-bit codes
 KERNEL_G = (1, 2, 8)  # query heads per kv head the split kernels are instantiated for (8: tcgen05 only)
 GQA_G = 8             # heads of the tcgen05 GQA kernel (path 2)
@@ -145,6 +146,35 @@ def plan_work(seg_arr, nseg: int, units: int, chunk_b: int) -> WorkPlan:
     check(lib().dq_attention_plan(seg_arr, nseg, units, chunk_b, n, work, ctypes.byref(nwork), wpart, p0, npt,
                                   ctypes.byref(total)), "attention_plan")
     return WorkPlan(n, total.value, list(work)[:3 * n], list(wpart)[:n], list(p0)[:units], list(npt)[:units])
+
+
+def split_tail(wp: WorkPlan, seg_units, nsplit: int) -> WorkPlan:
+    """``wp`` with its last ``nsplit`` items split into two halves each, queued after the
+    others: the scheduler's last round then runs half-length items.  Partial slots are
+    renumbered per unit in work-list order (dq_attention_plan's rule)."""
+    big, small = [], []
+    for i in range(wp.nwork):
+        s, b0, t = wp.work[3 * i: 3 * i + 3]
+        if i < wp.nwork - nsplit or t < 2:
+            big.append((s, b0, t))
+        else:
+            h = t // 2
+            small += [(s, b0, h), (s, b0 + h * 64, t - h)]
+    items = big + small
+    units = len(wp.unit_part0)
+    npt = [0] * units
+    for s, _, _ in items:
+        npt[seg_units[s]] += 1
+    p0, acc = [], 0
+    for u in range(units):
+        p0.append(acc)
+        acc += npt[u]
+    cur = list(p0)
+    wpart = []
+    for s, _, _ in items:
+        wpart.append(cur[seg_units[s]])
+        cur[seg_units[s]] += 1
+    return WorkPlan(len(items), acc, [x for it in items for x in it], wpart, p0, npt)
 
 
 class DecodeKvCache:
@@ -324,6 +354,11 @@ class DecodeKvCache:
                 and 1.5 * ctas <= wp.nwork <= 2 * ctas):
             chunk_b = MAX_CHUNK_B
             wp = plan_work(seg_arr, nseg, vunits, chunk_b)
+        if self.chunk_b is None and chunk_b == MAX_CHUNK_B and path0 and wp.nwork > 2 * ctas:
+            # several rounds of 512-row items: the last TAIL_SPLIT x grid items run as 256-row
+            # halves, evening out the scheduler's last round (C3: 230.2 -> 225.7 us; at 256-row
+            # items the 128-row halves cost more than they save: C2 64.3 -> 68.5 us)
+            wp = split_tail(wp, [sg.unit for sg in segs], int(TAIL_SPLIT * ctas))
         if hg > 1:  # a tile range's head groups back to back in the ticket order (L2 reuse)
             order = sorted(range(wp.nwork), key=lambda i: (wp.work[3 * i] // hg, wp.work[3 * i + 1],
                                                            wp.work[3 * i] % hg))

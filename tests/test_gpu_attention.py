@@ -116,6 +116,26 @@ def test_decode_attention_512_row_items(dq, bits, T, units, scale):
         assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
 
 
+def test_decode_attention_split_tail(dq):
+    """Several rounds of 512-row items (int2): the last TAIL_SPLIT x grid items run as 256-row
+    halves (attention.split_tail); ragged T, results against the oracle."""
+    from paper_2405_12591_b200.attention import TAIL_SPLIT, DecodeKvCache
+
+    rng = np.random.default_rng(7)
+    units, T, ctas = 12, 8000, 10
+    k = rng.standard_normal((units, T, 128)).astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = rng.standard_normal((units, 1, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=2, ctas=ctas)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    a = cache._layers[0].args
+    assert a.chunk_b == 512 and a.nwork == 2 * units + int(TAIL_SPLIT * ctas)
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), 2, [T], 0)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
 @pytest.mark.parametrize("scale,bits", [(20.0, 4), (50.0, 4), (20.0, 2), (20.0, 8)])
 @pytest.mark.parametrize("ctas", [None, 0])  # persistent grid / one CTA per item
 @pytest.mark.parametrize("tc", [False, True])
