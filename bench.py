@@ -215,17 +215,64 @@ def run_reference(args, cfg, world):
 # GPU side
 # ---------------------------------------------------------------------------
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock and throttle-reason sampler running during the timed region.
+
+    NVML (nvidia_ml_py) polled from a thread every 5 ms, with one sample taken as the region
+    opens and one as it closes, so even a ~40 ms region carries several samples; nvidia-smi
+    (-lms 100) is the fallback where NVML is unavailable."""
 
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.nvml = None
+        self.samples = []  # (sm_mhz, max_mhz, set of reason names)
+        self.lines = []
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID("GPU-" + uuid)
+        except Exception:
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [x for x in vis.split(",") if x.strip()]
+            idx = int(ids[self.index]) if ids and ids[self.index].strip().isdigit() else self.index
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+
+    def _sample(self):
+        nv, h = self.nvml
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        masks = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                             float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                             {n for n, m in zip(self.NAMES, masks) if bits & m}))
+
+    def _poll(self):
+        while not self.stop.wait(0.005):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def __enter__(self):
+        import threading
+        try:
+            self.nvml = self._nvml_handle()
+            self._sample()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -235,7 +282,14 @@ class Clocks:
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=1)
+            try:
+                self._sample()
+            except Exception:
+                pass
+            return
         if self.proc is not None:
             time.sleep(0.15)
             self.proc.terminate()
@@ -248,8 +302,11 @@ class Clocks:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
+        for clk, m, rs in self.samples:
+            sm.append(clk)
+            mx = m
+            reasons |= rs
+        for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -258,11 +315,11 @@ class Clocks:
                 mx = float(f[2])
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
+            for n, v in zip(self.NAMES, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sampler": "nvml" if self.samples else "nvidia-smi"}
 
 
 def run_ours(args, cfg):
