@@ -13,18 +13,21 @@
 //   Y[h,a,r,e] = sum_b P[h,a,b] code_v[r,b,e]                  (int8 tensor cores)
 //   O[h,c,e]   = scale_v * sum_{a,r} G0v[a,c,r] Y[h,a,r,e]     (CUDA cores, epilogue)
 //
-// Data movement: a persistent grid of (SMs x resident CTAs) CTAs draws work items
-// (<= 256 rows of one segment, dq_attention_plan; one partial each) from a ticket
-// counter (attn_kernel.cuh).  The packed K codes (DQ_LAYOUT_KTILE) and V codes (DQ_LAYOUT_VTILE) stream through a 3-stage x
-// 16 KB shared-memory ring by cp.async.bulk (TMA bulk copies completing on mbarriers);
-// the last warp to release a stage issues its refill, across sub-item boundaries (3
-// CTAs/SM -> 144 KB in flight per SM, no register cost).  Consumers read bank-conflict-free fragments (K tile rows are
-// XOR-swizzled by r in HBM) and widen codes to bytes (int4: one AND per 4 even codes,
-// one SHF+AND per 4 odd codes).  The codes multiply fixed-point W and P split into two
-// 8-bit limbs (hi*256 + lo) on the int8 tensor pipe (mma.sync m16n8k32, exact s32
-// accumulation); the excess-code offset is removed exactly in integers.  The reduction
-// index is permuted identically on both operands, which is free.  Full-precision K/V
-// never exist anywhere.
+// Data movement (path 0, attn_kernel.cuh): a persistent grid of (SMs x resident CTAs) CTAs
+// draws work items (<= 256 rows of one segment, or 512 for g = 1 with 2- / 4-bit codes;
+// dq_attention_plan; one partial each) from a self-resetting ticket counter.  A producer
+// warp streams the packed K codes (DQ_LAYOUT_KTILE) and V codes (DQ_LAYOUT_VTILE) through a
+// 5-stage x 16 KB shared-memory ring by cp.async.bulk (TMA bulk copies completing on
+// mbarriers), running ahead across item boundaries (2 CTAs/SM -> 160 KB in flight per SM).
+// Eight consumer warps read bank-conflict-free fragments (K tile rows are XOR-swizzled by r
+// in HBM) and widen codes to bytes (int4: one AND per 4 even codes, one SHF+AND per 4 odd
+// codes).  The codes multiply fixed-point W and P split into two 8-bit limbs (hi*256 + lo) on
+// the int8 tensor pipe (mma.sync m16n8k32, exact s32 accumulation); the excess-code offset is
+// removed exactly in integers.  The reduction index is permuted identically on both
+// operands, which is free.  Full-precision K/V never exist anywhere.  Paths 1 and 2
+// (attn_tc.cuh, attn_gqa.cuh) run the same contractions as tcgen05 UMMAs with TMEM
+// accumulators.  The prepare (W image), split and combine kernels are chained with
+// programmatic dependent launch.
 #include "attn_gqa.cuh"
 #include "attn_combine.cuh"
 

@@ -1,5 +1,5 @@
-// Combine step of the fused decode attention (attention.cu): the standalone combine
-// kernel, or the split kernel's last work item of a unit (fused combine).
+// Combine step of the fused decode attention (attention.cu): the partial merge, the dense
+// fp16 tail and the fused append, run by the combine kernels behind the split kernel (PDL).
 #pragma once
 
 #include "attn_frag.cuh"
