@@ -184,7 +184,7 @@ typedef struct dq_segment {
 
 typedef struct dq_attn_args {
   const uint16_t* q;      /* fp16 [units][g][128] (units = virtual units, see head_groups) */
-  uint16_t* out;          /* fp16 [units][g][128] */
+  uint16_t* out;          /* fp16 [units][g][128] (bf16 with out_bf16) */
   const dq_segment* segs; /* device array [nseg] */
   int32_t nseg;
   int32_t units;
@@ -220,7 +220,8 @@ typedef struct dq_attn_args {
   int32_t path;           /* split kernel: 0 = mma.sync (all plans), 1 = tcgen05 (int4, g = 1, r = 64, i1 = 8),
                              2 = tcgen05 GQA (int4, g = 8, r = 64, i1 = 8) */
   int32_t asym;           /* 1: every segment is in the asymmetric per-channel mode (path 0, 2- / 4-bit) */
-  int32_t pad2_;
+  int32_t out_bf16;       /* 1: out is bf16 [units][g][128] instead of fp16 (read directly by a model's bf16
+                             projections; the merged fp32 value is rounded once) */
 } dq_attn_args;
 
 /* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */

@@ -100,7 +100,7 @@ class AttnArgs(ctypes.Structure):
         ("head_groups", c_int32),
         ("path", c_int32),
         ("asym", c_int32),
-        ("pad2_", c_int32),
+        ("out_bf16", c_int32),
     ]
 
 

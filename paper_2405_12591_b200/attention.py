@@ -420,8 +420,10 @@ class DecodeKvCache:
         lay.keep = [seg_dev, work_dev, wpart_dev, sched, p0_dev, np_dev, part_o, part_ml, wimg]
 
     def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None,
-               append: tuple[torch.Tensor, torch.Tensor] | None = None) -> torch.Tensor:
-        """q: (units, g, 128) fp16 CUDA -> (units, g, 128) fp16.
+               append: tuple[torch.Tensor, torch.Tensor] | None = None,
+               out_dtype: torch.dtype = torch.float16) -> torch.Tensor:
+        """q: (units, g, 128) fp16 CUDA -> (units, g, 128) fp16 (or ``out_dtype=torch.bfloat16``:
+        the combine kernel rounds the merged fp32 output to bf16 once, for bf16 projections).
 
         ``append=(k_rows, v_rows)`` (each (units, 128)) fuses ``append_token`` into the same
         launch: the rows join the tail after this attention, exactly as attend + append_token.
@@ -432,11 +434,16 @@ class DecodeKvCache:
         if lay.args is None:
             self._build_args(layer)
         q = q.to(self.device, torch.float16).contiguous()
+        if out_dtype not in (torch.float16, torch.bfloat16):
+            raise Unsupported("out_dtype must be torch.float16 or torch.bfloat16")
         if out is None:
-            out = torch.empty_like(q)
+            out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+        elif out.dtype != out_dtype or out.shape != q.shape or not out.is_contiguous():
+            raise DimMismatch(f"out must be a contiguous {tuple(q.shape)} {out_dtype} tensor")
         a = lay.args
         a.q = q.data_ptr()
         a.out = out.data_ptr()
+        a.out_bf16 = 1 if out_dtype == torch.bfloat16 else 0
         if append is not None:
             k, v = self._rows(*append)
             a.app_k, a.app_v = k.data_ptr(), v.data_ptr()
@@ -444,6 +451,7 @@ class DecodeKvCache:
             check(lib().dq_decode_attention(ctypes.byref(a), stream_ptr()), "decode_attention")
         finally:
             a.app_k = a.app_v = None
+            a.out_bf16 = 0
         self.bytes_moved_read += self.read_bytes(layer)
         if append is not None:
             self._after_append(layer)

@@ -90,7 +90,7 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
 }
 
 // Merge of head h of virtual unit v: its work-item partials plus the tail partial (Mt, Lt, Ot;
-// Mt = -inf without a tail), fp16 output row.  Thread d < 128 owns dim d.
+// Mt = -inf without a tail), fp16 (or bf16: out_bf16) output row.  Thread d < 128 owns dim d.
 template <int G>
 __device__ __forceinline__ void merge_head(const dq_attn_args& args, int v, int h, int d, float Mt, float Lt, float Ot) {
   if (d >= 128) return;
@@ -111,8 +111,10 @@ __device__ __forceinline__ void merge_head(const dq_attn_args& args, int v, int 
     L += f * args.part_ml[s * 2 + 1];
     O += f * args.part_o[s * 128 + d];
   }
-  __half* out = reinterpret_cast<__half*>(args.out) + ((size_t)v * G + h) * 128;
-  out[d] = __float2half_rn(L > 0.f ? O / L : 0.f);
+  const float o = L > 0.f ? O / L : 0.f;
+  const size_t i = ((size_t)v * G + h) * 128 + d;
+  if (args.out_bf16) reinterpret_cast<__nv_bfloat16*>(args.out)[i] = __float2bfloat16_rn(o);  // one rounding
+  else reinterpret_cast<__half*>(args.out)[i] = __float2half_rn(o);
 }
 
 // One head: tail partial then merge (callers that have already waited for the split kernel)

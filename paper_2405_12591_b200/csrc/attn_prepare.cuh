@@ -41,7 +41,10 @@ __device__ __forceinline__ int w_chunk(int h, int limb, int r, int rr, int a, in
 // kPrepSplit CTAs per segment (blockIdx.y: a block of columns a; the W scales are per
 // column, so the blocks are independent), one thread per (h, a, rr) of W (threads beyond i1 / r idle): a
 // single wave of short-lived CTAs (the kernel is pure latency: ~16 KB in, ~16 KB out)
-constexpr int kPrepSplit = 4;  // CTAs per segment, each 8 / kPrepSplit columns a
+#ifndef DQ_PREP_SPLIT
+#define DQ_PREP_SPLIT 4
+#endif
+constexpr int kPrepSplit = DQ_PREP_SPLIT;  // CTAs per segment, each 8 / kPrepSplit columns a
 template <int G>
 constexpr int kPrepThreadsOf = G * (8 / kPrepSplit) * kMaxRW;
 

@@ -1,6 +1,7 @@
 // Shared helpers for the DecoQuant sm_100a kernels (see include/dquant_b200.h).
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -137,8 +137,8 @@ class DecoQuantLM:
         h = self._norm(x, y, L["ln1"])
         q, k, v = self._qkv_rope(h @ L["qkv"])
         # units = (sequence, kv head); query heads kv * g .. kv * g + g - 1 share a kv head
-        att = self.cache.attend(i, q, append=(k, v))
-        h = self._norm(x, att.view(B, s.heads * 128).to(torch.bfloat16) @ L["o"], L["ln2"])
+        att = self.cache.attend(i, q, append=(k, v), out_dtype=torch.bfloat16)  # bf16 straight from the combine
+        h = self._norm(x, att.view(B, s.heads * 128) @ L["o"], L["ln2"])
         return self._silu_mul(h @ L["gate_up"]) @ L["down"]
 
     def step(self, tokens: torch.Tensor) -> torch.Tensor:

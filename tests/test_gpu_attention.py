@@ -374,3 +374,36 @@ def test_export_segment_wire_format(dq):
         assert seg.local_tensors[1].payload == direct.local_tensors[1].payload
         assert seg.local_tensors[1].scale == direct.local_tensors[1].scale
         assert rel(dq.deco_dequantize(direct), dq.deco_dequantize(seg).cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("g,kernel_g", [(1, None), (2, None), (8, 8)])
+def test_bf16_output(dq, g, kernel_g):
+    """out_dtype=bf16: the combine kernel rounds the merged fp32 output to bf16 once.  Against
+    the fp16 output: within one bf16 ulp (the fp16 route rounds twice); against the oracle:
+    the bf16 rounding (2^-9 relative) on top of the tolerance."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(11 + g)
+    units, T = 3, 1024
+    k = rng.standard_normal((units, T, 128)).astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = torch.from_numpy(rng.standard_normal((units, g, 128)).astype(np.float16)).cuda()
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=4, chunk_len=64, kernel_g=kernel_g)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    for t in range(5):  # a dense tail as well
+        cache.append_token(0, torch.from_numpy(k[:, t]).cuda(), torch.from_numpy(v[:, t]).cuda())
+    o16 = cache.attend(0, q)
+    ob = cache.attend(0, q, out_dtype=torch.bfloat16)
+    assert ob.dtype == torch.bfloat16 and ob.shape == o16.shape
+    x, y = o16.float(), ob.float()
+    assert torch.all((x - y).abs() <= 2.0 ** -7 * x.abs().clamp_min(2.0 ** -20))
+    assert cache._layers[0].args.out_bf16 == 0  # reset after the call
+    kk = np.concatenate([k, k[:, :5]], 1).astype(np.float32)
+    vv = np.concatenate([v, v[:, :5]], 1).astype(np.float32)
+    for u in range(units):
+        ref = _oracle_attend(kk[u], vv[u], q[u].float().cpu().numpy(), 4, [T], 5)
+        assert rel(ref, y[u].cpu().numpy()) < TOL + 2.0 ** -8
+    from paper_2405_12591_b200.errors import DimMismatch
+
+    with pytest.raises(DimMismatch):
+        cache.attend(0, q, out=torch.empty_like(q), out_dtype=torch.bfloat16)

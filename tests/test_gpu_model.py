@@ -19,13 +19,16 @@ def test_tiny_model_step_attention_matches_oracle():
     captured = {}
     real_attend = lm.cache.attend
 
-    def spy(layer, q, out=None, append=None):
+    def spy(layer, q, out=None, append=None, out_dtype=torch.float16):
         if layer == 0:
             captured["q"] = q.float().cpu().numpy()
             captured["k"], captured["v"] = (t.float().cpu().numpy() for t in append)
-        o = real_attend(layer, q, out, append)
+            # the same attention in fp16 (no append: the prefix the model's call sees)
+            captured["out"] = real_attend(layer, q).float().cpu().numpy()
+        o = real_attend(layer, q, out, append, out_dtype=out_dtype)
         if layer == 0:
-            captured["out"] = o.float().cpu().numpy()
+            captured["out_model"] = o.float().cpu().numpy()
+            captured["out_dtype"] = o.dtype
         return o
 
     lm.cache.attend = spy
@@ -40,6 +43,11 @@ def test_tiny_model_step_attention_matches_oracle():
     ref = O.attention_units(captured["q"], k0, v0, 4)
     rel = np.linalg.norm(captured["out"] - ref) / np.linalg.norm(ref)
     assert rel < 1e-3, rel
+    # the model reads the attention as bf16 straight from the combine kernel: one rounding of
+    # the same merged value, so within one bf16 ulp of the fp16 output
+    assert captured["out_dtype"] == torch.bfloat16
+    x, y = captured["out"], captured["out_model"]
+    assert np.all(np.abs(x - y) <= 2.0 ** -7 * np.maximum(np.abs(x), 2.0 ** -20))
     assert lm.cache.tokens(0) == 521 and lm.cache.tokens(1) == 521
 
 
