@@ -34,7 +34,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+#ifndef DQ_WAIT_HINT
+#define DQ_WAIT_HINT 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if DQ_WAIT_HINT
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -42,8 +46,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680)  // suspend-time hint (ns): sleep in the wait, not spin
+      "r"(parity), "r"(DQ_WAIT_HINT)  // suspend-time hint (ns): sleep in the wait, not spin
       : "memory");
+#else
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 // (c0, c1) += (a0, a1) * (b0, b1) as one packed fp32x2 FMA (FFMA2, sm_100); a scalar
