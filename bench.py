@@ -6,9 +6,12 @@
 A *step* is one decode step of the attention hot path over every layer of the
 model shape: per layer, the fused int-k DecoQuant dequant + decode attention
 (K5) over each unit's compressed KV plus the append of the new token's K/V row
-into the fp16 tail (kvcache.py:116-123).  Units are (sequence, kv head) pairs;
-the KV cache is sharded by kv head across ranks (no collective on this path),
-and the global batch grows with N so per-GPU work is fixed ("weak").
+into the fp16 tail (kvcache.py:116-123).  Units are (sequence, kv head) pairs.
+Multi-GPU: one process per GPU (`--gpus N` relaunches itself under
+torch.distributed.run when not already under it).  C2 / C3 scale weakly (each rank
+a replica over its own batch); C4 / C5 shard the kv heads of a fixed batch across
+the ranks (strong).  The attention path has no collective; the ranks meet only at
+the barriers around the timed region and the max over ranks of the device times.
 
 Default workload (BASELINE.json configs[1]): LLaMA-2-7B shape (32 layers,
 32 kv heads, head dim 128), batch 16 per 32-head shard, 4K-token context
@@ -34,16 +37,102 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (workload, layers, kv_heads, g, batch per 32-head-equivalent shard, context, bits)
-    "c2": dict(workload="llama2-7b-shape decode, batch 16, 4K context, int4 DecoQuant KV", model="llama2-7b-shape",
-               layers=32, kv_heads=32, g=1, batch=16, T=4096, bits=4),
-    "c3": dict(workload="llama2-13b-shape decode, batch 32, 8K context, int2 DecoQuant KV", model="llama2-13b-shape",
-               layers=40, kv_heads=40, g=1, batch=32, T=8192, bits=2),
-    "c4": dict(workload="llama2-7b-shape long-context decode, batch 1, 32K context, int4", model="llama2-7b-shape",
-               layers=32, kv_heads=32, g=1, batch=1, T=32768, bits=4),
-    "c5": dict(workload="llama2-70b-shape GQA decode, batch 64, 16K context, int4", model="llama2-70b-shape",
-               layers=80, kv_heads=8, g=8, batch=64, T=16384, bits=4),
+    # name: workload, layers, kv_heads, g, batch, context T, bits, scaling over N GPUs:
+    #   weak   -- batch per GPU fixed (each rank holds every kv head of its own sequences' shard
+    #             of `batch` x kv_heads units: the global batch grows with N);
+    #   strong -- the global batch is fixed and the kv heads are sharded across the ranks
+    #             (BASELINE.json configs[3] "KV heads sharded across 2/4/8 B200", configs[4]
+    #             "one KV head per GPU on 8 x B200")
+    "c2": dict(workload="llama2-7b-shape decode attention, batch 16, 4K context, int4 DecoQuant KV",
+               model="llama2-7b-shape", layers=32, kv_heads=32, g=1, batch=16, T=4096, bits=4, scaling="weak"),
+    "c3": dict(workload="llama2-13b-shape decode attention, batch 32, 8K context, int2 DecoQuant KV",
+               model="llama2-13b-shape", layers=40, kv_heads=40, g=1, batch=32, T=8192, bits=2, scaling="weak"),
+    "c4": dict(workload="llama2-7b-shape long-context decode attention, batch 1, 32K context, int4",
+               model="llama2-7b-shape", layers=32, kv_heads=32, g=1, batch=1, T=32768, bits=4, scaling="strong"),
+    "c5": dict(workload="llama2-70b-shape GQA decode attention, batch 64, 16K context, int4",
+               model="llama2-70b-shape", layers=80, kv_heads=8, g=8, batch=64, T=16384, bits=4, scaling="strong"),
 }
+
+
+class Ranks:
+    """One process per GPU (torchrun env: RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*).
+
+    NCCL on GPUs, gloo without CUDA (the CPU plumbing test).  The decode attention path has
+    no collective: the process group carries only the barriers around the timed region and
+    the max-over-ranks of the device times."""
+
+    def __init__(self, backend=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+        self.dev = None
+        if self.backend == "nccl":
+            torch.cuda.set_device(self.local)
+            self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group("gloo")
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_objects(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def shard(cfg, world: int, rank: int):
+    """This rank's share of the config: (global batch, [lo, hi) kv heads, units).
+
+    Units are (sequence, kv head) pairs in sharding.local_units order; every rank holds the
+    same number (kv_heads % world == 0)."""
+    from paper_2405_12591_b200.sharding import kv_head_range, local_units
+
+    global_batch = cfg["batch"] * world if cfg["scaling"] == "weak" else cfg["batch"]
+    if cfg["scaling"] == "weak":  # every kv head of this rank's own sequences (no sharding needed)
+        lo, hi = 0, cfg["kv_heads"]
+        units = cfg["batch"] * cfg["kv_heads"]
+    else:
+        lo, hi = kv_head_range(cfg["kv_heads"], rank, world)
+        units = len(local_units(cfg["batch"], cfg["kv_heads"], rank, world))
+    return global_batch, (lo, hi), units
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: relaunch this command as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1; rank 0's JSON line is this process's output."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def parse():
@@ -66,6 +155,8 @@ def parse():
     ap.add_argument("--layers", type=int, default=None, help="override layer count (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--plumbing", action="store_true",
+                    help="rank plumbing only (launcher, shards, barriers, max over ranks; no kernels): CPU test")
     return ap.parse_args()
 
 
@@ -169,9 +260,9 @@ def cpu_model_name():
 
 
 def run_reference(args, cfg, world):
-    """--impl reference: the oracle port on host cores, rank 0 only."""
-    global_batch = cfg["batch"] * world
-    units_per_step = cfg["layers"] * global_batch * (cfg["kv_heads"] // world) * world
+    """--impl reference: the oracle port on host cores, rank 0 only, for the WHOLE job's units."""
+    global_batch = shard(cfg, world, 0)[0]
+    units_per_step = cfg["layers"] * global_batch * cfg["kv_heads"]
     arm = CpuArm(cfg)
     sample_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
@@ -196,12 +287,11 @@ def run_reference(args, cfg, world):
         "warmup": args.warmup,
         "ms_per_step": step_s * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": cfg["scaling"],
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic N(0,1) K/V rounded to fp16; oracle units encoded once per worker",
-        "config": {"workload": cfg["workload"], "global_batch": global_batch, "context": cfg["T"],
-                   "kv_bits": cfg["bits"], "layers": cfg["layers"], "kv_heads": cfg["kv_heads"], "g": cfg["g"]},
+        "config": config_keys(args, cfg, world, global_batch),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": arm.cores, "kind": "port",
                          "sample": f"{done} unit-reads (T={cfg['T']}, g={cfg['g']}) over {args.steps} steps on "
                                    f"{arm.cores} single-thread workers, extrapolated to {units_per_step} units/step",
@@ -322,27 +412,49 @@ class Clocks:
                 "samples": len(sm), "sampler": "nvml" if self.samples else "nvidia-smi"}
 
 
+def config_keys(args, cfg, world, global_batch):
+    """The `config` object both arms print (same keys, same values)."""
+    _, (lo, hi), units = shard(cfg, world, 0)
+    T, bits = cfg["T"], cfg["bits"]
+    kv_gb = (args.layers or cfg["layers"]) * units * 2 * (T * 128 * bits // 8 + 8 * 8 * 64 * 4 + 4) / 1e9
+    return {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
+            "kv_bits": bits, "tail_tokens": args.tail,
+            "quantizer": "per-channel asymmetric (opt-in)" if args.asym else "per-tensor symmetric (reference)",
+            "layers": args.layers or cfg["layers"], "kv_heads": cfg["kv_heads"], "g": cfg["g"],
+            "kv_heads_per_gpu": hi - lo, "units_per_gpu": units,
+            "parallelism": f"kv-head shards x{world}" if cfg["scaling"] == "strong" else f"data-parallel replicas x{world}",
+            "step": "attention only: fused dequant + decode attention + tail append per layer (no projections)",
+            "l2": f"inputs > L2: {kv_gb:.2f} GB of compressed KV streamed per step per GPU (126 MB L2)"}
+
+
+def run_plumbing(args, cfg):
+    """--plumbing: the launcher / rank / shard / timing path of run_ours without kernels (gloo on
+    CPU in tests/test_bench_ranks.py; the same Ranks and shard() the GPU run uses)."""
+    rk = Ranks()
+    global_batch, (lo, hi), units = shard(cfg, rk.world, rk.rank)
+    rk.barrier()
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rk.rank + 1))  # stand-in for the rank's timed steps
+    ms = rk.max((time.perf_counter() - t0) * 1e3)
+    shards = rk.gather_objects({"rank": rk.rank, "heads": [lo, hi], "units": units})
+    if rk.rank == 0:
+        print(json.dumps({"plumbing": True, "n_gpus": rk.world, "backend": rk.backend, "scaling": cfg["scaling"],
+                          "global_batch": global_batch, "ms_max": ms, "shards": shards}), flush=True)
+    rk.close()
+
+
 def run_ours(args, cfg):
-    import numpy as np
     import torch
-    import torch.distributed as dist
 
     from paper_2405_12591_b200.attention import DecodeKvCache
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    rk = Ranks("nccl")
+    world, rank, local, dev = rk.world, rk.rank, rk.local, rk.dev
     layers = args.layers or cfg["layers"]
     kv_heads, g, bits, T = cfg["kv_heads"], cfg["g"], cfg["bits"], cfg["T"]
     if kv_heads % world:
         raise SystemExit(f"{kv_heads} kv heads do not shard over {world} GPUs")
-    global_batch = cfg["batch"] * world
-    local_heads = kv_heads // world
-    units = global_batch * local_heads  # (sequence, local kv head) pairs on this rank
+    global_batch, (head_lo, head_hi), units = shard(cfg, world, rank)  # units: (sequence, kv head) pairs here
     chunk_len = 1024
 
     cache = DecodeKvCache(layers=layers, units=units, g=g, bits=bits, chunk_len=chunk_len, chunk_b=args.chunk_b,
@@ -379,16 +491,7 @@ def run_ours(args, cfg):
             # joins the tail (append fused into the combine kernel)
             cache.attend(layer, q[layer], out[layer], append=(kn[layer], vn[layer]))
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    barrier, max_over_ranks = rk.barrier, rk.max
 
     # steady state: a partly filled fp16 tail, appended through the public API
     for layer in range(layers):
@@ -473,18 +576,15 @@ def run_ours(args, cfg):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": cfg["scaling"],
         "vs_baseline": None,
         "dtype": "f16",
         "data": "synthetic: per-layer K/V ~ N(0,1) fp16 compressed by the K3 write path; q/k/v rows ~ N(0,1) fp16",
-        "config": {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
-                   "kv_bits": bits, "tail_tokens": args.tail, "quantizer": "per-channel asymmetric (opt-in)" if args.asym else "per-tensor symmetric (reference)",
-                   "layers": layers, "kv_heads": kv_heads, "g": g,
-                   "parallelism": f"kv-head shards x{world}", "units_per_gpu": units, "chunk_b": cache._layers[0].args.chunk_b,
-                   "split_ctas": cache.split_ctas, "kernel_g": cache._layers[0].kernel_g,
-                   "head_groups": g // cache._layers[0].kernel_g,
+        "config": config_keys(args, cfg, world, global_batch),
+        "kernel": {"chunk_b": cache._layers[0].args.chunk_b, "split_ctas": cache.split_ctas,
+                   "kernel_g": cache._layers[0].kernel_g, "head_groups": g // cache._layers[0].kernel_g,
                    "split_path": {0: "mma.sync", 1: "tcgen05", 2: "tcgen05-gqa"}[cache._layers[0].args.path],
-                   "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB streamed per step per GPU"},
+                   "step_bytes": step_bytes},
         "hbm_gbs_step": step_bytes / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src,
@@ -511,15 +611,21 @@ def run_ours(args, cfg):
                                 "cpu": cpu_model_name()}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    rk.close()
 
 
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))  # one rank per GPU under torch.distributed.run
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.plumbing:
+        run_plumbing(args, cfg)
+        return
     if args.impl == "reference":
         if rank == 0:
             run_reference(args, cfg, world)

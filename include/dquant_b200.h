@@ -19,6 +19,7 @@
  *   dq_plan_shapes ................ mpo.plan_shapes            mpo.py:73-96
  *   dq_pack / dq_unpack ............ quantize.pack/unpack/unpack_range  quantize.py:66-120
  *   dq_quantize_rtn ................ quantize.quantize_rtn      quantize.py:123-151
+ *   dq_quantize_rtn_f64 ............ quantize.quantize_rtn on float64 input (quantize.py:144 multiplies in f64)
  *   dq_dequantize .................. quantize.dequantize        quantize.py:154-157
  *   dq_decompose_batched ........... mpo.decompose (n=2)        mpo.py:153-178
  *   dq_deco_quantize_batched ....... compress.deco_quantize     compress.py:85-94
@@ -104,6 +105,9 @@ int dq_unpack(const uint8_t* payload, int64_t payload_bytes, int64_t start, int6
 int dq_quantize_workspace_size(int64_t count, size_t* h_bytes);
 int dq_quantize_rtn(const float* t, int64_t count, int32_t bits, float* scale, uint8_t* payload, int32_t* flags,
                     void* workspace, size_t workspace_bytes, void* stream);
+/* float64 input: amax and t*qmax/amax on the original f64 values, bit-exact with the reference */
+int dq_quantize_rtn_f64(const double* t, int64_t count, int32_t bits, float* scale, uint8_t* payload, int32_t* flags,
+                        void* workspace, size_t workspace_bytes, void* stream);
 int dq_dequantize(const uint8_t* payload, int64_t count, int32_t bits, const float* scale, float* out, void* stream);
 
 /* ---- K3 write path: batched n=2 TT-SVD (+ quantize) -------------------

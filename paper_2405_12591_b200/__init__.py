@@ -8,8 +8,9 @@ DecoQuant protocol and the KV cache.  Compute runs in ``libdquant_b200.so``
 The batched decode hot path is ``DecodeKvCache`` (attention.py).
 
 Also here: the quantisation-error sweeps of the paper's tables on the device path
-(``analysis``) and the DQT1 / DQZ1 interchange files (``formats``).  Out of scope
-(SURVEY.md 2 / 8f): the CLI and the dense tensor primitives.
+(``analysis``; its names are re-exported lazily, as in the reference's
+``__init__.py:10-20``) and the DQT1 / DQZ1 interchange files (``formats``).  Out of
+scope: the dense tensor primitives (``tensor.py``).
 """
 
 from .compress import (
@@ -26,7 +27,11 @@ from .kvcache import CacheConfig, KvCache, MemoryLedger, simulate_generation
 from .mpo import MpoChain, ShapePlan, decompose, plan_shapes, reconstruct, split_large_small
 from .quantize import QuantizedTensor, dequantize, pack, quantize_rtn, unpack
 
+_ANALYSIS = ("ErrorRecord", "OutlierStats", "decomposition_comparison", "default_suite", "iqr_stats",
+             "length_sweep", "migration_report", "strategy_sweep", "synth_activations")
+
 __all__ = [
+    *_ANALYSIS,
     "CacheConfig",
     "CompressionReport",
     "DecodeKvCache",
@@ -61,4 +66,8 @@ def __getattr__(name):
         from .attention import DecodeKvCache
 
         return DecodeKvCache
+    if name in _ANALYSIS:  # analysis imports the sweeps' device paths: loaded on first use
+        from . import analysis
+
+        return getattr(analysis, name)
     raise AttributeError(name)

@@ -88,6 +88,7 @@ class _Layer:
         self.args = None   # cached AttnArgs
         self.kernel_g = None  # heads per split-kernel instance used for this layer
         self.keep = []     # tensors referenced by args
+        self.gen = 0       # plan generation: bumped whenever the segment table / args change
 
 
 def compress_blocks(blocks: torch.Tensor, bits: int, layout: int, g0_dtype=torch.float16, asym: bool = False):
@@ -260,6 +261,7 @@ class DecodeKvCache:
                                        kch, vch))
         lay.tokens_sealed += T
         lay.args = None
+        lay.gen += 1
 
     def prefill(self, layer: int, keys: torch.Tensor, values: torch.Tensor):
         """keys/values: (units, T, 128) CUDA fp16 or fp32.  One segment per unit (kvcache.py:99-114)."""
@@ -417,6 +419,7 @@ class DecodeKvCache:
         a.wimg = wimg.data_ptr()
         a.wimg_stride = wib.value
         lay.args = a
+        lay.gen += 1
         lay.keep = [seg_dev, work_dev, wpart_dev, sched, p0_dev, np_dev, part_o, part_ml, wimg]
 
     def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None,
@@ -477,6 +480,7 @@ class DecodeKvCache:
             d.groups.append(SegmentGroup(**fields))
         d.tokens_sealed = s.tokens_sealed
         d.args = None
+        d.gen += 1
 
     # ---- accounting ----------------------------------------------------------
     def kernel_bytes(self, layer: int) -> int:

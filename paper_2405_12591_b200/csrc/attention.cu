@@ -291,7 +291,10 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
     attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr_pdl;
-    cfg.numAttrs = 1;
+    // the combine reads q and the tail before its griddepcontrol.wait, which is safe only behind
+    // the split kernel (it triggers after its own wait); with no split kernel in front (a
+    // tail-only layer, or a combine-only launch) the predecessor may be q's producer: no PDL edge
+    cfg.numAttrs = (a.nwork > 0 && (phases & 1)) ? 1 : 0;
     if (gq) {
       DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, combine_gqa_kernel, a));
     } else {

@@ -90,6 +90,48 @@ __global__ void quantize_pack_kernel(const float* __restrict__ t, int64_t count,
   }
 }
 
+// fp64 input (quantize.py:131-145 on a float64 array): max |t| as the bits of a non-negative
+// double (monotone as uint64) + finiteness
+__global__ void amax_f64_kernel(const double* __restrict__ t, int64_t count, unsigned long long* amax_bits,
+                                int32_t* flags) {
+  double m = 0.0;
+  bool nonfinite = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = t[i];
+    nonfinite |= !isfinite(v);
+    m = fmax(m, fabs(v));
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(amax_bits, (unsigned long long)__double_as_longlong(m));
+    if (nonfinite && flags) atomicOr(flags, (int)DQ_FLAG_NONFINITE);
+  }
+}
+
+__global__ void quantize_pack_f64_kernel(const double* __restrict__ t, int64_t count, int bits,
+                                         const unsigned long long* __restrict__ amax_bits, float* scale_out,
+                                         uint8_t* __restrict__ out) {
+  const int per = 8 / bits;
+  const int qmax = (1 << (bits - 1)) - 1;
+  const unsigned mask = (1u << bits) - 1u;
+  const double amax = __longlong_as_double((long long)*amax_bits);
+  bool degenerate;
+  const float scale = rtn_scale(amax, qmax, &degenerate);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = scale;
+  const int64_t nbytes = payload_bytes(count, bits);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nbytes; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned v = 0;
+    if (!degenerate) {
+      for (int k = 0; k < per; ++k) {
+        const int64_t idx = i * per + k;
+        if (idx < count) v |= ((unsigned)rtn_code_f64(t[idx], qmax, amax) & mask) << (k * bits);
+      }
+    }
+    out[i] = (uint8_t)v;
+  }
+}
+
 // quantize.py:154-157: f32(code) * f32(scale)
 __global__ void dequant_kernel(const uint8_t* __restrict__ payload, int64_t count, int bits,
                                const float* __restrict__ scale, float* __restrict__ out) {
@@ -147,6 +189,24 @@ extern "C" int dq_quantize_rtn(const float* t, int64_t count, int32_t bits, floa
   }
   quantize_pack_kernel<<<grid_for(payload_bytes(count, bits)), kThreads, 0, s>>>(t, count, bits, amax, scale,
                                                                                  payload);
+  DQ_LAUNCH_CHECK();
+  return DQ_OK;
+}
+
+extern "C" int dq_quantize_rtn_f64(const double* t, int64_t count, int32_t bits, float* scale, uint8_t* payload,
+                                   int32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!bits_ok(bits)) return fail(DQ_ERR_UNSUPPORTED_BITS, "bits must be one of (2, 4, 8), got %d", bits);
+  if (count < 0 || !scale || (count && (!t || !payload)) || !ws || ws_bytes < 256)
+    return fail(DQ_ERR_INVALID_ARG, "dq_quantize_rtn_f64: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* amax = (unsigned long long*)ws;
+  DQ_CUDA_TRY(cudaMemsetAsync(amax, 0, sizeof(unsigned long long), s));
+  if (count) {
+    amax_f64_kernel<<<grid_for(count), kThreads, 0, s>>>(t, count, amax, flags);
+    DQ_LAUNCH_CHECK();
+  }
+  quantize_pack_f64_kernel<<<grid_for(payload_bytes(count, bits)), kThreads, 0, s>>>(t, count, bits, amax, scale,
+                                                                                     payload);
   DQ_LAUNCH_CHECK();
   return DQ_OK;
 }

@@ -136,6 +136,14 @@ __device__ __forceinline__ int rtn_code(float t, int qmax, double amax) {
   return y < 0.0 ? -(int)c : (int)c;
 }
 
+// the same on an fp64 value (float64 input arrays: quantize.py:144 multiplies the original values)
+__device__ __forceinline__ int rtn_code_f64(double t, int qmax, double amax) {
+  const double y = __ddiv_rn(__dmul_rn(t, (double)qmax), amax);
+  double c = floor(__dadd_rn(fabs(y), 0.5));
+  if (c > (double)qmax) c = (double)qmax;
+  return y < 0.0 ? -(int)c : (int)c;
+}
+
 // quantize.py:135-140: f32(amax/qmax), or 1.0 when amax == 0 or the step underflows
 __host__ __device__ inline float rtn_scale(double amax, int qmax, bool* degenerate) {
   float s = amax > 0.0 ? (float)(amax / (double)qmax) : 1.0f;

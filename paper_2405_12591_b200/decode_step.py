@@ -13,7 +13,10 @@ step is captured once and replayed:
 - the host keeps the cache's token counters in step (``DecodeKvCache._after_append``).
 
 A replay that would seal a tail chunk (which re-plans the layer's segment table) is
-refused; call ``recapture()`` after sealing steps run eagerly.
+refused; call ``recapture()`` after sealing steps run eagerly.  Every layer's plan
+generation (``_Layer.gen``, bumped by a seal and by a re-plan) is recorded at capture:
+a replay after any re-plan raises instead of replaying stale segment tables, and the
+captured tables (``_Layer.keep``) are held by the graph so they outlive a re-plan.
 """
 
 from __future__ import annotations
@@ -86,16 +89,22 @@ class DecodeStepGraph:
         if self._sealing_ahead():
             raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
         tails = [lay.tail_len for lay in self.cache._layers]
+        self.gens = [lay.gen for lay in self.cache._layers]
+        self.keep = [list(lay.keep) for lay in self.cache._layers]  # device tables the graph points at
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self._body()
         for lay, t in zip(self.cache._layers, tails):  # the capture ran no device work
             lay.tail_len = t
+        if [lay.gen for lay in self.cache._layers] != self.gens:
+            raise ShapeMismatch("a layer was re-planned during the capture")
 
     def replay(self):
         """One decode step for every layer from the current host inputs into out_h."""
         if self._sealing_ahead():
             raise ShapeMismatch("a tail chunk seals on this token: run the step eagerly, then recapture()")
+        if [lay.gen for lay in self.cache._layers] != self.gens:
+            raise ShapeMismatch("a layer was re-planned (sealed chunk) since the capture: recapture()")
         self.graph.replay()
         for layer in range(self.cache.layers):
             self.cache._after_append(layer)

@@ -163,6 +163,8 @@ class DecoQuantLM:
         first = self.step(self._tok).clone()  # eager step: builds every layer's segment table
         torch.cuda.synchronize()
         tails = [lay.tail_len for lay in self.cache._layers]
+        self._gens = [lay.gen for lay in self.cache._layers]
+        self._keep = [list(lay.keep) for lay in self.cache._layers]  # tables the graph points at
         pos = self.pos.clone()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
@@ -175,6 +177,8 @@ class DecoQuantLM:
     def replay(self, tokens: torch.Tensor) -> torch.Tensor:
         if any(lay.tail_len + 1 >= self.cache.chunk_len for lay in self.cache._layers):
             raise ShapeMismatch("a tail chunk seals on this token: decode it eagerly, then capture() again")
+        if [lay.gen for lay in self.cache._layers] != self._gens:
+            raise ShapeMismatch("a layer was re-planned (sealed chunk) since the capture: capture() again")
         self._tok.copy_(tokens)
         self.graph.replay()
         for layer in range(self.shape.layers):

@@ -167,7 +167,11 @@ def unpack_range(payload, start: int, count: int, bits: int):
 def quantize_rtn(t, bits: int) -> QuantizedTensor:
     """One symmetric scale, round half away from zero (quantize.py:123-151)."""
     _check_bits(bits)
-    x, is_t = _as_device(t, torch.float32)
+    # the reference multiplies the ORIGINAL values in float64 (quantize.py:144): fp16 / fp32
+    # inputs are exact in fp32; float64 (and integer) inputs keep an fp64 path
+    src_dtype = t.dtype if isinstance(t, torch.Tensor) else np.asarray(t).dtype
+    f64 = src_dtype not in (torch.float16, torch.float32, torch.bfloat16, np.float16, np.float32)
+    x, is_t = _as_device(t, torch.float64 if f64 else torch.float32)
     shape = tuple(x.shape)
     x = x.reshape(-1)
     n = x.numel()
@@ -175,8 +179,8 @@ def quantize_rtn(t, bits: int) -> QuantizedTensor:
     out = torch.empty(payload_size(n, bits), dtype=torch.uint8, device=x.device)
     flags = torch.zeros(1, dtype=torch.int32, device=x.device)
     ws = torch.empty(256, dtype=torch.uint8, device=x.device)
-    check(lib().dq_quantize_rtn(ptr(x), n, bits, ptr(scale), ptr(out), ptr(flags), ptr(ws), 256, stream_ptr()),
-          "quantize_rtn")
+    fn = lib().dq_quantize_rtn_f64 if f64 else lib().dq_quantize_rtn
+    check(fn(ptr(x), n, bits, ptr(scale), ptr(out), ptr(flags), ptr(ws), 256, stream_ptr()), "quantize_rtn")
     if int(flags.item()) & _lib.FLAG_NONFINITE:
         raise NonFiniteInput("quantize_rtn requires finite entries")
     return QuantizedTensor(shape, bits, float(scale.item()), data=out, torch_out=is_t)

@@ -150,3 +150,23 @@ def test_sharding_ranges():
     assert sorted(units) == [(b, h) for b in range(2) for h in range(8)]
     with pytest.raises(ValueError):
         kv_head_range(6, 0, 4)
+
+
+# the reference's public names (dquant/__init__.py:38-79) minus the dense tensor primitives of
+# tensor.py (DenseTensor, QrResult, SvdResult, matmul, permute, qr, reshape, svd: out of scope)
+REFERENCE_ALL = [
+    "CacheConfig", "CompressionReport", "ErrorRecord", "KvCache", "MemoryLedger", "MpoChain", "OutlierStats",
+    "QuantizedMpo", "QuantizedTensor", "ShapePlan", "WorkingSetMeter", "compression_report", "deco_dequantize",
+    "deco_quantize", "decompose", "decomposition_comparison", "default_suite", "dequantize", "fused_matmul",
+    "fused_matmul_t", "iqr_stats", "length_sweep", "migration_report", "pack", "plan_shapes", "quantize_rtn",
+    "reconstruct", "simulate_generation", "split_large_small", "strategy_sweep", "synth_activations", "unpack",
+]
+
+
+def test_reference_names_exported():
+    """import paper_2405_12591_b200 as dquant: every reference name resolves (analysis lazily)."""
+    import paper_2405_12591_b200 as dq
+
+    for name in REFERENCE_ALL:
+        assert name in dq.__all__, name
+        assert getattr(dq, name) is not None, name

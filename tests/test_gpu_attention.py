@@ -407,3 +407,172 @@ def test_bf16_output(dq, g, kernel_g):
 
     with pytest.raises(DimMismatch):
         cache.attend(0, q, out=torch.empty_like(q), out_dtype=torch.bfloat16)
+
+
+# ---- north_star config shapes (BASELINE.json configs[3], configs[4], configs[2]) ------------
+
+@pytest.mark.parametrize("scale", [1.0, 20.0])
+def test_c4_shape_32k(dq, scale):
+    """C4: int4, g = 1, T = 32768 (16-64 partials per unit, a Gram over 65,536 columns), the
+    default plan (512-row items), plain and x20 outlier keys."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(32768 + int(scale))
+    units, T = 2, 32768
+    k = rng.standard_normal((units, T, 128)).astype(np.float32)
+    k[:, :, [3, 77]] *= scale
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = rng.standard_normal((units, 1, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=4)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    a = cache._layers[0].args
+    assert a.path == 0 and a.nwork >= 2 * 8
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), 4, [T], 0)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
+@pytest.mark.parametrize("scale", [1.0, 50.0])
+def test_c5_shape_gqa_16k(dq, scale):
+    """C5: g = 8 query heads per kv head, T = 16384, int4 on the tcgen05 GQA kernel (path 2),
+    plain and x50 outlier keys."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(16384 + int(scale))
+    units, g, T = 2, 8, 16384
+    k = rng.standard_normal((units, T, 128)).astype(np.float32)
+    k[:, :, [3, 77]] *= scale
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16)
+    q = rng.standard_normal((units, g, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=4)
+    cache.prefill(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    assert cache._layers[0].args.path == 2
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), 4, [T], 0)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
+def test_c3_shape_int2_tail512(dq):
+    """C3: int2, T = 8192 on the default plan (512-row items), plus a 512-token fp16 tail
+    appended through the fused append."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    rng = np.random.default_rng(8192)
+    units, T, tail = 2, 8192, 512
+    k = rng.standard_normal((units, T + tail, 128)).astype(np.float16)
+    v = rng.standard_normal((units, T + tail, 128)).astype(np.float16)
+    q = rng.standard_normal((units, 1, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=2)
+    kd, vd, qd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    cache.prefill(0, kd[:, :T], vd[:, :T])
+    for t in range(T, T + tail):
+        cache.attend(0, qd, append=(kd[:, t], vd[:, t]))
+    out = cache.attend(0, qd).float().cpu().numpy()
+    assert cache._layers[0].args.chunk_b == 512 and cache._layers[0].tail_len == tail
+    for u in range(units):
+        ref = _oracle_attend(k[u].astype(np.float32), v[u].astype(np.float32), q[u].astype(np.float32), 2, [T], tail)
+        assert rel(ref, out[u]) < TOL, (u, rel(ref, out[u]))
+
+
+@pytest.mark.parametrize("g", [1, 8])
+def test_decode_crosses_1024_seal(dq, g):
+    """Decode through the default 1024-token seal (kvcache.py:116-128): outputs against the
+    oracle's own cache lifecycle just before, at and after the step that seals the tail."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    units, P, chunk = 2, 1536, 1024
+    steps = chunk + 6
+    rng = np.random.default_rng(1024 + g)
+    k = rng.standard_normal((units, P + steps, 128)).astype(np.float32)
+    k[:, :, [9, 100]] *= 8.0
+    k = k.astype(np.float16)
+    v = rng.standard_normal((units, P + steps, 128)).astype(np.float16)
+    q = rng.standard_normal((steps, units, g, 128)).astype(np.float16)
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=4, chunk_len=chunk)
+    kd, vd, qd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    cache.prefill(0, kd[:, :P], vd[:, :P])
+    oracles = []
+    for u in range(units):
+        lay = O.LayerOracle(128, 4, chunk)
+        lay.prefill(k[u, :P].astype(np.float32), v[u, :P].astype(np.float32))
+        oracles.append(lay)
+    check = {chunk - 2, chunk - 1, chunk, chunk + 1, steps - 1}
+    for t in range(steps):
+        out = cache.attend(0, qd[t], append=(kd[:, P + t], vd[:, P + t]))
+        if t in check:
+            o = out.float().cpu().numpy()
+            for u in range(units):
+                ref = oracles[u].attend(q[t, u].astype(np.float32))
+                assert rel(ref, o[u]) < TOL, (t, u, rel(ref, o[u]))
+        for u in range(units):
+            oracles[u].append(k[u, P + t].astype(np.float32), v[u, P + t].astype(np.float32))
+    lay = cache._layers[0]
+    assert len(lay.groups) == 2 and lay.tail_len == steps - chunk
+    assert cache.tokens(0) == oracles[0].tokens == P + steps
+
+
+@pytest.mark.parametrize("g", [1, 8])
+def test_tail_only_q_from_previous_kernel(dq, g):
+    """A tail-only layer (no segments: no prepare / split kernels) whose q is written by the
+    kernel launched right before the attention: the combine must see that q (no PDL edge to
+    q's producer)."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+
+    units, steps = 4, 40
+    rng = np.random.default_rng(3 + g)
+    k = torch.from_numpy(rng.standard_normal((units, steps, 128)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.standard_normal((units, steps, 128)).astype(np.float16)).cuda()
+    x = torch.from_numpy(rng.standard_normal((steps, units, g, 128)).astype(np.float32)).cuda()
+    cache = DecodeKvCache(layers=1, units=units, g=g, bits=4, chunk_len=64, kernel_g=8 if g == 8 else None)
+    q = torch.empty((units, g, 128), dtype=torch.float16, device="cuda")
+    for t in range(steps):
+        torch.mul(x[t], 0.5, out=x[t])  # a kernel in front of q's producer
+        q.copy_(x[t])                   # q's producer, immediately before the attention
+        out = cache.attend(0, q, append=(k[:, t], v[:, t]))
+        if t == 0:
+            assert torch.count_nonzero(out) == 0
+            continue
+        qn = q.float().cpu().numpy().astype(np.float64)
+        kk, vv = k[:, :t].float().cpu().numpy(), v[:, :t].float().cpu().numpy()
+        o = out.float().cpu().numpy()
+        for u in range(units):
+            s = qn[u] @ kk[u].T / np.sqrt(128)
+            p = np.exp(s - s.max(1, keepdims=True))
+            p /= p.sum(1, keepdims=True)
+            assert rel(p @ vv[u], o[u]) < TOL, (t, u)
+
+
+def test_step_graph_refuses_stale_plan(dq):
+    """A replay after a re-plan (here a seal run eagerly) raises instead of replaying the
+    captured segment tables; recapture() restores replays."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+    from paper_2405_12591_b200.decode_step import DecodeStepGraph
+    from paper_2405_12591_b200.errors import ShapeMismatch
+
+    L, U, g, chunk = 2, 2, 1, 8
+    cache = DecodeKvCache(layers=L, units=U, g=g, bits=4, chunk_len=chunk)
+    kv = torch.randn((L, 2, U, 520, 128), device="cuda").half()
+    for layer in range(L):
+        cache.prefill(layer, kv[layer, 0], kv[layer, 1])
+    q_h = torch.randn((L, U, g, 128)).half().pin_memory()
+    k_h = torch.randn((L, U, 128)).half().pin_memory()
+    v_h = torch.randn((L, U, 128)).half().pin_memory()
+    out_h = torch.empty((L, U, g, 128), dtype=torch.float16).pin_memory()
+    st = DecodeStepGraph(cache, q_h, k_h, v_h, out_h)
+    while cache._layers[0].tail_len + 1 < chunk:
+        st.replay()
+    with pytest.raises(ShapeMismatch):
+        st.replay()  # this token seals
+    for layer in range(L):  # the sealing step, eagerly
+        cache.attend(layer, q_h[layer].cuda(), append=(k_h[layer].cuda(), v_h[layer].cuda()))
+    assert cache._layers[0].tail_len == 0
+    with pytest.raises(ShapeMismatch):
+        st.replay()  # stale: layer 0 was re-planned
+    st.recapture()
+    st.replay()
+    torch.cuda.synchronize()
+    assert cache.tokens(0) == 520 + chunk + 2

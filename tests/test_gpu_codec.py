@@ -101,3 +101,23 @@ def test_requantize_reference_core1(golden, dq, bits):
         q = dq.quantize_rtn(g[f"{name}_core1"], bits)
         assert np.float32(q.scale).tobytes() == g[f"{name}_scale"].tobytes(), name
         assert q.payload == g[f"{name}_payload"].tobytes(), name
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_quantize_rtn_float64_golden(dq, bits):
+    """float64 input keeps the reference's fp64 arithmetic on the original values
+    (quantize.py:131-145): near-tie values 1 ulp from a rounding boundary, values beyond the
+    fp32 range, subnormal maxima -- bit-exact scale and payload."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_f64.npz"))
+    names = sorted({k[:-2] for k in g.files if k.endswith("_t")})
+    for n in names:
+        t = g[n + "_t"]
+        q = dq.quantize_rtn(t, bits)
+        assert np.float32(q.scale).tobytes() == g[f"{n}_{bits}_scale"].tobytes(), n
+        assert q.payload == g[f"{n}_{bits}_payload"].tobytes(), n
+        qt = dq.quantize_rtn(torch.from_numpy(t).cuda(), bits)  # torch float64 CUDA input too
+        assert qt.payload == q.payload
+    # the advisor's example: 2.5 - 1e-12 rounds to 2 in fp64 and to 3 after an fp32 cast
+    assert dq.unpack(dq.quantize_rtn(np.array([7.0, 2.5 - 1e-12]), 4).payload, 2, 4).tolist() == [7, 2]

@@ -120,3 +120,19 @@ def test_attention_composition_sane():
     p = np.exp(s - s.max(1, keepdims=True))
     p /= p.sum(1, keepdims=True)
     assert rel(p @ v, lay.attend(q)) < 1e-6
+
+
+def test_oracle_rtn_float64_golden():
+    """float64 inputs (ties 1 ulp away, values beyond the fp32 range, subnormals) against the
+    reference's own quantize_rtn (tests/golden/make_golden_f64.py)."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_f64.npz"))
+    names = sorted({k[:-2] for k in g.files if k.endswith("_t")})
+    assert len(names) >= 5
+    with np.errstate(over="ignore"):
+        for n in names:
+            for bits in (2, 4, 8):
+                s, c = O.rtn(g[n + "_t"], bits)
+                assert np.float32(s).tobytes() == g[f"{n}_{bits}_scale"].tobytes(), (n, bits)
+                assert O.pack_codes(c.reshape(-1), bits).tobytes() == g[f"{n}_{bits}_payload"].tobytes(), (n, bits)
