@@ -117,26 +117,48 @@ __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __ha
 }
 
 
+// consumer teams of the mma.sync split kernel: 2 (one CTA per SM, a shared slot pool) for g = 1,
+// 1 (two CTAs per SM) for g = 2, whose 32 KB W image per team leaves no room for a second team
+#ifndef DQ_ATTN_TEAMS_G1
+#define DQ_ATTN_TEAMS_G1 2
+#endif
+template <int G>
+constexpr int kTeamsOf = G == 1 ? DQ_ATTN_TEAMS_G1 : 1;
+
 template <int BITS, int G, int NT = kTiles, bool ASYM = false>
 int set_attrs() {
+  constexpr int T = kTeamsOf<G>;
   static bool attr = false;
   if (!attr) {
-    const int smem = (int)sizeof(AttnSmem<G, NT, ASYM>);
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT, ASYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     smem));
-    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT, ASYM>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     100));
+    const int smem = (int)sizeof(AttnSmem<G, NT, ASYM, T>);
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT, ASYM, T>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<BITS, G, NT, ASYM, T>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
   return DQ_OK;
 }
 
+// launch the mma.sync split kernel instance (BITS, G, NT, ASYM) with its team count
+template <int BITS, int G, int NT, bool ASYM>
+int launch_split(cudaLaunchConfig_t cfg, const dq_attn_args& a) {
+  constexpr int T = kTeamsOf<G>;
+  const int rc = set_attrs<BITS, G, NT, ASYM>();
+  if (rc != DQ_OK) return rc;
+  cfg.blockDim = dim3(kCtaThreadsOf<T>);
+  cfg.dynamicSmemBytes = sizeof(AttnSmem<G, NT, ASYM, T>);
+  DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, NT, ASYM, T>, a));
+  return DQ_OK;
+}
+
 template <int BITS, int G>
 int occupancy(int* per_sm) {
+  constexpr int T = kTeamsOf<G>;
   const int rc = set_attrs<BITS, G>();
   if (rc != DQ_OK) return rc;
-  DQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, decode_attn_kernel<BITS, G>, kCtaThreads,
-                                                            sizeof(AttnSmem<G>)));
+  DQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, decode_attn_kernel<BITS, G, kTiles, false, T>,
+                                                            kCtaThreadsOf<T>, sizeof(AttnSmem<G, kTiles, false, T>)));
   return DQ_OK;
 }
 
@@ -233,7 +255,6 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
       // overlap the prepare kernel; it waits (griddepcontrol.wait) only for the W images
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(a.nctas > 0 && a.nctas < a.nwork ? a.nctas : a.nwork));
-      cfg.blockDim = dim3(kCtaThreads);
       cfg.stream = s;
       cudaLaunchAttribute attr_pdl[1];
       attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -241,33 +262,19 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
       cfg.attrs = attr_pdl;
       cfg.numAttrs = 1;
       if (a.asym && BITS == 8) return fail(DQ_ERR_UNSUPPORTED, "the asymmetric mode covers 2- and 4-bit codes");
+      int rc = DQ_OK;
       if (a.chunk_b > kCB) {  // 8-tile work items (g = 1, 2- and 4-bit codes)
         if constexpr (G == 1 && BITS <= 4) {
-          if (a.asym) {
-            const int rc = set_attrs<BITS, G, 2 * kTiles, true>();
-            if (rc != DQ_OK) return rc;
-            cfg.dynamicSmemBytes = sizeof(AttnSmem<G, 2 * kTiles, true>);
-            DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, 2 * kTiles, true>, a));
-          } else {
-            const int rc = set_attrs<BITS, G, 2 * kTiles>();
-            if (rc != DQ_OK) return rc;
-            cfg.dynamicSmemBytes = sizeof(AttnSmem<G, 2 * kTiles>);
-            DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, 2 * kTiles>, a));
-          }
+          rc = a.asym ? launch_split<BITS, G, 2 * kTiles, true>(cfg, a) : launch_split<BITS, G, 2 * kTiles, false>(cfg, a);
         } else {
           return fail(DQ_ERR_UNSUPPORTED, "work items of more than %d rows need g = 1 and 2- or 4-bit codes", kCB);
         }
       } else if (a.asym) {
-        if constexpr (BITS <= 4) {
-          const int rc = set_attrs<BITS, G, kTiles, true>();
-          if (rc != DQ_OK) return rc;
-          cfg.dynamicSmemBytes = sizeof(AttnSmem<G, kTiles, true>);
-          DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G, kTiles, true>, a));
-        }
+        if constexpr (BITS <= 4) rc = launch_split<BITS, G, kTiles, true>(cfg, a);
       } else {
-        cfg.dynamicSmemBytes = sizeof(AttnSmem<G>);
-        DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, G>, a));
+        rc = launch_split<BITS, G, kTiles, false>(cfg, a);
       }
+      if (rc != DQ_OK) return rc;
     }
   }
   if (phases & 2) {

@@ -1,18 +1,25 @@
 // The split kernel of the fused decode attention; see attention.cu for the math.
 //
-// Persistent and dynamically scheduled: a grid of (SMs x resident CTAs) CTAs; CTA c runs
-// work item c first, then items drawn from a global ticket counter (self-resetting: the
-// last CTA to retire zeroes it for the next launch), so CTAs that the SM's warp scheduler
-// favours simply take more items.  A work item (sub-item) is <= kTiles 64-row b tiles of
-// one segment (dq_attention_plan).  The code stages of a CTA's successive items form ONE
-// stream through the shared-memory ring, so the copies of item j+1 are in flight while
-// item j is in its softmax and epilogue.
+// Persistent and dynamically scheduled: a grid of (SMs x resident CTAs) CTAs draws work
+// items from a global ticket counter (self-resetting: the last CTA to retire zeroes it for
+// the next launch).  A work item (sub-item) is <= NT 64-row b tiles of one segment
+// (dq_attention_plan).
 //
-// Warp roles: 8 consumer warps (MMA, softmax, epilogue; they also issue the W-image and
-// G0v copies at their own barrier points) and 1 producer warp whose lane 0 issues the
-// code stages: it waits on the stage's `empty` mbarrier (one arrival per consumer warp)
-// and re-arms `full` with the copy's byte count.  Consumer barriers are named barrier 1
-// over the 256 consumer threads.
+// Warp roles: TEAMS consumer teams of 8 warps (MMA, softmax, epilogue; they issue their own
+// W-image and G0v copies at their own barrier points) and 1 producer warp whose lane 0 issues
+// every code stage (cp.async.bulk, completing on the slot's `full` mbarrier).
+//
+// TEAMS = 2 (one CTA per SM, the default for g = 1): the two teams work on different items
+// and share ONE pool of ring slots.  A team in its softmax or epilogue holds no more than
+// kTeamPrefetch stages of its next phase (the producer reads the phase each team has begun,
+// `started`), so the other team can keep up to S - kTeamPrefetch slots in flight: the SM
+// keeps streaming at its share of HBM through either team's fixed per-item phases.  (With
+// two CTAs of one team each, a CTA in its softmax sits on a full private ring, and the other
+// CTA's 80 KB in flight cannot carry the SM's share: 32-36 of 44 GB/s.)  Slots
+// are handed out from a free mask, so the producer publishes each team's n-th slot (and the
+// parity of its `full` phase) in the team's stage queue `sq`, behind an mbarrier `sqbar`.
+// TEAMS = 1: two CTAs per SM, each its own producer and pool (the former design, kept for
+// the g = 2 instantiations whose 32 KB W image leaves no room for two teams).
 #pragma once
 
 #include "attn_prepare.cuh"
@@ -23,17 +30,16 @@ namespace attn {
 #ifndef DQ_ATTN_WARPS
 #define DQ_ATTN_WARPS 8
 #endif
-constexpr int kWarps = DQ_ATTN_WARPS;       // consumer warps (8, or 16 with one CTA per SM)
-constexpr int kThreads = kWarps * 32;       // consumer threads
-constexpr int kCtaThreads = kThreads + 32;  // + the producer warp
+constexpr int kWarps = DQ_ATTN_WARPS;       // consumer warps per team
+constexpr int kThreads = kWarps * 32;       // consumer threads per team
+constexpr int kCtaThreads = kThreads + 32;  // one team + the producer warp
 constexpr int kD = 128;
 constexpr int kMaxR = 64;
 constexpr int kCB = 256;              // b rows per sub-item (at most)
 constexpr int kTiles = kCB / kI2Pad;  // 64-row tiles per sub-item (at most)
 constexpr int kNG = kCB / 16;         // 16-row groups per sub-item
 constexpr int kStageBytes = 16384;
-// ring depth and CTAs per SM: 2 CTAs x 5 x 16 KB stages for g = 1 (deep enough for a CTA
-// to keep streaming the next item through its own softmax + epilogue); g = 2 needs a
+// TEAMS = 1: ring depth and CTAs per SM: 2 CTAs x 5 x 16 KB stages for g = 1; g = 2 needs a
 // 32 KB W image, so 2 CTAs x 3 stages
 #ifndef DQ_ATTN_STAGES_G1
 #define DQ_ATTN_STAGES_G1 5
@@ -43,9 +49,19 @@ constexpr int kStageBytes = 16384;
 #endif
 template <int G>
 constexpr int kStagesOf = G == 1 ? DQ_ATTN_STAGES_G1 : 3;
-template <int G>
-constexpr int kCtasPerSm = G == 1 ? DQ_ATTN_CTAS_G1 : 2;
-constexpr int kSubRing = 8;           // descriptor ring (the producer runs <= 3 items ahead)
+template <int G, int TEAMS = 1>
+constexpr int kCtasPerSm = TEAMS > 1 ? 1 : (G == 1 ? DQ_ATTN_CTAS_G1 : 2);
+constexpr int kSubRing = 8;  // descriptor ring per team (the producer runs <= 3 items ahead)
+constexpr int kQ = 32;       // per-team stage queue (>= ring slots)
+// stages of a team's NEXT phase the producer issues while the team has not begun it
+#ifndef DQ_TEAM_PREFETCH
+#define DQ_TEAM_PREFETCH 3
+#endif
+constexpr int kTeamPrefetch = DQ_TEAM_PREFETCH;
+constexpr int kSmemCap = 227 * 1024;  // dynamic shared memory per CTA (sm_100)
+
+template <int TEAMS>
+constexpr int kCtaThreadsOf = TEAMS * kThreads + 32;
 
 template <int BITS>
 constexpr int kPBits = 15;  // P / tile max in (0.5, 1] -> round(P * 2^(kPBits - e)); Y sums per 64-row tile
@@ -60,21 +76,21 @@ struct SubItem {
   int seg, wb0, nbt, part;
   int r, i1, i2, item;
   int RK, nK, RV, nslices;  // K stages: RK bond rows x nbt tiles; V stages: (tile, slice of RV rows)
-  int stages, pad_[3];      // nbt == 0: end of this CTA's items
+  int stages, pad_[3];      // nbt == 0: end of this team's items
 };
 
-// NT: 64-row tiles per work item (4, or 8 for g = 1: twice the bytes per fixed per-item cost)
-template <int G, int NT = kTiles, bool ASYM = false>
-struct AttnSmem {
-  // 8-tile items with the asymmetric channel table: one stage less keeps 2 CTAs per SM
-  static constexpr int kStages = (ASYM && NT > kTiles) ? kStagesOf<G> - 1 : kStagesOf<G>;
-  alignas(128) unsigned char ring[kStages][kStageBytes];
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+// per-team state: descriptors, stage queue, W image / G0v, P, reductions
+template <int G, int NT, bool ASYM>
+struct TeamSmem {
   uint64_t wbar;   // W image (attn_prepare.cuh) by TMA, one phase per sub-item
   uint64_t g0bar;  // G0v prefetch, one phase per sub-item
-  uint64_t descfull[kSubRing];      // descriptor j written (producer arrival), phase j / kSubRing
-  SubItem sub[kSubRing];            // descriptor ring: the CTA's j-th item lives in slot j % kSubRing
+  uint64_t descfull[kSubRing];  // descriptor j written (producer arrival), phase j / kSubRing
+  uint64_t sqbar[kQ];           // stage n's slot published (producer arrival), phase n / kQ
+  int sq[kQ];                   // stage n of the team: ring slot | (full-barrier parity << 8)
+  int started;                  // phase the consumers began: 2j = K of item j, 2j + 1 = V of item j
+  int pad_[3];
+  int kend[kSubRing], vend[kSubRing];  // producer: team stage index where item j's K / V phase ends
+  SubItem sub[kSubRing];        // the team's j-th item lives in slot j % kSubRing
   alignas(16) WMeta<G> wmeta;  // per-column W scales and excess corrections (TMA target)
   int gamma[G][8][NT];     // excess correction of Y per 64-row tile: kExcess * sum_b Pint[a][b]
   float lsum[G][kWarps];   // probability mass per warp
@@ -94,6 +110,27 @@ struct AttnSmem {
   float rowmax[G][kWarps];
   // asymmetric mode: the segment's V channel table [2][r][16] (scales, zero points; r <= kMaxR)
   alignas(16) float vch[ASYM ? 2 * kMaxR * 16 : 4];
+};
+
+template <int G, int NT, bool ASYM, int TEAMS>
+constexpr int ring_stages() {
+  if constexpr (TEAMS == 1) {
+    // 8-tile items with the asymmetric channel table: one stage less keeps 2 CTAs per SM
+    return (ASYM && NT > kTiles) ? kStagesOf<G> - 1 : kStagesOf<G>;
+  } else {
+    const int s = (kSmemCap - TEAMS * (int)sizeof(TeamSmem<G, NT, ASYM>) - 256) / (kStageBytes + 16);
+    return s > 24 ? 24 : s;
+  }
+}
+
+// NT: 64-row tiles per work item (4, or 8 for g = 1: twice the bytes per fixed per-item cost)
+template <int G, int NT = kTiles, bool ASYM = false, int TEAMS = 1>
+struct AttnSmem {
+  static constexpr int kStages = ring_stages<G, NT, ASYM, TEAMS>();
+  alignas(128) unsigned char ring[kStages][kStageBytes];
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  TeamSmem<G, NT, ASYM> team[TEAMS];
 };
 
 // stage geometry of a sub-item with r bond rows and nbt tiles
@@ -134,38 +171,15 @@ __device__ __forceinline__ void load_sub(SubItem& d, const dq_attn_args& a, int 
   d = t;
 }
 
-// issue local stage `st` of a sub-item into its ring slot (one thread)
-template <int BITS>
-__device__ __forceinline__ void issue_stage(const SubItem& d, int st, unsigned char* slot_buf, uint64_t* bar) {
-  constexpr int RB = 2 * BITS;
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  const int bt0 = d.wb0 / kI2Pad;
-  if (st < d.nK) {
-    const int rk0 = st * d.RK;
-    const int nr = min(d.RK, d.r - rk0);
-    const uint32_t chunk = (uint32_t)(nr * kI2Pad * RB);
-    mbar_expect_tx(bar, chunk * d.nbt);
-    const unsigned char* src = d.kc + ((size_t)bt0 * d.r + rk0) * kI2Pad * RB;
-    for (int j = 0; j < d.nbt; ++j) bulk_g2s(slot_buf + j * chunk, src + (size_t)j * d.r * kI2Pad * RB, chunk, bar);
-  } else {
-    const int v = st - d.nK;
-    const int btl = v / d.nslices, sl = v - btl * d.nslices;
-    const uint32_t bytes = (uint32_t)(d.RV * 16 * kI2Pad * BITS / 8);
-    mbar_expect_tx(bar, bytes);
-    const unsigned char* src = d.vc + ((size_t)(bt0 + btl) * d.r + sl * d.RV) * 16 * kI2Pad * BITS / 8;
-    bulk_g2s(slot_buf, src, bytes, bar);
-  }
-}
-
-// the W image (limb chunks + metadata) of a sub-item's segment onto wbar (one thread)
+// the W image (limb chunks + metadata) of a sub-item's segment onto the team's wbar (one thread)
 template <int G, int NT, bool ASYM>
-__device__ __forceinline__ void issue_wimg(AttnSmem<G, NT, ASYM>& sm, const dq_attn_args& a, const SubItem& d) {
+__device__ __forceinline__ void issue_wimg(TeamSmem<G, NT, ASYM>& tm, const dq_attn_args& a, const SubItem& d) {
   const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
   const uint32_t wb = (uint32_t)(G * 2 * d.r * 8 * 16);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  mbar_expect_tx(&sm.wbar, wb + (uint32_t)sizeof(WMeta<G>));
-  bulk_g2s(sm.wg.w, img, wb, &sm.wbar);
-  bulk_g2s(&sm.wmeta, img + kWChunkBytes<G>, (uint32_t)sizeof(WMeta<G>), &sm.wbar);
+  mbar_expect_tx(&tm.wbar, wb + (uint32_t)sizeof(WMeta<G>));
+  bulk_g2s(tm.wg.w, img, wb, &tm.wbar);
+  bulk_g2s(&tm.wmeta, img + kWChunkBytes<G>, (uint32_t)sizeof(WMeta<G>), &tm.wbar);
 }
 
 template <int NT>
@@ -173,124 +187,261 @@ __device__ __forceinline__ int p_chunk(int h, int limb, int a, int bg) {
   return ((h * 2 + limb) * 8 + a) * (4 * NT) + (bg ^ (4 * (a & 1)));
 }
 
-template <int BITS, int G, int NT = kTiles, bool ASYM = false>
-__global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel(dq_attn_args args) {
-  constexpr int kStages = AttnSmem<G, NT, ASYM>::kStages;
+// non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// named barrier (1 + team) over one team's consumer threads
+__device__ __forceinline__ void team_sync(int team) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "r"(kThreads) : "memory");
+}
+
+// ---- the producer (lane 0 of the last warp) ---------------------------------------------
+// Per team: the issue geometry of the item being streamed (registers) and the next item's
+// descriptor, loaded into the team's descriptor ring as soon as its ticket is drawn.  Every
+// iteration reclaims the slots the teams released (test_wait on `empty`, in each team's stage
+// order), then issues one stage into a free slot for the eligible team with the fewest stages
+// in flight.  A team is eligible while its next stage lies before the end of the phase its
+// consumers have begun + kTeamPrefetch (TEAMS = 2; a lone team is never capped).
+struct Issue {  // what issuing a stage needs, kept in registers
+  const unsigned char* kc;
+  const unsigned char* vc;
+  int bt0, nbt, r, RK, nK, RV, nslices, stages;
+};
+
+__device__ __forceinline__ Issue issue_of(const SubItem& d) {
+  Issue it;
+  it.kc = d.kc;
+  it.vc = d.vc;
+  it.bt0 = d.wb0 / kI2Pad;
+  it.nbt = d.nbt;
+  it.r = d.r;
+  it.RK = d.RK;
+  it.nK = d.nK;
+  it.RV = d.RV;
+  it.nslices = d.nslices;
+  it.stages = d.stages;
+  return it;
+}
+
+// issue local stage `st` of an item into its ring slot (one thread)
+template <int BITS>
+__device__ __forceinline__ void issue_stage(const Issue& d, int st, unsigned char* slot_buf, uint64_t* bar) {
+  constexpr int RB = 2 * BITS;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (st < d.nK) {
+    const int rk0 = st * d.RK;
+    const int nr = min(d.RK, d.r - rk0);
+    const uint32_t chunk = (uint32_t)(nr * kI2Pad * RB);
+    mbar_expect_tx(bar, chunk * d.nbt);
+    const unsigned char* src = d.kc + ((size_t)d.bt0 * d.r + rk0) * kI2Pad * RB;
+    for (int j = 0; j < d.nbt; ++j) bulk_g2s(slot_buf + j * chunk, src + (size_t)j * d.r * kI2Pad * RB, chunk, bar);
+  } else {
+    const int v = st - d.nK;
+    const int btl = v / d.nslices, sl = v - btl * d.nslices;
+    const uint32_t bytes = (uint32_t)(d.RV * 16 * kI2Pad * BITS / 8);
+    mbar_expect_tx(bar, bytes);
+    const unsigned char* src = d.vc + ((size_t)(d.bt0 + btl) * d.r + sl * d.RV) * 16 * kI2Pad * BITS / 8;
+    bulk_g2s(slot_buf, src, bytes, bar);
+  }
+}
+
+struct TeamProd {
+  Issue cur;
+  int ls;        // next local stage of cur
+  int k;         // descriptors published
+  int issued, reclaimed;
+  bool hc, hn;   // streaming an item / the next item's descriptor is loaded (slot k % kSubRing)
+};
+
+template <int BITS, int G, int NT, bool ASYM, int TEAMS>
+__device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args) {
+  using TS = TeamSmem<G, NT, ASYM>;
+  constexpr int S = AttnSmem<G, NT, ASYM, TEAMS>::kStages;
+  uint32_t freemask = S >= 32 ? ~0u : ((1u << S) - 1u);
+  uint32_t parity = 0;  // bit s: parity of slot s's next use
+  bool waited = false;  // griddepcontrol.wait before the first ticket (the counter is shared with
+                        // the previous launch on these args)
+  TeamProd P[TEAMS];
+
+  // descriptor P.k (loaded into its ring slot, or the end marker) becomes current and is published
+  auto advance = [&](TeamProd& p, TS& tm) {
+    const int ds = p.k % kSubRing;
+    p.hc = p.hn;
+    p.hn = false;
+    p.ls = 0;
+    if (p.hc) {
+      p.cur = issue_of(tm.sub[ds]);
+      tm.kend[ds] = p.issued + p.cur.nK;
+      tm.vend[ds] = p.issued + p.cur.stages;
+    } else {
+      tm.sub[ds].nbt = 0;
+    }
+    mbar_arrive(&tm.descfull[ds]);  // release: the descriptor is visible to its waiters
+    ++p.k;
+  };
+  auto reclaim = [&](TeamProd& p, TS& tm) {
+    while (p.reclaimed < p.issued) {
+      const int e = tm.sq[p.reclaimed % kQ];
+      if (!mbar_test(&sm.empty[e & 0xFF], (uint32_t)(e >> 8))) break;
+      freemask |= 1u << (e & 0xFF);
+      ++p.reclaimed;
+    }
+  };
+  auto eligible = [&](const TeamProd& p, TS& tm) -> bool {
+    if (!p.hc || p.issued - p.reclaimed >= kQ) return false;
+    if (TEAMS == 1) return true;
+    const int ph = *reinterpret_cast<volatile int*>(&tm.started);
+    const int jp = (ph >> 1) % kSubRing;
+    const int end = (ph & 1) ? tm.vend[jp] : tm.kend[jp];
+    return p.issued < end + kTeamPrefetch;
+  };
+  auto step = [&](TeamProd& p, TS& tm) {
+    const int slot = __ffs(freemask) - 1;
+    freemask &= freemask - 1;
+    const uint32_t par = (parity >> slot) & 1u;
+    parity ^= 1u << slot;
+    tm.sq[p.issued % kQ] = slot | (int)(par << 8);
+    mbar_arrive(&tm.sqbar[p.issued % kQ]);
+    issue_stage<BITS>(p.cur, p.ls, sm.ring[slot], &sm.full[slot]);
+    ++p.issued;
+    ++p.ls;
+    if (p.ls == min(3, p.cur.stages)) {
+      if (!waited) {
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        waited = true;
+      }
+      // the team's next item: ticket, then its descriptor straight into the ring slot
+      const int nx = TEAMS * (int)gridDim.x + atomicAdd(args.sched, 1);
+      p.hn = nx < args.nwork;
+      if (p.hn) load_sub<BITS>(tm.sub[p.k % kSubRing], args, nx);
+    }
+    if (p.ls == p.cur.stages) advance(p, tm);  // item fully issued: the next one becomes current
+  };
+
+#pragma unroll
+  for (int t = 0; t < TEAMS; ++t) {
+    const int first = (int)blockIdx.x + t * (int)gridDim.x;
+    P[t].k = P[t].issued = P[t].reclaimed = 0;
+    P[t].hn = first < args.nwork;
+    if (P[t].hn) load_sub<BITS>(sm.team[t].sub[0], args, first);
+    advance(P[t], sm.team[t]);
+  }
+  for (;;) {
+    reclaim(P[0], sm.team[0]);
+    if constexpr (TEAMS > 1) reclaim(P[1], sm.team[1]);
+    bool any = P[0].hc;
+    if constexpr (TEAMS > 1) any |= P[1].hc;
+    if (!any) break;
+    if (!freemask) continue;
+    const bool e0 = eligible(P[0], sm.team[0]);
+    if constexpr (TEAMS > 1) {
+      const bool e1 = eligible(P[1], sm.team[1]);
+      if (e1 && (!e0 || P[1].issued - P[1].reclaimed < P[0].issued - P[0].reclaimed)) {
+        step(P[1], sm.team[1]);
+        continue;
+      }
+    }
+    if (e0) step(P[0], sm.team[0]);
+  }
+  // retire: the last CTA to finish drawing resets the counters for the next launch
+  if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  __threadfence();
+  if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
+    args.sched[0] = 0;
+    args.sched[1] = 0;
+  }
+}
+
+template <int BITS, int G, int NT = kTiles, bool ASYM = false, int TEAMS = 1>
+__global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) decode_attn_kernel(dq_attn_args args) {
   constexpr int RB = 2 * BITS;
   constexpr int X = kExcess<BITS>;
   constexpr bool SA = BITS == 8;  // A operand (codes) signed
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  AttnSmem<G, NT, ASYM>& sm = *reinterpret_cast<AttnSmem<G, NT, ASYM>*>(smem_raw);
+  AttnSmem<G, NT, ASYM, TEAMS>& sm = *reinterpret_cast<AttnSmem<G, NT, ASYM, TEAMS>*>(smem_raw);
+  constexpr int S = AttnSmem<G, NT, ASYM, TEAMS>::kStages;
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = warp_all / kWarps;                 // == TEAMS for the producer warp
+  const int warp = warp_all - team * kWarps;          // warp within the team
+  const int tid = (int)threadIdx.x - team * kThreads;  // thread within the team
   const int gid = lane >> 2, tid4 = lane & 3;
 
   // ---- prologue: barriers ---------------------------------------------------------------
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kWarps);
     }
-    for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.descfull[s], 1);
-    mbar_init(&sm.wbar, 1);
-    mbar_init(&sm.g0bar, 1);
+    for (int t = 0; t < TEAMS; ++t) {
+      for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.team[t].descfull[s], 1);
+      for (int s = 0; s < kQ; ++s) mbar_init(&sm.team[t].sqbar[s], 1);
+      mbar_init(&sm.team[t].wbar, 1);
+      mbar_init(&sm.team[t].g0bar, 1);
+      sm.team[t].started = 0;  // item 0's K phase: issue it whole before the consumers arrive
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (tid < G * 8 * NT) {
-    (&sm.gamma[0][0][0])[tid] = 0;
-    (&sm.pmax[0][0][0])[tid] = 0u;
+  if (team < TEAMS && tid < G * 8 * NT) {
+    (&sm.team[team].gamma[0][0][0])[tid] = 0;
+    (&sm.team[team].pmax[0][0][0])[tid] = 0u;
   }
-  __syncthreads();  // barrier inits visible to all 9 warps
+  __syncthreads();  // barrier inits visible to every warp
 
-  if (warp == kWarps) {
-    // ---- producer: descriptors and code stages of this CTA's items, in order ----------------
-    // (the code does not depend on the prepare kernel, so no griddepcontrol.wait here)
-    if (lane == 0) {
-      SubItem nd;
-      bool have = (int)blockIdx.x < args.nwork;
-      if (have) load_sub<BITS>(nd, args, blockIdx.x);
-      int g = 0;  // global stage index
-      for (int k = 0;; ++k) {
-        const int ds = k % kSubRing;
-        if (!have) {
-          sm.sub[ds].nbt = 0;
-          mbar_arrive(&sm.descfull[ds]);
-          break;
-        }
-        const SubItem d = nd;
-        sm.sub[ds] = d;
-        mbar_arrive(&sm.descfull[ds]);  // release: the descriptor is visible to its waiters
-        bool nhave = false;
-        for (int ls = 0; ls < d.stages; ++ls, ++g) {
-          const int slot = g % kStages;
-          if (g >= kStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kStages - 1) & 1));
-          issue_stage<BITS>(d, ls, sm.ring[slot], &sm.full[slot]);
-          if (ls == min(2, d.stages - 1)) {
-            // the ticket counter is shared with the previous launch on these args: under
-            // programmatic dependent launch, wait for that grid before drawing from it
-            if (k == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");
-            // the next item, fetched while the ring is full: ticket, then its descriptor
-            const int nxt = (int)gridDim.x + atomicAdd(args.sched, 1);
-            nhave = nxt < args.nwork;
-            if (nhave) load_sub<BITS>(nd, args, nxt);
-          }
-        }
-        have = nhave;
-      }
-      // retire: the last CTA to draw its final ticket resets the counters for the next launch
-      __threadfence();
-      if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
-        args.sched[0] = 0;
-        args.sched[1] = 0;
-      }
-    }
+  if (team == TEAMS) {
+    // ---- producer: descriptors and code stages of this CTA's items ----------------------
+    // (the code does not depend on the prepare kernel, so no griddepcontrol.wait before
+    // the first stages)
+    if (lane == 0) produce<BITS, G, NT, ASYM, TEAMS>(sm, args);
     return;
   }
+  TeamSmem<G, NT, ASYM>& tm = sm.team[team];
 
   if (tid == 0) {
-    mbar_wait(&sm.descfull[0], 0);
+    mbar_wait(&tm.descfull[0], 0);
     // programmatic dependent launch: everything above overlapped the prepare kernel; its
     // output (the per-segment W images) is read from here on
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
-    if (sm.sub[0].nbt > 0) issue_wimg<G, NT, ASYM>(sm, args, sm.sub[0]);
+    if (tm.sub[0].nbt > 0) issue_wimg<G, NT, ASYM>(tm, args, tm.sub[0]);
   }
 
-  int st = 0;  // running global stage index (identical in every consumer thread)
-  auto release = [&](int s) {
+  int st = 0;  // the team's running stage index (identical in every thread of the team)
+  auto acquire = [&]() -> int {  // slot of stage st, once its codes have landed
+    mbar_wait(&tm.sqbar[st % kQ], (uint32_t)((st / kQ) & 1));
+    const int e = tm.sq[st % kQ];
+    mbar_wait(&sm.full[e & 0xFF], (uint32_t)(e >> 8));
+    return e & 0xFF;
+  };
+  auto release = [&](int slot) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[s % kStages]);
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+  };
+  auto begin_phase = [&](int ph) {
+    if (tid == 0) *reinterpret_cast<volatile int*>(&tm.started) = ph;
   };
 
   for (int j = 0;; ++j) {
-    mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
-    const SubItem d = sm.sub[j % kSubRing];
+    mbar_wait(&tm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
+    const SubItem d = tm.sub[j % kSubRing];
     if (d.nbt == 0) break;
-    const int wi = d.item;
     const int r = d.r, i1 = d.i1, i2 = d.i2, wb0 = d.wb0;
     const int nbt = d.nbt;
-#ifdef DQ_ATTN_WARP_TRACE  // profiling build: trace = [nwork][kWarps][8] per-warp stamps
-    auto stamp = [&](int) {};
-    auto wstamp = [&](int k) {
-      if (args.trace && lane == 0) args.trace[((size_t)wi * kWarps + warp) * 8 + k] = global_ns();
-    };
-#else
-    auto stamp = [&](int k) {  // optional per-sub-item phase timestamps (profiling only)
-      if (args.trace && tid == 0) args.trace[(size_t)wi * 8 + k] = global_ns();
-    };
-    auto wstamp = [&](int) {};
-#endif
-    stamp(0);
-#ifndef DQ_ATTN_WARP_TRACE  // slots 6 and 7 of the per-item trace (the per-warp trace uses them)
-    if (args.trace && tid == 0) {
-      args.trace[(size_t)wi * 8 + 6] = blockIdx.x;
-      args.trace[(size_t)wi * 8 + 7] = sm_id();
-    }
-#endif
-    mbar_wait(&sm.wbar, (uint32_t)(j & 1));
+    begin_phase(2 * j);
+    mbar_wait(&tm.wbar, (uint32_t)(j & 1));
 
-    stamp(1);
-    wstamp(0);
     // ---- phase 1: S = W . codes_k on the int8 tensor pipe ------------------------------
     constexpr int kWpt = kWarps / NT;       // warps per 64-row tile
     constexpr int MT = 4 / kWpt;            // 16-row m-tiles per warp
@@ -316,8 +467,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         int bt[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          cs[q] = kscale * sm.wmeta.cs[h][2 * tid4 + q][grp];
-          bt[q] = sm.wmeta.beta[h][2 * tid4 + q][grp];
+          cs[q] = kscale * tm.wmeta.cs[h][2 * tid4 + q][grp];
+          bt[q] = tm.wmeta.beta[h][2 * tid4 + q][grp];
         }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
@@ -339,13 +490,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       row_off[mt][0] = (tid4 * kI2Pad + (b0 ^ swz)) * RB;
       row_off[mt][1] = (tid4 * kI2Pad + ((b0 + 8) ^ swz)) * RB;
     }
-    const uint4* wthr = sm.wg.w + tid4 * 8 + (gid ^ (2 * tid4));
+    const uint4* wthr = tm.wg.w + tid4 * 8 + (gid ^ (2 * tid4));
     const int wl = r * 8;  // chunks per (head, limb)
     for (int ks = 0; ks < d.nK; ++ks, ++st) {
-      const int slot = st % kStages;
-      mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
+      const int slot = acquire();
 #ifdef DQ_ATTN_NULL_CONSUMER  // measurement only: the memory pipeline without the contractions
-      release(st);
+      release(slot);
       continue;
 #endif
       const int rk0 = ks * d.RK;
@@ -376,25 +526,21 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
           if (rk0 + q0 + 4 == kGroupR) flush_group(0);  // leading bond rows carry their own W scale
         }
       }
-      release(st);
+      release(slot);
     }
     if (r > kGroupR) flush_group(1);
 #ifdef DQ_ATTN_NULL_STREAM  // measurement only: the producer / ring / scheduler alone
-    for (int vs = 0; vs < nbt * d.nslices; ++vs, ++st) {
-      mbar_wait(&sm.full[st % kStages], (uint32_t)((st / kStages) & 1));
-      release(st);
-    }
-    named_sync(kThreads);
+    begin_phase(2 * j + 1);
+    for (int vs = 0; vs < nbt * d.nslices; ++vs, ++st) release(acquire());
+    team_sync(team);
     if (tid == 0) {
       const int jn = j + 1;
-      mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(sm, args, sm.sub[jn % kSubRing]);
+      mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
+      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(tm, args, tm.sub[jn % kSubRing]);
     }
     continue;
 #endif
 
-    stamp(2);
-    wstamp(1);
     // ---- phase 2: softmax of the sub-item straight from the accumulators --------------
     float sv[MT][G][4];
     float mh[G];
@@ -412,10 +558,9 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
           m = fmaxf(m, sv[mt][h][k]);
         }
       for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) sm.rowmax[h][warp] = m;
+      if (lane == 0) tm.rowmax[h][warp] = m;
     }
-    named_sync(kThreads);  // every warp is past phase 1: the W buffer is dead
-    wstamp(2);
+    team_sync(team);  // every warp is past phase 1: the W buffer is dead
     if (lane == 0 && warp < i1) {  // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
       // one copy per a, issued by warp a, into blocks of 2r + 1 float4s: the epilogue's lanes
       // tid4 = 0..3 read a = 2 tid4 + aa, and the pad puts their blocks 32 bytes apart in the
@@ -425,21 +570,21 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       const uint32_t cb = ASYM ? (uint32_t)(2 * r * 16 * 4) : 0u;
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       if (warp == 0) {
-        mbar_expect_tx(&sm.g0bar, (uint32_t)(i1 * r * 32) + cb);
-        if (ASYM) bulk_g2s(sm.vch, args.segs[d.seg].v_ch, cb, &sm.g0bar);
+        mbar_expect_tx(&tm.g0bar, (uint32_t)(i1 * r * 32) + cb);
+        if (ASYM) bulk_g2s(tm.vch, args.segs[d.seg].v_ch, cb, &tm.g0bar);
       }
-      bulk_g2s(sm.wg.g0v + warp * (2 * r + 1), reinterpret_cast<const float4*>(d.vg0) + warp * 2 * r,
-               (uint32_t)(r * 32), &sm.g0bar);
+      bulk_g2s(tm.wg.g0v + warp * (2 * r + 1), reinterpret_cast<const float4*>(d.vg0) + warp * 2 * r,
+               (uint32_t)(r * 32), &tm.g0bar);
     }
-    unsigned char* pb = reinterpret_cast<unsigned char*>(sm.pr.p);
+    unsigned char* pb = reinterpret_cast<unsigned char*>(tm.pr.p);
     // P = exp2(s - m) in fixed point with one scale per (h, a, 64-row tile), set by that
     // tile's largest probability: small probabilities far from the peak keep their
     // relative precision (the V side combines its accumulators per tile anyway)
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      float m = sm.rowmax[h][0];
+      float m = tm.rowmax[h][0];
 #pragma unroll
-      for (int w = 1; w < kWarps; ++w) m = fmaxf(m, sm.rowmax[h][w]);
+      for (int w = 1; w < kWarps; ++w) m = fmaxf(m, tm.rowmax[h][w]);
       mh[h] = m;
       float tmax[2] = {0.f, 0.f};
 #pragma unroll
@@ -456,11 +601,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
         v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
         v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
-        if (gid == 0 && jt < nbt) atomicMax(&sm.pmax[h][2 * tid4 + q][jt], __float_as_uint(v));
+        if (gid == 0 && jt < nbt) atomicMax(&tm.pmax[h][2 * tid4 + q][jt], __float_as_uint(v));
       }
     }
-    named_sync(kThreads);  // per-tile probability maxima complete
-    wstamp(3);
+    team_sync(team);  // per-tile probability maxima complete
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float lsum = 0.f;
@@ -468,7 +612,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       float pq[2], pinv[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const float pm = __uint_as_float(sm.pmax[h][2 * tid4 + q][min(jt, NT - 1)]);
+        const float pm = __uint_as_float(tm.pmax[h][2 * tid4 + q][min(jt, NT - 1)]);
         pq[q] = pow2_sub_exp(pm, kPBits<BITS>);
         pinv[q] = pow2_exp_sub(pm, kPBits<BITS>);
       }
@@ -495,15 +639,14 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         v += __shfl_xor_sync(0xffffffffu, v, 8);
         v += __shfl_xor_sync(0xffffffffu, v, 16);
         // gamma = X sum_b Pint (symmetric), sum_b Pint (asymmetric: the zero point is per channel)
-        if (X && gid == 0 && jt < nbt) atomicAdd(&sm.gamma[h][2 * tid4 + q][jt], ASYM ? v : X * v);
+        if (X && gid == 0 && jt < nbt) atomicAdd(&tm.gamma[h][2 * tid4 + q][jt], ASYM ? v : X * v);
       }
       for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-      if (lane == 0) sm.lsum[h][warp] = lsum;
+      if (lane == 0) tm.lsum[h][warp] = lsum;
     }
-    named_sync(kThreads);  // P limbs, gamma and lsum complete
-    wstamp(4);
+    team_sync(team);  // P limbs, gamma and lsum complete
+    begin_phase(2 * j + 1);
 
-    stamp(3);
     // ---- phase 3: Y = codes_v . P^T on the int8 tensor pipe ----------------------------
     // warp w owns bond rows w*rw .. w*rw+rw-1 (an m-tile = one bond row x 16 e)
     const int rw = r / kWarps;
@@ -519,13 +662,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
 #pragma unroll
         for (int k = 0; k < 4; ++k) accv[t][h][k] = 0.f;
     const int nV = nbt * d.nslices;
-    if (ASYM) mbar_wait(&sm.g0bar, (uint32_t)(j & 1));  // the V zero points seed the accumulators
+    if (ASYM) mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // the V zero points seed the accumulators
     for (int vs = 0, btl = 0, sl = 0; vs < nV; ++vs, ++st) {
-      const int slot = st % kStages;
-      mbar_wait(&sm.full[slot], (uint32_t)((st / kStages) & 1));
+      const int slot = acquire();
 #ifdef DQ_ATTN_NULL_CONSUMER
       if (++sl == d.nslices) sl = 0, ++btl;
-      release(st);
+      release(slot);
       continue;
 #endif
       if (sl == my_slice) {
@@ -534,12 +676,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         float pinv[G][2];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          ph[h] = sm.pr.p[p_chunk<NT>(h, 0, gid, btl * 4 + tid4)];
-          pl_[h] = sm.pr.p[p_chunk<NT>(h, 1, gid, btl * 4 + tid4)];
+          ph[h] = tm.pr.p[p_chunk<NT>(h, 0, gid, btl * 4 + tid4)];
+          pl_[h] = tm.pr.p[p_chunk<NT>(h, 1, gid, btl * 4 + tid4)];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            gam[h][q] = sm.gamma[h][2 * tid4 + q][btl];
-            pinv[h][q] = pow2_exp_sub(__uint_as_float(sm.pmax[h][2 * tid4 + q][btl]), kPBits<BITS>);
+            gam[h][q] = tm.gamma[h][2 * tid4 + q][btl];
+            pinv[h][q] = pow2_exp_sub(__uint_as_float(tm.pmax[h][2 * tid4 + q][btl]), kPBits<BITS>);
           }
         }
         const unsigned char* buf = sm.ring[slot];
@@ -553,8 +695,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
             int z0 = 1, z1 = 1;  // asymmetric: zero points of (bond row, e = gid / gid + 8)
             if (ASYM) {
               const int rr = warp * rw + t;
-              z0 = (int)sm.vch[r * 16 + rr * 16 + gid];  // zero points follow the scales
-              z1 = (int)sm.vch[r * 16 + rr * 16 + gid + 8];
+              z0 = (int)tm.vch[r * 16 + rr * 16 + gid];  // zero points follow the scales
+              z1 = (int)tm.vch[r * 16 + rr * 16 + gid + 8];
             }
 #pragma unroll
             for (int h = 0; h < G; ++h) {
@@ -573,12 +715,10 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
           }
         }
       }
-      release(st);
+      release(slot);
       if (++sl == d.nslices) sl = 0, ++btl;
     }
 
-    stamp(4);
-    wstamp(5);
     // ---- phase 4: O = scale_v * G0v . Y on CUDA cores, reduce, write the partial -------
     // accv[t][h]: rows e = gid (k 0,1) / gid+8 (k 2,3); cols a = 2*tid4 + (k & 1)
     float part[G][16];  // [h][c*2 + (e == gid+8)]
@@ -586,8 +726,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
     for (int h = 0; h < G; ++h)
 #pragma unroll
       for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
-    mbar_wait(&sm.g0bar, (uint32_t)(j & 1));  // fp32 G0v [a][rr][c] (normalised), in the W buffer
-    const float4* g0v = sm.wg.g0v;
+    mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // fp32 G0v [a][rr][c] (normalised), in the W buffer
+    const float4* g0v = tm.wg.g0v;
 #ifdef DQ_ATTN_NULL_FOLD  // measurement only: no G0v fold (wrong results), Y still consumed
 #pragma unroll
     for (int t = 0; t < kRw; ++t)
@@ -602,7 +742,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
       if (t < rw) {
         const int rr = warp * rw + t;
         // asymmetric: the per-(bond row, e) channel scales of V
-        const float s0 = ASYM ? sm.vch[rr * 16 + gid] : 1.f, s1 = ASYM ? sm.vch[rr * 16 + gid + 8] : 1.f;
+        const float s0 = ASYM ? tm.vch[rr * 16 + gid] : 1.f, s1 = ASYM ? tm.vch[rr * 16 + gid + 8] : 1.f;
 #pragma unroll
         for (int aa = 0; aa < 2; ++aa) {
           const int a = 2 * tid4 + aa;
@@ -629,16 +769,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
         v += __shfl_xor_sync(0xffffffffu, v, 2);
         part[h][k] = v;
       }
-    named_sync(kThreads);  // every warp is past the V stages and G0v: P and W/G0v buffers are free
-    wstamp(6);
+    team_sync(team);  // every warp is past the V stages and G0v: P and W/G0v buffers are free
     if (tid == 0) {
       const int jn = j + 1;
-      mbar_wait(&sm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (sm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(sm, args, sm.sub[jn % kSubRing]);
+      mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
+      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(tm, args, tm.sub[jn % kSubRing]);
     }
     if (tid < G * 8 * NT) {
-      (&sm.gamma[0][0][0])[tid] = 0;
-      (&sm.pmax[0][0][0])[tid] = 0u;
+      (&tm.gamma[0][0][0])[tid] = 0;
+      (&tm.pmax[0][0][0])[tid] = 0u;
     }
 #pragma unroll
     for (int h = 0; h < G; ++h)
@@ -652,26 +791,24 @@ __global__ void __launch_bounds__(kCtaThreads, kCtasPerSm<G>) decode_attn_kernel
             v0 = part[h][2 * k];
             v1 = part[h][2 * k + 1];
           }
-        sm.pr.red[warp][h][c * 16 + gid] = v0;
-        sm.pr.red[warp][h][c * 16 + gid + 8] = v1;
+        tm.pr.red[warp][h][c * 16 + gid] = v0;
+        tm.pr.red[warp][h][c * 16 + gid + 8] = v1;
       }
-    named_sync(kThreads);
+    team_sync(team);
     for (int i = tid; i < G * kD; i += kThreads) {
       const int h = i / kD, dd = i % kD;
       float v = 0.f;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) v += sm.pr.red[w][h][dd];
+      for (int w = 0; w < kWarps; ++w) v += tm.pr.red[w][h][dd];
       args.part_o[((size_t)d.part * G + h) * kD + dd] = v * d.vscale;
     }
     if (tid < G) {
       float l = 0.f;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) l += sm.lsum[tid][w];
+      for (int w = 0; w < kWarps; ++w) l += tm.lsum[tid][w];
       args.part_ml[((size_t)d.part * G + tid) * 2 + 0] = mh[tid];  // log2 domain
       args.part_ml[((size_t)d.part * G + tid) * 2 + 1] = l;
     }
-    stamp(5);
-    wstamp(7);
   }
 }
 

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_attn_tc_kernel(dq_attn_a
         for (int ls = 0; ls < d.stages; ++ls, ++g) {
           const int slot = g % kTcStages;
           if (g >= kTcStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kTcStages - 1) & 1));
-          issue_stage<4>(d, ls, sm.ring[slot], &sm.full[slot]);
+          issue_stage<4>(issue_of(d), ls, sm.ring[slot], &sm.full[slot]);
           if (ls == min(2, d.stages - 1)) {
             // the ticket counter is shared with the previous launch on these args: under
             // programmatic dependent launch, wait for that grid before drawing from it

@@ -78,12 +78,13 @@ __global__ void quantize_pack_kernel(const float* __restrict__ t, int64_t count,
   const float scale = rtn_scale(amax, qmax, &degenerate);
   if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = scale;
   const int64_t nbytes = payload_bytes(count, bits);
+  const double rinv = amax > 0.0 ? 1.0 / amax : 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nbytes; i += (int64_t)gridDim.x * blockDim.x) {
     unsigned v = 0;
     if (!degenerate) {
       for (int k = 0; k < per; ++k) {
         const int64_t idx = i * per + k;
-        if (idx < count) v |= ((unsigned)rtn_code(t[idx], qmax, amax) & mask) << (k * bits);
+        if (idx < count) v |= ((unsigned)rtn_code_fast(t[idx], qmax, amax, rinv) & mask) << (k * bits);
       }
     }
     out[i] = (uint8_t)v;

@@ -144,6 +144,22 @@ __device__ __forceinline__ int rtn_code_f64(double t, int qmax, double amax) {
   return y < 0.0 ? -(int)c : (int)c;
 }
 
+// rtn_code without the fp64 division on the common path: y ~ RN(t*qmax) * RN(1/amax) is within
+// ~2^-51 relative of RN(RN(t*qmax)/amax) (|y| <= 127), so whenever |y| + 1/2 lies more than 1e-9
+// from an integer the rounded code is the same; near a rounding boundary (exact ties
+// included) the exact division decides
+__device__ __forceinline__ int rtn_code_fast(float t, int qmax, double amax, double rinv) {
+  const double yt = __dmul_rn((double)t, (double)qmax);
+  const double ya = yt * rinv;
+  const double f = fabs(ya) + 0.5;
+  const double fl = floor(f);
+  if (f - fl > 1e-9 && fl + 1.0 - f > 1e-9) {
+    const int c = min((int)fl, qmax);
+    return ya < 0.0 ? -c : c;
+  }
+  return rtn_code(t, qmax, amax);
+}
+
 // quantize.py:135-140: f32(amax/qmax), or 1.0 when amax == 0 or the step underflows
 __host__ __device__ inline float rtn_scale(double amax, int qmax, bool* degenerate) {
   float s = amax > 0.0 ? (float)(amax / (double)qmax) : 1.0f;

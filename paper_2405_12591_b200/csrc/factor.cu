@@ -28,6 +28,14 @@ constexpr int kR = 64;       // max bond dimension handled (i1, j1 <= 8)
 constexpr int kTile = 64;    // contraction tile
 constexpr int kThreads = 256;
 constexpr int kMaxSweeps = 40;
+// rotation threshold relative to sqrt(g_pp g_qq): ~20 ulp.  Rotations below it only stir the
+// rounding noise of the converged matrix (a 1-ulp threshold can keep that going for dozens
+// of sweeps); the eigenvectors it leaves are accurate to ~1e-14, far inside the 1e-5 factor
+// tolerance
+#ifndef DQ_JACOBI_TOL
+#define DQ_JACOBI_TOL 2e-15
+#endif
+constexpr double kJacobiTol = DQ_JACOBI_TOL;
 
 struct Dims {
   int rows, cols;
@@ -136,6 +144,16 @@ __global__ void __launch_bounds__(kThreads) gram_kernel(const void* __restrict__
 }
 
 // ---- parallel cyclic Jacobi eigensolver on one r x r Gram per CTA ---------
+// Round-robin (circle-method) ordering: every round rotates N/2 disjoint pairs (p, q).
+// One round = (a) warp 0 computes the N/2 rotation angles, (b) every thread applies both
+// sides of the rotation, G <- J^T G J, to its 2x2 blocks (pair i rows x pair j columns, i <= j,
+// mirrored) and V <- V J to its column pairs: two CTA barriers per round.  The angle t is
+// computed in fp32 on the fp64 entries scaled by 1/max(diag G) (an inexact angle only slows
+// the annihilation, it is not an error), then c = (1 + t^2)^-1/2 by rsqrtf + two fp64 Newton
+// steps and s = t c, so every rotation is orthogonal to fp64 rounding.  A pair is rotated
+// while |g_pq| > max(1e-16 sqrt(|g_pp g_qq|), 1e-17 max(diag G)): the absolute floor stops
+// rotations among numerically-zero eigenvalues (rank-deficient blocks: repeated or
+// all-equal rows) that the relative test alone would chase forever.
 struct JacobiSmem {
   double g[kR][kR + 1];
   double v[kR][kR + 1];
@@ -143,8 +161,15 @@ struct JacobiSmem {
   int pp[kR / 2], qq[kR / 2];
   double lam[kR];
   int perm[kR];
-  int rotations;
+  int rotated;  // any rotation in the finished sweep
 };
+
+__device__ __forceinline__ double rsqrt_f64(double x) {
+  double y = (double)rsqrtf((float)x);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  return y;
+}
 
 __global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restrict__ G, Dims d,
                                                           double* __restrict__ U, double* __restrict__ lam_out,
@@ -164,69 +189,110 @@ __global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restri
     sm.v[p][q] = p == q ? 1.0 : 0.0;
   }
   __syncthreads();
+  if (threadIdx.x < 32) {  // max diagonal: the scale of the angle arithmetic
+    double m = 0.0;
+    for (int p = threadIdx.x; p < r; p += 32) m = fmax(m, fabs(sm.g[p][p]));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) sm.lam[0] = m;
+  }
+  __syncthreads();
+  const double gmax = sm.lam[0];
+  const double inv_gmax = gmax > 0.0 ? 1.0 / gmax : 0.0;
+  const double abs_floor = 1e-17 * gmax;
+  // blocks (i, j), i <= j, of the pair grid: npairs * (npairs + 1) / 2 per round
+  const int nblocks = npairs * (npairs + 1) / 2;
 
-  bool converged = false;
-  for (int sweep = 0; sweep < kMaxSweeps && !converged; ++sweep) {
-    if (threadIdx.x == 0) sm.rotations = 0;
-    __syncthreads();
+  bool converged = gmax == 0.0;
+  int sweep = 0;
+  for (; sweep < kMaxSweeps && !converged; ++sweep) {
+    bool rot = false;  // warp 0: any rotation this sweep
     for (int round = 0; round < N - 1; ++round) {
-      if (threadIdx.x < npairs) {
-        const int i = threadIdx.x;
-        // circle method: slot 0 fixed, slots 1..N-1 rotate by `round`
-        const int sa = i, sb = N - 1 - i;
-        int pa = sa == 0 ? 0 : ((sa - 1 + round) % (N - 1)) + 1;
-        int pb = ((sb - 1 + round) % (N - 1)) + 1;
-        int p = min(pa, pb), q = max(pa, pb);
-        double cc = 1.0, ss = 0.0;
-        if (q < r) {
-          const double app = sm.g[p][p], aqq = sm.g[q][q], apq = sm.g[p][q];
-          const double thr = 1e-16 * sqrt(fabs(app) * fabs(aqq));
-          if (apq != 0.0 && fabs(apq) > thr) {
-            // sym.schur2 (Golub & Van Loan 8.4.2)
-            const double tau = (aqq - app) / (2.0 * apq);
-            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            cc = 1.0 / sqrt(1.0 + t * t);
-            ss = t * cc;
-            if (ss != 0.0) atomicAdd(&sm.rotations, 1);
+      if (threadIdx.x < 32) {
+        for (int i = threadIdx.x; i < npairs; i += 32) {
+          // circle method: slot 0 fixed, slots 1..N-1 rotate by `round`
+          const int sa = i, sb = N - 1 - i;
+          const int pa = sa == 0 ? 0 : ((sa - 1 + round) % (N - 1)) + 1;
+          const int pb = ((sb - 1 + round) % (N - 1)) + 1;
+          const int p = min(pa, pb), q = max(pa, pb);
+          double cc = 1.0, ss = 0.0;
+          if (q < r) {
+            const double app = sm.g[p][p], aqq = sm.g[q][q], apq = sm.g[p][q];
+            const double thr = fmax(kJacobiTol * sqrt(fabs(app) * fabs(aqq)), abs_floor);
+            if (fabs(apq) > thr) {
+              // sym.schur2 (Golub & Van Loan 8.4.2) with tau in fp32
+              const float tau = (float)((aqq - app) * inv_gmax) / (2.f * (float)(apq * inv_gmax));
+              const float at = fabsf(tau);
+              const float t = at > 1e15f ? 0.5f / tau : copysignf(1.f, tau) / (at + sqrtf(fmaf(tau, tau, 1.f)));
+              const double td = (double)t;
+              cc = rsqrt_f64(fma(td, td, 1.0));
+              ss = td * cc;
+              rot |= ss != 0.0;
+            }
           }
+          sm.pp[i] = p;
+          sm.qq[i] = q;
+          sm.c[i] = cc;
+          sm.s[i] = ss;
         }
-        sm.pp[i] = p;
-        sm.qq[i] = q;
-        sm.c[i] = cc;
-        sm.s[i] = ss;
       }
       __syncthreads();
-      // rows: G <- J^T G
-      for (int idx = threadIdx.x; idx < npairs * N; idx += blockDim.x) {
-        const int i = idx / N, k = idx - i * N;
-        const double ss = sm.s[i];
-        if (ss == 0.0 || k >= r || sm.qq[i] >= r) continue;
-        const int p = sm.pp[i], q = sm.qq[i];
-        const double cc = sm.c[i];
-        const double gp = sm.g[p][k], gq = sm.g[q][k];
-        sm.g[p][k] = cc * gp - ss * gq;
-        sm.g[q][k] = ss * gp + cc * gq;
+      // G <- J^T G J on 2x2 blocks (rows of pair i, columns of pair j), mirrored below the diagonal
+      for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+        // b -> (i, j) with i <= j: row-major over the upper triangle
+        int i = 0, rem = b;
+        while (rem >= npairs - i) {
+          rem -= npairs - i;
+          ++i;
+        }
+        const int j = i + rem;
+        const double si = sm.s[i], sj = sm.s[j];
+        if (si == 0.0 && sj == 0.0) continue;
+        const int pi = sm.pp[i], qi = sm.qq[i], pj = sm.pp[j], qj = sm.qq[j];
+        if (qi >= r || qj >= r) continue;
+        const double ci = sm.c[i], cj = sm.c[j];
+        const double a = sm.g[pi][pj], bq = sm.g[pi][qj], cq = sm.g[qi][pj], dd = sm.g[qi][qj];
+        // left: rows (pi, qi) by pair i
+        const double l0 = ci * a - si * cq, l1 = ci * bq - si * dd;
+        const double l2 = si * a + ci * cq, l3 = si * bq + ci * dd;
+        // right: columns (pj, qj) by pair j
+        const double n00 = cj * l0 - sj * l1, n01 = sj * l0 + cj * l1;
+        const double n10 = cj * l2 - sj * l3, n11 = sj * l2 + cj * l3;
+        sm.g[pi][pj] = n00;
+        sm.g[pi][qj] = n01;
+        sm.g[qi][pj] = n10;
+        sm.g[qi][qj] = n11;
+        if (i != j) {
+          sm.g[pj][pi] = n00;
+          sm.g[qj][pi] = n01;
+          sm.g[pj][qi] = n10;
+          sm.g[qj][qi] = n11;
+        } else {
+          sm.g[qi][pi] = n01;  // diagonal block: keep it exactly symmetric
+        }
       }
-      __syncthreads();
-      // columns: G <- G J, V <- V J
-      for (int idx = threadIdx.x; idx < npairs * N; idx += blockDim.x) {
-        const int i = idx / N, k = idx - i * N;
-        const double ss = sm.s[i];
-        if (ss == 0.0 || k >= r || sm.qq[i] >= r) continue;
-        const int p = sm.pp[i], q = sm.qq[i];
-        const double cc = sm.c[i];
-        const double gp = sm.g[k][p], gq = sm.g[k][q];
-        sm.g[k][p] = cc * gp - ss * gq;
-        sm.g[k][q] = ss * gp + cc * gq;
+      // V <- V J: rows k, column pairs j
+      for (int idx = threadIdx.x; idx < npairs * r; idx += blockDim.x) {
+        const int j = idx / r, k = idx - j * r;
+        const double sj = sm.s[j];
+        if (sj == 0.0 || sm.qq[j] >= r) continue;
+        const int p = sm.pp[j], q = sm.qq[j];
+        const double cj = sm.c[j];
         const double vp = sm.v[k][p], vq = sm.v[k][q];
-        sm.v[k][p] = cc * vp - ss * vq;
-        sm.v[k][q] = ss * vp + cc * vq;
+        sm.v[k][p] = cj * vp - sj * vq;
+        sm.v[k][q] = sj * vp + cj * vq;
       }
       __syncthreads();
     }
-    converged = sm.rotations == 0;
+    if (threadIdx.x < 32) {
+      rot = __any_sync(0xffffffffu, rot);
+      if (threadIdx.x == 0) sm.rotated = rot;
+    }
     __syncthreads();
+    converged = !sm.rotated;
   }
+#ifdef DQ_JACOBI_STATS  // measurement builds: sweeps of the first blocks
+  if (threadIdx.x == 0 && blk < 4) printf("jacobi block %d: converged %d after %d sweeps\n", (int)blk, (int)converged, sweep);
+#endif
   if (!converged && threadIdx.x == 0 && flags) atomicOr(flags, (int)DQ_FLAG_JACOBI_NOCONV);
 
   // sort eigenvalues descending (ties by index), orient each vector
@@ -399,6 +465,7 @@ __global__ void quantize_core_kernel(const float* __restrict__ core1, int64_t co
   if (blockIdx.x == 0 && threadIdx.x == 0) scale[blk] = sc;
   const float* src = core1 + blk * core_elems;
   uint8_t* dst = payload + blk * payload_stride;
+  const double rinv = am > 0.0 ? 1.0 / am : 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < out_bytes; i += (int64_t)gridDim.x * blockDim.x) {
     unsigned v = 0;
     for (int k = 0; k < per; ++k) {
@@ -407,11 +474,230 @@ __global__ void quantize_core_kernel(const float* __restrict__ core1, int64_t co
       int rr, b, e;
       int code = 0;  // padding slots and degenerate blocks hold the code 0
       if (geom_coords(geom, slot, rr, b, e) && !degenerate)
-        code = rtn_code(src[((int64_t)rr * geom.i2 + b) * geom.j2 + e], qmax, am);
+        code = rtn_code_fast(src[((int64_t)rr * geom.i2 + b) * geom.j2 + e], qmax, am, rinv);
       v |= geom_encode(code, geom) << (k * bits);
     }
     dst[i] = (uint8_t)v;
   }
+}
+
+// ---- fast path for 128-wide rows (j = (8, 16), m = 8 i1 <= n = 16 i2): X tiles ------------
+// X[p = (a, c)][k = (b, e)] = M[a i2 + b][16 c + e].  A chunk of kNb b values is gathered from
+// i1 * kNb whole rows of M with 16-byte coalesced loads (the interleave is the scatter into
+// shared memory), converted to fp64 once, and contracted by a 16 x 16 grid of threads with
+// 4 x 4 register tiles: a warp spans 4 x 8 tiles, so its fp64 operand loads are broadcasts
+// (4 shared-memory wavefronts per 16 DFMA per k).  The next chunk's loads are in flight while
+// the current one is contracted.
+constexpr int kNb = 4;             // b values per chunk: 64 k columns
+constexpr int kXk = 16 * kNb;      // k columns per chunk
+constexpr int kXp = kR + 2;        // padded p pitch (doubles) of xs[k][p]
+// 16-byte loads per thread per chunk: i1 <= 8 rows a x kNb rows b x (16 | 32) uint4 per row
+template <bool F16>
+constexpr int kXLoads = 8 * kNb * (F16 ? 16 : 32) / kThreads;
+
+template <bool F16>
+struct XTile {
+  uint4 v[kXLoads<F16>];
+};
+
+// issue the loads of chunk [b0, b0 + kNb) (rows a*i2 + b, a < i1); rows outside read as 0
+template <bool F16>
+__device__ __forceinline__ void xtile_load(XTile<F16>& t, const void* blk, const Dims& d, int b0) {
+  constexpr int per_row = F16 ? 16 : 32;
+#pragma unroll
+  for (int j = 0; j < kXLoads<F16>; ++j) {
+    const int idx = threadIdx.x + j * kThreads;  // (a, b_local, q)
+    const int q = idx % per_row, ab = idx / per_row;
+    const int a = ab / kNb, b = b0 + ab % kNb;
+    t.v[j] = make_uint4(0u, 0u, 0u, 0u);
+    if (a < d.i1 && b < d.i2) {
+      const uint4* row =
+          reinterpret_cast<const uint4*>((const char*)blk + (size_t)(a * d.i2 + b) * d.cols * (F16 ? 2 : 4));
+      t.v[j] = __ldg(row + q);
+    }
+  }
+}
+
+// scatter the loaded chunk into xs[k = (b_local, e)][p = (a, c)] as fp64
+template <bool F16>
+__device__ __forceinline__ void xtile_store(const XTile<F16>& t, double (*xs)[kXp]) {
+  constexpr int per_row = F16 ? 16 : 32;
+#pragma unroll
+  for (int j = 0; j < kXLoads<F16>; ++j) {
+    const int idx = threadIdx.x + j * kThreads;
+    const int q = idx % per_row, ab = idx / per_row;
+    const int a = ab / kNb, bl = ab % kNb;
+    if constexpr (F16) {  // 8 halves: c = q / 2, e = 8 (q & 1) + 0..7
+      const int c = q >> 1, e0 = (q & 1) * 8;
+      const __half2* h = reinterpret_cast<const __half2*>(&t.v[j]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __half22float2(h[u]);
+        xs[bl * 16 + e0 + 2 * u][a * 8 + c] = (double)f.x;
+        xs[bl * 16 + e0 + 2 * u + 1][a * 8 + c] = (double)f.y;
+      }
+    } else {  // 4 floats: c = q / 4, e = 4 (q & 3) + 0..3
+      const int c = q >> 2, e0 = (q & 3) * 4;
+      const float* f = reinterpret_cast<const float*>(&t.v[j]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xs[bl * 16 + e0 + u][a * 8 + c] = (double)f[u];
+    }
+  }
+}
+
+template <bool F16>
+__device__ __forceinline__ bool xtile_finite(const XTile<F16>& t) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < kXLoads<F16>; ++j) {
+    if constexpr (F16) {
+      const __half2* h = reinterpret_cast<const __half2*>(&t.v[j]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __half22float2(h[u]);
+        ok &= isfinite(f.x) && isfinite(f.y);
+      }
+    } else {
+      const float* f = reinterpret_cast<const float*>(&t.v[j]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ok &= isfinite(f[u]);
+    }
+  }
+  return ok;
+}
+
+// thread (tp, tq) of the 16 x 16 tile grid: a warp spans 4 tp x 8 tq
+__device__ __forceinline__ void tile_coords(int& tp, int& tq) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  tp = (w >> 1) * 4 + (l >> 3);
+  tq = (w & 1) * 8 + (l & 7);
+}
+
+// G[blk] (+)= X X^T over b in [b_begin, b_end); grid (nblk, splits); atomics only when split
+template <bool F16>
+__global__ void __launch_bounds__(kThreads) gram128_kernel(const void* __restrict__ in, Dims d, int bchunk,
+                                                           double* __restrict__ G, int32_t* flags) {
+  __shared__ double xs[kXk][kXp];
+  const int64_t blk = blockIdx.x;
+  const void* base = block_ptr(in, d, blk);
+  const int b_begin = blockIdx.y * bchunk, b_end = min(d.i2, b_begin + bchunk);
+  int tp, tq;
+  tile_coords(tp, tq);
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  bool finite = true;
+  XTile<F16> t;
+  if (b_begin < b_end) xtile_load(t, base, d, b_begin);
+  for (int b0 = b_begin; b0 < b_end; b0 += kNb) {
+    __syncthreads();  // the previous chunk is consumed
+    finite &= xtile_finite(t);
+    xtile_store(t, xs);
+    __syncthreads();
+    if (b0 + kNb < b_end) xtile_load(t, base, d, b0 + kNb);  // in flight during the contraction
+    const int kn = min(kNb, b_end - b0) * 16;
+#pragma unroll 4
+    for (int k = 0; k < kn; ++k) {
+      const double2 a01 = *reinterpret_cast<const double2*>(&xs[k][tp * 4]);
+      const double2 a23 = *reinterpret_cast<const double2*>(&xs[k][tp * 4 + 2]);
+      const double2 b01 = *reinterpret_cast<const double2*>(&xs[k][tq * 4]);
+      const double2 b23 = *reinterpret_cast<const double2*>(&xs[k][tq * 4 + 2]);
+      const double a[4] = {a01.x, a01.y, a23.x, a23.y}, b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+  }
+  if (!finite && flags) atomicOr(flags, (int)DQ_FLAG_NONFINITE);
+  double* g = G + blk * kR * kR;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int p = tp * 4 + i, q = tq * 4 + j;
+      if (p < d.r && q < d.r && p <= q) {
+        if (gridDim.y > 1) atomicAdd(&g[p * kR + q], acc[i][j]);
+        else g[p * kR + q] = acc[i][j];
+      }
+    }
+}
+
+// case A projection on 128-wide rows: core1[k][(b, e)] = sum_p U[p][k] / sqrt(s_k) X[p][(b, e)];
+// grid (nblk, splits over b)
+template <bool F16>
+__global__ void __launch_bounds__(kThreads) project128_kernel(const void* __restrict__ in, Dims d, int bchunk,
+                                                              const double* __restrict__ U,
+                                                              const double* __restrict__ lam,
+                                                              float* __restrict__ core0, float* __restrict__ core1,
+                                                              unsigned* __restrict__ amax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double (*ws)[kXp] = reinterpret_cast<double (*)[kXp]>(smem_raw);                            // ws[p][k]
+  double (*xs)[kXp] = reinterpret_cast<double (*)[kXp]>(smem_raw + sizeof(double) * kR * kXp);  // xs[col][p]
+  const int64_t blk = blockIdx.x;
+  const void* base = block_ptr(in, d, blk);
+  const double* u = U + blk * kR * kR;
+  const double* lm = lam + blk * kR;
+  const int r = d.r;
+  const int b_begin = blockIdx.y * bchunk, b_end = min(d.i2, b_begin + bchunk);
+  XTile<F16> t;
+  if (b_begin < b_end) xtile_load(t, base, d, b_begin);
+  for (int idx = threadIdx.x; idx < kR * kR; idx += kThreads) {
+    const int p = idx / kR, k = idx % kR;
+    double v = 0.0;
+    if (p < r && k < r) {
+      const double sk = sval(lm, k);
+      v = sk > 0.0 ? u[p * kR + k] / sqrt(sk) : 0.0;
+    }
+    ws[p][k] = v;
+  }
+  if (blockIdx.y == 0) {
+    for (int idx = threadIdx.x; idx < r * r; idx += kThreads) {
+      const int p = idx / r, k = idx % r;
+      core0[blk * (int64_t)d.m * r + idx] = (float)(u[p * kR + k] * sqrt(sval(lm, k)));
+    }
+  }
+  int tk, tc;
+  tile_coords(tk, tc);
+  float local_max = 0.f;
+  float* out = core1 + blk * (int64_t)r * d.n;
+  for (int b0 = b_begin; b0 < b_end; b0 += kNb) {
+    __syncthreads();
+    xtile_store(t, xs);
+    __syncthreads();
+    if (b0 + kNb < b_end) xtile_load(t, base, d, b0 + kNb);
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+#pragma unroll 4
+    for (int p = 0; p < r; ++p) {
+      const double2 a01 = *reinterpret_cast<const double2*>(&ws[p][tk * 4]);
+      const double2 a23 = *reinterpret_cast<const double2*>(&ws[p][tk * 4 + 2]);
+      const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+      double b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = xs[tc * 4 + j][p];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    const int col0 = b0 * 16 + tc * 4, ncol = min(kNb, b_end - b0) * 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = tk * 4 + i;
+      if (k >= r || tc * 4 >= ncol) continue;
+      const float4 v = make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
+      *reinterpret_cast<float4*>(&out[(int64_t)k * d.n + col0]) = v;
+      local_max = fmaxf(local_max, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  }
+  for (int o = 16; o; o >>= 1) local_max = fmaxf(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&amax[blk], __float_as_uint(local_max));
 }
 
 // ---- opt-in per-channel asymmetric quantisation (dq_deco_quantize_asym_batched) ----------
@@ -511,27 +797,60 @@ int check_args(const void* blocks, int32_t dtype, int64_t nblk, int64_t rows, in
 // gram -> jacobi -> projection (core0 f32 + core1 f32 + amax)
 int factor_core(const void* blocks, const Dims& d, int64_t nblk, float* core0, float* core1, const Workspace& w,
                 int32_t* flags, cudaStream_t s) {
-  DQ_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)nblk * kR * kR * 8, s));
   DQ_CUDA_TRY(cudaMemsetAsync(w.amax, 0, (size_t)nblk * 4, s));
+  // 128-wide rows in case A (every KV block: j = (8, 16)): the X-tile kernels (coalesced row
+  // loads, fp64 tiles in shared memory); anything else: the generic element-wise gathers
+  const bool fast = d.cols == 128 && d.j1 == 8 && d.j2 == 16 && d.caseA;
   // split the contraction so that the batch fills ~2 waves of 148 SMs
   const int64_t target = 296;
-  int64_t splits = ceil_div(target, nblk);
-  int64_t chunk = round_up(ceil_div(d.kd, splits), kTile);
-  if (chunk < 4 * kTile) chunk = 4 * kTile;
-  splits = ceil_div(d.kd, chunk);
-  gram_kernel<<<dim3((unsigned)nblk, (unsigned)splits), kThreads, 0, s>>>(blocks, d, (int)chunk, w.G, flags);
-  DQ_LAUNCH_CHECK();
   constexpr int kProjSmem = (int)(sizeof(double) * kR * (kR + 2) + sizeof(double) * kR * (kTile + 2));
+  constexpr int kProj128Smem = (int)(sizeof(double) * (kR + kXk) * kXp);
   static bool attr_set = false;
   if (!attr_set) {
     DQ_CUDA_TRY(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(JacobiSmem)));
     DQ_CUDA_TRY(cudaFuncSetAttribute(project_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kProjSmem));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(project128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kProj128Smem));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(project128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kProj128Smem));
     attr_set = true;
   }
+  if (fast) {
+    int64_t splits = ceil_div(target, nblk);
+    int64_t bchunk = round_up(ceil_div(d.i2, splits), kNb);
+    if (bchunk < 4 * kNb) bchunk = 4 * kNb;
+    splits = ceil_div(d.i2, bchunk);
+    if (splits > 1) DQ_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)nblk * kR * kR * 8, s));
+    if (d.dtype == DQ_F16)
+      gram128_kernel<true><<<dim3((unsigned)nblk, (unsigned)splits), kThreads, 0, s>>>(blocks, d, (int)bchunk, w.G,
+                                                                                      flags);
+    else
+      gram128_kernel<false><<<dim3((unsigned)nblk, (unsigned)splits), kThreads, 0, s>>>(blocks, d, (int)bchunk, w.G,
+                                                                                       flags);
+  } else {
+    DQ_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)nblk * kR * kR * 8, s));
+    int64_t splits = ceil_div(target, nblk);
+    int64_t chunk = round_up(ceil_div(d.kd, splits), kTile);
+    if (chunk < 4 * kTile) chunk = 4 * kTile;
+    splits = ceil_div(d.kd, chunk);
+    gram_kernel<<<dim3((unsigned)nblk, (unsigned)splits), kThreads, 0, s>>>(blocks, d, (int)chunk, w.G, flags);
+  }
+  DQ_LAUNCH_CHECK();
   jacobi_kernel<<<(unsigned)nblk, kThreads, sizeof(JacobiSmem), s>>>(w.G, d, w.U, w.lam, flags);
   DQ_LAUNCH_CHECK();
-  if (d.caseA) {
+  if (fast) {
+    int64_t csplits = ceil_div(target, nblk);
+    int64_t bchunk = round_up(ceil_div(d.i2, csplits), kNb);
+    if (bchunk < 4 * kNb) bchunk = 4 * kNb;
+    csplits = ceil_div(d.i2, bchunk);
+    if (d.dtype == DQ_F16)
+      project128_kernel<true><<<dim3((unsigned)nblk, (unsigned)csplits), kThreads, kProj128Smem, s>>>(
+          blocks, d, (int)bchunk, w.U, w.lam, core0, core1, w.amax);
+    else
+      project128_kernel<false><<<dim3((unsigned)nblk, (unsigned)csplits), kThreads, kProj128Smem, s>>>(
+          blocks, d, (int)bchunk, w.U, w.lam, core0, core1, w.amax);
+  } else if (d.caseA) {
     int64_t csplits = ceil_div(target, nblk);
     int64_t cchunk = round_up(ceil_div(d.n, csplits), kTile);
     if (cchunk < 4 * kTile) cchunk = 4 * kTile;
