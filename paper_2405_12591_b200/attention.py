@@ -297,6 +297,58 @@ class DecodeKvCache:
             self.tail_len[layer].zero_()
             lay.tail_len = 0
 
+    def import_segment(self, layer: int, keys: list, values: list):
+        """Append one sealed segment per unit from reference-form chains (``QuantizedMpo``, n = 2,
+        e.g. ``formats.read_mpo`` of a DQZ1 file the reference wrote): the wire-order payloads
+        are relaid into the attention layouts on the device, core0 into the normalised G0.
+
+        ``keys[u]`` / ``values[u]``: unit u's K / V chain; every chain must cover the same T rows
+        of ``dim`` columns at this cache's bits (one segment group, kvcache.py:124-128)."""
+        lay = self._layer(layer)
+        if self.asym:
+            raise Unsupported("reference chains carry one symmetric scale: not an asymmetric cache")
+        if len(keys) != self.units or len(values) != self.units:
+            raise DimMismatch(f"need one K and one V chain per unit ({self.units})")
+        chains = list(keys) + list(values)
+        T = chains[0].rows
+        for q in chains:
+            if q.plan.n != 2 or q.cols != self.dim or q.rows != T:
+                raise ShapeMismatch(f"every chain must be an n = 2 chain of ({T}, {self.dim})")
+            if q.bits != self.bits:
+                raise UnsupportedBits(f"chain bits {q.bits} differ from the cache's {self.bits}")
+        if lay.tail_len:
+            raise AlreadyPrefilled("import a segment before decoding into the tail")
+        p = _lib.plan2(T, self.dim)
+        U, dev = self.units, self.device
+        nbytes = payload_size(p.r * p.i2 * p.j2, self.bits)
+
+        def stack(which):
+            qs = chains[:U] if which == "k" else chains[U:]
+            wire = torch.stack([torch.as_tensor(q.local_tensors[1].data, device=dev).reshape(-1) for q in qs])
+            if wire.shape[1] != nbytes:
+                raise ShapeMismatch("payload size disagrees with the plan")
+            layout = _lib.LAYOUT_KTILE if which == "k" else _lib.LAYOUT_VTILE
+            lb = _lib.layout_bytes(p, self.bits, layout)
+            dst = torch.empty((U, lb), dtype=torch.uint8, device=dev)
+            check(lib().dq_relayout(ptr(wire), _lib.LAYOUT_REF, nbytes, ptr(dst), layout, lb, U,
+                                    ctypes.byref(p), self.bits, stream_ptr()), "relayout")
+            core0 = torch.stack([torch.as_tensor(q.local_tensors[0], dtype=torch.float32, device=dev).reshape(-1)
+                                 for q in qs]).reshape(U, 1, p.i1, p.j1, p.r).contiguous()
+            g0 = torch.empty((U, p.i1 * p.r * p.j1), dtype=torch.float32, device=dev)
+            norm = torch.empty(U, dtype=torch.float32, device=dev)
+            check(lib().dq_core0_relayout(ptr(core0), U, ctypes.byref(p), ptr(g0), _lib.DQ_F32, ptr(norm),
+                                          stream_ptr()), "core0_relayout")
+            scale = torch.tensor([q.local_tensors[1].scale for q in qs], dtype=torch.float32, device=dev)
+            return dst, core0, g0, norm, scale
+
+        kp, kc0, kg, kn, ks = stack("k")
+        vp, vc0, vg, vn, vs = stack("v")
+        i2p = -(-p.i2 // _lib.I2_PAD) * _lib.I2_PAD
+        lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, kn, vn, lay.tokens_sealed))
+        lay.tokens_sealed += T
+        lay.args = None
+        lay.gen += 1
+
     # ---- attention -----------------------------------------------------------
     def _build_args(self, layer: int):
         lay = self._layers[layer]

@@ -265,10 +265,22 @@ struct TeamProd {
   bool hc, hn;   // streaming an item / the next item's descriptor is loaded (slot k % kSubRing)
 };
 
+__device__ __forceinline__ bool elect_lane() {
+  uint32_t p;
+  asm volatile("{\n.reg .pred P;\n.reg .b32 r;\nelect.sync r|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}" : "=r"(p));
+  return p != 0;
+}
+
+// The whole producer warp runs this converged: every lane holds the same (warp-uniform) state,
+// one elected lane performs the stores, arrivals and copies.  (A lone `lane == 0` loop makes
+// the compiler wrap each bulk copy's operands in a register-to-uniform broadcast loop: at
+// ~150 dependent instructions per stage the issue rate, not HBM, bounded the pool.)
 template <int BITS, int G, int NT, bool ASYM, int TEAMS>
 __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args) {
   using TS = TeamSmem<G, NT, ASYM>;
   constexpr int S = AttnSmem<G, NT, ASYM, TEAMS>::kStages;
+  static_assert((kQ & (kQ - 1)) == 0 && (kSubRing & (kSubRing - 1)) == 0, "power-of-two rings");
+  const bool leader = elect_lane();
   uint32_t freemask = S >= 32 ? ~0u : ((1u << S) - 1u);
   uint32_t parity = 0;  // bit s: parity of slot s's next use
   bool waited = false;  // griddepcontrol.wait before the first ticket (the counter is shared with
@@ -277,23 +289,26 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
 
   // descriptor P.k (loaded into its ring slot, or the end marker) becomes current and is published
   auto advance = [&](TeamProd& p, TS& tm) {
-    const int ds = p.k % kSubRing;
+    const int ds = p.k & (kSubRing - 1);
     p.hc = p.hn;
     p.hn = false;
     p.ls = 0;
-    if (p.hc) {
-      p.cur = issue_of(tm.sub[ds]);
-      tm.kend[ds] = p.issued + p.cur.nK;
-      tm.vend[ds] = p.issued + p.cur.stages;
-    } else {
-      tm.sub[ds].nbt = 0;
+    __syncwarp();  // the leader's descriptor stores are visible to the warp
+    if (p.hc) p.cur = issue_of(tm.sub[ds]);
+    if (leader) {
+      if (p.hc) {
+        tm.kend[ds] = p.issued + p.cur.nK;
+        tm.vend[ds] = p.issued + p.cur.stages;
+      } else {
+        tm.sub[ds].nbt = 0;
+      }
+      mbar_arrive(&tm.descfull[ds]);  // release: the descriptor is visible to its waiters
     }
-    mbar_arrive(&tm.descfull[ds]);  // release: the descriptor is visible to its waiters
     ++p.k;
   };
   auto reclaim = [&](TeamProd& p, TS& tm) {
     while (p.reclaimed < p.issued) {
-      const int e = tm.sq[p.reclaimed % kQ];
+      const int e = tm.sq[p.reclaimed & (kQ - 1)];
       if (!mbar_test(&sm.empty[e & 0xFF], (uint32_t)(e >> 8))) break;
       freemask |= 1u << (e & 0xFF);
       ++p.reclaimed;
@@ -303,7 +318,7 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
     if (!p.hc || p.issued - p.reclaimed >= kQ) return false;
     if (TEAMS == 1) return true;
     const int ph = *reinterpret_cast<volatile int*>(&tm.started);
-    const int jp = (ph >> 1) % kSubRing;
+    const int jp = (ph >> 1) & (kSubRing - 1);
     const int end = (ph & 1) ? tm.vend[jp] : tm.kend[jp];
     return p.issued < end + kTeamPrefetch;
   };
@@ -312,9 +327,11 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
     freemask &= freemask - 1;
     const uint32_t par = (parity >> slot) & 1u;
     parity ^= 1u << slot;
-    tm.sq[p.issued % kQ] = slot | (int)(par << 8);
-    mbar_arrive(&tm.sqbar[p.issued % kQ]);
-    issue_stage<BITS>(p.cur, p.ls, sm.ring[slot], &sm.full[slot]);
+    if (leader) {
+      tm.sq[p.issued & (kQ - 1)] = slot | (int)(par << 8);
+      mbar_arrive(&tm.sqbar[p.issued & (kQ - 1)]);
+      issue_stage<BITS>(p.cur, p.ls, sm.ring[slot], &sm.full[slot]);
+    }
     ++p.issued;
     ++p.ls;
     if (p.ls == min(3, p.cur.stages)) {
@@ -323,9 +340,11 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
         waited = true;
       }
       // the team's next item: ticket, then its descriptor straight into the ring slot
-      const int nx = TEAMS * (int)gridDim.x + atomicAdd(args.sched, 1);
+      int nx = 0;
+      if (leader) nx = atomicAdd(args.sched, 1);
+      nx = TEAMS * (int)gridDim.x + __shfl_sync(0xffffffffu, nx, __ffs(__ballot_sync(0xffffffffu, leader)) - 1);
       p.hn = nx < args.nwork;
-      if (p.hn) load_sub<BITS>(tm.sub[p.k % kSubRing], args, nx);
+      if (p.hn && leader) load_sub<BITS>(tm.sub[p.k & (kSubRing - 1)], args, nx);
     }
     if (p.ls == p.cur.stages) advance(p, tm);  // item fully issued: the next one becomes current
   };
@@ -335,7 +354,7 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
     const int first = (int)blockIdx.x + t * (int)gridDim.x;
     P[t].k = P[t].issued = P[t].reclaimed = 0;
     P[t].hn = first < args.nwork;
-    if (P[t].hn) load_sub<BITS>(sm.team[t].sub[0], args, first);
+    if (P[t].hn && leader) load_sub<BITS>(sm.team[t].sub[0], args, first);
     advance(P[t], sm.team[t]);
   }
   for (;;) {
@@ -357,10 +376,12 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
   }
   // retire: the last CTA to finish drawing resets the counters for the next launch
   if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  __threadfence();
-  if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
-    args.sched[0] = 0;
-    args.sched[1] = 0;
+  if (leader) {
+    __threadfence();
+    if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
+      args.sched[0] = 0;
+      args.sched[1] = 0;
+    }
   }
 }
 
@@ -404,7 +425,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     // ---- producer: descriptors and code stages of this CTA's items ----------------------
     // (the code does not depend on the prepare kernel, so no griddepcontrol.wait before
     // the first stages)
-    if (lane == 0) produce<BITS, G, NT, ASYM, TEAMS>(sm, args);
+    produce<BITS, G, NT, ASYM, TEAMS>(sm, args);  // the whole warp, converged
     return;
   }
   TeamSmem<G, NT, ASYM>& tm = sm.team[team];

@@ -298,10 +298,11 @@ __global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restri
   // sort eigenvalues descending (ties by index), orient each vector
   if (threadIdx.x < r) {
     const int i = threadIdx.x;
-    const double li = sm.g[i][i];
+    auto key = [](double x) { return x == x ? x : -INFINITY; };
+    const double li = key(sm.g[i][i]);
     int rank = 0;
     for (int j = 0; j < r; ++j) {
-      const double lj = sm.g[j][j];
+      const double lj = key(sm.g[j][j]);
       rank += (lj > li) || (lj == li && j < i);
     }
     sm.perm[rank] = i;
@@ -325,6 +326,254 @@ __global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restri
     const double sgn = sm.v[bidx][src] < 0.0 ? -1.0 : 1.0;
     for (int p = threadIdx.x & 31; p < r; p += 32) u[p * kR + col] = sgn * sm.v[p][src];
     if ((threadIdx.x & 31) == 0) lam_out[blk * kR + col] = sm.g[src][src];
+  }
+}
+
+// ---- tridiagonal eigensolver on one r x r Gram per CTA (the default) -------------------
+// Householder reduction to tridiagonal form with the transformation accumulated in place
+// (EISPACK tred2), then implicit QL with Wilkinson-type shifts on the tridiagonal (tqli).
+// About 30x less shared-memory traffic than the cyclic Jacobi above (which moves the whole
+// r x r G and V per round, ~570 rounds): the 64-thread CTA parallelises every row / column
+// loop of the reduction; the QL bulge chases run on thread 0 and record their rotations,
+// which every thread then applies to its own row of the eigenvector matrix.  Plane
+// rotations use rsqrt (fp32 seed + two fp64 Newton steps), exactly orthogonal to fp64
+// rounding.  Eigenvalues are sorted descending and the vectors oriented as in jacobi_kernel.
+constexpr int kEigThreads = 64;
+
+struct EigSmem {
+  double a[kR][kR + 1];  // the matrix, then the accumulated transformation / eigenvectors
+  double d[kR], e[kR];
+  double rc[kR], rs[kR];  // rotations of one QL chase, by index i
+  double red[kEigThreads / 32];
+  double sh[4];          // broadcast scalars
+  int ish[4];
+  int perm[kR];
+};
+
+__device__ __forceinline__ double eig_block_sum(double v, EigSmem& sm) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();  // red[] from any previous reduction has been read
+  if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kEigThreads / 32; ++w) s += sm.red[w];
+  return s;
+}
+
+// 1 / sqrt(f^2 + g^2) and the hypotenuse
+__device__ __forceinline__ double hyp(double f, double g, double* rinv) {
+  const double q = fma(f, f, g * g);
+  if (q > 1e-30 && q < 1e30) {
+    const double ri = rsqrt_f64(q);
+    *rinv = ri;
+    return q * ri;
+  }
+  const double r = sqrt(q);
+  *rinv = r > 0.0 ? 1.0 / r : 0.0;
+  return r;
+}
+
+__global__ void __launch_bounds__(kEigThreads) eig_tql_kernel(const double* __restrict__ G, Dims d_,
+                                                              double* __restrict__ U, double* __restrict__ lam_out,
+                                                              int32_t* flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EigSmem& sm = *reinterpret_cast<EigSmem*>(smem_raw);
+  const int64_t blk = blockIdx.x;
+  const int n = d_.r;
+  const int t = threadIdx.x;
+  const double* g = G + blk * kR * kR;
+  for (int idx = t; idx < n * n; idx += kEigThreads) {
+    const int p = idx / n, q = idx % n;
+    sm.a[p][q] = p <= q ? g[p * kR + q] : g[q * kR + p];
+  }
+  __syncthreads();
+
+  // ---- Householder reduction (tred2), rows i = n-1 .. 1 ----------------------------------
+  for (int i = n - 1; i > 0; --i) {
+    const int l = i - 1;
+    double h = 0.0;
+    if (l > 0) {
+      double part = 0.0;
+      for (int k = t; k <= l; k += kEigThreads) part += fabs(sm.a[i][k]);
+      const double scale = eig_block_sum(part, sm);
+      if (scale == 0.0) {
+        if (t == 0) sm.e[i] = sm.a[i][l];
+      } else {
+        part = 0.0;
+        for (int k = t; k <= l; k += kEigThreads) {
+          const double v = sm.a[i][k] / scale;
+          sm.a[i][k] = v;
+          part += v * v;
+        }
+        h = eig_block_sum(part, sm);
+        const double f = sm.a[i][l];
+        const double gg = f >= 0.0 ? -sqrt(h) : sqrt(h);
+        h -= f * gg;
+        __syncthreads();  // every thread has read a[i][l]
+        if (t == 0) {
+          sm.e[i] = scale * gg;
+          sm.a[i][l] = f - gg;
+        }
+        __syncthreads();
+        const double hinv = 1.0 / h;
+        part = 0.0;
+        for (int j = t; j <= l; j += kEigThreads) {
+          sm.a[j][i] = sm.a[i][j] * hinv;
+          double acc = 0.0;
+          for (int k = 0; k <= j; ++k) acc = fma(sm.a[j][k], sm.a[i][k], acc);
+          for (int k = j + 1; k <= l; ++k) acc = fma(sm.a[k][j], sm.a[i][k], acc);
+          const double ej = acc * hinv;
+          sm.e[j] = ej;
+          part = fma(ej, sm.a[i][j], part);
+        }
+        const double ff = eig_block_sum(part, sm);
+        const double hh = ff / (h + h);
+        for (int j = t; j <= l; j += kEigThreads) sm.e[j] = fma(-hh, sm.a[i][j], sm.e[j]);
+        __syncthreads();
+        for (int j = t; j <= l; j += kEigThreads) {
+          const double fj = sm.a[i][j], gj = sm.e[j];
+          for (int k = 0; k <= j; ++k) sm.a[j][k] -= fma(fj, sm.e[k], gj * sm.a[i][k]);
+        }
+      }
+    } else {
+      if (t == 0) sm.e[i] = sm.a[i][l];
+    }
+    if (t == 0) sm.d[i] = h;
+    __syncthreads();
+  }
+  if (t == 0) {
+    sm.d[0] = 0.0;
+    sm.e[0] = 0.0;
+  }
+  __syncthreads();
+  // accumulate the transformations: a <- Q
+  for (int i = 0; i < n; ++i) {
+    const int l = i - 1;
+    if (sm.d[i] != 0.0) {
+      for (int j = t; j <= l; j += kEigThreads) {
+        double acc = 0.0;
+        for (int k = 0; k <= l; ++k) acc = fma(sm.a[i][k], sm.a[k][j], acc);
+        for (int k = 0; k <= l; ++k) sm.a[k][j] = fma(-acc, sm.a[k][i], sm.a[k][j]);
+      }
+    }
+    __syncthreads();
+    if (t == 0) {
+      sm.d[i] = sm.a[i][i];
+      sm.a[i][i] = 1.0;
+    }
+    for (int j = t; j <= l; j += kEigThreads) sm.a[j][i] = sm.a[i][j] = 0.0;
+    __syncthreads();
+  }
+
+  // ---- implicit QL on (d, e) (tqli), eigenvectors in the rows of a --------------------
+  if (t == 0) {
+    for (int i = 1; i < n; ++i) sm.e[i - 1] = sm.e[i];
+    sm.e[n - 1] = 0.0;
+  }
+  __syncthreads();
+  bool failed = false;
+  for (int l = 0; l < n; ++l) {
+    for (int iter = 0;; ++iter) {
+      // thread 0: find the split point m, run one chase, record its rotations
+      if (t == 0) {
+        int m = l;
+        for (; m < n - 1; ++m) {
+          const double dd = fabs(sm.d[m]) + fabs(sm.d[m + 1]);
+          if (fabs(sm.e[m]) <= 2.220446049250313e-16 * dd) break;
+        }
+        int lo = m, hi = m;  // rotations recorded for i in [lo, hi)
+        if (m != l && iter < 40) {
+          double gq = (sm.d[l + 1] - sm.d[l]) / (2.0 * sm.e[l]);
+          double ri;
+          double r = hyp(gq, 1.0, &ri);
+          gq = sm.d[m] - sm.d[l] + sm.e[l] / (gq + copysign(r, gq));
+          double s = 1.0, c = 1.0, p = 0.0;
+          int i = m - 1;
+          bool deflated = false;
+          for (; i >= l; --i) {
+            const double f = s * sm.e[i], b = c * sm.e[i];
+            r = hyp(f, gq, &ri);
+            sm.e[i + 1] = r;
+            if (r == 0.0) {
+              sm.d[i + 1] -= p;
+              sm.e[m] = 0.0;
+              deflated = true;
+              break;
+            }
+            s = f * ri;
+            c = gq * ri;
+            gq = sm.d[i + 1] - p;
+            r = (sm.d[i] - gq) * s + 2.0 * c * b;
+            p = s * r;
+            sm.d[i + 1] = gq + p;
+            gq = c * r - b;
+            sm.rc[i] = c;
+            sm.rs[i] = s;
+          }
+          lo = deflated ? i + 1 : l;
+          if (!deflated) {
+            sm.d[l] -= p;
+            sm.e[l] = gq;
+            sm.e[m] = 0.0;
+          }
+        }
+        sm.ish[0] = lo;
+        sm.ish[1] = hi;
+        sm.ish[2] = m;
+      }
+      __syncthreads();
+      const int lo = sm.ish[0], hi = sm.ish[1], m = sm.ish[2];
+      if (m == l) break;
+      if (iter >= 40) {
+        failed = true;
+        break;
+      }
+      // apply the chase's rotations (i = hi-1 .. lo) to row t of the eigenvector matrix
+      if (t < n) {
+        double* row = sm.a[t];
+        for (int i = hi - 1; i >= lo; --i) {
+          const double c = sm.rc[i], s = sm.rs[i];
+          const double f = row[i + 1];
+          row[i + 1] = fma(s, row[i], c * f);
+          row[i] = fma(c, row[i], -s * f);
+        }
+      }
+      __syncthreads();  // rc / rs and the split search see the finished chase
+    }
+    if (failed) break;
+  }
+  if (failed && t == 0 && flags) atomicOr(flags, (int)DQ_FLAG_JACOBI_NOCONV);
+
+  // sort eigenvalues descending (ties by index), orient each vector (as jacobi_kernel)
+  if (t < n) {  // a NaN (non-finite input, already flagged) sorts last: perm stays a permutation
+    auto key = [](double x) { return x == x ? x : -INFINITY; };
+    const double li = key(sm.d[t]);
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = key(sm.d[j]);
+      rank += (lj > li) || (lj == li && j < t);
+    }
+    sm.perm[rank] = t;
+  }
+  __syncthreads();
+  double* u = U + blk * kR * kR;
+  for (int col = t / 32; col < n; col += kEigThreads / 32) {
+    const int src = sm.perm[col];
+    double best = -1.0;
+    int bidx = 0;
+    for (int p = t & 31; p < n; p += 32) {
+      const double a = fabs(sm.a[p][src]);
+      if (a > best) { best = a; bidx = p; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    }
+    const double sgn = sm.a[bidx][src] < 0.0 ? -1.0 : 1.0;
+    for (int p = t & 31; p < n; p += 32) u[p * kR + col] = sgn * sm.a[p][src];
+    if ((t & 31) == 0) lam_out[blk * kR + col] = sm.d[src];
   }
 }
 
@@ -491,6 +740,9 @@ __global__ void quantize_core_kernel(const float* __restrict__ core1, int64_t co
 constexpr int kNb = 4;             // b values per chunk: 64 k columns
 constexpr int kXk = 16 * kNb;      // k columns per chunk
 constexpr int kXp = kR + 2;        // padded p pitch (doubles) of xs[k][p]
+constexpr int kXpP = kR + 4;       // pitch (doubles) of the DMMA operand tiles: 136 words = 8 banks
+                                   // per row, so a fragment (8 rows x 4 consecutive) hits 64 distinct
+                                   // bank slots (two wavefronts, no conflict)
 // 16-byte loads per thread per chunk: i1 <= 8 rows a x kNb rows b x (16 | 32) uint4 per row
 template <bool F16>
 constexpr int kXLoads = 8 * kNb * (F16 ? 16 : 32) / kThreads;
@@ -518,31 +770,50 @@ __device__ __forceinline__ void xtile_load(XTile<F16>& t, const void* blk, const
   }
 }
 
-// scatter the loaded chunk into xs[k = (b_local, e)][p = (a, c)] as fp64
-template <bool F16>
-__device__ __forceinline__ void xtile_store(const XTile<F16>& t, double (*xs)[kXp]) {
+// scatter the loaded chunk into shared memory as fp64: PK = true: xs[p = (a, c)][k = (b_local, e)]
+// (the Gram's operand, both fragments read along k), PK = false: xs[k][p] (the projection's B)
+template <bool F16, bool PK>
+__device__ __forceinline__ void xtile_store(const XTile<F16>& t, double* xs) {
   constexpr int per_row = F16 ? 16 : 32;
 #pragma unroll
   for (int j = 0; j < kXLoads<F16>; ++j) {
     const int idx = threadIdx.x + j * kThreads;
     const int q = idx % per_row, ab = idx / per_row;
     const int a = ab / kNb, bl = ab % kNb;
-    if constexpr (F16) {  // 8 halves: c = q / 2, e = 8 (q & 1) + 0..7
-      const int c = q >> 1, e0 = (q & 1) * 8;
+    constexpr int NE = F16 ? 8 : 4;  // consecutive e per 16-byte load
+    const int c = q / (16 / NE), e0 = (q % (16 / NE)) * NE;
+    double v[NE];
+    if constexpr (F16) {
       const __half2* h = reinterpret_cast<const __half2*>(&t.v[j]);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float2 f = __half22float2(h[u]);
-        xs[bl * 16 + e0 + 2 * u][a * 8 + c] = (double)f.x;
-        xs[bl * 16 + e0 + 2 * u + 1][a * 8 + c] = (double)f.y;
+        v[2 * u] = (double)f.x;
+        v[2 * u + 1] = (double)f.y;
       }
-    } else {  // 4 floats: c = q / 4, e = 4 (q & 3) + 0..3
-      const int c = q >> 2, e0 = (q & 3) * 4;
+    } else {
       const float* f = reinterpret_cast<const float*>(&t.v[j]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xs[bl * 16 + e0 + u][a * 8 + c] = (double)f[u];
+      for (int u = 0; u < 4; ++u) v[u] = (double)f[u];
+    }
+    const int p = a * 8 + c, k0 = bl * 16 + e0;
+    if constexpr (PK) {
+      double2* dst = reinterpret_cast<double2*>(xs + p * kXpP + k0);
+#pragma unroll
+      for (int u = 0; u < NE / 2; ++u) dst[u] = make_double2(v[2 * u], v[2 * u + 1]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < NE; ++u) xs[(k0 + u) * kXpP + p] = v[u];
     }
   }
+}
+
+// D(8x8) += A(8x4, row) . B(4x8, col) in fp64 on the tensor pipe.  Fragments: a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], d = D[lane/4][2 (lane%4) + {0, 1}]
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
 
 template <bool F16>
@@ -573,60 +844,56 @@ __device__ __forceinline__ void tile_coords(int& tp, int& tq) {
   tq = (w & 1) * 8 + (l & 7);
 }
 
-// G[blk] (+)= X X^T over b in [b_begin, b_end); grid (nblk, splits); atomics only when split
+// G[blk] (+)= X X^T over b in [b_begin, b_end) on the fp64 tensor pipe (DMMA m8n8k4): warp w
+// owns the 8 x 64 row strip w of G (8 accumulator tiles); per k-step of 4 it loads one A
+// fragment and 8 B fragments (all from xs[p][k]).  grid (nblk, splits); atomics only when split
 template <bool F16>
 __global__ void __launch_bounds__(kThreads) gram128_kernel(const void* __restrict__ in, Dims d, int bchunk,
                                                            double* __restrict__ G, int32_t* flags) {
-  __shared__ double xs[kXk][kXp];
+  __shared__ __align__(16) double xs[kR * kXpP];
   const int64_t blk = blockIdx.x;
   const void* base = block_ptr(in, d, blk);
   const int b_begin = blockIdx.y * bchunk, b_end = min(d.i2, b_begin + bchunk);
-  int tp, tq;
-  tile_coords(tp, tq);
-  double acc[4][4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  double acc[8][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
   bool finite = true;
   XTile<F16> t;
   if (b_begin < b_end) xtile_load(t, base, d, b_begin);
+  const double* arow = xs + (w * 8 + g) * kXpP + t4;
   for (int b0 = b_begin; b0 < b_end; b0 += kNb) {
     __syncthreads();  // the previous chunk is consumed
     finite &= xtile_finite(t);
-    xtile_store(t, xs);
+    xtile_store<F16, true>(t, xs);
     __syncthreads();
     if (b0 + kNb < b_end) xtile_load(t, base, d, b0 + kNb);  // in flight during the contraction
     const int kn = min(kNb, b_end - b0) * 16;
-#pragma unroll 4
-    for (int k = 0; k < kn; ++k) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&xs[k][tp * 4]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&xs[k][tp * 4 + 2]);
-      const double2 b01 = *reinterpret_cast<const double2*>(&xs[k][tq * 4]);
-      const double2 b23 = *reinterpret_cast<const double2*>(&xs[k][tq * 4 + 2]);
-      const double a[4] = {a01.x, a01.y, a23.x, a23.y}, b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll 2
+    for (int k = 0; k < kn; k += 4) {
+      const double a = arow[k];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      for (int j = 0; j < 8; ++j) dmma(acc[j][0], acc[j][1], a, xs[(j * 8 + g) * kXpP + k + t4]);
     }
   }
   if (!finite && flags) atomicOr(flags, (int)DQ_FLAG_NONFINITE);
-  double* g = G + blk * kR * kR;
+  double* gp = G + blk * kR * kR;
+  const int p = w * 8 + g;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int j = 0; j < 8; ++j)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int p = tp * 4 + i, q = tq * 4 + j;
+    for (int i = 0; i < 2; ++i) {
+      const int q = j * 8 + 2 * t4 + i;
       if (p < d.r && q < d.r && p <= q) {
-        if (gridDim.y > 1) atomicAdd(&g[p * kR + q], acc[i][j]);
-        else g[p * kR + q] = acc[i][j];
+        if (gridDim.y > 1) atomicAdd(&gp[p * kR + q], acc[j][i]);
+        else gp[p * kR + q] = acc[j][i];
       }
     }
 }
 
-// case A projection on 128-wide rows: core1[k][(b, e)] = sum_p U[p][k] / sqrt(s_k) X[p][(b, e)];
-// grid (nblk, splits over b)
+// case A projection on 128-wide rows: core1[k][(b, e)] = sum_p U[p][k] / sqrt(s_k) X[p][(b, e)] on the
+// fp64 tensor pipe: A = W^T from ws[k][p], B = X from xs[col][p]; warp w owns the bond rows
+// 8w..8w+7 x the chunk's 64 columns.  grid (nblk, splits over b)
 template <bool F16>
 __global__ void __launch_bounds__(kThreads) project128_kernel(const void* __restrict__ in, Dims d, int bchunk,
                                                               const double* __restrict__ U,
@@ -634,8 +901,8 @@ __global__ void __launch_bounds__(kThreads) project128_kernel(const void* __rest
                                                               float* __restrict__ core0, float* __restrict__ core1,
                                                               unsigned* __restrict__ amax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double (*ws)[kXp] = reinterpret_cast<double (*)[kXp]>(smem_raw);                            // ws[p][k]
-  double (*xs)[kXp] = reinterpret_cast<double (*)[kXp]>(smem_raw + sizeof(double) * kR * kXp);  // xs[col][p]
+  double* ws = reinterpret_cast<double*>(smem_raw);  // ws[k][p] = U[p][k] / sqrt(s_k)
+  double* xs = ws + kR * kXpP;                        // xs[col][p]
   const int64_t blk = blockIdx.x;
   const void* base = block_ptr(in, d, blk);
   const double* u = U + blk * kR * kR;
@@ -651,7 +918,7 @@ __global__ void __launch_bounds__(kThreads) project128_kernel(const void* __rest
       const double sk = sval(lm, k);
       v = sk > 0.0 ? u[p * kR + k] / sqrt(sk) : 0.0;
     }
-    ws[p][k] = v;
+    ws[k * kXpP + p] = v;
   }
   if (blockIdx.y == 0) {
     for (int idx = threadIdx.x; idx < r * r; idx += kThreads) {
@@ -659,41 +926,35 @@ __global__ void __launch_bounds__(kThreads) project128_kernel(const void* __rest
       core0[blk * (int64_t)d.m * r + idx] = (float)(u[p * kR + k] * sqrt(sval(lm, k)));
     }
   }
-  int tk, tc;
-  tile_coords(tk, tc);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const double* arow = ws + (w * 8 + g) * kXpP + t4;
   float local_max = 0.f;
   float* out = core1 + blk * (int64_t)r * d.n;
   for (int b0 = b_begin; b0 < b_end; b0 += kNb) {
     __syncthreads();
-    xtile_store(t, xs);
+    xtile_store<F16, false>(t, xs);
     __syncthreads();
     if (b0 + kNb < b_end) xtile_load(t, base, d, b0 + kNb);
-    double acc[4][4];
+    double acc[8][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 2
+    for (int p = 0; p < r; p += 4) {
+      const double a = arow[p];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-#pragma unroll 4
-    for (int p = 0; p < r; ++p) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&ws[p][tk * 4]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&ws[p][tk * 4 + 2]);
-      const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-      double b[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = xs[tc * 4 + j][p];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      for (int j = 0; j < 8; ++j) dmma(acc[j][0], acc[j][1], a, xs[(j * 8 + g) * kXpP + p + t4]);
     }
-    const int col0 = b0 * 16 + tc * 4, ncol = min(kNb, b_end - b0) * 16;
+    const int k = w * 8 + g, ncol = min(kNb, b_end - b0) * 16;
+    if (k < r) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int k = tk * 4 + i;
-      if (k >= r || tc * 4 >= ncol) continue;
-      const float4 v = make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
-      *reinterpret_cast<float4*>(&out[(int64_t)k * d.n + col0]) = v;
-      local_max = fmaxf(local_max, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      for (int j = 0; j < 8; ++j) {
+        const int c = j * 8 + 2 * t4;
+        if (c < ncol) {
+          const float2 v = make_float2((float)acc[j][0], (float)acc[j][1]);
+          *reinterpret_cast<float2*>(&out[(int64_t)k * d.n + b0 * 16 + c]) = v;
+          local_max = fmaxf(local_max, fmaxf(fabsf(v.x), fabsf(v.y)));
+        }
+      }
     }
   }
   for (int o = 16; o; o >>= 1) local_max = fmaxf(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
@@ -804,11 +1065,13 @@ int factor_core(const void* blocks, const Dims& d, int64_t nblk, float* core0, f
   // split the contraction so that the batch fills ~2 waves of 148 SMs
   const int64_t target = 296;
   constexpr int kProjSmem = (int)(sizeof(double) * kR * (kR + 2) + sizeof(double) * kR * (kTile + 2));
-  constexpr int kProj128Smem = (int)(sizeof(double) * (kR + kXk) * kXp);
+  constexpr int kProj128Smem = (int)(sizeof(double) * 2 * kR * kXpP);
   static bool attr_set = false;
   if (!attr_set) {
     DQ_CUDA_TRY(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(JacobiSmem)));
+    DQ_CUDA_TRY(cudaFuncSetAttribute(eig_tql_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(EigSmem)));
     DQ_CUDA_TRY(cudaFuncSetAttribute(project_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kProjSmem));
     DQ_CUDA_TRY(cudaFuncSetAttribute(project128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kProj128Smem));
@@ -837,7 +1100,11 @@ int factor_core(const void* blocks, const Dims& d, int64_t nblk, float* core0, f
     gram_kernel<<<dim3((unsigned)nblk, (unsigned)splits), kThreads, 0, s>>>(blocks, d, (int)chunk, w.G, flags);
   }
   DQ_LAUNCH_CHECK();
+#ifdef DQ_EIG_JACOBI  // the cyclic Jacobi eigensolver (measurement / cross-check builds)
   jacobi_kernel<<<(unsigned)nblk, kThreads, sizeof(JacobiSmem), s>>>(w.G, d, w.U, w.lam, flags);
+#else
+  eig_tql_kernel<<<(unsigned)nblk, kEigThreads, sizeof(EigSmem), s>>>(w.G, d, w.U, w.lam, flags);
+#endif
   DQ_LAUNCH_CHECK();
   if (fast) {
     int64_t csplits = ceil_div(target, nblk);

@@ -74,3 +74,82 @@ def test_device_cache_segment_export_roundtrip(tmp_path):
         c0 = seg.local_tensors[0]
         c0 = c0.cpu().numpy() if isinstance(c0, torch.Tensor) else np.asarray(c0)
         assert np.array_equal(np.asarray(back.local_tensors[0]), c0)
+
+
+def _chain_from_oracle(e):
+    """oracle Encoded (the reference's algorithm, pinned to its goldens) -> QuantizedMpo"""
+    from paper_2405_12591_b200 import QuantizedMpo, QuantizedTensor, plan_shapes
+
+    p = e.plan
+    qt = QuantizedTensor((e.r, p.i2, p.j2, 1), e.bits, float(e.scale), payload=e.payload)
+    return QuantizedMpo(plan=plan_shapes(p.i1 * p.i2, p.j1 * p.j2, 2), bits=e.bits, local_tensors=(e.core0, qt))
+
+
+@pytest.mark.parametrize("T,bits", [(1024, 4), (1009, 2)])
+def test_import_dqz1_chains_into_decode_cache(T, bits):
+    """DQZ1 files (written from reference-algorithm chains) -> DecodeKvCache.import_segment ->
+    fused decode attention, against the oracle over the same chains; plus export -> DQZ1 ->
+    import round trip (identical attention output)."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+    from paper_2405_12591_b200.formats import mpo_bytes, parse_mpo
+
+    units = 2
+    rng = np.random.default_rng(T + bits)
+    k = rng.standard_normal((units, T, 128)).astype(np.float16).astype(np.float32)
+    v = rng.standard_normal((units, T, 128)).astype(np.float16).astype(np.float32)
+    q = rng.standard_normal((units, 1, 128)).astype(np.float16)
+    ek = [O.encode(k[u], bits) for u in range(units)]
+    ev = [O.encode(v[u], bits) for u in range(units)]
+    kq = [parse_mpo(mpo_bytes(_chain_from_oracle(e))) for e in ek]  # through the DQZ1 bytes
+    vq = [parse_mpo(mpo_bytes(_chain_from_oracle(e))) for e in ev]
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=bits)
+    cache.import_segment(0, kq, vq)
+    out = cache.attend(0, torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for u in range(units):
+        lay = O.LayerOracle(128, bits, 1 << 30)
+        lay.k_segs.append(ek[u])
+        lay.v_segs.append(ev[u])
+        lay.rows.append(T)
+        ref = lay.attend(q[u].astype(np.float32))
+        assert np.linalg.norm(ref - out[u]) / np.linalg.norm(ref) < 1e-3
+    # export -> bytes -> import into a second cache: the same segments, the same output
+    kx = [parse_mpo(mpo_bytes(cache.export_segment(0, 0, u, "k"))) for u in range(units)]
+    vx = [parse_mpo(mpo_bytes(cache.export_segment(0, 0, u, "v"))) for u in range(units)]
+    assert all(mpo_bytes(a) == mpo_bytes(b) for a, b in zip(kx, kq))
+    c2 = DecodeKvCache(layers=1, units=units, g=1, bits=bits)
+    c2.import_segment(0, kx, vx)
+    assert torch.equal(c2.attend(0, torch.from_numpy(q).cuda()), cache.attend(0, torch.from_numpy(q).cuda()))
+
+
+def test_cli_quantize_dequantize(tmp_path):
+    """cli quantize -> DQZ1 (reference bytes for the reference's chain), dequantize -> DQT1 within
+    1e-3 of the oracle reconstruction; exit codes of the reference's cli.py (2 malformed, 3 bad
+    parameters, 4 unknown subcommand)."""
+    import json as _json
+    import subprocess
+    import sys
+
+    from paper_2405_12591_b200.formats import read_tensor, write_tensor
+
+    root = os.path.dirname(HERE)
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((512, 128)).astype(np.float16).astype(np.float32)
+    write_tensor(tmp_path / "m.dqt", m)
+
+    def run(*a):
+        return subprocess.run([sys.executable, "-m", "paper_2405_12591_b200.cli", *a], capture_output=True,
+                              text=True, cwd=root, timeout=300)
+
+    r = run("quantize", "--input", str(tmp_path / "m.dqt"), "--bits", "4", "--out", str(tmp_path / "m.dqz"))
+    assert r.returncode == 0, r.stderr
+    summary = _json.loads(r.stdout)
+    e = O.encode(m, 4)
+    assert summary["bytes_compressed"] == O.ratio_report(e)[2] and summary["n"] == 2
+    r = run("dequantize", "--input", str(tmp_path / "m.dqz"), "--out", str(tmp_path / "r.dqt"))
+    assert r.returncode == 0, r.stderr
+    rec = read_tensor(tmp_path / "r.dqt")
+    ref = O.decode(e)
+    assert np.linalg.norm(rec - ref) / np.linalg.norm(ref) < 1e-3
+    assert run("quantize", "--input", str(tmp_path / "m.dqt"), "--bits", "3", "--out", "x").returncode == 3
+    assert run("dequantize", "--input", str(tmp_path / "m.dqt"), "--out", "x").returncode == 2
+    assert run("frobnicate").returncode == 4
