@@ -148,6 +148,9 @@ def parse():
                     help="split kernel: 1 = tcgen05, 0 = mma.sync, default: tcgen05 where eligible")
     ap.add_argument("--tail", type=int, default=0,
                     help="fp16 tail tokens per unit before the timed region (steady state: e.g. 512)")
+    ap.add_argument("--seal", action="store_true",
+                    help="steady state across a chunk seal: the tail is filled so that the 1024-token chunk "
+                         "seals (K3 compresses it into a segment) in the middle of the timed region")
     ap.add_argument("--asym", type=int, default=0, choices=[0, 1],
                     help="1: the opt-in per-channel asymmetric quantizer (not the reference scheme)")
     ap.add_argument("--ctas", type=int, default=None,
@@ -418,7 +421,7 @@ def config_keys(args, cfg, world, global_batch):
     T, bits = cfg["T"], cfg["bits"]
     kv_gb = (args.layers or cfg["layers"]) * units * 2 * (T * 128 * bits // 8 + 8 * 8 * 64 * 4 + 4) / 1e9
     return {"workload": cfg["workload"], "global_batch": global_batch, "seq_len": T, "context": T,
-            "kv_bits": bits, "tail_tokens": args.tail,
+            "kv_bits": bits, "tail_tokens": args.tail if not args.seal else "seal mid-region",
             "quantizer": "per-channel asymmetric (opt-in)" if args.asym else "per-tensor symmetric (reference)",
             "layers": args.layers or cfg["layers"], "kv_heads": cfg["kv_heads"], "g": cfg["g"],
             "kv_heads_per_gpu": hi - lo, "units_per_gpu": units,
@@ -493,13 +496,16 @@ def run_ours(args, cfg):
 
     barrier, max_over_ranks = rk.barrier, rk.max
 
-    # steady state: a partly filled fp16 tail, appended through the public API
-    for layer in range(layers):
-        for _ in range(args.tail):
-            cache.append_token(layer, kn[layer], vn[layer])
+    # steady state: a partly filled fp16 tail (DecodeKvCache.extend_tail: the state of
+    # that many append_token calls); --seal fills it so the chunk seals at timed step K // 2
+    fill = chunk_len - 1 - args.warmup - args.steps // 2 if args.seal else args.tail
+    if fill > 0:
+        for layer in range(layers):
+            cache.extend_tail(layer, torch.randn((units, fill, 128), generator=gen, device=dev).half(),
+                              torch.randn((units, fill, 128), generator=gen, device=dev).half())
     torch.cuda.synchronize()
-    appended = args.tail + args.warmup + args.steps + 1 + max(3, args.warmup // 2) + max(3, args.steps // 2)
-    if appended + 1 >= chunk_len:
+    appended = fill + args.warmup + args.steps + 1 + max(3, args.warmup // 2) + max(3, args.steps // 2)
+    if appended + 1 >= chunk_len and not args.seal:
         raise SystemExit("steps too large: the tail would seal a chunk inside the timed region")
 
     # ---- device-resident timed region ----------------------------------------------
@@ -507,17 +513,28 @@ def run_ours(args, cfg):
         step()
     torch.cuda.synchronize()
     barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with Clocks(local) as clk:
         torch.cuda.synchronize()
-        ev0.record()
-        for _ in range(args.steps):
+        evs[0].record()
+        for i in range(args.steps):
             step()
-        ev1.record()
+            evs[i + 1].record()
         torch.cuda.synchronize()
     barrier()
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    ms = max_over_ranks(evs[0].elapsed_time(evs[-1]) / args.steps)
     value = global_batch / (ms / 1e3)
+    seal = None
+    if args.seal:  # the sealing step against the others (device timeline, host work included)
+        med = statistics.median(step_ms)
+        ev_ms = max(step_ms) - med
+        seal = {"chunk_len": chunk_len, "blocks": 2 * units * layers, "block": f"{chunk_len}x128",
+                "sealing_step_ms": max(step_ms), "median_step_ms": med, "event_ms": ev_ms,
+                "amortised_ms_per_step": ev_ms / chunk_len, "fraction_of_step": ev_ms / chunk_len / med}
+        for layer in range(layers):  # the sealed layers build their tables outside the later timed parts
+            cache.attend(layer, q[layer], out[layer])
+        torch.cuda.synchronize()
 
     # ---- split-kernel launches alone, for the roofline -------------------------------
     kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(layers)]
@@ -592,6 +609,7 @@ def run_ours(args, cfg):
                      "bytes_per_launch": kern_bytes,
                      "launch_ms": kern_ms, "peak_kind": peak_kind},
         "memory_per_token_vs_fp16": actual_bytes / fp16_bytes,
+        **({"seal": seal} if seal else {}),
         "write_path": {"blocks": 2 * units * layers, "block": f"{T}x128", "seconds": write_s,
                        "blocks_per_s": 2 * units * layers / write_s},
         "e2e": {"value": global_batch / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,

@@ -166,6 +166,8 @@ def lib():
             )
         handle = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("DQ_LIB") and not hasattr(handle, name):
+                continue  # an older variant build (A/B measurements): bind what it has
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
@@ -211,9 +213,9 @@ def layout_bytes(p: Plan2, bits: int, layout: int) -> int:
     return out.value
 
 
-def raise_flags(flags: torch.Tensor, what: str) -> None:
+def raise_flags(flags, what: str) -> None:
     """Read the device flags word (synchronises) and raise the matching error."""
-    f = int(flags.item())
+    f = int(flags.item()) if isinstance(flags, torch.Tensor) else int(flags)
     if f & FLAG_NONFINITE:
         raise errors.NonFiniteSvdInput(f"{what}: input contains NaN or infinity")
     if f & FLAG_RANGE_OVERFLOW:

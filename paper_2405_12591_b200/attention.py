@@ -24,6 +24,7 @@ import ctypes
 import math
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -34,13 +35,21 @@ from .mpo import plan_shapes
 from .quantize import SUPPORTED_BITS, QuantizedTensor, UnsupportedBits, payload_size
 
 HEAD_DIM = 128
+# numpy view of dq_segment (the ctypes record of _lib.Segment), for column-wise table builds
+_SEG_DTYPE = np.dtype({"names": [f[0] for f in _lib.Segment._fields_],
+                       "formats": [np.uint64 if f[1] is ctypes.c_void_p else
+                                   (np.float32 if f[1] is ctypes.c_float else np.int32)
+                                   for f in _lib.Segment._fields_],
+                       "offsets": [getattr(_lib.Segment, f[0]).offset for f in _lib.Segment._fields_],
+                       "itemsize": ctypes.sizeof(_lib.Segment)})
 DEFAULT_CHUNK_B = 256
 TAIL_SPLIT = 0.2  # fraction of the persistent grid whose last 512-row items are halved (split_tail)
 MAX_CHUNK_B = 512  # > 256: 8-tile items, mma.sync split kernel with g = 1 and 2- / 4-bit codes
 KERNEL_G = (1, 2, 8)  # query heads per kv head the split kernels are instantiated for (8: tcgen05 only)
 GQA_G = 8             # heads of the tcgen05 GQA kernel (path 2)
 MAX_G = 16          # wider GQA groups run as g / kernel_g head groups over the same codes
-MAX_BLOCKS_PER_CALL = 512  # bounds the K3 fp32 core1 scratch
+MAX_BLOCKS_PER_CALL = 4096   # K3 blocks per call; the fp32 core1 scratch is capped at
+K3_SCRATCH_BYTES = 2 << 30    # 2 GB: T = 1024 -> 4096 blocks per call, T = 4096 -> 1024
 
 
 @dataclass
@@ -63,6 +72,7 @@ class SegmentGroup:
     token0: int
     k_ch: torch.Tensor | None = None  # asymmetric mode: (units, 2, r, 16) f32 channel scales, zero points
     v_ch: torch.Tensor | None = None
+    v_g0f16: torch.Tensor | None = None  # fp16 copy of v_g0h for the mma.sync split kernel (path 0)
 
     def reference_bytes(self, bits: int) -> int:
         """compression_report().bytes_compressed of one unit's K (or V) block (compress.py:234-248);
@@ -73,11 +83,13 @@ class SegmentGroup:
         return payload_size(p.r * p.i2 * p.j2, bits) + scales + 2 * (p.i1 * p.j1 * p.r)
 
     def stream_bytes(self) -> int:
-        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k and G0v, scales
-        (the channel tables in the asymmetric mode)."""
+        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k (prepare
+        kernel), G0v (fp16 on the mma.sync path, fp32 on the tcgen05 paths), scales (the channel
+        tables in the asymmetric mode)."""
         ch = 2 * self.k_ch[0].numel() * 4 if self.k_ch is not None else 0
+        vg = self.v_g0f16 if self.v_g0f16 is not None else self.v_g0h
         return (self.k_payload.shape[1] + self.v_payload.shape[1] + self.k_g0h.element_size() * self.k_g0h.shape[1]
-                + self.v_g0h.element_size() * self.v_g0h.shape[1] + 8 + ch)
+                + vg.element_size() * vg.shape[1] + 8 + ch)
 
 
 class _Layer:
@@ -89,20 +101,29 @@ class _Layer:
         self.kernel_g = None  # heads per split-kernel instance used for this layer
         self.keep = []     # tensors referenced by args
         self.gen = 0       # plan generation: bumped whenever the segment table / args change
+        self.seal_pending = False  # the tail is full: sealed (batched) before the next use
 
 
-def compress_blocks(blocks: torch.Tensor, bits: int, layout: int, g0_dtype=torch.float16, asym: bool = False):
+def compress_blocks(blocks: torch.Tensor, bits: int, layout: int, g0_dtype=torch.float16, asym: bool = False,
+                    flags: torch.Tensor | None = None):
     """K3 over (nblk, T, 128) fp16/fp32 CUDA blocks in slices of MAX_BLOCKS_PER_CALL.
 
     Returns (payload (nblk, bytes), core0 f32, g0 [a][r][c] normalised in g0_dtype, norm f32, scale f32, plan);
     with ``asym`` the scale is 1 and the per-channel tables come back as a 7th item (nblk, 2, r, 16).
+    Errors (non-finite input, no convergence) raise here, after a sync; with a device ``flags``
+    word they are OR-ed into it instead, and nothing synchronises.
     """
     nblk = blocks.shape[0]
     outs = []
-    for s in range(0, nblk, MAX_BLOCKS_PER_CALL):
+    # large calls keep the latency-bound eigensolver (one CTA per block) in many full waves
+    per = max(64, min(MAX_BLOCKS_PER_CALL, K3_SCRATCH_BYTES // (64 * 2 * blocks.shape[1] * 4)))
+    for s in range(0, nblk, per):
         fn = deco_quantize_asym_batched if asym else deco_quantize_batched
-        res = fn(blocks[s:s + MAX_BLOCKS_PER_CALL], bits, layout)
-        _lib.raise_flags(res["flags"], "deco_quantize")
+        res = fn(blocks[s:s + per], bits, layout)
+        if flags is None:
+            _lib.raise_flags(res["flags"], "deco_quantize")
+        else:
+            flags.bitwise_or_(res["flags"])
         outs.append(res)
     p = outs[0]["plan"]
     payload = torch.cat([o["payload"] for o in outs]) if len(outs) > 1 else outs[0]["payload"]
@@ -235,6 +256,7 @@ class DecodeKvCache:
         self.tail_v = torch.zeros(shape, dtype=torch.float16, device=self.device)
         self.tail_len = torch.zeros((layers, units), dtype=torch.int32, device=self.device)
         self.bytes_moved_read = 0
+        self._pending = []  # deferred seal error words: (pinned host copy, event, layer)
 
     # ---- lifecycle -----------------------------------------------------------
     def _layer(self, layer: int) -> _Layer:
@@ -246,22 +268,64 @@ class DecodeKvCache:
         lay = self._layer(layer)
         return lay.tokens_sealed + lay.tail_len
 
-    def _add_group(self, layer: int, keys: torch.Tensor, values: torch.Tensor):
-        lay = self._layer(layer)
+    def _add_group(self, layer: int, keys: torch.Tensor, values: torch.Tensor, deferred: bool = False):
+        """Compress (units, T, 128) K / V into a new segment group of ``layer`` (a list of layers
+        with keys / values (len(layers) * units, T, 128): one batched K3 call for all of them).
+        ``deferred`` (seals inside decoding): no host sync -- the device error word is copied back
+        asynchronously and raised by the first later call that finds it on the host."""
+        layers = layer if isinstance(layer, list) else [layer]
+        for ly in layers:
+            self._layer(ly)
         T = keys.shape[1]
+        flags = torch.zeros(1, dtype=torch.int32, device=self.device) if deferred else None
         # fp32 G0 on the score side: scores of outlier-heavy keys are large, and the fp16
         # rounding of G0k (2^-11) would show up as absolute logit error
-        kres = compress_blocks(keys, self.bits, _lib.LAYOUT_KTILE, torch.float32, self.asym)
-        vres = compress_blocks(values, self.bits, _lib.LAYOUT_VTILE, torch.float32, self.asym)
-        kp, kc0, kg, kn, ks, p = kres[:6]
-        vp, vc0, vg, vn, vs, _ = vres[:6]
-        kch, vch = (kres[6], vres[6]) if self.asym else (None, None)
+        kres = compress_blocks(keys, self.bits, _lib.LAYOUT_KTILE, torch.float32, self.asym, flags)
+        vres = compress_blocks(values, self.bits, _lib.LAYOUT_VTILE, torch.float32, self.asym, flags)
+        if deferred:
+            host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            host.copy_(flags, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending.append((host, ev, layers))
+        p = kres[5]
         i2p = -(-p.i2 // _lib.I2_PAD) * _lib.I2_PAD
-        lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, kn, vn, lay.tokens_sealed,
-                                       kch, vch))
-        lay.tokens_sealed += T
-        lay.args = None
-        lay.gen += 1
+        U = self.units
+        for i, ly in enumerate(layers):
+            lay = self._layers[ly]
+            sl = slice(i * U, (i + 1) * U)
+            kp, kc0, kg, kn, ks = (x[sl] for x in kres[:5])
+            vp, vc0, vg, vn, vs = (x[sl] for x in vres[:5])
+            kch, vch = (kres[6][sl], vres[6][sl]) if self.asym else (None, None)
+            lay.groups.append(SegmentGroup(T, p, i2p, kp, vp, kc0, vc0, kg, vg, ks, vs, kn, vn, lay.tokens_sealed,
+                                           kch, vch))
+            lay.tokens_sealed += T
+            lay.args = None
+            lay.gen += 1
+
+    def _flush_seals(self):
+        """Seal every full tail (kvcache.py:124-128) in ONE batched K3 call.  A tail that reaches
+        chunk_len stays in place until its layer is next read or written; in lock-step decoding
+        every layer fills at the same step, so all of them compress together (32 x 1024 blocks at
+        C2 instead of 32 calls of 1024: the eigensolver's one CTA per block then runs in full
+        waves).  Results are identical to sealing at the append (the reference's point)."""
+        full = [ly for ly, lay in enumerate(self._layers) if lay.seal_pending]
+        if not full:
+            return
+        runs = []  # contiguous layer runs: their tails are one (n * units, chunk, 128) view
+        for ly in full:
+            if runs and runs[-1][-1] == ly - 1:
+                runs[-1].append(ly)
+            else:
+                runs.append([ly])
+        for run in runs:
+            a, b = run[0], run[-1] + 1
+            self._add_group(run, self.tail_k[a:b].reshape(-1, self.chunk_len, self.dim),
+                            self.tail_v[a:b].reshape(-1, self.chunk_len, self.dim), deferred=True)
+            self.tail_len[a:b].zero_()
+            for ly in run:
+                self._layers[ly].tail_len = 0
+                self._layers[ly].seal_pending = False
 
     def prefill(self, layer: int, keys: torch.Tensor, values: torch.Tensor):
         """keys/values: (units, T, 128) CUDA fp16 or fp32.  One segment per unit (kvcache.py:99-114)."""
@@ -278,24 +342,63 @@ class DecodeKvCache:
 
     def append_token(self, layer: int, k_rows: torch.Tensor, v_rows: torch.Tensor):
         """k_rows/v_rows: (units, 128).  Seals the tail at chunk_len (kvcache.py:116-128)."""
-        self._layer(layer)
+        if self._layer(layer).seal_pending:
+            self._flush_seals()
+        if self._pending:
+            self._check_seals()
         k, v = self._rows(k_rows, v_rows)
         check(lib().dq_tail_append(ptr(k), ptr(v), self.units, ptr(self.tail_k[layer]), ptr(self.tail_v[layer]),
                                    ptr(self.tail_len[layer]), self.chunk_len, stream_ptr()), "tail_append")
         self._after_append(layer)
+
+    def extend_tail(self, layer: int, k_rows: torch.Tensor, v_rows: torch.Tensor):
+        """Append n tokens per unit at once (k_rows / v_rows: (units, n, 128)): the same state as n
+        append_token calls that do not reach chunk_len (the seal, kvcache.py:124-128, stays with
+        the single-token path)."""
+        lay = self._layer(layer)
+        if lay.seal_pending:
+            self._flush_seals()
+        n = k_rows.shape[1] if k_rows.ndim == 3 else -1
+        if k_rows.shape != (self.units, n, self.dim) or v_rows.shape != k_rows.shape:
+            raise DimMismatch(f"rows must be ({self.units}, n, {self.dim})")
+        if lay.tail_len + n >= self.chunk_len:
+            raise ShapeMismatch("extend_tail would reach chunk_len: append the sealing token with append_token")
+        t0 = lay.tail_len
+        self.tail_k[layer, :, t0:t0 + n].copy_(k_rows)
+        self.tail_v[layer, :, t0:t0 + n].copy_(v_rows)
+        self.tail_len[layer].add_(n)
+        lay.tail_len += n
 
     def _rows(self, k_rows: torch.Tensor, v_rows: torch.Tensor):
         if k_rows.shape != (self.units, self.dim) or v_rows.shape != (self.units, self.dim):
             raise DimMismatch(f"rows must be ({self.units}, {self.dim})")
         return (k_rows.to(self.device, torch.float16).contiguous(), v_rows.to(self.device, torch.float16).contiguous())
 
+    def _check_seals(self, wait: bool = False):
+        """Raise the error of a deferred seal whose device flags have reached the host."""
+        pending, self._pending = self._pending, []
+        for i, (host, ev, layer) in enumerate(pending):
+            if wait:
+                ev.synchronize()
+            if ev.query():
+                if int(host.item()):
+                    self._pending += pending[i + 1:]  # raise once; the later seals stay pending
+                    _lib.raise_flags(int(host.item()), f"deco_quantize (chunk sealed in layers {layer})")
+            else:
+                self._pending.append((host, ev, layer))
+
+    def check_errors(self):
+        """Seal any full tail, wait for every deferred seal and raise its error, if any (the
+        reference raises inside append_token; a seal inside decoding reports at the first later
+        call that sees it)."""
+        self._flush_seals()
+        self._check_seals(wait=True)
+
     def _after_append(self, layer: int):
         lay = self._layers[layer]
         lay.tail_len += 1
         if lay.tail_len == self.chunk_len:
-            self._add_group(layer, self.tail_k[layer], self.tail_v[layer])
-            self.tail_len[layer].zero_()
-            lay.tail_len = 0
+            lay.seal_pending = True  # compressed by _flush_seals before this layer is used again
 
     def import_segment(self, layer: int, keys: list, values: list):
         """Append one sealed segment per unit from reference-form chains (``QuantizedMpo``, n = 2,
@@ -352,9 +455,6 @@ class DecodeKvCache:
     # ---- attention -----------------------------------------------------------
     def _build_args(self, layer: int):
         lay = self._layers[layer]
-        segs = []
-        # the kernel sees g0h = core0 / norm, so the per-segment scale carries the norm back
-        scales = [((grp.k_scale * grp.k_norm).cpu(), (grp.v_scale * grp.v_norm).cpu()) for grp in lay.groups]
         full_plans = all(grp.plan.i1 == 8 and grp.plan.r == 64 for grp in lay.groups)
         gk = self.kernel_g
         if gk == GQA_G and not full_plans:
@@ -364,28 +464,38 @@ class DecodeKvCache:
         hg = self.g // gk
         vunits = self.units * hg
         lay.kernel_g = gk
-        for grp, (ks, vs) in zip(lay.groups, scales):
+        if gk == GQA_G:
+            path = 2
+        else:
+            eligible = self.bits == 4 and gk == 1 and full_plans
+            if self.tc and not eligible:
+                raise Unsupported("the tcgen05 path needs 4-bit codes, one head (or 8) per kernel and i1 = 8, "
+                                  "r = 64 plans")
+            path = 1 if (eligible and self.tc) else 0
+        if path == 0:  # the mma.sync kernel folds an fp16 copy of G0v (made once per group)
+            for grp in lay.groups:
+                if grp.v_g0f16 is None:
+                    grp.v_g0f16 = grp.v_g0h.to(torch.float16)
+        # the segment table, built column-wise (numpy view of the dq_segment records): one record
+        # per (group, unit, head group); the scales are filled in on the device below (no sync)
+        nseg = len(lay.groups) * vunits
+        seg_arr = (_lib.Segment * max(nseg, 1))()
+        rec = np.frombuffer(seg_arr, dtype=_SEG_DTYPE, count=nseg) if nseg else None
+        u_of = np.repeat(np.arange(self.units, dtype=np.int64), hg)
+        for gi, grp in enumerate(lay.groups):
             p = grp.plan
-            kb, vb = grp.k_payload.shape[1], grp.v_payload.shape[1]
-            kgb = grp.k_g0h.shape[1] * grp.k_g0h.element_size()
-            vgb = grp.v_g0h.shape[1] * grp.v_g0h.element_size()
-            for u in range(self.units):
-                for hk in range(hg):  # one virtual unit per head group, same codes
-                    s = _lib.Segment()
-                    s.k_codes = grp.k_payload.data_ptr() + u * kb
-                    s.v_codes = grp.v_payload.data_ptr() + u * vb
-                    s.k_g0 = grp.k_g0h.data_ptr() + u * kgb
-                    s.v_g0 = grp.v_g0h.data_ptr() + u * vgb
-                    s.k_scale = float(ks[u])
-                    s.v_scale = float(vs[u])
-                    s.T, s.i1, s.i2, s.r, s.i2p = grp.T, p.i1, p.i2, p.r, grp.i2p
-                    s.unit, s.token0 = u * hg + hk, grp.token0
-                    if grp.k_ch is not None:
-                        s.k_ch = grp.k_ch[u].data_ptr()
-                        s.v_ch = grp.v_ch[u].data_ptr()
-                    segs.append(s)
-        nseg = len(segs)
-        seg_arr = (_lib.Segment * max(nseg, 1))(*segs)
+            r = rec[gi * vunits:(gi + 1) * vunits]
+            r["k_codes"] = grp.k_payload.data_ptr() + u_of * grp.k_payload.shape[1]
+            r["v_codes"] = grp.v_payload.data_ptr() + u_of * grp.v_payload.shape[1]
+            r["k_g0"] = grp.k_g0h.data_ptr() + u_of * grp.k_g0h.shape[1] * grp.k_g0h.element_size()
+            vg = grp.v_g0f16 if path == 0 else grp.v_g0h
+            r["v_g0"] = vg.data_ptr() + u_of * vg.shape[1] * vg.element_size()
+            r["T"], r["i1"], r["i2"], r["r"], r["i2p"] = grp.T, p.i1, p.i2, p.r, grp.i2p
+            r["unit"] = np.arange(vunits, dtype=np.int32)
+            r["token0"] = grp.token0
+            if grp.k_ch is not None:
+                r["k_ch"] = grp.k_ch.data_ptr() + u_of * grp.k_ch[0].numel() * 4
+                r["v_ch"] = grp.v_ch.data_ptr() + u_of * grp.v_ch[0].numel() * 4
         # work plan (host) -> device tables
         ctas = self.ctas
         if ctas is None:
@@ -412,7 +522,7 @@ class DecodeKvCache:
             # several rounds of 512-row items: the last TAIL_SPLIT x grid items run as 256-row
             # halves, evening out the scheduler's last round (C3: 230.2 -> 225.7 us; at 256-row
             # items the 128-row halves cost more than they save: C2 64.3 -> 68.5 us)
-            wp = split_tail(wp, [sg.unit for sg in segs], int(TAIL_SPLIT * ctas))
+            wp = split_tail(wp, rec["unit"].tolist(), int(TAIL_SPLIT * ctas))
         if hg > 1:  # a tile range's head groups back to back in the ticket order (L2 reuse)
             order = sorted(range(wp.nwork), key=lambda i: (wp.work[3 * i] // hg, wp.work[3 * i + 1],
                                                            wp.work[3 * i] % hg))
@@ -420,10 +530,22 @@ class DecodeKvCache:
             wp.work_part = [wp.work_part[i] for i in order]
         dev = self.device
 
-        def i32(arr, n):
-            return torch.tensor(list(arr)[:n], dtype=torch.int32).to(dev)
+        staged = []  # pinned host copies: the uploads do not wait for the stream
 
-        seg_dev = torch.frombuffer(bytearray(bytes(seg_arr)), dtype=torch.uint8).to(dev)
+        def up(host: torch.Tensor) -> torch.Tensor:
+            h = host.pin_memory()
+            staged.append(h)
+            return h.to(dev, non_blocking=True)
+
+        def i32(arr, n):
+            return up(torch.tensor(list(arr)[:n], dtype=torch.int32))
+
+        seg_dev = up(torch.frombuffer(bytearray(bytes(seg_arr)), dtype=torch.uint8))
+        if nseg:  # the kernel sees g0h = core0 / norm: each segment's scale carries the norm back
+            rec_f = seg_dev[:nseg * ctypes.sizeof(_lib.Segment)].view(torch.float32).view(nseg, -1)
+            ko, vo = _lib.Segment.k_scale.offset // 4, _lib.Segment.v_scale.offset // 4
+            rec_f[:, ko] = torch.cat([(g.k_scale * g.k_norm).repeat_interleave(hg) for g in lay.groups])
+            rec_f[:, vo] = torch.cat([(g.v_scale * g.v_norm).repeat_interleave(hg) for g in lay.groups])
         nwork = wp.nwork
         work_dev = i32(wp.work, 3 * nwork)
         wpart_dev = i32(wp.work_part, nwork)
@@ -439,14 +561,7 @@ class DecodeKvCache:
         a.units = vunits
         a.g = gk
         a.head_groups = hg
-        if gk == GQA_G:
-            a.path = 2
-        else:
-            eligible = self.bits == 4 and gk == 1 and full_plans
-            if self.tc and not eligible:
-                raise Unsupported("the tcgen05 path needs 4-bit codes, one head (or 8) per kernel and i1 = 8, "
-                                  "r = 64 plans")
-            a.path = 1 if (eligible and self.tc) else 0
+        a.path = path
         a.bits = self.bits
         a.asym = 1 if self.asym else 0
         a.tail_k = self.tail_k[layer].data_ptr()
@@ -472,7 +587,7 @@ class DecodeKvCache:
         a.wimg_stride = wib.value
         lay.args = a
         lay.gen += 1
-        lay.keep = [seg_dev, work_dev, wpart_dev, sched, p0_dev, np_dev, part_o, part_ml, wimg]
+        lay.keep = [seg_dev, work_dev, wpart_dev, sched, p0_dev, np_dev, part_o, part_ml, wimg, *staged]
 
     def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None,
                append: tuple[torch.Tensor, torch.Tensor] | None = None,
@@ -484,6 +599,10 @@ class DecodeKvCache:
         launch: the rows join the tail after this attention, exactly as attend + append_token.
         """
         lay = self._layer(layer)
+        if lay.seal_pending:
+            self._flush_seals()
+        if self._pending:
+            self._check_seals()
         if q.shape != (self.units, self.g, self.dim):
             raise DimMismatch(f"q must be ({self.units}, {self.g}, {self.dim})")
         if lay.args is None:
@@ -515,6 +634,8 @@ class DecodeKvCache:
     def launch(self, layer: int, q: torch.Tensor, out: torch.Tensor, phases: int = 3):
         """Low-level launch (bench/profiling): phases bit 0 = split kernel, bit 1 = combine."""
         lay = self._layers[layer]
+        if lay.seal_pending:
+            self._flush_seals()
         if lay.args is None:
             self._build_args(layer)
         a = lay.args
@@ -524,6 +645,7 @@ class DecodeKvCache:
 
     def clone_layer(self, src: int, dst: int):
         """Copy layer ``src``'s sealed segments into empty layer ``dst`` (distinct device memory)."""
+        self._flush_seals()
         s, d = self._layer(src), self._layer(dst)
         if d.groups or d.tail_len:
             raise AlreadyPrefilled("destination layer already holds tokens")
@@ -549,6 +671,10 @@ class DecodeKvCache:
         return seg + tail + qo
 
     def ledger(self):
+        self._flush_seals()
+        return self._ledger()
+
+    def _ledger(self):
         """(bytes_fp16_equivalent, bytes_actual) with the reference's accounting (kvcache.py:130-141)."""
         fp16 = actual = 0
         for lay in self._layers:
@@ -560,6 +686,7 @@ class DecodeKvCache:
 
     def export_segment(self, layer: int, index: int, unit: int, which: str = "k") -> QuantizedMpo:
         """Segment ``index`` of ``unit`` as a reference-form QuantizedMpo (wire-order payload)."""
+        self._flush_seals()
         grp = self._layer(layer).groups[index]
         if grp.k_ch is not None:
             raise Unsupported("asymmetric segments have no reference (symmetric per-tensor) form")

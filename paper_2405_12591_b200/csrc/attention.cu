@@ -117,10 +117,11 @@ __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __ha
 }
 
 
-// consumer teams of the mma.sync split kernel: 2 (one CTA per SM, a shared slot pool) for g = 1,
-// 1 (two CTAs per SM) for g = 2, whose 32 KB W image per team leaves no room for a second team
+// consumer teams of the mma.sync split kernel: 1 = two CTAs per SM, each a FIFO ring (the default:
+// C2 62.5 us per layer); 2 = one CTA per SM, two teams sharing a slot pool (DQ_ATTN_TEAMS_G1=2,
+// g = 1 only: measured 69 us)
 #ifndef DQ_ATTN_TEAMS_G1
-#define DQ_ATTN_TEAMS_G1 2
+#define DQ_ATTN_TEAMS_G1 1
 #endif
 template <int G>
 constexpr int kTeamsOf = G == 1 ? DQ_ATTN_TEAMS_G1 : 1;

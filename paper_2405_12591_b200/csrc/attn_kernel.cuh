@@ -9,7 +9,7 @@
 // W-image and G0v copies at their own barrier points) and 1 producer warp whose lane 0 issues
 // every code stage (cp.async.bulk, completing on the slot's `full` mbarrier).
 //
-// TEAMS = 2 (one CTA per SM, the default for g = 1): the two teams work on different items
+// TEAMS = 2 (one CTA per SM, opt-in: DQ_ATTN_TEAMS_G1=2): the two teams work on different items
 // and share ONE pool of ring slots.  A team in its softmax or epilogue holds no more than
 // kTeamPrefetch stages of its next phase (the producer reads the phase each team has begun,
 // `started`), so the other team can keep up to S - kTeamPrefetch slots in flight: the SM
@@ -18,8 +18,10 @@
 // CTA's 80 KB in flight cannot carry the SM's share: 32-36 of 44 GB/s.)  Slots
 // are handed out from a free mask, so the producer publishes each team's n-th slot (and the
 // parity of its `full` phase) in the team's stage queue `sq`, behind an mbarrier `sqbar`.
-// TEAMS = 1: two CTAs per SM, each its own producer and pool (the former design, kept for
-// the g = 2 instantiations whose 32 KB W image leaves no room for two teams).
+// TEAMS = 1 (the default): two CTAs per SM, each with its own FIFO ring of slots (stage n in slot
+// n % S, no stage queue).  Measured on C2: 62.5 us per layer for TEAMS = 1 against 69 us for
+// TEAMS = 2 -- the shared pool does not hide the fixed phases better than the sibling CTA does,
+// and its per-stage queue costs the consumers an extra wait.
 #pragma once
 
 #include "attn_prepare.cuh"
@@ -51,7 +53,7 @@ template <int G>
 constexpr int kStagesOf = G == 1 ? DQ_ATTN_STAGES_G1 : 3;
 template <int G, int TEAMS = 1>
 constexpr int kCtasPerSm = TEAMS > 1 ? 1 : (G == 1 ? DQ_ATTN_CTAS_G1 : 2);
-constexpr int kSubRing = 8;  // descriptor ring per team (the producer runs <= 3 items ahead)
+constexpr int kSubRing = 4;  // descriptor ring per team (in use: the current item, the next, one fetched)
 constexpr int kQ = 32;       // per-team stage queue (>= ring slots)
 // stages of a team's NEXT phase the producer issues while the team has not begun it
 #ifndef DQ_TEAM_PREFETCH
@@ -61,7 +63,7 @@ constexpr int kTeamPrefetch = DQ_TEAM_PREFETCH;
 constexpr int kSmemCap = 227 * 1024;  // dynamic shared memory per CTA (sm_100)
 
 template <int TEAMS>
-constexpr int kCtaThreadsOf = TEAMS * kThreads + 32;
+constexpr int kCtaThreadsOf = TEAMS * kThreads + 32 * (TEAMS + 1);  // + a producer warp per team + the fetcher
 
 template <int BITS>
 constexpr int kPBits = 15;  // P / tile max in (0.5, 1] -> round(P * 2^(kPBits - e)); Y sums per 64-row tile
@@ -71,7 +73,7 @@ constexpr int kPBits = 15;  // P / tile max in (0.5, 1] -> round(P * 2^(kPBits -
 struct SubItem {
   const unsigned char* kc;
   const unsigned char* vc;
-  const float* vg0;
+  const void* vg0;  // fp16 G0v [a][rr][8 c] (the path-0 copy, attention.py)
   float kscale, vscale;
   int seg, wb0, nbt, part;
   int r, i1, i2, item;
@@ -80,27 +82,30 @@ struct SubItem {
 };
 
 // per-team state: descriptors, stage queue, W image / G0v, P, reductions
-template <int G, int NT, bool ASYM>
+template <int G, int NT, bool ASYM, int QN = kQ>
 struct TeamSmem {
-  uint64_t wbar;   // W image (attn_prepare.cuh) by TMA, one phase per sub-item
+  uint64_t wbar;   // W image (attn_prepare.cuh) by TMA (issued by the producer), one phase per sub-item
+  uint64_t wfree;  // the consumers are past an item's K phase: its W buffer may be refilled
   uint64_t g0bar;  // G0v prefetch, one phase per sub-item
   uint64_t descfull[kSubRing];  // descriptor j written (producer arrival), phase j / kSubRing
-  uint64_t sqbar[kQ];           // stage n's slot published (producer arrival), phase n / kQ
-  int sq[kQ];                   // stage n of the team: ring slot | (full-barrier parity << 8)
+  uint64_t sqbar[QN];           // stage n's slot published (producer arrival), phase n / kQ (TEAMS = 2)
+  int sq[QN];                   // stage n of the team: ring slot | (full-barrier parity << 8)
   int started;                  // phase the consumers began: 2j = K of item j, 2j + 1 = V of item j
-  int pad_[3];
+  int fetched;                  // descriptors the fetcher warp has written into `sub` (release / acquire)
+  int taken;                    // descriptors the producer has made current
+  int pad_;
   int kend[kSubRing], vend[kSubRing];  // producer: team stage index where item j's K / V phase ends
   SubItem sub[kSubRing];        // the team's j-th item lives in slot j % kSubRing
   alignas(16) WMeta<G> wmeta;  // per-column W scales and excess corrections (TMA target)
   int gamma[G][8][NT];     // excess correction of Y per 64-row tile: kExcess * sum_b Pint[a][b]
   float lsum[G][kWarps];   // probability mass per warp
   unsigned pmax[G][8][NT];  // largest probability per (h, a, tile), float bits
-  // K phase: W limbs, 16-byte chunks [((h*2 + limb)*r + rr)*8 + (a ^ 2*(rr&3))];
-  // V phase + epilogue (aliased, W is dead): fp32 G0v [a][rr][c] by TMA
-  union {
-    uint4 w[G * 2 * kMaxR * 8];
-    float4 g0v[8 * (kMaxR * 2 + 1)];  // [a][rr][c] with a 16-byte pad per a (kG0vPad)
-  } wg;
+  // K phase: W limbs, 16-byte chunks [((h*2 + limb)*r + rr)*8 + (a ^ 2*(rr&3))] (the next
+  // item's image lands here as soon as this item's K phase is done)
+  uint4 w[G * 2 * kMaxR * 8];
+  // epilogue: fp16 G0v [a][rr][8 c] (normalised), r + 1 chunks per a (a 16-byte pad: the lanes
+  // tid4 = 0..3 read a = 2 tid4 + aa four banks apart); loaded at the previous item's end
+  uint4 g0v[8 * (kMaxR + 1)];
   // V phase: P limbs [((h*2 + limb)*8 + a)*(4 NT) + (bg ^ 4*(a&1))];
   // epilogue (aliased, P is dead): cross-warp reduction of the O partial
   union {
@@ -112,13 +117,18 @@ struct TeamSmem {
   alignas(16) float vch[ASYM ? 2 * kMaxR * 16 : 4];
 };
 
+template <int TEAMS>
+constexpr int kQOf = TEAMS > 1 ? kQ : 1;  // a lone team reads its FIFO ring: no stage queue
+
 template <int G, int NT, bool ASYM, int TEAMS>
 constexpr int ring_stages() {
+  constexpr int team = (int)sizeof(TeamSmem<G, NT, ASYM, kQOf<TEAMS>>);
   if constexpr (TEAMS == 1) {
-    // 8-tile items with the asymmetric channel table: one stage less keeps 2 CTAs per SM
-    return (ASYM && NT > kTiles) ? kStagesOf<G> - 1 : kStagesOf<G>;
+    // as many stages (<= kStagesOf) as keep 2 CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
+    constexpr int s = (228 * 1024 / 2 - 1024 - team - 256) / (kStageBytes + 16);
+    return s < kStagesOf<G> ? s : kStagesOf<G>;
   } else {
-    const int s = (kSmemCap - TEAMS * (int)sizeof(TeamSmem<G, NT, ASYM>) - 256) / (kStageBytes + 16);
+    const int s = (kSmemCap - TEAMS * team - 256) / (kStageBytes + 16);
     return s > 24 ? 24 : s;
   }
 }
@@ -130,7 +140,9 @@ struct AttnSmem {
   alignas(128) unsigned char ring[kStages][kStageBytes];
   uint64_t full[kStages];
   uint64_t empty[kStages];
-  TeamSmem<G, NT, ASYM> team[TEAMS];
+  unsigned freemask;        // the slot pool: bit s set = slot s free (shared by the team producers)
+  int slot_use[kStages];    // uses of each slot so far: the parity of its full / empty phases
+  TeamSmem<G, NT, ASYM, kQOf<TEAMS>> team[TEAMS];
 };
 
 // stage geometry of a sub-item with r bond rows and nbt tiles
@@ -171,15 +183,24 @@ __device__ __forceinline__ void load_sub(SubItem& d, const dq_attn_args& a, int 
   d = t;
 }
 
-// the W image (limb chunks + metadata) of a sub-item's segment onto the team's wbar (one thread)
-template <int G, int NT, bool ASYM>
-__device__ __forceinline__ void issue_wimg(TeamSmem<G, NT, ASYM>& tm, const dq_attn_args& a, const SubItem& d) {
-  const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
-  const uint32_t wb = (uint32_t)(G * 2 * d.r * 8 * 16);
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+// the W image (limb chunks + metadata) of a segment onto the team's wbar (one thread)
+template <int G, int NT, bool ASYM, int QN>
+__device__ __forceinline__ void issue_wimg(TeamSmem<G, NT, ASYM, QN>& tm, const dq_attn_args& a, int seg, int r) {
+  const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)seg * a.wimg_stride;
+  const uint32_t wb = (uint32_t)(G * 2 * r * 8 * 16);
   mbar_expect_tx(&tm.wbar, wb + (uint32_t)sizeof(WMeta<G>));
-  bulk_g2s(tm.wg.w, img, wb, &tm.wbar);
+  bulk_g2s(tm.w, img, wb, &tm.wbar);
   bulk_g2s(&tm.wmeta, img + kWChunkBytes<G>, (uint32_t)sizeof(WMeta<G>), &tm.wbar);
+}
+
+// fp16 G0v (one copy per a into its padded block) and, asymmetric, the V channel table (one thread)
+template <int G, int NT, bool ASYM, int QN>
+__device__ __forceinline__ void issue_g0v(TeamSmem<G, NT, ASYM, QN>& tm, const dq_attn_args& a, const SubItem& d) {
+  const uint32_t cb = ASYM ? (uint32_t)(2 * d.r * 16 * 4) : 0u;
+  mbar_expect_tx(&tm.g0bar, (uint32_t)(d.i1 * d.r * 16) + cb);
+  if (ASYM) bulk_g2s(tm.vch, a.segs[d.seg].v_ch, cb, &tm.g0bar);
+  const uint4* src = reinterpret_cast<const uint4*>(d.vg0);
+  for (int aa = 0; aa < d.i1; ++aa) bulk_g2s(tm.g0v + aa * (d.r + 1), src + aa * d.r, (uint32_t)(d.r * 16), &tm.g0bar);
 }
 
 template <int NT>
@@ -236,10 +257,11 @@ __device__ __forceinline__ Issue issue_of(const SubItem& d) {
 }
 
 // issue local stage `st` of an item into its ring slot (one thread)
+// (no proxy fence: the slot's previous contents were only read by the consumers, whose release
+// the producer observed on the slot's `empty` mbarrier before reissuing it)
 template <int BITS>
 __device__ __forceinline__ void issue_stage(const Issue& d, int st, unsigned char* slot_buf, uint64_t* bar) {
   constexpr int RB = 2 * BITS;
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (st < d.nK) {
     const int rk0 = st * d.RK;
     const int nr = min(d.RK, d.r - rk0);
@@ -260,9 +282,11 @@ __device__ __forceinline__ void issue_stage(const Issue& d, int st, unsigned cha
 struct TeamProd {
   Issue cur;
   int ls;        // next local stage of cur
-  int k;         // descriptors published
+  int k;         // descriptors taken
   int issued, reclaimed;
-  bool hc, hn;   // streaming an item / the next item's descriptor is loaded (slot k % kSubRing)
+  bool hc;       // streaming an item
+  bool wpend;    // the current item's W image is not issued yet
+  int wseg, wr;  // its segment and bond dimension
 };
 
 __device__ __forceinline__ bool elect_lane() {
@@ -271,116 +295,206 @@ __device__ __forceinline__ bool elect_lane() {
   return p != 0;
 }
 
-// The whole producer warp runs this converged: every lane holds the same (warp-uniform) state,
-// one elected lane performs the stores, arrivals and copies.  (A lone `lane == 0` loop makes
-// the compiler wrap each bulk copy's operands in a register-to-uniform broadcast loop: at
-// ~150 dependent instructions per stage the issue rate, not HBM, bounded the pool.)
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+// ---- the fetcher (lane 0 of the warp after the producer) ----------------------------------
+// Keeps each team's next descriptors ready in its ring (ticket from the global counter, then the
+// work-list entry and the segment: dependent global loads of ~1 us that used to stall the
+// producer once per item), at most kFetchAhead ahead of what the producer has taken.
+// descriptors a team holds beyond its current item: 1 = the next item only (C2 62.5 us per layer;
+// 2: 68 us -- tickets drawn early leave the last round unbalanced)
+#ifndef DQ_FETCH_AHEAD
+#define DQ_FETCH_AHEAD 1
+#endif
+constexpr int kFetchAhead = DQ_FETCH_AHEAD;
+
 template <int BITS, int G, int NT, bool ASYM, int TEAMS>
-__device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args) {
-  using TS = TeamSmem<G, NT, ASYM>;
-  constexpr int S = AttnSmem<G, NT, ASYM, TEAMS>::kStages;
-  static_assert((kQ & (kQ - 1)) == 0 && (kSubRing & (kSubRing - 1)) == 0, "power-of-two rings");
-  const bool leader = elect_lane();
-  uint32_t freemask = S >= 32 ? ~0u : ((1u << S) - 1u);
-  uint32_t parity = 0;  // bit s: parity of slot s's next use
+__device__ void fetch(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args) {
+  int fk[TEAMS];
+  bool done[TEAMS];
   bool waited = false;  // griddepcontrol.wait before the first ticket (the counter is shared with
                         // the previous launch on these args)
-  TeamProd P[TEAMS];
-
-  // descriptor P.k (loaded into its ring slot, or the end marker) becomes current and is published
-  auto advance = [&](TeamProd& p, TS& tm) {
-    const int ds = p.k & (kSubRing - 1);
-    p.hc = p.hn;
-    p.hn = false;
-    p.ls = 0;
-    __syncwarp();  // the leader's descriptor stores are visible to the warp
-    if (p.hc) p.cur = issue_of(tm.sub[ds]);
-    if (leader) {
-      if (p.hc) {
-        tm.kend[ds] = p.issued + p.cur.nK;
-        tm.vend[ds] = p.issued + p.cur.stages;
-      } else {
-        tm.sub[ds].nbt = 0;
-      }
-      mbar_arrive(&tm.descfull[ds]);  // release: the descriptor is visible to its waiters
+  int left = TEAMS;
+#pragma unroll
+  for (int t = 0; t < TEAMS; ++t) {
+    const int first = (int)blockIdx.x + t * (int)gridDim.x;
+    done[t] = first >= args.nwork;
+    if (done[t]) {
+      sm.team[t].sub[0].nbt = 0;
+      --left;
+    } else {
+      load_sub<BITS>(sm.team[t].sub[0], args, first);
     }
-    ++p.k;
-  };
-  auto reclaim = [&](TeamProd& p, TS& tm) {
-    while (p.reclaimed < p.issued) {
-      const int e = tm.sq[p.reclaimed & (kQ - 1)];
-      if (!mbar_test(&sm.empty[e & 0xFF], (uint32_t)(e >> 8))) break;
-      freemask |= 1u << (e & 0xFF);
-      ++p.reclaimed;
-    }
-  };
-  auto eligible = [&](const TeamProd& p, TS& tm) -> bool {
-    if (!p.hc || p.issued - p.reclaimed >= kQ) return false;
-    if (TEAMS == 1) return true;
-    const int ph = *reinterpret_cast<volatile int*>(&tm.started);
-    const int jp = (ph >> 1) & (kSubRing - 1);
-    const int end = (ph & 1) ? tm.vend[jp] : tm.kend[jp];
-    return p.issued < end + kTeamPrefetch;
-  };
-  auto step = [&](TeamProd& p, TS& tm) {
-    const int slot = __ffs(freemask) - 1;
-    freemask &= freemask - 1;
-    const uint32_t par = (parity >> slot) & 1u;
-    parity ^= 1u << slot;
-    if (leader) {
-      tm.sq[p.issued & (kQ - 1)] = slot | (int)(par << 8);
-      mbar_arrive(&tm.sqbar[p.issued & (kQ - 1)]);
-      issue_stage<BITS>(p.cur, p.ls, sm.ring[slot], &sm.full[slot]);
-    }
-    ++p.issued;
-    ++p.ls;
-    if (p.ls == min(3, p.cur.stages)) {
+    fk[t] = 1;
+    st_release(&sm.team[t].fetched, 1);
+  }
+  while (left > 0) {
+    bool idle = true;
+#pragma unroll
+    for (int t = 0; t < TEAMS; ++t) {
+      if (done[t] || fk[t] - ld_acquire(&sm.team[t].taken) >= kFetchAhead) continue;
+      idle = false;
       if (!waited) {
         asm volatile("griddepcontrol.wait;\n" ::: "memory");
         waited = true;
       }
-      // the team's next item: ticket, then its descriptor straight into the ring slot
-      int nx = 0;
-      if (leader) nx = atomicAdd(args.sched, 1);
-      nx = TEAMS * (int)gridDim.x + __shfl_sync(0xffffffffu, nx, __ffs(__ballot_sync(0xffffffffu, leader)) - 1);
-      p.hn = nx < args.nwork;
-      if (p.hn && leader) load_sub<BITS>(tm.sub[p.k & (kSubRing - 1)], args, nx);
-    }
-    if (p.ls == p.cur.stages) advance(p, tm);  // item fully issued: the next one becomes current
-  };
-
-#pragma unroll
-  for (int t = 0; t < TEAMS; ++t) {
-    const int first = (int)blockIdx.x + t * (int)gridDim.x;
-    P[t].k = P[t].issued = P[t].reclaimed = 0;
-    P[t].hn = first < args.nwork;
-    if (P[t].hn && leader) load_sub<BITS>(sm.team[t].sub[0], args, first);
-    advance(P[t], sm.team[t]);
-  }
-  for (;;) {
-    reclaim(P[0], sm.team[0]);
-    if constexpr (TEAMS > 1) reclaim(P[1], sm.team[1]);
-    bool any = P[0].hc;
-    if constexpr (TEAMS > 1) any |= P[1].hc;
-    if (!any) break;
-    if (!freemask) continue;
-    const bool e0 = eligible(P[0], sm.team[0]);
-    if constexpr (TEAMS > 1) {
-      const bool e1 = eligible(P[1], sm.team[1]);
-      if (e1 && (!e0 || P[1].issued - P[1].reclaimed < P[0].issued - P[0].reclaimed)) {
-        step(P[1], sm.team[1]);
-        continue;
+      const int nx = TEAMS * (int)gridDim.x + atomicAdd(args.sched, 1);
+      SubItem& dst = sm.team[t].sub[fk[t] & (kSubRing - 1)];
+      if (nx < args.nwork) {
+        load_sub<BITS>(dst, args, nx);
+      } else {
+        dst.nbt = 0;
+        done[t] = true;
+        --left;
       }
+      st_release(&sm.team[t].fetched, ++fk[t]);
     }
-    if (e0) step(P[0], sm.team[0]);
+    if (idle) __nanosleep(64);
   }
   // retire: the last CTA to finish drawing resets the counters for the next launch
   if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (leader) {
-    __threadfence();
-    if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
-      args.sched[0] = 0;
-      args.sched[1] = 0;
+  __threadfence();
+  if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
+    args.sched[0] = 0;
+    args.sched[1] = 0;
+  }
+}
+
+// ---- the producers: one warp per team, converged --------------------------------------------
+// Every lane holds the same (warp-uniform) state and one elected lane performs the stores,
+// arrivals and copies (a lone `lane == 0` loop makes the compiler wrap each bulk copy's
+// operands in a register-to-uniform broadcast loop).  Team t's producer claims slots from the
+// CTA's pool (shared-memory atomics on `freemask`), publishes each one in the team's stage
+// queue and issues the copies; it returns the slots its consumers released (test_wait on
+// `empty`, in stage order).  Its issue limit is the end of the phase its consumers have begun
+// + kTeamPrefetch (TEAMS = 1: none), so a team in its softmax or epilogue leaves the rest of
+// the pool to the other team.
+template <int BITS, int G, int NT, bool ASYM, int TEAMS>
+__device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args, int t) {
+  using TS = TeamSmem<G, NT, ASYM, kQOf<TEAMS>>;
+  static_assert((kQ & (kQ - 1)) == 0 && (kSubRing & (kSubRing - 1)) == 0, "power-of-two rings");
+  TS& tm = sm.team[t];
+  const bool leader = elect_lane();
+  const int leader_lane = __ffs(__ballot_sync(0xffffffffu, leader)) - 1;
+  TeamProd p;
+  p.k = p.issued = p.reclaimed = 0;
+  p.wpend = false;
+  bool waited = false;  // griddepcontrol.wait done: the prepare kernel's W images are readable
+
+  // the W image of item k (= p.k - 1, the current one) into the team's W buffer, once the
+  // consumers are past item k - 1's K phase (wfree); item 0's waits for the prepare kernel
+  auto issue_w = [&](bool block) {
+    const int k = p.k - 1;
+    if (k > 0) {
+      if (block) mbar_wait_spin(&tm.wfree, (uint32_t)((k - 1) & 1));
+      else if (!mbar_test(&tm.wfree, (uint32_t)((k - 1) & 1))) return;
+    }
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      waited = true;
+    }
+    if (leader) issue_wimg(tm, args, p.wseg, p.wr);
+    p.wpend = false;
+  };
+  // descriptor p.k (from the fetcher) becomes current and is published to the consumers
+  auto advance = [&]() {
+    const int ds = p.k & (kSubRing - 1);
+    while (ld_acquire(&tm.fetched) <= p.k) {
+    }
+    if (p.wpend) issue_w(true);  // the previous item's image is still due (a short item)
+    p.ls = 0;
+    p.hc = tm.sub[ds].nbt > 0;
+    if (p.hc) {
+      p.cur = issue_of(tm.sub[ds]);
+      p.wpend = true;
+      p.wseg = tm.sub[ds].seg;
+      p.wr = tm.sub[ds].r;
+    }
+    if (leader) {
+      if (p.hc) {
+        tm.kend[ds] = p.issued + p.cur.nK;
+        tm.vend[ds] = p.issued + p.cur.stages;
+      }
+      mbar_arrive(&tm.descfull[ds]);  // release: the descriptor is visible to its waiters
+      st_release(&tm.taken, p.k + 1);
+    }
+    ++p.k;
+    __syncwarp();
+  };
+  auto reclaim = [&]() {
+    uint32_t back = 0;
+    while (p.reclaimed < p.issued) {
+      const int e = tm.sq[p.reclaimed & (kQ - 1)];
+      if (!mbar_test(&sm.empty[e & 0xFF], (uint32_t)(e >> 8))) break;
+      back |= 1u << (e & 0xFF);
+      ++p.reclaimed;
+    }
+    if (back && leader) atomicOr(&sm.freemask, back);
+  };
+  advance();
+  if constexpr (TEAMS == 1) {  // a private FIFO ring: stage n in slot n % S, no queue needed
+    constexpr int S = AttnSmem<G, NT, ASYM, TEAMS>::kStages;
+    while (p.hc) {
+      const int slot = p.issued % S;
+      if (p.issued >= S) {
+        const uint32_t par = (uint32_t)((p.issued / S - 1) & 1);
+        while (!mbar_test(&sm.empty[slot], par))
+          if (p.wpend && p.k > 1) issue_w(false);  // while the ring is full
+      }
+      if (leader) issue_stage<BITS>(p.cur, p.ls, sm.ring[slot], &sm.full[slot]);
+      ++p.issued;
+      // item 0's image once the ring is primed (it waits for the prepare kernel); later ones as
+      // soon as the previous item's K phase is done
+      if (p.wpend && (p.k > 1 || p.issued >= S)) issue_w(false);
+      if (++p.ls == p.cur.stages) advance();
+    }
+    if (p.wpend) issue_w(true);
+    return;
+  }
+  for (;;) {
+    reclaim();
+    if (p.wpend && (p.k > 1 || p.issued >= 4)) issue_w(false);
+    if (!p.hc) {
+      if (p.reclaimed == p.issued) break;  // every slot of this team is back in the pool
+      continue;
+    }
+    int lim = 0x7fffffff;
+    if (TEAMS > 1) {
+      const int ph = *reinterpret_cast<volatile int*>(&tm.started);
+      const int jp = (ph >> 1) & (kSubRing - 1);
+      lim = ((ph & 1) ? tm.vend[jp] : tm.kend[jp]) + kTeamPrefetch;
+    }
+    while (p.hc && p.issued < lim && p.issued - p.reclaimed < kQ) {
+      int slot = -1, par = 0;
+      if (leader) {
+        unsigned m = *reinterpret_cast<volatile unsigned*>(&sm.freemask);
+        while (m) {
+          const int b = __ffs(m) - 1;
+          const unsigned old = atomicAnd(&sm.freemask, ~(1u << b));
+          if (old & (1u << b)) {
+            slot = b;
+            par = atomicAdd(&sm.slot_use[b], 1) & 1;
+            break;
+          }
+          m = old & ~(1u << b);
+        }
+        if (slot >= 0) {
+          tm.sq[p.issued & (kQ - 1)] = slot | (par << 8);
+          mbar_arrive(&tm.sqbar[p.issued & (kQ - 1)]);
+          issue_stage<BITS>(p.cur, p.ls, sm.ring[slot], &sm.full[slot]);
+        }
+      }
+      slot = __shfl_sync(0xffffffffu, slot, leader_lane);
+      if (slot < 0) break;
+      ++p.issued;
+      if (++p.ls == p.cur.stages) advance();  // item fully issued: the next one becomes current
     }
   }
 }
@@ -395,7 +509,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
   constexpr int S = AttnSmem<G, NT, ASYM, TEAMS>::kStages;
 
   const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int team = warp_all / kWarps;                 // == TEAMS for the producer warp
+  const int team = warp_all / kWarps;                 // == TEAMS for the producer / fetcher warps
   const int warp = warp_all - team * kWarps;          // warp within the team
   const int tid = (int)threadIdx.x - team * kThreads;  // thread within the team
   const int gid = lane >> 2, tid4 = lane & 3;
@@ -405,13 +519,18 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kWarps);
+      sm.slot_use[s] = 0;
     }
+    sm.freemask = S >= 32 ? ~0u : ((1u << S) - 1u);
     for (int t = 0; t < TEAMS; ++t) {
       for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.team[t].descfull[s], 1);
-      for (int s = 0; s < kQ; ++s) mbar_init(&sm.team[t].sqbar[s], 1);
+      for (int s = 0; s < kQOf<TEAMS>; ++s) mbar_init(&sm.team[t].sqbar[s], 1);
       mbar_init(&sm.team[t].wbar, 1);
+      mbar_init(&sm.team[t].wfree, 1);
       mbar_init(&sm.team[t].g0bar, 1);
       sm.team[t].started = 0;  // item 0's K phase: issue it whole before the consumers arrive
+      sm.team[t].fetched = 0;
+      sm.team[t].taken = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -422,25 +541,31 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
   __syncthreads();  // barrier inits visible to every warp
 
   if (team == TEAMS) {
-    // ---- producer: descriptors and code stages of this CTA's items ----------------------
-    // (the code does not depend on the prepare kernel, so no griddepcontrol.wait before
-    // the first stages)
-    produce<BITS, G, NT, ASYM, TEAMS>(sm, args);  // the whole warp, converged
+    // ---- producer: the code stages of this CTA's items (the code does not depend on the
+    // prepare kernel, so no griddepcontrol.wait before the first stages); the next warp
+    // fetches the work items
+    if (warp < TEAMS) produce<BITS, G, NT, ASYM, TEAMS>(sm, args, warp);  // the whole warp, converged
+    else if (lane == 0) fetch<BITS, G, NT, ASYM, TEAMS>(sm, args);
     return;
   }
-  TeamSmem<G, NT, ASYM>& tm = sm.team[team];
+  TeamSmem<G, NT, ASYM, kQOf<TEAMS>>& tm = sm.team[team];
 
   if (tid == 0) {
     mbar_wait(&tm.descfull[0], 0);
-    // programmatic dependent launch: everything above overlapped the prepare kernel; its
-    // output (the per-segment W images) is read from here on
+    if (tm.sub[0].nbt > 0) issue_g0v(tm, args, tm.sub[0]);
+    // programmatic dependent launch: the combine may be scheduled once every CTA is here (the
+    // producer waits for the prepare kernel before its first W-image copy)
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
-    if (tm.sub[0].nbt > 0) issue_wimg<G, NT, ASYM>(tm, args, tm.sub[0]);
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   }
 
   int st = 0;  // the team's running stage index (identical in every thread of the team)
   auto acquire = [&]() -> int {  // slot of stage st, once its codes have landed
+    if constexpr (TEAMS == 1) {
+      const int slot = st % S;
+      mbar_wait(&sm.full[slot], (uint32_t)((st / S) & 1));
+      return slot;
+    }
     mbar_wait(&tm.sqbar[st % kQ], (uint32_t)((st / kQ) & 1));
     const int e = tm.sq[st % kQ];
     mbar_wait(&sm.full[e & 0xFF], (uint32_t)(e >> 8));
@@ -462,6 +587,19 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     const int nbt = d.nbt;
     begin_phase(2 * j);
     mbar_wait(&tm.wbar, (uint32_t)(j & 1));
+#ifdef DQ_ATTN_TRACE  // measurement builds: per-item phase stamps [nwork][8] (global ns)
+    auto stamp = [&](int k) {
+      if (args.trace && tid == 0) args.trace[(size_t)d.item * 8 + k] = global_ns();
+    };
+    if (args.trace && tid == 0) {
+      args.trace[(size_t)d.item * 8 + 5] = blockIdx.x;
+      args.trace[(size_t)d.item * 8 + 6] = sm_id();
+      args.trace[(size_t)d.item * 8 + 7] = team;
+    }
+#else
+    auto stamp = [](int) {};
+#endif
+    stamp(0);
 
     // ---- phase 1: S = W . codes_k on the int8 tensor pipe ------------------------------
     constexpr int kWpt = kWarps / NT;       // warps per 64-row tile
@@ -511,7 +649,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       row_off[mt][0] = (tid4 * kI2Pad + (b0 ^ swz)) * RB;
       row_off[mt][1] = (tid4 * kI2Pad + ((b0 + 8) ^ swz)) * RB;
     }
-    const uint4* wthr = tm.wg.w + tid4 * 8 + (gid ^ (2 * tid4));
+    const uint4* wthr = tm.w + tid4 * 8 + (gid ^ (2 * tid4));
     const int wl = r * 8;  // chunks per (head, limb)
     for (int ks = 0; ks < d.nK; ++ks, ++st) {
       const int slot = acquire();
@@ -550,14 +688,17 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       release(slot);
     }
     if (r > kGroupR) flush_group(1);
+    stamp(1);
 #ifdef DQ_ATTN_NULL_STREAM  // measurement only: the producer / ring / scheduler alone
     begin_phase(2 * j + 1);
     for (int vs = 0; vs < nbt * d.nslices; ++vs, ++st) release(acquire());
     team_sync(team);
     if (tid == 0) {
+      mbar_arrive(&tm.wfree);
+      mbar_wait(&tm.g0bar, (uint32_t)(j & 1));
       const int jn = j + 1;
       mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(tm, args, tm.sub[jn % kSubRing]);
+      if (tm.sub[jn % kSubRing].nbt > 0) issue_g0v(tm, args, tm.sub[jn % kSubRing]);
     }
     continue;
 #endif
@@ -582,21 +723,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       if (lane == 0) tm.rowmax[h][warp] = m;
     }
     team_sync(team);  // every warp is past phase 1: the W buffer is dead
-    if (lane == 0 && warp < i1) {  // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
-      // one copy per a, issued by warp a, into blocks of 2r + 1 float4s: the epilogue's lanes
-      // tid4 = 0..3 read a = 2 tid4 + aa, and the pad puts their blocks 32 bytes apart in the
-      // banks (an unpadded 2r-float4 stride maps all four onto the same banks: a 4-way
-      // conflict per load, 10 us of a C2 layer).  A copy completing before warp 0's expect_tx
-      // only takes the transaction count negative; the phase needs that arrival.
-      const uint32_t cb = ASYM ? (uint32_t)(2 * r * 16 * 4) : 0u;
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      if (warp == 0) {
-        mbar_expect_tx(&tm.g0bar, (uint32_t)(i1 * r * 32) + cb);
-        if (ASYM) bulk_g2s(tm.vch, args.segs[d.seg].v_ch, cb, &tm.g0bar);
-      }
-      bulk_g2s(tm.wg.g0v + warp * (2 * r + 1), reinterpret_cast<const float4*>(d.vg0) + warp * 2 * r,
-               (uint32_t)(r * 32), &tm.g0bar);
-    }
+    if (tid == 0) mbar_arrive(&tm.wfree);  // the producer may load the next item's W image
     unsigned char* pb = reinterpret_cast<unsigned char*>(tm.pr.p);
     // P = exp2(s - m) in fixed point with one scale per (h, a, 64-row tile), set by that
     // tile's largest probability: small probabilities far from the peak keep their
@@ -667,6 +794,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     }
     team_sync(team);  // P limbs, gamma and lsum complete
     begin_phase(2 * j + 1);
+    stamp(2);
 
     // ---- phase 3: Y = codes_v . P^T on the int8 tensor pipe ----------------------------
     // warp w owns bond rows w*rw .. w*rw+rw-1 (an m-tile = one bond row x 16 e)
@@ -740,6 +868,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       if (++sl == d.nslices) sl = 0, ++btl;
     }
 
+    stamp(3);
     // ---- phase 4: O = scale_v * G0v . Y on CUDA cores, reduce, write the partial -------
     // accv[t][h]: rows e = gid (k 0,1) / gid+8 (k 2,3); cols a = 2*tid4 + (k & 1)
     float part[G][16];  // [h][c*2 + (e == gid+8)]
@@ -747,8 +876,8 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     for (int h = 0; h < G; ++h)
 #pragma unroll
       for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
-    mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // fp32 G0v [a][rr][c] (normalised), in the W buffer
-    const float4* g0v = tm.wg.g0v;
+    mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // fp16 G0v [a][rr][c] (normalised), loaded at the last item's end
+    const uint4* g0v = tm.g0v;
 #ifdef DQ_ATTN_NULL_FOLD  // measurement only: no G0v fold (wrong results), Y still consumed
 #pragma unroll
     for (int t = 0; t < kRw; ++t)
@@ -768,8 +897,12 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
         for (int aa = 0; aa < 2; ++aa) {
           const int a = 2 * tid4 + aa;
           if (a < i1) {
-            const float4 g_lo = g0v[a * (2 * r + 1) + 2 * rr], g_hi = g0v[a * (2 * r + 1) + 2 * rr + 1];
-            const float gc[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
+            const uint4 gh = g0v[a * (r + 1) + rr];
+            const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gh.x));
+            const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&gh.y));
+            const float2 g45 = __half22float2(*reinterpret_cast<const __half2*>(&gh.z));
+            const float2 g67 = __half22float2(*reinterpret_cast<const __half2*>(&gh.w));
+            const float gc[8] = {g01.x, g01.y, g23.x, g23.y, g45.x, g45.y, g67.x, g67.y};
 #pragma unroll
             for (int h = 0; h < G; ++h) {
               const float y0 = ASYM ? accv[t][h][aa] * s0 : accv[t][h][aa];
@@ -790,11 +923,11 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
         v += __shfl_xor_sync(0xffffffffu, v, 2);
         part[h][k] = v;
       }
-    team_sync(team);  // every warp is past the V stages and G0v: P and W/G0v buffers are free
-    if (tid == 0) {
+    team_sync(team);  // every warp is past the V stages and G0v: P and the G0v buffer are free
+    if (tid == 0) {  // the next item's G0v (its descriptor is out: this item was fully issued)
       const int jn = j + 1;
       mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg<G, NT, ASYM>(tm, args, tm.sub[jn % kSubRing]);
+      if (tm.sub[jn % kSubRing].nbt > 0) issue_g0v(tm, args, tm.sub[jn % kSubRing]);
     }
     if (tid < G * 8 * NT) {
       (&tm.gamma[0][0][0])[tid] = 0;
@@ -830,6 +963,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       args.part_ml[((size_t)d.part * G + tid) * 2 + 0] = mh[tid];  // log2 domain
       args.part_ml[((size_t)d.part * G + tid) * 2 + 1] = l;
     }
+    stamp(4);
   }
 }
 

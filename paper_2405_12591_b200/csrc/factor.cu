@@ -447,6 +447,9 @@ __global__ void __launch_bounds__(kEigThreads) eig_tql_kernel(const double* __re
     sm.e[0] = 0.0;
   }
   __syncthreads();
+#if defined(DQ_EIG_STOP) && DQ_EIG_STOP == 1  // measurement only: the reduction alone
+  return;
+#endif
   // accumulate the transformations: a <- Q
   for (int i = 0; i < n; ++i) {
     const int l = i - 1;
@@ -466,6 +469,9 @@ __global__ void __launch_bounds__(kEigThreads) eig_tql_kernel(const double* __re
     __syncthreads();
   }
 
+#if defined(DQ_EIG_STOP) && DQ_EIG_STOP == 2  // measurement only: reduction + accumulation
+  return;
+#endif
   // ---- implicit QL on (d, e) (tqli), eigenvectors in the rows of a --------------------
   if (t == 0) {
     for (int i = 1; i < n; ++i) sm.e[i - 1] = sm.e[i];
@@ -544,6 +550,9 @@ __global__ void __launch_bounds__(kEigThreads) eig_tql_kernel(const double* __re
     if (failed) break;
   }
   if (failed && t == 0 && flags) atomicOr(flags, (int)DQ_FLAG_JACOBI_NOCONV);
+#ifdef DQ_EIG_STATS  // measurement only: QL chases of the first blocks
+  if (t == 0 && blk < 4) printf("eig block %d: n %d\n", (int)blk, n);
+#endif
 
   // sort eigenvalues descending (ties by index), orient each vector (as jacobi_kernel)
   if (t < n) {  // a NaN (non-finite input, already flagged) sorts last: perm stays a permutation
@@ -961,6 +970,68 @@ __global__ void __launch_bounds__(kThreads) project128_kernel(const void* __rest
   if ((threadIdx.x & 31) == 0) atomicMax(&amax[blk], __float_as_uint(local_max));
 }
 
+// ---- quantize + pack into the attention layouts, j2 = 16 (every 128-wide KV block) ----------
+// One thread per 16-code run of the destination: KTILE rows (bt, rr, swizzled b) hold 16 e,
+// VTILE runs (bt, rr, e) hold 16 consecutive b.  The coordinates come from one 32-bit
+// division per run instead of three 64-bit ones per code (quantize_core_kernel, any layout).
+template <int BITS, bool VT>
+__global__ void __launch_bounds__(kThreads) quantize_tile16_kernel(const float* __restrict__ core1, int64_t core_elems,
+                                                                   CoreGeom geom, const unsigned* __restrict__ amax,
+                                                                   uint8_t* __restrict__ payload,
+                                                                   int64_t payload_stride, float* __restrict__ scale,
+                                                                   int32_t* flags) {
+  constexpr int kQmax = (1 << (BITS - 1)) - 1, kX = 1 << (BITS - 1), kMask = (1 << BITS) - 1;
+  const int64_t blk = blockIdx.y;
+  const float amax_f = __uint_as_float(amax[blk]);
+  if (!isfinite(amax_f) && blockIdx.x == 0 && threadIdx.x == 0 && flags) atomicOr(flags, (int)DQ_FLAG_NONFINITE);
+  const double am = (double)amax_f;
+  bool degenerate;
+  const float sc = rtn_scale(am, kQmax, &degenerate);
+  if (blockIdx.x == 0 && threadIdx.x == 0) scale[blk] = sc;
+  const double rinv = am > 0.0 ? 1.0 / am : 0.0;
+  const float* src = core1 + blk * core_elems;
+  uint8_t* dst = payload + blk * payload_stride;
+  const int r = geom.r, i2 = geom.i2;
+  const int runs = r * (geom.i2p / kI2Pad) * (VT ? 16 * 4 : kI2Pad);  // 16-code runs per core
+  for (int run = blockIdx.x * kThreads + threadIdx.x; run < runs; run += gridDim.x * kThreads) {
+    float v[16];
+    int b0, bstep, e0, estep, rr;
+    if constexpr (VT) {  // run = ((bt * r + rr) * 16 + e) * 4 + quarter: 16 consecutive b at one e
+      const int q = run & 3, e = (run >> 2) & 15, btr = run >> 6;
+      rr = btr % r;
+      b0 = (btr / r) * kI2Pad + q * 16;
+      bstep = 1;
+      e0 = e;
+      estep = 0;
+    } else {  // run = (bt * r + rr) * 64 + swizzled row: 16 e of one b
+      const int bsw = run & 63, btr = run >> 6;
+      rr = btr % r;
+      b0 = (btr / r) * kI2Pad + (bsw ^ ktile_swizzle(rr, BITS));
+      bstep = 0;
+      e0 = 0;
+      estep = 1;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int b = b0 + k * bstep, e = e0 + k * estep;
+      v[k] = b < i2 ? src[((int64_t)rr * i2 + b) * 16 + e] : 0.f;
+    }
+    uint32_t w[BITS];  // 16 codes x BITS bits, low code first
+#pragma unroll
+    for (int i = 0; i < BITS; ++i) w[i] = 0u;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int code = (degenerate || b0 + k * bstep >= i2) ? 0 : rtn_code_fast(v[k], kQmax, am, rinv);
+      const uint32_t u = (uint32_t)((code + kX) & kMask);  // excess code (DQ_LAYOUT_KTILE / VTILE)
+      w[(k * BITS) / 32] |= u << ((k * BITS) % 32);
+    }
+    uint8_t* out = dst + (int64_t)run * 2 * BITS;  // 16 codes = 2 BITS bytes, runs in slot order
+    if constexpr (BITS == 8) *reinterpret_cast<uint4*>(out) = make_uint4(w[0], w[1], w[2], w[3]);
+    else if constexpr (BITS == 4) *reinterpret_cast<uint2*>(out) = make_uint2(w[0], w[1]);
+    else *reinterpret_cast<uint32_t*>(out) = w[0];
+  }
+}
+
 // ---- opt-in per-channel asymmetric quantisation (dq_deco_quantize_asym_batched) ----------
 // channel (rr, e) of core1 [r][i2][j2] over b: scale, zero point (fp64 arithmetic, f32 scale)
 __global__ void asym_channels_kernel(const float* __restrict__ core1, int64_t core_elems, int r, int i2, int j2,
@@ -1186,6 +1257,22 @@ extern "C" int dq_deco_quantize_batched(const void* blocks, int32_t dtype, int64
   st = factor_core(blocks, d, nblk, core0, w.core1, w, flags, s);
   if (st) return st;
   CoreGeom g = make_geom(p, bits, layout);
+  if (layout != DQ_LAYOUT_REF && g.j2 == 16) {
+    const int64_t runs = (int64_t)g.r * (g.i2p / kI2Pad) * 64;
+    int64_t gx = ceil_div(runs, kThreads);
+    if (gx > 256) gx = 256;
+    const dim3 grid((unsigned)gx, (unsigned)nblk);
+    const int64_t ce = (int64_t)d.r * d.n;
+#define DQ_QT16(B, V) \
+  quantize_tile16_kernel<B, V><<<grid, kThreads, 0, s>>>(w.core1, ce, g, w.amax, payload, payload_stride, scale, flags)
+    const bool vt = layout == DQ_LAYOUT_VTILE;
+    if (bits == 2) { if (vt) DQ_QT16(2, true); else DQ_QT16(2, false); }
+    else if (bits == 4) { if (vt) DQ_QT16(4, true); else DQ_QT16(4, false); }
+    else { if (vt) DQ_QT16(8, true); else DQ_QT16(8, false); }
+#undef DQ_QT16
+    DQ_LAUNCH_CHECK();
+    return DQ_OK;
+  }
   int64_t gx = ceil_div(out_bytes, kThreads);
   if (gx > 64) gx = 64;
   quantize_core_kernel<<<dim3((unsigned)gx, (unsigned)nblk), kThreads, 0, s>>>(

@@ -82,6 +82,7 @@ class DecodeStepGraph:
 
     def recapture(self):
         """(Re)build the graph: one eager step (it is a real decode step), then the capture."""
+        self.cache._flush_seals()  # full tails of an eager sealing step are compressed first
         if self._sealing_ahead():
             raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
         self._body()  # eager step: builds every layer's segment table outside the capture

@@ -155,6 +155,7 @@ class DecoQuantLM:
         """Run one eager decode step on `tokens` (zeros by default) and record the step as a CUDA
         graph (replay() runs it; the cache's host-side token counters advance per replay).
         Returns the eager step's next tokens.  Refused when a tail chunk would seal inside."""
+        self.cache._flush_seals()
         if any(lay.tail_len + 2 >= self.cache.chunk_len for lay in self.cache._layers):
             raise ShapeMismatch("a tail chunk seals within the next steps: decode them eagerly first")
         self._tok = torch.zeros(self.batch, dtype=torch.int64, device=self.dev)

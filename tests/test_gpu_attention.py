@@ -569,10 +569,40 @@ def test_step_graph_refuses_stale_plan(dq):
         st.replay()  # this token seals
     for layer in range(L):  # the sealing step, eagerly
         cache.attend(layer, q_h[layer].cuda(), append=(k_h[layer].cuda(), v_h[layer].cuda()))
-    assert cache._layers[0].tail_len == 0
+    assert all(lay.seal_pending for lay in cache._layers)  # full tails wait for one batched K3 call
+    cache.check_errors()
+    assert cache._layers[0].tail_len == 0 and len(cache._layers[1].groups) == 2
     with pytest.raises(ShapeMismatch):
         st.replay()  # stale: layer 0 was re-planned
     st.recapture()
     st.replay()
     torch.cuda.synchronize()
     assert cache.tokens(0) == 520 + chunk + 2
+
+
+def test_seal_error_is_deferred_not_lost(dq):
+    """A non-finite row in a chunk that seals while decoding: no host sync at the seal; the
+    error (NonFiniteSvdInput, as the reference's LinAlgError) surfaces at check_errors() and at
+    the first later call once the device flags are on the host."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+    from paper_2405_12591_b200.errors import NonFiniteInput
+
+    units, chunk = 2, 32
+    cache = DecodeKvCache(layers=1, units=units, g=1, bits=4, chunk_len=chunk)
+    cache.prefill(0, torch.randn((units, 256, 128), device="cuda").half(),
+                  torch.randn((units, 256, 128), device="cuda").half())
+    rows = torch.randn((chunk, units, 128), device="cuda").half()
+    rows[5, 1, 7] = float("nan")
+    for t in range(chunk):
+        cache.append_token(0, rows[t], rows[t])
+    assert cache._layers[0].seal_pending  # full tail: sealed at the layer's next use
+    with pytest.raises(NonFiniteInput):
+        cache.check_errors()
+    assert not cache._pending and len(cache._layers[0].groups) == 2
+    cache2 = DecodeKvCache(layers=1, units=units, g=1, bits=4, chunk_len=chunk)
+    for t in range(chunk + 1):  # the last append seals the full tail first (no sync, no raise)
+        cache2.append_token(0, rows[t % chunk], rows[t % chunk])
+    assert len(cache2._layers[0].groups) == 1 and cache2._layers[0].tail_len == 1
+    torch.cuda.synchronize()
+    with pytest.raises(NonFiniteInput):
+        cache2.append_token(0, rows[0], rows[0])
