@@ -49,6 +49,10 @@ CONFIGS = {
                model="llama2-13b-shape", layers=40, kv_heads=40, g=1, batch=32, T=8192, bits=2, scaling="weak"),
     "c4": dict(workload="llama2-7b-shape long-context decode attention, batch 1, 32K context, int4",
                model="llama2-7b-shape", layers=32, kv_heads=32, g=1, batch=1, T=32768, bits=4, scaling="strong"),
+    # configs[0]: the write / reconstruct path alone (run_c1): 32 heads x 2048 tokens x 128, int4, n = 2
+    "c1": dict(workload="synthetic KV tensor 32 heads x 2048 tokens x 128, 2-factor MPO, int4: decompose / "
+                        "quantize / reconstruct", model="kv-tensor", layers=1, kv_heads=32, g=1, batch=1, T=2048,
+               bits=4, scaling="weak"),
     "c5": dict(workload="llama2-70b-shape GQA decode attention, batch 64, 16K context, int4",
                model="llama2-70b-shape", layers=80, kv_heads=8, g=8, batch=64, T=16384, bits=4, scaling="strong"),
 }
@@ -430,6 +434,110 @@ def config_keys(args, cfg, world, global_batch):
             "l2": f"inputs > L2: {kv_gb:.2f} GB of compressed KV streamed per step per GPU (126 MB L2)"}
 
 
+def _c1_cpu_worker(seed):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+
+    from oracle import dquant_oracle as O
+
+    rng = np.random.default_rng(seed)
+    m = rng.standard_normal((2048, 128)).astype(np.float16).astype(np.float32)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < 3.0:
+        O.encode(m, 4)
+        n += 1
+    return n, time.perf_counter() - t0
+
+
+def run_c1(args, cfg):
+    """BASELINE.json configs[0]: K3 (decompose + quantize) and K4 (reconstruct) on the 32-head
+    2048 x 128 tensor, int4: per-block time, fp64 rate against the measured FP64 peak, parity
+    against the CPU oracle (the reference's algorithm) and the oracle's own rate on host cores."""
+    import numpy as np
+    import torch
+
+    from oracle import dquant_oracle as O
+    from paper_2405_12591_b200 import _lib
+    from paper_2405_12591_b200.compress import deco_quantize_batched
+    from paper_2405_12591_b200.csrc_info import FP64_PEAK_TFLOPS
+
+    torch.cuda.set_device(0)
+    heads, T = cfg["kv_heads"], cfg["T"]
+    rng = np.random.default_rng(0)
+    k = rng.standard_normal((heads, T, 128)).astype(np.float16)
+    kd = torch.from_numpy(k).cuda()
+
+    def k3(x):
+        r = deco_quantize_batched(x, 4)
+        return r
+
+    def k4(r, nblk):
+        out = torch.empty((nblk, T, 128), dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().dq_deco_dequantize_batched(
+            r["core0"].data_ptr(), r["payload"].data_ptr(), r["payload"].shape[1], _lib.LAYOUT_REF,
+            r["scale"].data_ptr(), nblk, T, 128, 4, out.data_ptr(), _lib.DQ_F32, _lib.stream_ptr()), "k4")
+        return out
+
+    def timed(fn, reps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    # the 32-head tensor (one call), and a throughput batch of 1024 blocks
+    res = k3(kd)
+    _lib.raise_flags(res["flags"], "c1")
+    ms32 = timed(lambda: k3(kd), args.steps)
+    big = kd.repeat(32, 1, 1)
+    ms1024 = timed(lambda: k3(big), max(3, args.steps // 4))
+    rec_ms = timed(lambda: k4(res, heads), args.steps)
+    rec_big = deco_quantize_batched(big, 4)
+    rec_ms_big = timed(lambda: k4(rec_big, big.shape[0]), max(3, args.steps // 4))
+    # parity: payload bytes (after sign alignment there is nothing to align for the codes' bytes
+    # when the factor signs match) and reconstruction vs the oracle
+    rec = k4(res, heads).cpu().numpy()
+    errs = []
+    for h in range(heads):
+        e = O.encode(k[h].astype(np.float32), 4)
+        ref = O.decode(e)
+        errs.append(float(np.linalg.norm(rec[h] - ref) / np.linalg.norm(ref)))
+    m, n = 64, 2 * T
+    fp64_flop = 2 * m * m * n + 2 * m * m * n  # Gram (full 64 x 64 tiles) + projection
+    tflops = big.shape[0] * fp64_flop / (ms1024 / 1e3) / 1e12
+    in_bytes, out_bytes = T * 128 * 2, T * 128 * 4
+    line = {
+        "metric": "C1 write path: deco_quantize blocks/s (2048 x 128, int4, n = 2)",
+        "value": big.shape[0] / (ms1024 / 1e3), "unit": "blocks/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms32, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) rounded to fp16",
+        "config": {"workload": cfg["workload"], "heads": heads, "T": T, "bits": 4, "n": 2},
+        "k3": {"us_per_block_32": ms32 * 1e3 / heads, "us_per_block_1024": ms1024 * 1e3 / big.shape[0],
+               "fp64_tflops": tflops, "fp64_peak_tflops": FP64_PEAK_TFLOPS, "fp64_frac": tflops / FP64_PEAK_TFLOPS,
+               "fp64_flop_per_block": fp64_flop},
+        "k4": {"us_per_block_32": rec_ms * 1e3 / heads, "gbs_1024": big.shape[0] * (in_bytes // 4 + out_bytes)
+               / (rec_ms_big / 1e3) / 1e9, "us_per_block_1024": rec_ms_big * 1e3 / big.shape[0]},
+        "parity": {"reconstruction_rel_frob_max": max(errs), "tolerance": 1e-3},
+    }
+    if not args.no_cpu_baseline:
+        import multiprocessing as mp
+
+        cores = os.cpu_count() or 1
+        with mp.get_context("spawn").Pool(cores) as pool:
+            outs = pool.map(_c1_cpu_worker, range(cores))
+        rate = sum(n / dt for n, dt in outs)
+        line["cpu_baseline"] = {"value": rate, "unit": "blocks/s", "cores": cores, "kind": "port",
+                                "sample": f"oracle encode (2048 x 128, int4) for 3 s on each of {cores} "
+                                          "single-thread workers", "cpu": cpu_model_name()}
+    print(json.dumps(line), flush=True)
+
+
 def run_plumbing(args, cfg):
     """--plumbing: the launcher / rank / shard / timing path of run_ours without kernels (gloo on
     CPU in tests/test_bench_ranks.py; the same Ranks and shard() the GPU run uses)."""
@@ -643,6 +751,12 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.plumbing:
         run_plumbing(args, cfg)
+        return
+    if args.config == "c1":
+        if rank == 0 and args.impl != "reference":
+            run_c1(args, cfg)
+        elif rank == 0:
+            print(json.dumps({"impl": "reference", "unavailable": "c1 reports its CPU arm as cpu_baseline"}))
         return
     if args.impl == "reference":
         if rank == 0:

@@ -172,8 +172,7 @@ typedef struct dq_segment {
   const uint8_t* k_codes; /* DQ_LAYOUT_KTILE */
   const uint8_t* v_codes; /* DQ_LAYOUT_VTILE */
   const float* k_g0;      /* fp32 [i1][r][8]  (dq_core0_relayout, normalised): score side */
-  const void* v_g0;       /* [i1][r][8] normalised (dq_core0_relayout): output side; fp16 for the mma.sync
-                             split kernel (path 0), fp32 for the tcgen05 paths 1 and 2 */
+  const float* v_g0;      /* fp32 [i1][r][8]  (dq_core0_relayout, normalised): output side */
   float k_scale, v_scale; /* quantizer scale times the G0 normalisation factor */
   int32_t T;          /* tokens in the segment */
   int32_t i1, i2, r;  /* plan of (T,128) */

@@ -72,7 +72,6 @@ class SegmentGroup:
     token0: int
     k_ch: torch.Tensor | None = None  # asymmetric mode: (units, 2, r, 16) f32 channel scales, zero points
     v_ch: torch.Tensor | None = None
-    v_g0f16: torch.Tensor | None = None  # fp16 copy of v_g0h for the mma.sync split kernel (path 0)
 
     def reference_bytes(self, bits: int) -> int:
         """compression_report().bytes_compressed of one unit's K (or V) block (compress.py:234-248);
@@ -83,13 +82,11 @@ class SegmentGroup:
         return payload_size(p.r * p.i2 * p.j2, bits) + scales + 2 * (p.i1 * p.j1 * p.r)
 
     def stream_bytes(self) -> int:
-        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k (prepare
-        kernel), G0v (fp16 on the mma.sync path, fp32 on the tcgen05 paths), scales (the channel
-        tables in the asymmetric mode)."""
+        """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k and G0v, scales
+        (the channel tables in the asymmetric mode)."""
         ch = 2 * self.k_ch[0].numel() * 4 if self.k_ch is not None else 0
-        vg = self.v_g0f16 if self.v_g0f16 is not None else self.v_g0h
         return (self.k_payload.shape[1] + self.v_payload.shape[1] + self.k_g0h.element_size() * self.k_g0h.shape[1]
-                + vg.element_size() * vg.shape[1] + 8 + ch)
+                + self.v_g0h.element_size() * self.v_g0h.shape[1] + 8 + ch)
 
 
 class _Layer:
@@ -472,10 +469,7 @@ class DecodeKvCache:
                 raise Unsupported("the tcgen05 path needs 4-bit codes, one head (or 8) per kernel and i1 = 8, "
                                   "r = 64 plans")
             path = 1 if (eligible and self.tc) else 0
-        if path == 0:  # the mma.sync kernel folds an fp16 copy of G0v (made once per group)
-            for grp in lay.groups:
-                if grp.v_g0f16 is None:
-                    grp.v_g0f16 = grp.v_g0h.to(torch.float16)
+
         # the segment table, built column-wise (numpy view of the dq_segment records): one record
         # per (group, unit, head group); the scales are filled in on the device below (no sync)
         nseg = len(lay.groups) * vunits
@@ -488,8 +482,7 @@ class DecodeKvCache:
             r["k_codes"] = grp.k_payload.data_ptr() + u_of * grp.k_payload.shape[1]
             r["v_codes"] = grp.v_payload.data_ptr() + u_of * grp.v_payload.shape[1]
             r["k_g0"] = grp.k_g0h.data_ptr() + u_of * grp.k_g0h.shape[1] * grp.k_g0h.element_size()
-            vg = grp.v_g0f16 if path == 0 else grp.v_g0h
-            r["v_g0"] = vg.data_ptr() + u_of * vg.shape[1] * vg.element_size()
+            r["v_g0"] = grp.v_g0h.data_ptr() + u_of * grp.v_g0h.shape[1] * grp.v_g0h.element_size()
             r["T"], r["i1"], r["i2"], r["r"], r["i2p"] = grp.T, p.i1, p.i2, p.r, grp.i2p
             r["unit"] = np.arange(vunits, dtype=np.int32)
             r["token0"] = grp.token0

@@ -73,7 +73,7 @@ constexpr int kPBits = 15;  // P / tile max in (0.5, 1] -> round(P * 2^(kPBits -
 struct SubItem {
   const unsigned char* kc;
   const unsigned char* vc;
-  const void* vg0;  // fp16 G0v [a][rr][8 c] (the path-0 copy, attention.py)
+  const float* vg0;  // fp32 G0v [a][rr][8 c] (normalised)
   float kscale, vscale;
   int seg, wb0, nbt, part;
   int r, i1, i2, item;
@@ -84,8 +84,7 @@ struct SubItem {
 // per-team state: descriptors, stage queue, W image / G0v, P, reductions
 template <int G, int NT, bool ASYM, int QN = kQ>
 struct TeamSmem {
-  uint64_t wbar;   // W image (attn_prepare.cuh) by TMA (issued by the producer), one phase per sub-item
-  uint64_t wfree;  // the consumers are past an item's K phase: its W buffer may be refilled
+  uint64_t wbar;   // W image (attn_prepare.cuh) by TMA, one phase per sub-item
   uint64_t g0bar;  // G0v prefetch, one phase per sub-item
   uint64_t descfull[kSubRing];  // descriptor j written (producer arrival), phase j / kSubRing
   uint64_t sqbar[QN];           // stage n's slot published (producer arrival), phase n / kQ (TEAMS = 2)
@@ -100,12 +99,14 @@ struct TeamSmem {
   int gamma[G][8][NT];     // excess correction of Y per 64-row tile: kExcess * sum_b Pint[a][b]
   float lsum[G][kWarps];   // probability mass per warp
   unsigned pmax[G][8][NT];  // largest probability per (h, a, tile), float bits
-  // K phase: W limbs, 16-byte chunks [((h*2 + limb)*r + rr)*8 + (a ^ 2*(rr&3))] (the next
-  // item's image lands here as soon as this item's K phase is done)
-  uint4 w[G * 2 * kMaxR * 8];
-  // epilogue: fp16 G0v [a][rr][8 c] (normalised), r + 1 chunks per a (a 16-byte pad: the lanes
-  // tid4 = 0..3 read a = 2 tid4 + aa four banks apart); loaded at the previous item's end
-  uint4 g0v[8 * (kMaxR + 1)];
+  // K phase: W limbs, 16-byte chunks [((h*2 + limb)*r + rr)*8 + (a ^ 2*(rr&3))];
+  // V phase + epilogue (aliased, W is dead): fp32 G0v [a][rr][c] by TMA.  (Measured: separate
+  // W and fp16 G0v buffers, the next W image loaded by the producer right after the K phase,
+  // shorten the gap between items but lengthen the epilogue: C2 66 us against 62 us.)
+  union {
+    uint4 w[G * 2 * kMaxR * 8];
+    float4 g0v[8 * (kMaxR * 2 + 1)];  // [a][rr][c] with a 16-byte pad per a (kG0vPad)
+  } wg;
   // V phase: P limbs [((h*2 + limb)*8 + a)*(4 NT) + (bg ^ 4*(a&1))];
   // epilogue (aliased, P is dead): cross-warp reduction of the O partial
   union {
@@ -183,24 +184,15 @@ __device__ __forceinline__ void load_sub(SubItem& d, const dq_attn_args& a, int 
   d = t;
 }
 
-// the W image (limb chunks + metadata) of a segment onto the team's wbar (one thread)
+// the W image (limb chunks + metadata) of a sub-item's segment onto the team's wbar (one thread)
 template <int G, int NT, bool ASYM, int QN>
-__device__ __forceinline__ void issue_wimg(TeamSmem<G, NT, ASYM, QN>& tm, const dq_attn_args& a, int seg, int r) {
-  const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)seg * a.wimg_stride;
-  const uint32_t wb = (uint32_t)(G * 2 * r * 8 * 16);
+__device__ __forceinline__ void issue_wimg(TeamSmem<G, NT, ASYM, QN>& tm, const dq_attn_args& a, const SubItem& d) {
+  const unsigned char* img = static_cast<const unsigned char*>(a.wimg) + (size_t)d.seg * a.wimg_stride;
+  const uint32_t wb = (uint32_t)(G * 2 * d.r * 8 * 16);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   mbar_expect_tx(&tm.wbar, wb + (uint32_t)sizeof(WMeta<G>));
-  bulk_g2s(tm.w, img, wb, &tm.wbar);
+  bulk_g2s(tm.wg.w, img, wb, &tm.wbar);
   bulk_g2s(&tm.wmeta, img + kWChunkBytes<G>, (uint32_t)sizeof(WMeta<G>), &tm.wbar);
-}
-
-// fp16 G0v (one copy per a into its padded block) and, asymmetric, the V channel table (one thread)
-template <int G, int NT, bool ASYM, int QN>
-__device__ __forceinline__ void issue_g0v(TeamSmem<G, NT, ASYM, QN>& tm, const dq_attn_args& a, const SubItem& d) {
-  const uint32_t cb = ASYM ? (uint32_t)(2 * d.r * 16 * 4) : 0u;
-  mbar_expect_tx(&tm.g0bar, (uint32_t)(d.i1 * d.r * 16) + cb);
-  if (ASYM) bulk_g2s(tm.vch, a.segs[d.seg].v_ch, cb, &tm.g0bar);
-  const uint4* src = reinterpret_cast<const uint4*>(d.vg0);
-  for (int aa = 0; aa < d.i1; ++aa) bulk_g2s(tm.g0v + aa * (d.r + 1), src + aa * d.r, (uint32_t)(d.r * 16), &tm.g0bar);
 }
 
 template <int NT>
@@ -285,8 +277,6 @@ struct TeamProd {
   int k;         // descriptors taken
   int issued, reclaimed;
   bool hc;       // streaming an item
-  bool wpend;    // the current item's W image is not issued yet
-  int wseg, wr;  // its segment and bond dimension
 };
 
 __device__ __forceinline__ bool elect_lane() {
@@ -385,38 +375,14 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
   const int leader_lane = __ffs(__ballot_sync(0xffffffffu, leader)) - 1;
   TeamProd p;
   p.k = p.issued = p.reclaimed = 0;
-  p.wpend = false;
-  bool waited = false;  // griddepcontrol.wait done: the prepare kernel's W images are readable
-
-  // the W image of item k (= p.k - 1, the current one) into the team's W buffer, once the
-  // consumers are past item k - 1's K phase (wfree); item 0's waits for the prepare kernel
-  auto issue_w = [&](bool block) {
-    const int k = p.k - 1;
-    if (k > 0) {
-      if (block) mbar_wait_spin(&tm.wfree, (uint32_t)((k - 1) & 1));
-      else if (!mbar_test(&tm.wfree, (uint32_t)((k - 1) & 1))) return;
-    }
-    if (!waited) {
-      asm volatile("griddepcontrol.wait;\n" ::: "memory");
-      waited = true;
-    }
-    if (leader) issue_wimg(tm, args, p.wseg, p.wr);
-    p.wpend = false;
-  };
   // descriptor p.k (from the fetcher) becomes current and is published to the consumers
   auto advance = [&]() {
     const int ds = p.k & (kSubRing - 1);
     while (ld_acquire(&tm.fetched) <= p.k) {
     }
-    if (p.wpend) issue_w(true);  // the previous item's image is still due (a short item)
     p.ls = 0;
     p.hc = tm.sub[ds].nbt > 0;
-    if (p.hc) {
-      p.cur = issue_of(tm.sub[ds]);
-      p.wpend = true;
-      p.wseg = tm.sub[ds].seg;
-      p.wr = tm.sub[ds].r;
-    }
+    if (p.hc) p.cur = issue_of(tm.sub[ds]);
     if (leader) {
       if (p.hc) {
         tm.kend[ds] = p.issued + p.cur.nK;
@@ -443,24 +409,15 @@ __device__ void produce(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& ar
     constexpr int S = AttnSmem<G, NT, ASYM, TEAMS>::kStages;
     while (p.hc) {
       const int slot = p.issued % S;
-      if (p.issued >= S) {
-        const uint32_t par = (uint32_t)((p.issued / S - 1) & 1);
-        while (!mbar_test(&sm.empty[slot], par))
-          if (p.wpend && p.k > 1) issue_w(false);  // while the ring is full
-      }
+      if (p.issued >= S) mbar_wait_spin(&sm.empty[slot], (uint32_t)((p.issued / S - 1) & 1));
       if (leader) issue_stage<BITS>(p.cur, p.ls, sm.ring[slot], &sm.full[slot]);
       ++p.issued;
-      // item 0's image once the ring is primed (it waits for the prepare kernel); later ones as
-      // soon as the previous item's K phase is done
-      if (p.wpend && (p.k > 1 || p.issued >= S)) issue_w(false);
       if (++p.ls == p.cur.stages) advance();
     }
-    if (p.wpend) issue_w(true);
     return;
   }
   for (;;) {
     reclaim();
-    if (p.wpend && (p.k > 1 || p.issued >= 4)) issue_w(false);
     if (!p.hc) {
       if (p.reclaimed == p.issued) break;  // every slot of this team is back in the pool
       continue;
@@ -526,7 +483,6 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.team[t].descfull[s], 1);
       for (int s = 0; s < kQOf<TEAMS>; ++s) mbar_init(&sm.team[t].sqbar[s], 1);
       mbar_init(&sm.team[t].wbar, 1);
-      mbar_init(&sm.team[t].wfree, 1);
       mbar_init(&sm.team[t].g0bar, 1);
       sm.team[t].started = 0;  // item 0's K phase: issue it whole before the consumers arrive
       sm.team[t].fetched = 0;
@@ -552,11 +508,11 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
 
   if (tid == 0) {
     mbar_wait(&tm.descfull[0], 0);
-    if (tm.sub[0].nbt > 0) issue_g0v(tm, args, tm.sub[0]);
-    // programmatic dependent launch: the combine may be scheduled once every CTA is here (the
-    // producer waits for the prepare kernel before its first W-image copy)
+    // programmatic dependent launch: everything above overlapped the prepare kernel; its
+    // output (the per-segment W images) is read from here on
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
+    if (tm.sub[0].nbt > 0) issue_wimg(tm, args, tm.sub[0]);
   }
 
   int st = 0;  // the team's running stage index (identical in every thread of the team)
@@ -649,7 +605,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       row_off[mt][0] = (tid4 * kI2Pad + (b0 ^ swz)) * RB;
       row_off[mt][1] = (tid4 * kI2Pad + ((b0 + 8) ^ swz)) * RB;
     }
-    const uint4* wthr = tm.w + tid4 * 8 + (gid ^ (2 * tid4));
+    const uint4* wthr = tm.wg.w + tid4 * 8 + (gid ^ (2 * tid4));
     const int wl = r * 8;  // chunks per (head, limb)
     for (int ks = 0; ks < d.nK; ++ks, ++st) {
       const int slot = acquire();
@@ -694,11 +650,9 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     for (int vs = 0; vs < nbt * d.nslices; ++vs, ++st) release(acquire());
     team_sync(team);
     if (tid == 0) {
-      mbar_arrive(&tm.wfree);
-      mbar_wait(&tm.g0bar, (uint32_t)(j & 1));
       const int jn = j + 1;
       mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (tm.sub[jn % kSubRing].nbt > 0) issue_g0v(tm, args, tm.sub[jn % kSubRing]);
+      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg(tm, args, tm.sub[jn % kSubRing]);
     }
     continue;
 #endif
@@ -723,7 +677,21 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       if (lane == 0) tm.rowmax[h][warp] = m;
     }
     team_sync(team);  // every warp is past phase 1: the W buffer is dead
-    if (tid == 0) mbar_arrive(&tm.wfree);  // the producer may load the next item's W image
+    if (lane == 0 && warp < i1) {  // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
+      // one copy per a, issued by warp a, into blocks of 2r + 1 float4s: the epilogue's lanes
+      // tid4 = 0..3 read a = 2 tid4 + aa, and the pad puts their blocks 32 bytes apart in the
+      // banks (an unpadded 2r-float4 stride maps all four onto the same banks: a 4-way
+      // conflict per load, 10 us of a C2 layer).  A copy completing before warp 0's expect_tx
+      // only takes the transaction count negative; the phase needs that arrival.
+      const uint32_t cb = ASYM ? (uint32_t)(2 * r * 16 * 4) : 0u;
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      if (warp == 0) {
+        mbar_expect_tx(&tm.g0bar, (uint32_t)(i1 * r * 32) + cb);
+        if (ASYM) bulk_g2s(tm.vch, args.segs[d.seg].v_ch, cb, &tm.g0bar);
+      }
+      bulk_g2s(tm.wg.g0v + warp * (2 * r + 1), reinterpret_cast<const float4*>(d.vg0) + warp * 2 * r,
+               (uint32_t)(r * 32), &tm.g0bar);
+    }
     unsigned char* pb = reinterpret_cast<unsigned char*>(tm.pr.p);
     // P = exp2(s - m) in fixed point with one scale per (h, a, 64-row tile), set by that
     // tile's largest probability: small probabilities far from the peak keep their
@@ -876,8 +844,8 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     for (int h = 0; h < G; ++h)
 #pragma unroll
       for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
-    mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // fp16 G0v [a][rr][c] (normalised), loaded at the last item's end
-    const uint4* g0v = tm.g0v;
+    mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // fp32 G0v [a][rr][c] (normalised), in the W buffer
+    const float4* g0v = tm.wg.g0v;
 #ifdef DQ_ATTN_NULL_FOLD  // measurement only: no G0v fold (wrong results), Y still consumed
 #pragma unroll
     for (int t = 0; t < kRw; ++t)
@@ -897,12 +865,8 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
         for (int aa = 0; aa < 2; ++aa) {
           const int a = 2 * tid4 + aa;
           if (a < i1) {
-            const uint4 gh = g0v[a * (r + 1) + rr];
-            const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gh.x));
-            const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&gh.y));
-            const float2 g45 = __half22float2(*reinterpret_cast<const __half2*>(&gh.z));
-            const float2 g67 = __half22float2(*reinterpret_cast<const __half2*>(&gh.w));
-            const float gc[8] = {g01.x, g01.y, g23.x, g23.y, g45.x, g45.y, g67.x, g67.y};
+            const float4 g_lo = g0v[a * (2 * r + 1) + 2 * rr], g_hi = g0v[a * (2 * r + 1) + 2 * rr + 1];
+            const float gc[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
 #pragma unroll
             for (int h = 0; h < G; ++h) {
               const float y0 = ASYM ? accv[t][h][aa] * s0 : accv[t][h][aa];
@@ -923,11 +887,11 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
         v += __shfl_xor_sync(0xffffffffu, v, 2);
         part[h][k] = v;
       }
-    team_sync(team);  // every warp is past the V stages and G0v: P and the G0v buffer are free
-    if (tid == 0) {  // the next item's G0v (its descriptor is out: this item was fully issued)
+    team_sync(team);  // every warp is past the V stages and G0v: P and W/G0v buffers are free
+    if (tid == 0) {
       const int jn = j + 1;
       mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (tm.sub[jn % kSubRing].nbt > 0) issue_g0v(tm, args, tm.sub[jn % kSubRing]);
+      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg(tm, args, tm.sub[jn % kSubRing]);
     }
     if (tid < G * 8 * NT) {
       (&tm.gamma[0][0][0])[tid] = 0;

@@ -343,10 +343,10 @@ constexpr int kEigThreads = 64;
 struct EigSmem {
   double a[kR][kR + 1];  // the matrix, then the accumulated transformation / eigenvectors
   double d[kR], e[kR];
-  double rc[kR], rs[kR];  // rotations of one QL chase, by index i
+  double rc[2][kR], rs[2][kR];  // rotations of two QL chases (double-buffered), by index i
   double red[kEigThreads / 32];
   double sh[4];          // broadcast scalars
-  int ish[4];
+  int ish[2][4];
   int perm[kR];
 };
 
@@ -473,81 +473,111 @@ __global__ void __launch_bounds__(kEigThreads) eig_tql_kernel(const double* __re
   return;
 #endif
   // ---- implicit QL on (d, e) (tqli), eigenvectors in the rows of a --------------------
+  // Thread 0 runs the bulge chases back to back, recording each chase's rotations into one of
+  // two buffers; warp 1 applies chase c - 1 to the eigenvector rows (two per lane) while
+  // thread 0 computes chase c: one barrier per chase, and the row updates leave the serial
+  // path.  The chase keeps its state in registers and loads the next step's d / e one step
+  // ahead (a step reads only entries the chase has not written yet).
   if (t == 0) {
     for (int i = 1; i < n; ++i) sm.e[i - 1] = sm.e[i];
     sm.e[n - 1] = 0.0;
   }
   __syncthreads();
   bool failed = false;
-  for (int l = 0; l < n; ++l) {
-    for (int iter = 0;; ++iter) {
-      // thread 0: find the split point m, run one chase, record its rotations
-      if (t == 0) {
+  int ql_l = 0, ql_iter = 0;  // thread 0: the eigenvalue being isolated, its iterations
+  for (int c = 0;; ++c) {
+    const int buf = c & 1;
+    if (t == 0) {
+      int status = 1, lo = 0, hi = 0;  // 0: a chase on rotations [lo, hi), 1: done, 2: no convergence
+      while (ql_l < n) {
+        const int l = ql_l;
         int m = l;
         for (; m < n - 1; ++m) {
           const double dd = fabs(sm.d[m]) + fabs(sm.d[m + 1]);
           if (fabs(sm.e[m]) <= 2.220446049250313e-16 * dd) break;
         }
-        int lo = m, hi = m;  // rotations recorded for i in [lo, hi)
-        if (m != l && iter < 40) {
-          double gq = (sm.d[l + 1] - sm.d[l]) / (2.0 * sm.e[l]);
-          double ri;
-          double r = hyp(gq, 1.0, &ri);
-          gq = sm.d[m] - sm.d[l] + sm.e[l] / (gq + copysign(r, gq));
-          double s = 1.0, c = 1.0, p = 0.0;
-          int i = m - 1;
-          bool deflated = false;
-          for (; i >= l; --i) {
-            const double f = s * sm.e[i], b = c * sm.e[i];
-            r = hyp(f, gq, &ri);
-            sm.e[i + 1] = r;
-            if (r == 0.0) {
-              sm.d[i + 1] -= p;
-              sm.e[m] = 0.0;
-              deflated = true;
-              break;
-            }
-            s = f * ri;
-            c = gq * ri;
-            gq = sm.d[i + 1] - p;
-            r = (sm.d[i] - gq) * s + 2.0 * c * b;
-            p = s * r;
-            sm.d[i + 1] = gq + p;
-            gq = c * r - b;
-            sm.rc[i] = c;
-            sm.rs[i] = s;
-          }
-          lo = deflated ? i + 1 : l;
-          if (!deflated) {
-            sm.d[l] -= p;
-            sm.e[l] = gq;
-            sm.e[m] = 0.0;
-          }
+        if (m == l) {
+          ++ql_l;
+          ql_iter = 0;
+          continue;
         }
-        sm.ish[0] = lo;
-        sm.ish[1] = hi;
-        sm.ish[2] = m;
-      }
-      __syncthreads();
-      const int lo = sm.ish[0], hi = sm.ish[1], m = sm.ish[2];
-      if (m == l) break;
-      if (iter >= 40) {
-        failed = true;
+        if (ql_iter++ >= 40) {
+          status = 2;
+          break;
+        }
+        double gq = (sm.d[l + 1] - sm.d[l]) / (2.0 * sm.e[l]);
+        double ri;
+        double r = hyp(gq, 1.0, &ri);
+        gq = sm.d[m] - sm.d[l] + sm.e[l] / (gq + copysign(r, gq));
+        double s = 1.0, cc = 1.0, p = 0.0;
+        int i = m - 1;
+        double ei = sm.e[i], di1 = sm.d[i + 1], di = sm.d[i];
+        bool deflated = false;
+        for (; i >= l; --i) {
+          const double ei_n = i > l ? sm.e[i - 1] : 0.0, di_n = i > l ? sm.d[i - 1] : 0.0;
+          const double f = s * ei, b = cc * ei;
+          r = hyp(f, gq, &ri);
+          sm.e[i + 1] = r;
+          if (r == 0.0) {
+            sm.d[i + 1] -= p;
+            sm.e[m] = 0.0;
+            deflated = true;
+            break;
+          }
+          s = f * ri;
+          cc = gq * ri;
+          gq = di1 - p;
+          r = (di - gq) * s + 2.0 * cc * b;
+          p = s * r;
+          sm.d[i + 1] = gq + p;
+          gq = cc * r - b;
+          sm.rc[buf][i] = cc;
+          sm.rs[buf][i] = s;
+          ei = ei_n;
+          di1 = di;
+          di = di_n;
+        }
+        lo = deflated ? i + 1 : l;
+        hi = m;
+        if (!deflated) {
+          sm.d[l] -= p;
+          sm.e[l] = gq;
+          sm.e[m] = 0.0;
+        }
+        status = 0;
         break;
       }
-      // apply the chase's rotations (i = hi-1 .. lo) to row t of the eigenvector matrix
-      if (t < n) {
-        double* row = sm.a[t];
-        for (int i = hi - 1; i >= lo; --i) {
-          const double c = sm.rc[i], s = sm.rs[i];
-          const double f = row[i + 1];
-          row[i + 1] = fma(s, row[i], c * f);
-          row[i] = fma(c, row[i], -s * f);
+      sm.ish[buf][0] = lo;
+      sm.ish[buf][1] = hi;
+      sm.ish[buf][2] = status;
+    }
+    if (t >= 32 && c > 0 && sm.ish[buf ^ 1][2] == 0) {
+      // chase c - 1 on rows t - 32 and t (i = hi - 1 .. lo, the chase's own order)
+      const int lo = sm.ish[buf ^ 1][0], hi = sm.ish[buf ^ 1][1];
+      const double* rcs = sm.rc[buf ^ 1];
+      const double* rss = sm.rs[buf ^ 1];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row_i = t - 32 + 32 * h;
+        if (row_i < n) {
+          double* row = sm.a[row_i];
+          double nxt = row[hi];
+          for (int i = hi - 1; i >= lo; --i) {
+            const double c_ = rcs[i], s_ = rss[i];
+            const double cur = row[i];
+            row[i + 1] = fma(s_, cur, c_ * nxt);
+            nxt = fma(c_, cur, -s_ * nxt);
+          }
+          row[lo] = nxt;
         }
       }
-      __syncthreads();  // rc / rs and the split search see the finished chase
     }
-    if (failed) break;
+    __syncthreads();
+    const int status = sm.ish[buf][2];
+    if (status != 0) {
+      failed = status == 2;
+      break;
+    }
   }
   if (failed && t == 0 && flags) atomicOr(flags, (int)DQ_FLAG_JACOBI_NOCONV);
 #ifdef DQ_EIG_STATS  // measurement only: QL chases of the first blocks
