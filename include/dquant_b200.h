@@ -22,6 +22,7 @@
  *   dq_quantize_rtn_f64 ............ quantize.quantize_rtn on float64 input (quantize.py:144 multiplies in f64)
  *   dq_dequantize .................. quantize.dequantize        quantize.py:154-157
  *   dq_decompose_batched ........... mpo.decompose (n=2)        mpo.py:153-178
+ *   dq_sym_eig_batched ............. the SVDs of mpo.decompose for n > 2 (per TT stage, Gram form)
  *   dq_deco_quantize_batched ....... compress.deco_quantize     compress.py:85-94
  *   dq_deco_quantize_asym_batched .. (opt-in per-channel asymmetric mode of north_star; no
  *                                    reference counterpart, parity against the oracle only)
@@ -121,6 +122,13 @@ int dq_decompose_workspace_size(int64_t nblk, int64_t rows, int64_t cols, size_t
 int dq_decompose_batched(const void* blocks, int32_t in_dtype, int64_t nblk, int64_t rows, int64_t cols,
                          float* core0, float* core1, int32_t* flags, void* workspace, size_t workspace_bytes,
                          void* stream);
+/* K3's eigensolver alone (Householder + implicit QL, fp64): nblk symmetric n x n matrices (n <= 64),
+ * gram [nblk][64][64] (upper triangle read, row stride 64) -> vectors [nblk][64][64] (column k =
+ * eigenvector k, largest-|entry| positive) and values [nblk][64] in descending order; no convergence
+ * -> DQ_FLAG_JACOBI_NOCONV in *flags.  The TT-SVD stages of chains longer than 2 (mpo.py:153-178)
+ * are Gram -> this -> projection. */
+int dq_sym_eig_batched(const double* gram, int64_t nblk, int32_t n, double* vectors, double* values, int32_t* flags,
+                       void* stream);
 /* same as dq_decompose_batched with an explicit n=2 plan (any split whose bond r <= 64) */
 int dq_decompose_plan_batched(const void* blocks, int32_t in_dtype, int64_t nblk, const dq_plan2* h_plan,
                               float* core0, float* core1, int32_t* flags, void* workspace, size_t workspace_bytes,
@@ -157,11 +165,15 @@ int dq_relayout(const uint8_t* src, int32_t src_layout, int64_t src_stride, uint
 /* ---- generic fused reads (any n=2 plan with i1*j1 <= 64) -----------------
  * x: p x cols (f32) -> out: p x rows (f32) = x @ W^T
  * x: p x rows (f32) -> out: p x cols (f32) = x @ W
+ * meter (optional, device uint64[2], WorkingSetMeter compress.py:23-33): the kernels add their own
+ * measurement -- [0] = max dequantized codes one CTA holds at once, [1] += codes dequantized.
  */
 int dq_fused_matmul_t(const float* x, int64_t p, const float* core0, const uint8_t* payload, int32_t layout,
-                      const float* scale, int64_t rows, int64_t cols, int32_t bits, float* out, void* stream);
+                      const float* scale, int64_t rows, int64_t cols, int32_t bits, float* out, uint64_t* meter,
+                      void* stream);
 int dq_fused_matmul(const float* x, int64_t p, const float* core0, const uint8_t* payload, int32_t layout,
-                    const float* scale, int64_t rows, int64_t cols, int32_t bits, float* out, void* stream);
+                    const float* scale, int64_t rows, int64_t cols, int32_t bits, float* out, uint64_t* meter,
+                    void* stream);
 
 /* ---- K5 fused dequant + decode attention (D = 128, j = (8,16)) -----------
  * One "unit" is one (sequence, kv head) of one layer; g query heads attend to it.

@@ -122,6 +122,7 @@ SIGNATURES = {
     "dq_decompose_workspace_size": (c_int32, [c_int64, c_int64, c_int64, POINTER(c_size_t)]),
     "dq_decompose_batched": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_size_t, c_void_p]),
+    "dq_sym_eig_batched": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dq_decompose_plan_batched": (c_int32, [c_void_p, c_int32, c_int64, POINTER(Plan2), c_void_p, c_void_p, c_void_p,
                                             c_void_p, c_size_t, c_void_p]),
     "dq_deco_quantize_batched": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p,
@@ -135,9 +136,9 @@ SIGNATURES = {
     "dq_relayout": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int32, c_int64, c_int64, POINTER(Plan2),
                               c_int32, c_void_p]),
     "dq_fused_matmul_t": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_int64, c_int64,
-                                    c_int32, c_void_p, c_void_p]),
+                                    c_int32, c_void_p, c_void_p, c_void_p]),
     "dq_fused_matmul": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_int64, c_int64,
-                                  c_int32, c_void_p, c_void_p]),
+                                  c_int32, c_void_p, c_void_p, c_void_p]),
     "dq_attention_plan": (c_int32, [POINTER(Segment), c_int32, c_int32, c_int32, c_int32, POINTER(c_int32),
                                     POINTER(c_int32), POINTER(c_int32), POINTER(c_int32), POINTER(c_int32),
                                     POINTER(c_int32)]),

@@ -29,7 +29,6 @@ from .quantize import QuantizedTensor, _check_bits, dequantize, payload_size, qu
 
 TILE_ELEMENTS = 64 * 64
 # codes one CTA of the fused kernels holds dequantized at any moment (one per thread)
-_FUSED_INFLIGHT = 256
 
 
 class WorkingSetMeter:
@@ -339,13 +338,13 @@ def _fused(x, q: QuantizedMpo, meter, transposed: bool):
     p = xs[0]
     out = torch.empty((p, q.rows if transposed else q.cols), dtype=torch.float32, device=qt.data.device)
     fn = lib().dq_fused_matmul_t if transposed else lib().dq_fused_matmul
+    mdev = torch.zeros(2, dtype=torch.int64, device=qt.data.device) if meter is not None else None
     check(fn(ptr(xd), p, ptr(core0), ptr(qt.data), _lib.LAYOUT_REF, ptr(scale), q.rows, q.cols, q.bits, ptr(out),
-             stream_ptr()), "fused_matmul_t" if transposed else "fused_matmul")
-    if meter is not None:
-        # each CTA converts one code per thread at a time; nothing larger is ever dequantized
-        ctas = p * max(1, -(-q.plan.i_factors[1] // 256)) if transposed else p
-        for _ in range(ctas):
-            meter.record(min(_FUSED_INFLIGHT, qt.count))
+             ptr(mdev), stream_ptr()), "fused_matmul_t" if transposed else "fused_matmul")
+    if meter is not None:  # what the kernels measured (reads.cu meter_report)
+        peak, total = (int(v) for v in mdev.cpu())
+        meter.record(peak)
+        meter.total_unpacked += total - peak
     return out if is_t else out.cpu().numpy()
 
 

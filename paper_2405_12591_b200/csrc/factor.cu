@@ -1266,6 +1266,23 @@ extern "C" int dq_decompose_plan_batched(const void* blocks, int32_t dtype, int6
   return factor_core(blocks, d, nblk, core0, core1, w, flags, (cudaStream_t)stream);
 }
 
+extern "C" int dq_sym_eig_batched(const double* gram, int64_t nblk, int32_t n, double* vectors, double* values,
+                                  int32_t* flags, void* stream) {
+  if (n < 1 || n > kR) return fail(DQ_ERR_UNSUPPORTED, "dq_sym_eig_batched: n = %d outside 1..%d", n, kR);
+  if (nblk < 0 || (nblk && (!gram || !vectors || !values))) return fail(DQ_ERR_INVALID_ARG, "dq_sym_eig_batched: bad arguments");
+  if (nblk == 0) return DQ_OK;
+  static bool attr = false;
+  if (!attr) {
+    DQ_CUDA_TRY(cudaFuncSetAttribute(eig_tql_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem)));
+    attr = true;
+  }
+  Dims d{};
+  d.r = n;
+  eig_tql_kernel<<<(unsigned)nblk, kEigThreads, sizeof(EigSmem), (cudaStream_t)stream>>>(gram, d, vectors, values, flags);
+  DQ_LAUNCH_CHECK();
+  return DQ_OK;
+}
+
 extern "C" int dq_deco_quantize_batched(const void* blocks, int32_t dtype, int64_t nblk, int64_t rows, int64_t cols,
                                         int32_t bits, int32_t layout, float* core0, uint8_t* payload,
                                         int64_t payload_stride, float* scale, int32_t* flags, void* ws, size_t wsb,

@@ -63,13 +63,100 @@ __global__ void __launch_bounds__(kThreads) reconstruct_kernel(const float* __re
   }
 }
 
+// ---- K4 for 128-wide rows (j = (8, 16)) on the fp64 tensor pipe ---------------------------
+// Per CTA: one block x 8 b values.  D[(a, c)][(b, e)] = sum_r G0[(a, c)][r] dq[r][(b, e)] is a
+// (64 x 64) . (64 x 128) GEMM: DMMA m8n8k4, warp w owns the 8 rows (a, c) = 8w.. x 128 columns.
+// Operands are staged as fp32 (G0 as stored, dq = f32(code) * f32(scale): quantize.py:154-157)
+// and widened exactly to fp64 in the fragments: the same f64 accumulation of the same f32
+// values as the reference's reconstruct (mpo.py:181-198).
+constexpr int kK4Pitch = 68;  // floats per row of the operand tiles (conflict-light fragment reads)
+
+__device__ __forceinline__ void dmma64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kThreads) reconstruct128_kernel(const float* __restrict__ core0,
+                                                                  const uint8_t* __restrict__ payload,
+                                                                  int64_t payload_stride, CoreGeom geom,
+                                                                  const float* __restrict__ scale, int i1,
+                                                                  void* __restrict__ out, int out_dtype) {
+  extern __shared__ __align__(16) float k4s[];
+  float* g0 = k4s;                   // [p = (a, c)][r]
+  float* dq = k4s + 64 * kK4Pitch;   // [(b, e)][r]
+  const int r = geom.r, i2 = geom.i2;
+  const int64_t blk = blockIdx.x;
+  const int b0 = blockIdx.y * 8;
+  const float s = scale[blk];
+  const float* c0 = core0 + blk * (int64_t)i1 * 8 * r;
+  const uint8_t* pl = payload + blk * payload_stride;
+  for (int i = threadIdx.x; i < 64 * 64; i += kThreads) {
+    const int p = i / 64, rr = i % 64;
+    g0[p * kK4Pitch + rr] = (p < i1 * 8 && rr < r) ? c0[p * r + rr] : 0.f;
+  }
+  for (int i = threadIdx.x; i < 128 * 64; i += kThreads) {
+    const int rr = i / 128, be = i % 128, bl = be / 16, e = be % 16;
+    float v = 0.f;
+    if (rr < r && b0 + bl < i2) v = __fmul_rn((float)geom_read(pl, geom, rr, b0 + bl, e), s);
+    dq[be * kK4Pitch + rr] = v;
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  double acc[16][2];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = 0.0;
+  const float* arow = g0 + (w * 8 + g) * kK4Pitch + t4;
+  for (int k = 0; k < r; k += 4) {
+    const double a = (double)arow[k];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) dmma64(acc[j][0], acc[j][1], a, (double)dq[(j * 8 + g) * kK4Pitch + k + t4]);
+  }
+  const int p = w * 8 + g, aa = p / 8, c = p % 8;
+  if (aa >= i1) return;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int be = j * 8 + 2 * t4, bl = be / 16, e = be % 16;
+    if (b0 + bl >= i2) continue;
+    const int64_t o = blk * (int64_t)i1 * i2 * 128 + ((int64_t)aa * i2 + b0 + bl) * 128 + c * 16 + e;
+    if (out_dtype == DQ_F16) {
+      *reinterpret_cast<__half2*>(static_cast<__half*>(out) + o) =
+          __halves2half2(__float2half_rn((float)acc[j][0]), __float2half_rn((float)acc[j][1]));
+    } else {
+      *reinterpret_cast<float2*>(static_cast<float*>(out) + o) = make_float2((float)acc[j][0], (float)acc[j][1]);
+    }
+  }
+}
+
 // ---- x @ W^T: one CTA per (query row p, tile of 256 b) ----------------------
 //   Wt[a][r][e] = sum_c x[p, c*j2+e] * core0[a,c,r]   (staged in shared memory)
 //   out[p, a*i2+b] = scale * sum_{r,e} Wt[a][r][e] * code[r,b,e]
+// WorkingSetMeter (compress.py:23-33), measured by the kernels: meter[0] = the most dequantized
+// codes one CTA holds at once (atomicMax), meter[1] = codes dequantized in total (atomicAdd)
+__device__ __forceinline__ void meter_report(unsigned long long* meter, long long held, long long unpacked) {
+  if (!meter) return;
+  for (int o = 16; o; o >>= 1) {
+    held += __shfl_xor_sync(0xffffffffu, held, o);
+    unpacked += __shfl_xor_sync(0xffffffffu, unpacked, o);
+  }
+  __shared__ unsigned long long red[2];
+  if (threadIdx.x == 0) red[0] = red[1] = 0ull;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&red[0], (unsigned long long)held);
+    atomicAdd(&red[1], (unsigned long long)unpacked);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&meter[0], red[0]);
+    atomicAdd(&meter[1], red[1]);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) fused_t_kernel(const float* __restrict__ x, const float* __restrict__ core0,
                                                            const uint8_t* __restrict__ payload, CoreGeom geom,
                                                            const float* __restrict__ scale, int i1, int j1, int cols,
-                                                           float* __restrict__ out) {
+                                                           float* __restrict__ out, unsigned long long* meter) {
   extern __shared__ float smem[];
   const int r = geom.r, i2 = geom.i2, j2 = geom.j2;
   float* xs = smem;             // [cols]
@@ -87,18 +174,22 @@ __global__ void __launch_bounds__(kThreads) fused_t_kernel(const float* __restri
   }
   __syncthreads();
   const int b = blockIdx.y * kThreads + threadIdx.x;
-  if (b >= i2) return;
+  const bool live = b < i2;
   double acc[8];
 #pragma unroll
   for (int a = 0; a < 8; ++a) acc[a] = 0.0;
-  for (int rr = 0; rr < r; ++rr)
-    for (int e = 0; e < j2; ++e) {
-      const double cv = (double)geom_read(payload, geom, rr, b, e);
-      if (cv == 0.0) continue;
+  if (live) {
+    for (int rr = 0; rr < r; ++rr)
+      for (int e = 0; e < j2; ++e) {
+        const double cv = (double)geom_read(payload, geom, rr, b, e);  // one code at a time per thread
+        if (cv == 0.0) continue;
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
-        if (a < i1) acc[a] = fma((double)wt[(a * r + rr) * j2 + e], cv, acc[a]);
-    }
+        for (int a = 0; a < 8; ++a)
+          if (a < i1) acc[a] = fma((double)wt[(a * r + rr) * j2 + e], cv, acc[a]);
+      }
+  }
+  meter_report(meter, live ? 1 : 0, live ? (long long)r * j2 : 0);
+  if (!live) return;
   const double s = (double)*scale;
   for (int a = 0; a < i1; ++a) out[(int64_t)p * rows + a * i2 + b] = (float)(acc[a] * s);
 }
@@ -109,7 +200,7 @@ __global__ void __launch_bounds__(kThreads) fused_t_kernel(const float* __restri
 __global__ void __launch_bounds__(kThreads) fused_n_kernel(const float* __restrict__ x, const float* __restrict__ core0,
                                                            const uint8_t* __restrict__ payload, CoreGeom geom,
                                                            const float* __restrict__ scale, int i1, int j1, int cols,
-                                                           float* __restrict__ out) {
+                                                           float* __restrict__ out, unsigned long long* meter) {
   extern __shared__ float smem[];
   const int r = geom.r, i2 = geom.i2, j2 = geom.j2;
   const int rows = i1 * i2;
@@ -118,11 +209,14 @@ __global__ void __launch_bounds__(kThreads) fused_n_kernel(const float* __restri
   const int p = blockIdx.x;
   for (int i = threadIdx.x; i < rows; i += kThreads) xs[i] = x[(int64_t)p * rows + i];
   __syncthreads();
+  long long held = 0, unpacked = 0;
   for (int i = threadIdx.x; i < r * j2; i += kThreads) {
     const int rr = i / j2, e = i - rr * j2;
     double acc[8];
 #pragma unroll
     for (int a = 0; a < 8; ++a) acc[a] = 0.0;
+    held = 1;  // one code at a time per thread
+    unpacked += i2;
     for (int b = 0; b < i2; ++b) {
       const double cv = (double)geom_read(payload, geom, rr, b, e);
       if (cv == 0.0) continue;
@@ -132,6 +226,7 @@ __global__ void __launch_bounds__(kThreads) fused_n_kernel(const float* __restri
     }
     for (int a = 0; a < i1; ++a) y[(a * r + rr) * j2 + e] = (float)acc[a];
   }
+  meter_report(meter, held, unpacked);
   __syncthreads();
   const double s = (double)*scale;
   for (int i = threadIdx.x; i < cols; i += kThreads) {
@@ -228,6 +323,19 @@ extern "C" int dq_deco_dequantize_batched(const float* core0, const uint8_t* pay
   if (nblk == 0) return DQ_OK;
   if (!core0 || !payload || !scale || !out) return fail(DQ_ERR_INVALID_ARG, "null pointer");
   CoreGeom g = make_geom(p, bits, layout);
+  if (cols == 128 && p.j1 == 8 && p.j2 == 16 && p.r <= 64) {  // every KV block: the tensor-pipe kernel
+    dim3 grid((unsigned)nblk, (unsigned)ceil_div(p.i2, 8));
+    constexpr int k4smem = (int)sizeof(float) * 192 * kK4Pitch;
+    static bool attr = false;
+    if (!attr) {
+      DQ_CUDA_TRY(cudaFuncSetAttribute(reconstruct128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k4smem));
+      attr = true;
+    }
+    reconstruct128_kernel<<<grid, kThreads, k4smem, (cudaStream_t)stream>>>(core0, payload, payload_stride, g, scale,
+                                                                       (int)p.i1, out, out_dtype);
+    DQ_LAUNCH_CHECK();
+    return DQ_OK;
+  }
   const size_t smem = sizeof(float) * ((size_t)p.i1 * p.j1 * p.r + (size_t)p.r * kBT * p.j2);
   if (smem > 200 * 1024) return fail(DQ_ERR_UNSUPPORTED, "plan too large for the reconstruct kernel");
   DQ_CUDA_TRY(cudaFuncSetAttribute(reconstruct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -240,7 +348,7 @@ extern "C" int dq_deco_dequantize_batched(const float* core0, const uint8_t* pay
 
 extern "C" int dq_fused_matmul_t(const float* x, int64_t np, const float* core0, const uint8_t* payload,
                                  int32_t layout, const float* scale, int64_t rows, int64_t cols, int32_t bits,
-                                 float* out, void* stream) {
+                                 float* out, uint64_t* meter, void* stream) {
   if (rows < 1 || cols < 1) return fail(DQ_ERR_SHAPE_MISMATCH, "dimensions must be >= 1");
   dq_plan2 p = make_plan2(rows, cols);
   int st = check_geom(p, bits, layout);
@@ -254,14 +362,14 @@ extern "C" int dq_fused_matmul_t(const float* x, int64_t np, const float* core0,
   DQ_CUDA_TRY(cudaFuncSetAttribute(fused_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)np, (unsigned)ceil_div(p.i2, kThreads));
   fused_t_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(x, core0, payload, g, scale, (int)p.i1, (int)p.j1,
-                                                                (int)cols, out);
+                                                                (int)cols, out, (unsigned long long*)meter);
   DQ_LAUNCH_CHECK();
   return DQ_OK;
 }
 
 extern "C" int dq_fused_matmul(const float* x, int64_t np, const float* core0, const uint8_t* payload,
                                int32_t layout, const float* scale, int64_t rows, int64_t cols, int32_t bits,
-                               float* out, void* stream) {
+                               float* out, uint64_t* meter, void* stream) {
   if (rows < 1 || cols < 1) return fail(DQ_ERR_SHAPE_MISMATCH, "dimensions must be >= 1");
   dq_plan2 p = make_plan2(rows, cols);
   int st = check_geom(p, bits, layout);
@@ -274,7 +382,8 @@ extern "C" int dq_fused_matmul(const float* x, int64_t np, const float* core0, c
   if (smem > 200 * 1024) return fail(DQ_ERR_UNSUPPORTED, "plan too large for the fused kernel");
   DQ_CUDA_TRY(cudaFuncSetAttribute(fused_n_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fused_n_kernel<<<(unsigned)np, kThreads, smem, (cudaStream_t)stream>>>(x, core0, payload, g, scale, (int)p.i1,
-                                                                        (int)p.j1, (int)cols, out);
+                                                                        (int)p.j1, (int)cols, out,
+                                                                        (unsigned long long*)meter);
   DQ_LAUNCH_CHECK();
   return DQ_OK;
 }

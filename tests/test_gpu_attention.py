@@ -44,9 +44,16 @@ def test_generic_fused_reads_golden(golden, dq, name):
     assert qt.payload == g[f"{name}_payload"].tobytes()
     assert rel(g[f"{name}_mmt"], dq.fused_matmul_t(g[f"{name}_xt"], q)) < 1e-5
     assert rel(g[f"{name}_mm"], dq.fused_matmul(g[f"{name}_x"], q)) < 1e-5
+    # the working set is what the kernels report (reads.cu meter_report), not a formula: at most
+    # one tile (test_compress.py:112-121), and every code of the core dequantized once per row of x
     meter = dq.WorkingSetMeter()
     dq.fused_matmul(g[f"{name}_x"], q, meter)
     assert 0 < meter.peak_elements <= 64 * 64
+    assert meter.total_unpacked == g[f"{name}_x"].shape[0] * qt.count
+    meter_t = dq.WorkingSetMeter()
+    dq.fused_matmul_t(g[f"{name}_xt"], q, meter_t)
+    assert 0 < meter_t.peak_elements <= 64 * 64
+    assert meter_t.total_unpacked == g[f"{name}_xt"].shape[0] * qt.count
 
 
 def _oracle_attend(k, v, q, bits, segs_T, tail):
