@@ -222,7 +222,8 @@ typedef struct dq_attn_args {
   int32_t* sched;            /* device [2] scheduler counters, zero before the first launch (self-resetting) */
   float* part_o;          /* workspace [total_parts][g][128] f32 */
   float* part_ml;         /* workspace [total_parts][g][2]   f32 (max, sum) */
-  int32_t phases;         /* bit 0: split kernel, bit 1: combine kernel, bit 2: prepare kernel; 0: all */
+  int32_t phases;         /* bit 0: split kernel, bit 1: combine kernel, bit 2: prepare kernel; 0: all;
+                             bit 3: launch the split kernel without its PDL edge (timing) */
   int32_t nctas;          /* persistent split-kernel CTAs (dq_attention_ctas); <= 0 or >= nwork: one per item */
   int64_t* trace;         /* optional (profiling): [nwork][8] global-timer stamps per work item */
   void* wimg;             /* workspace [nseg][wimg_stride]: per-segment W images (prepare kernel) */

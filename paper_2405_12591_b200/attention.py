@@ -651,7 +651,17 @@ class DecodeKvCache:
 
     # ---- accounting ----------------------------------------------------------
     def kernel_bytes(self, layer: int) -> int:
-        """Algorithmic bytes of one split-kernel launch: compressed segments + q."""
+        """Algorithmic bytes of one split-kernel launch: per unit and segment, K and V
+        each 128*T*bits/8 code bytes + the small core as fp16 (2*i1*8*r) + a 4-byte scale, plus q.
+        (The build stores the small cores as fp32, and the split kernel reads G0v but not G0k:
+        ``stream_bytes`` counts what it streams.)"""
+        lay = self._layers[layer]
+        per = sum(2 * (payload_size(g.plan.r * g.plan.i2 * g.plan.j2, self.bits) + 2 * g.plan.i1 * 8 * g.plan.r + 4)
+                  for g in lay.groups)
+        return per * self.units + self.units * self.g * self.dim * 2
+
+    def stream_bytes(self, layer: int) -> int:
+        """Bytes one split-kernel launch is given to stream: packed cores, fp32 G0k and G0v, scales, q."""
         lay = self._layers[layer]
         return sum(g.stream_bytes() for g in lay.groups) * self.units + self.units * self.g * self.dim * 2
 

@@ -178,7 +178,7 @@ int launch_tc(Kernel kernel, size_t smem, int threads, const dq_attn_args& a, cu
   attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_pdl;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (a.phases & 8) ? 0 : 1;  // phases bit 3: no PDL edge (back-to-back timing)
   DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, a));
   return DQ_OK;
 }
@@ -261,7 +261,7 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
       attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr_pdl;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = (phases & 8) ? 0 : 1;  // bit 3: no PDL edge (back-to-back timing of the split kernel)
       if (a.asym && BITS == 8) return fail(DQ_ERR_UNSUPPORTED, "the asymmetric mode covers 2- and 4-bit codes");
       int rc = DQ_OK;
       if (a.chunk_b > kCB) {  // 8-tile work items (g = 1, 2- and 4-bit codes)
