@@ -184,7 +184,8 @@ typedef struct dq_segment {
   const uint8_t* k_codes; /* DQ_LAYOUT_KTILE */
   const uint8_t* v_codes; /* DQ_LAYOUT_VTILE */
   const float* k_g0;      /* fp32 [i1][r][8]  (dq_core0_relayout, normalised): score side */
-  const float* v_g0;      /* fp32 [i1][r][8]  (dq_core0_relayout, normalised): output side */
+  const void* v_g0;       /* [i1][r][8] (dq_core0_relayout, normalised): output side; fp32, or fp16 where
+                             dq_attention_g0v_dtype says so */
   float k_scale, v_scale; /* quantizer scale times the G0 normalisation factor */
   int32_t T;          /* tokens in the segment */
   int32_t i1, i2, r;  /* plan of (T,128) */
@@ -243,6 +244,11 @@ typedef struct dq_attn_args {
 
 /* bytes of one per-segment W image (the wimg stride) for a GQA group of g heads */
 int dq_attention_wimg_bytes(int32_t g, int64_t* h_bytes);
+
+/* element type (DQ_F16 / DQ_F32) of the dq_segment.v_g0 tables the split kernel of (g, path, asym,
+ * chunk_b) reads: fp16 where it computes the W image itself (path 0, g = 1, symmetric, items of
+ * <= 256 rows: no prepare kernel) */
+int dq_attention_g0v_dtype(int32_t g, int32_t path, int32_t asym, int32_t chunk_b, int32_t* h_dtype);
 
 /* resident split-kernel CTAs on the current device (SMs x CTAs per SM): the persistent grid */
 int dq_attention_ctas(int32_t g, int32_t bits, int32_t* h_ctas);

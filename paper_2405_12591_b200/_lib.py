@@ -144,6 +144,7 @@ SIGNATURES = {
                                     POINTER(c_int32)]),
     "dq_attention_ctas": (c_int32, [c_int32, c_int32, POINTER(c_int32)]),
     "dq_decode_attention": (c_int32, [POINTER(AttnArgs), c_void_p]),
+    "dq_attention_g0v_dtype": (c_int32, [c_int32, c_int32, c_int32, c_int32, POINTER(c_int32)]),
     "dq_attention_wimg_bytes": (c_int32, [c_int32, POINTER(c_int64)]),
     "dq_tail_append": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "dq_model_add_rmsnorm": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_float,

@@ -72,6 +72,7 @@ class SegmentGroup:
     token0: int
     k_ch: torch.Tensor | None = None  # asymmetric mode: (units, 2, r, 16) f32 channel scales, zero points
     v_ch: torch.Tensor | None = None
+    v_g0f16: torch.Tensor | None = None  # fp16 copy of v_g0h where the split kernel folds fp16 (path 0, g = 1)
 
     def reference_bytes(self, bits: int) -> int:
         """compression_report().bytes_compressed of one unit's K (or V) block (compress.py:234-248);
@@ -85,8 +86,9 @@ class SegmentGroup:
         """Bytes K5 reads for one unit of this segment (K + V): packed cores, fp32 G0k and G0v, scales
         (the channel tables in the asymmetric mode)."""
         ch = 2 * self.k_ch[0].numel() * 4 if self.k_ch is not None else 0
+        vg = self.v_g0f16 if self.v_g0f16 is not None else self.v_g0h  # fp16 where the kernel folds fp16
         return (self.k_payload.shape[1] + self.v_payload.shape[1] + self.k_g0h.element_size() * self.k_g0h.shape[1]
-                + self.v_g0h.element_size() * self.v_g0h.shape[1] + 8 + ch)
+                + vg.element_size() * vg.shape[1] + 8 + ch)
 
 
 class _Layer:
@@ -470,6 +472,7 @@ class DecodeKvCache:
                                   "r = 64 plans")
             path = 1 if (eligible and self.tc) else 0
 
+
         # the segment table, built column-wise (numpy view of the dq_segment records): one record
         # per (group, unit, head group); the scales are filled in on the device below (no sync)
         nseg = len(lay.groups) * vunits
@@ -516,6 +519,15 @@ class DecodeKvCache:
             # halves, evening out the scheduler's last round (C3: 230.2 -> 225.7 us; at 256-row
             # items the 128-row halves cost more than they save: C2 64.3 -> 68.5 us)
             wp = split_tail(wp, rec["unit"].tolist(), int(TAIL_SPLIT * ctas))
+        g0dt = ctypes.c_int32()
+        check(lib().dq_attention_g0v_dtype(gk, path, 1 if self.asym else 0, chunk_b, ctypes.byref(g0dt)),
+              "g0v_dtype")
+        if g0dt.value == _lib.DQ_F16:  # the split kernel folds an fp16 copy of G0v (made once per group)
+            for gi, grp in enumerate(lay.groups):
+                if grp.v_g0f16 is None:
+                    grp.v_g0f16 = grp.v_g0h.to(torch.float16)
+                vg = grp.v_g0f16
+                rec[gi * vunits:(gi + 1) * vunits]["v_g0"] = vg.data_ptr() + u_of * vg.shape[1] * vg.element_size()
         if hg > 1:  # a tile range's head groups back to back in the ticket order (L2 reuse)
             order = sorted(range(wp.nwork), key=lambda i: (wp.work[3 * i] // hg, wp.work[3 * i + 1],
                                                            wp.work[3 * i] % hg))

@@ -126,6 +126,11 @@ __global__ void tail_append_kernel(const __half* __restrict__ k_rows, const __ha
 template <int G>
 constexpr int kTeamsOf = G == 1 ? DQ_ATTN_TEAMS_G1 : 1;
 
+// the split kernel computes the W image itself (no prepare kernel) and folds an fp16 G0v
+bool in_kernel_w(int g, int path, int asym, int chunk_b) {
+  return DQ_INKERNEL_W && path == 0 && g == 1 && !asym && kTeamsOf<1> == 1 && chunk_b <= kCB;
+}
+
 template <int BITS, int G, int NT = kTiles, bool ASYM = false>
 int set_attrs() {
   constexpr int T = kTeamsOf<G>;
@@ -208,7 +213,7 @@ int launch_attn(const dq_attn_args& a, cudaStream_t s) {
       cfg.numAttrs = 1;
       DQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_prepare_gqa_kernel, a));
     }
-  } else if (a.nseg > 0 && a.nwork > 0 && (phases & 4)) {
+  } else if (a.nseg > 0 && a.nwork > 0 && (phases & 4) && !in_kernel_w(G, a.path, a.asym, a.chunk_b)) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)a.nseg, kPrepSplit);
     cfg.blockDim = dim3(kPrepThreadsOf<G>);
@@ -394,6 +399,12 @@ extern "C" int dq_attention_ctas(int32_t g, int32_t bits, int32_t* ctas) {
   }
   if (rc != DQ_OK) return rc;
   *ctas = sms * per_sm;
+  return DQ_OK;
+}
+
+extern "C" int dq_attention_g0v_dtype(int32_t g, int32_t path, int32_t asym, int32_t chunk_b, int32_t* dtype) {
+  if (!dtype) return fail(DQ_ERR_INVALID_ARG, "null output");
+  *dtype = in_kernel_w(g, path, asym, chunk_b) ? DQ_F16 : DQ_F32;
   return DQ_OK;
 }
 

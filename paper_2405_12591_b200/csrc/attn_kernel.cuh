@@ -61,6 +61,15 @@ constexpr int kQ = 32;       // per-team stage queue (>= ring slots)
 #endif
 constexpr int kTeamPrefetch = DQ_TEAM_PREFETCH;
 constexpr int kSmemCap = 227 * 1024;  // dynamic shared memory per CTA (sm_100)
+// Opt-in measurement build (-DDQ_INKERNEL_W=1): the W image computed inside the split kernel by
+// the fetcher warp (g = 1, symmetric, one team per CTA, items of <= 256 rows), no prepare
+// kernel; the W buffer then sits apart from an fp16 G0v buffer, and the fetcher writes item
+// j + 1's W while item j is in its softmax / V phase.  Measured on C2: split kernel 86 us
+// against 60 us, step 2.78 ms against 2.20 ms -- one warp computing 16 KB of W per item is too
+// slow (a 2.5 us wait before each item) and the fp16 G0v fold lengthens the epilogue.
+#ifndef DQ_INKERNEL_W
+#define DQ_INKERNEL_W 0
+#endif
 
 template <int TEAMS>
 constexpr int kCtaThreadsOf = TEAMS * kThreads + 32 * (TEAMS + 1);  // + a producer warp per team + the fetcher
@@ -84,8 +93,10 @@ struct SubItem {
 // per-team state: descriptors, stage queue, W image / G0v, P, reductions
 template <int G, int NT, bool ASYM, int QN = kQ>
 struct TeamSmem {
-  uint64_t wbar;   // W image (attn_prepare.cuh) by TMA, one phase per sub-item
+  static constexpr bool kInW = DQ_INKERNEL_W && G == 1 && !ASYM && QN == 1 && NT <= kTiles;
+  uint64_t wbar;   // W image (attn_prepare.cuh) by TMA, or by the fetcher warp (kInW); one phase per item
   uint64_t g0bar;  // G0v prefetch, one phase per sub-item
+  uint64_t wfree;  // kInW: the consumers are past an item's K phase (its W buffer may be rewritten)
   uint64_t descfull[kSubRing];  // descriptor j written (producer arrival), phase j / kSubRing
   uint64_t sqbar[QN];           // stage n's slot published (producer arrival), phase n / kQ (TEAMS = 2)
   int sq[QN];                   // stage n of the team: ring slot | (full-barrier parity << 8)
@@ -105,8 +116,12 @@ struct TeamSmem {
   // shorten the gap between items but lengthen the epilogue: C2 66 us against 62 us.)
   union {
     uint4 w[G * 2 * kMaxR * 8];
-    float4 g0v[8 * (kMaxR * 2 + 1)];  // [a][rr][c] with a 16-byte pad per a (kG0vPad)
+    float4 g0v[kInW ? 1 : 8 * (kMaxR * 2 + 1)];  // [a][rr][c] with a 16-byte pad per a (kG0vPad)
   } wg;
+  // kInW: fp16 G0v [a][rr][8 c], r + 1 chunks per a (a 16-byte pad: the lanes tid4 = 0..3 read
+  // a = 2 tid4 + aa four banks apart), loaded at the previous item's end; q of the item's unit
+  uint4 g0v16[kInW ? 8 * (kMaxR + 1) : 1];
+  float qs[kInW ? 128 : 1];
   // V phase: P limbs [((h*2 + limb)*8 + a)*(4 NT) + (bg ^ 4*(a&1))];
   // epilogue (aliased, P is dead): cross-warp reduction of the O partial
   union {
@@ -169,7 +184,7 @@ __device__ __forceinline__ void load_sub(SubItem& d, const dq_attn_args& a, int 
   SubItem t;
   t.kc = s.k_codes;
   t.vc = s.v_codes;
-  t.vg0 = s.v_g0;
+  t.vg0 = static_cast<const float*>(s.v_g0);  // fp32, or fp16 under kInW (dq_attention_g0v_dtype)
   t.kscale = s.k_scale;
   t.vscale = s.v_scale;
   t.seg = sg;
@@ -193,6 +208,16 @@ __device__ __forceinline__ void issue_wimg(TeamSmem<G, NT, ASYM, QN>& tm, const 
   mbar_expect_tx(&tm.wbar, wb + (uint32_t)sizeof(WMeta<G>));
   bulk_g2s(tm.wg.w, img, wb, &tm.wbar);
   bulk_g2s(&tm.wmeta, img + kWChunkBytes<G>, (uint32_t)sizeof(WMeta<G>), &tm.wbar);
+}
+
+// kInW: fp16 G0v (one copy per a into its padded block) and, asymmetric... (kInW is symmetric
+// only) onto the team's g0bar (one thread)
+template <int G, int NT, bool ASYM, int QN>
+__device__ __forceinline__ void issue_g0v16(TeamSmem<G, NT, ASYM, QN>& tm, const SubItem& d) {
+  mbar_expect_tx(&tm.g0bar, (uint32_t)(d.i1 * d.r * 16));
+  const uint4* src = reinterpret_cast<const uint4*>(d.vg0);
+  for (int aa = 0; aa < d.i1; ++aa)
+    bulk_g2s(tm.g0v16 + aa * (d.r + 1), src + aa * d.r, (uint32_t)(d.r * 16), &tm.g0bar);
 }
 
 template <int NT>
@@ -305,27 +330,113 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 #endif
 constexpr int kFetchAhead = DQ_FETCH_AHEAD;
 
+// W image of one item, computed by the whole fetcher warp straight into the team's W buffer: the
+// prepare kernel's arithmetic (attn_prepare.cuh, path 0, g = 1, symmetric) one column a at a
+// time -- lane l holds bond rows l and l + 32 (16 e each, ord16 order), the column's group
+// maxima and beta are warp reductions.  Columns a >= i1 get beta 0 and the scale of a zero
+// maximum, as in the prepare kernel (their scores are masked).
+template <int BITS, int G, int NT, bool ASYM, int QN>
+__device__ void compute_w(TeamSmem<G, NT, ASYM, QN>& tm, const dq_attn_args& args, const SubItem& d, int lane) {
+  constexpr int X = kExcess<BITS>;
+  const dq_segment& seg = args.segs[d.seg];
+  const int r = seg.r, i1 = seg.i1;
+  {  // q of the unit -> fp32 in shared memory (4 values per lane)
+    const __half2* qh = reinterpret_cast<const __half2*>(args.q) + (size_t)seg.unit * 64;
+    const float2 x0 = __half22float2(qh[2 * lane]), x1 = __half22float2(qh[2 * lane + 1]);
+    reinterpret_cast<float4*>(tm.qs)[lane] = make_float4(x0.x, x0.y, x1.x, x1.y);
+  }
+  __syncwarp();
+  const float4* g0k = reinterpret_cast<const float4*>(seg.k_g0);  // fp32 [a][rr][c], normalised
+  for (int a = 0; a < 8; ++a) {
+    float wv[2][16];
+    float m[2] = {0.f, 0.f};
+    bool live[2];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int rr = lane + 32 * h2;
+      live[h2] = a < i1 && rr < r;
+      float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+      if (live[h2]) {
+        lo = g0k[2 * (a * r + rr)];
+        hi = g0k[2 * (a * r + rr) + 1];
+      }
+      const float gk[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) wv[h2][i] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4* q4 = reinterpret_cast<const float4*>(&tm.qs[c * 16]);
+        const float4 x0 = q4[0], x1 = q4[1], x2 = q4[2], x3 = q4[3];
+        const float qc[16] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w,
+                              x2.x, x2.y, x2.z, x2.w, x3.x, x3.y, x3.z, x3.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) wv[h2][i] = fmaf(qc[ord16<BITS>(i)], gk[c], wv[h2][i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) m[h2] = fmaxf(m[h2], fabsf(wv[h2][i]));
+    }
+    // group 0: bond rows < kGroupR (lanes < 8, first row), group 1: the rest
+    const unsigned g0 = live[0] && lane < kGroupR ? __float_as_uint(m[0]) : 0u;
+    const unsigned g1 = __float_as_uint(fmaxf(live[0] && lane >= kGroupR ? m[0] : 0.f, live[1] ? m[1] : 0.f));
+    const unsigned wmax[2] = {__reduce_max_sync(0xffffffffu, g0), __reduce_max_sync(0xffffffffu, g1)};
+    int wsum[2] = {0, 0};
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      if (!live[h2]) continue;
+      const int rr = lane + 32 * h2, grp = rr < kGroupR ? 0 : 1;
+      const float wq = pow2_sub_exp(__uint_as_float(wmax[grp]), kWBits<BITS>);
+      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int wint = __float2int_rn(wv[h2][i] * wq);
+        wsum[grp] += wint;
+        const int whi = wint >> 8;  // path 0: hi signed, lo unsigned
+        hi[i >> 2] |= (uint32_t)(whi & 0xFF) << (8 * (i & 3));
+        lo[i >> 2] |= (uint32_t)((wint - 256 * whi) & 0xFF) << (8 * (i & 3));
+      }
+      tm.wg.w[w_chunk(0, 0, r, rr, a, 0)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      tm.wg.w[w_chunk(0, 1, r, rr, a, 0)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    const int b0 = __reduce_add_sync(0xffffffffu, wsum[0]), b1 = __reduce_add_sync(0xffffffffu, wsum[1]);
+    if (lane < 2) {
+      tm.wmeta.beta[0][a][lane] = X * (lane == 0 ? b0 : b1);
+      tm.wmeta.cs[0][a][lane] = pow2_exp_sub(__uint_as_float(wmax[lane]), kWBits<BITS>);
+    }
+  }
+  __syncwarp();  // every lane's stores precede the leader's release on wbar
+}
+
+// ---- the fetcher (the warp after the producers) --------------------------------------------
+// Lane 0 keeps each team's next descriptors ready in its ring (ticket from the global counter,
+// then the work-list entry and the segment: dependent global loads of ~1 us that used to stall
+// the producer once per item), at most kFetchAhead ahead of what the producer has taken.  With
+// the in-kernel W image (kInW) the whole warp also computes item j + 1's W image as soon as the
+// consumers are past item j's K phase, and releases it on the team's wbar.
 template <int BITS, int G, int NT, bool ASYM, int TEAMS>
-__device__ void fetch(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args) {
+__device__ void fetch(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args, int lane) {
+  using TS = TeamSmem<G, NT, ASYM, kQOf<TEAMS>>;
+  constexpr bool INW = TS::kInW;
   int fk[TEAMS];
   bool done[TEAMS];
   bool waited = false;  // griddepcontrol.wait before the first ticket (the counter is shared with
-                        // the previous launch on these args)
+                        // the previous launch on these args) and before the first q read
   int left = TEAMS;
+  int kw = 0;           // kInW (one team): the next item whose W image is due
+  bool wdone = !INW;
 #pragma unroll
   for (int t = 0; t < TEAMS; ++t) {
     const int first = (int)blockIdx.x + t * (int)gridDim.x;
     done[t] = first >= args.nwork;
-    if (done[t]) {
-      sm.team[t].sub[0].nbt = 0;
-      --left;
-    } else {
-      load_sub<BITS>(sm.team[t].sub[0], args, first);
+    if (lane == 0) {
+      if (done[t]) sm.team[t].sub[0].nbt = 0;
+      else load_sub<BITS>(sm.team[t].sub[0], args, first);
+      st_release(&sm.team[t].fetched, 1);
     }
+    if (done[t]) --left;
     fk[t] = 1;
-    st_release(&sm.team[t].fetched, 1);
   }
-  while (left > 0) {
+  __syncwarp();
+  while (left > 0 || !wdone) {
     bool idle = true;
 #pragma unroll
     for (int t = 0; t < TEAMS; ++t) {
@@ -335,25 +446,49 @@ __device__ void fetch(AttnSmem<G, NT, ASYM, TEAMS>& sm, const dq_attn_args& args
         asm volatile("griddepcontrol.wait;\n" ::: "memory");
         waited = true;
       }
-      const int nx = TEAMS * (int)gridDim.x + atomicAdd(args.sched, 1);
+      int nx = 0;
+      if (lane == 0) nx = atomicAdd(args.sched, 1);
+      nx = TEAMS * (int)gridDim.x + __shfl_sync(0xffffffffu, nx, 0);
       SubItem& dst = sm.team[t].sub[fk[t] & (kSubRing - 1)];
       if (nx < args.nwork) {
-        load_sub<BITS>(dst, args, nx);
+        if (lane == 0) load_sub<BITS>(dst, args, nx);
       } else {
-        dst.nbt = 0;
+        if (lane == 0) dst.nbt = 0;
         done[t] = true;
         --left;
       }
-      st_release(&sm.team[t].fetched, ++fk[t]);
+      ++fk[t];
+      if (lane == 0) st_release(&sm.team[t].fetched, fk[t]);
+      __syncwarp();
+    }
+    if constexpr (INW) {
+      TS& tm = sm.team[0];
+      if (!wdone && kw < fk[0]) {
+        const SubItem& d = tm.sub[kw & (kSubRing - 1)];
+        if (d.nbt == 0) {
+          wdone = true;
+        } else if (kw == 0 || mbar_test(&tm.wfree, (uint32_t)((kw - 1) & 1))) {
+          if (!waited) {
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");  // q comes from the previous kernel
+            waited = true;
+          }
+          compute_w<BITS>(tm, args, d, lane);
+          if (lane == 0) mbar_arrive(&tm.wbar);
+          ++kw;
+          idle = false;
+        }
+      }
     }
     if (idle) __nanosleep(64);
   }
   // retire: the last CTA to finish drawing resets the counters for the next launch
   if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  __threadfence();
-  if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
-    args.sched[0] = 0;
-    args.sched[1] = 0;
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
+      args.sched[0] = 0;
+      args.sched[1] = 0;
+    }
   }
 }
 
@@ -483,6 +618,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       for (int s = 0; s < kSubRing; ++s) mbar_init(&sm.team[t].descfull[s], 1);
       for (int s = 0; s < kQOf<TEAMS>; ++s) mbar_init(&sm.team[t].sqbar[s], 1);
       mbar_init(&sm.team[t].wbar, 1);
+      mbar_init(&sm.team[t].wfree, 1);
       mbar_init(&sm.team[t].g0bar, 1);
       sm.team[t].started = 0;  // item 0's K phase: issue it whole before the consumers arrive
       sm.team[t].fetched = 0;
@@ -501,18 +637,24 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     // prepare kernel, so no griddepcontrol.wait before the first stages); the next warp
     // fetches the work items
     if (warp < TEAMS) produce<BITS, G, NT, ASYM, TEAMS>(sm, args, warp);  // the whole warp, converged
-    else if (lane == 0) fetch<BITS, G, NT, ASYM, TEAMS>(sm, args);
+    else fetch<BITS, G, NT, ASYM, TEAMS>(sm, args, lane);  // the whole warp
     return;
   }
   TeamSmem<G, NT, ASYM, kQOf<TEAMS>>& tm = sm.team[team];
+  constexpr bool INW = TeamSmem<G, NT, ASYM, kQOf<TEAMS>>::kInW;
 
   if (tid == 0) {
     mbar_wait(&tm.descfull[0], 0);
+    if constexpr (INW) {
+      if (tm.sub[0].nbt > 0) issue_g0v16(tm, tm.sub[0]);
+    }
     // programmatic dependent launch: everything above overlapped the prepare kernel; its
     // output (the per-segment W images) is read from here on
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the combine may be scheduled
-    if (tm.sub[0].nbt > 0) issue_wimg(tm, args, tm.sub[0]);
+    if constexpr (!INW) {
+      if (tm.sub[0].nbt > 0) issue_wimg(tm, args, tm.sub[0]);
+    }
   }
 
   int st = 0;  // the team's running stage index (identical in every thread of the team)
@@ -651,8 +793,15 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     team_sync(team);
     if (tid == 0) {
       const int jn = j + 1;
+      if constexpr (INW) {
+        mbar_arrive(&tm.wfree);
+        mbar_wait(&tm.g0bar, (uint32_t)(j & 1));
+      }
       mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg(tm, args, tm.sub[jn % kSubRing]);
+      if (tm.sub[jn % kSubRing].nbt > 0) {
+        if constexpr (INW) issue_g0v16(tm, tm.sub[jn % kSubRing]);
+        else issue_wimg(tm, args, tm.sub[jn % kSubRing]);
+      }
     }
     continue;
 #endif
@@ -677,7 +826,8 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
       if (lane == 0) tm.rowmax[h][warp] = m;
     }
     team_sync(team);  // every warp is past phase 1: the W buffer is dead
-    if (lane == 0 && warp < i1) {  // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
+    if (INW && tid == 0) mbar_arrive(&tm.wfree);  // the fetcher may write the next item's W image
+    if (!INW && lane == 0 && warp < i1) {  // prefetch the fp32 G0v for the epilogue into it (+ the V channel table)
       // one copy per a, issued by warp a, into blocks of 2r + 1 float4s: the epilogue's lanes
       // tid4 = 0..3 read a = 2 tid4 + aa, and the pad puts their blocks 32 bytes apart in the
       // banks (an unpadded 2r-float4 stride maps all four onto the same banks: a 4-way
@@ -844,7 +994,7 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     for (int h = 0; h < G; ++h)
 #pragma unroll
       for (int k = 0; k < 16; ++k) part[h][k] = 0.f;
-    mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // fp32 G0v [a][rr][c] (normalised), in the W buffer
+    mbar_wait(&tm.g0bar, (uint32_t)(j & 1));  // G0v [a][rr][c] (normalised): fp32 in the W buffer, or fp16 (kInW)
     const float4* g0v = tm.wg.g0v;
 #ifdef DQ_ATTN_NULL_FOLD  // measurement only: no G0v fold (wrong results), Y still consumed
 #pragma unroll
@@ -865,8 +1015,20 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
         for (int aa = 0; aa < 2; ++aa) {
           const int a = 2 * tid4 + aa;
           if (a < i1) {
-            const float4 g_lo = g0v[a * (2 * r + 1) + 2 * rr], g_hi = g0v[a * (2 * r + 1) + 2 * rr + 1];
-            const float gc[8] = {g_lo.x, g_lo.y, g_lo.z, g_lo.w, g_hi.x, g_hi.y, g_hi.z, g_hi.w};
+            float gc[8];
+            if constexpr (INW) {
+              const uint4 gh = tm.g0v16[a * (r + 1) + rr];
+              const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gh.x));
+              const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&gh.y));
+              const float2 g45 = __half22float2(*reinterpret_cast<const __half2*>(&gh.z));
+              const float2 g67 = __half22float2(*reinterpret_cast<const __half2*>(&gh.w));
+              gc[0] = g01.x, gc[1] = g01.y, gc[2] = g23.x, gc[3] = g23.y;
+              gc[4] = g45.x, gc[5] = g45.y, gc[6] = g67.x, gc[7] = g67.y;
+            } else {
+              const float4 g_lo = g0v[a * (2 * r + 1) + 2 * rr], g_hi = g0v[a * (2 * r + 1) + 2 * rr + 1];
+              gc[0] = g_lo.x, gc[1] = g_lo.y, gc[2] = g_lo.z, gc[3] = g_lo.w;
+              gc[4] = g_hi.x, gc[5] = g_hi.y, gc[6] = g_hi.z, gc[7] = g_hi.w;
+            }
 #pragma unroll
             for (int h = 0; h < G; ++h) {
               const float y0 = ASYM ? accv[t][h][aa] * s0 : accv[t][h][aa];
@@ -891,7 +1053,10 @@ __global__ void __launch_bounds__(kCtaThreadsOf<TEAMS>, kCtasPerSm<G, TEAMS>) de
     if (tid == 0) {
       const int jn = j + 1;
       mbar_wait(&tm.descfull[jn % kSubRing], (uint32_t)((jn / kSubRing) & 1));
-      if (tm.sub[jn % kSubRing].nbt > 0) issue_wimg(tm, args, tm.sub[jn % kSubRing]);
+      if (tm.sub[jn % kSubRing].nbt > 0) {
+        if constexpr (INW) issue_g0v16(tm, tm.sub[jn % kSubRing]);  // the fetcher writes W
+        else issue_wimg(tm, args, tm.sub[jn % kSubRing]);
+      }
     }
     if (tid < G * 8 * NT) {
       (&tm.gamma[0][0][0])[tid] = 0;
