@@ -7,7 +7,7 @@
 //   Y[(r,e), (h,l,a)]  = sum_b code_v[(r,e), b] . P_l[b, (h,a)]          M = 128 (r,e), N = 128, K = b
 //
 // A operands (the codes) are widened from the shared-memory ring into tensor memory by the
-// consumer warps (tcgen05.st: lane = row, 4 K-bytes per column); B operands sit in shared
+// widening warps (tcgen05.st: lane = row, 4 K-bytes per column); B operands sit in shared
 // memory as K-major core matrices: the W image streams through the ring in 16 KB slices of
 // 8 bond rows next to the K codes of the same bond rows (so no 128 KB W buffer: the ring is
 // 5 x 32 KB deep), P is written by the softmax.  One elected lane of the MMA warp issues
@@ -16,11 +16,13 @@
 //
 // Per work item (<= 256 rows b = 2 M-blocks): 8 K stages (8 bond rows x all tiles + W slice)
 // -> S in TMEM (2 x 128 columns) -> softmax from TMEM -> P limbs in shared memory -> 8 V
-// stages (one M-block of 8 bond rows x all tiles each) -> Y per stage (128 columns, double-
-// buffered in the S columns) -> the epilogue folds Y with G0v on CUDA cores while the next
-// stage's UMMAs run.  TMEM: 4 A buffers [0, 256), S / Y [256, 512).  16 consumer warps (4
-// warpgroups: a warp reaches TMEM lanes 32 (warp % 4) ..): K widening by (M-block, bond-row
-// half), softmax by (M-block, head half), V widening by tile, the Y fold by head pair.
+// stages (one M-block of 8 bond rows x all tiles each) -> Y per stage (128 columns) -> the
+// epilogue folds Y with G0v on CUDA cores.  Items overlap: the ring carries item j+1's K
+// stages next to item j's V stages, so the next S accumulates in its own columns while the
+// math warps run item j's softmax and fold.  TMEM: 2 A buffers [0, 128), S [128, 384), Y
+// [384, 512).  16 math warps (4 warpgroups: a warp reaches TMEM lanes 32 (warp % 4) ..):
+// softmax by (M-block, head half), the Y fold by head pair; a widening warpgroup turns every
+// ring stage into a TMEM A operand.
 //
 // Numerics (exact integer products, as path 0): codes excess-coded u8; W = two signed 8-bit
 // limbs of a 14-bit fixed point with one scale per (h, a) column; P = exp2(s - m_h) as a
@@ -44,8 +46,12 @@ constexpr int kGqProducer = kGqWarps + kGqWide;    // producer warp (20), then t
 constexpr int kGqMma = kGqProducer + 1;
 constexpr int kGqThreads = kGqCons + kGqWide * 32 + 64;
 constexpr int kGqTmemUsers = kGqCons + kGqWide * 32 + 32;  // threads that touch TMEM (final barrier)
-constexpr int kGqNumA = 4;                         // TMEM A buffers (64 columns each)
-constexpr uint32_t kGqColA = 0, kGqColSY = 256;    // A: 4 x 64 columns; S / Y: 2 x 128 columns
+constexpr int kGqNumA = 2;                         // TMEM A buffers (64 columns each)
+constexpr uint32_t kGqColA = 0, kGqColS = 128, kGqColY = 384;  // A: 2 x 64 columns; S: 2 x 128; Y: 128
+#ifndef DQ_GQ_KA
+#define DQ_GQ_KA 8
+#endif
+constexpr int kGqKA = DQ_GQ_KA;  // K stages of item j+1 ahead of item j's first V stage
 constexpr int kGqPBits = 15;
 constexpr int kGqVTileBytes = 8 * 16 * kI2Pad / 2;  // V stage per tile: 8 bond rows x 16 e x 64 b
 
@@ -67,7 +73,7 @@ struct GqSmem {
   SubItem sub[kSubRing];
   uint64_t full[kGqStages], empty[kGqStages];
   uint64_t g0bar, descfull[kSubRing];
-  uint64_t afull[kGqNumA], afree[kGqNumA], sfull, pfull, yfull[2], yfree[2];
+  uint64_t afull[kGqNumA], afree[kGqNumA], sfull, sfree, pfull, yfull, yfree;
   uint32_t tmem;
 };
 static_assert(sizeof(GqSmem) <= 232448, "path-2 shared memory exceeds the 227 KB opt-in limit");
@@ -81,6 +87,29 @@ __device__ __forceinline__ void gq_load_sub(SubItem& d, const dq_attn_args& a, i
   d.RV = 8;
   d.nslices = d.r / 8;
   d.stages = d.nK + d.nslices;
+}
+
+// Stage i of block j: nkn K stages of item j+1 (0 when there is none) and nv V stages of item
+// j: the first min(kGqKA, nkn) K stages, then V and K alternately, then the rest.  Returns
+// whether it is a K stage; idx = its index among the item's K (or V) stages.
+__device__ __forceinline__ bool gq_block_stage(int i, int nkn, int nv, int& idx) {
+  const int ka = min(kGqKA, nkn);
+  if (i < ka) {
+    idx = i;
+    return true;
+  }
+  const int t = i - ka, m = min(nv, nkn - ka);
+  if (t < 2 * m) {
+    idx = (t & 1) ? ka + (t >> 1) : (t >> 1);
+    return (t & 1) != 0;
+  }
+  const int u = t - 2 * m;
+  if (nv > m) {
+    idx = m + u;
+    return false;
+  }
+  idx = ka + m + u;
+  return true;
 }
 
 // stage `st` of item `d` (the k-th item of this CTA) into ring slot `buf` (one thread)
@@ -175,12 +204,11 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       mbar_init(&sm.afull[b], kGqWide);
       mbar_init(&sm.afree[b], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.yfull[b], 1);
-      mbar_init(&sm.yfree[b], kGqWarps);
-    }
     mbar_init(&sm.sfull, 1);
+    mbar_init(&sm.sfree, kGqWarps);
     mbar_init(&sm.pfull, 1);
+    mbar_init(&sm.yfull, 1);
+    mbar_init(&sm.yfree, kGqWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (tid < kGqG * 8) {
@@ -197,38 +225,62 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
 
+  // Stage order (producer, widening warps and MMA warp walk the same sequence): item 0's K
+  // stages, then per item j one block of item j+1's K stages interleaved with item j's V stages
+  // (gq_block_stage).  S has its own columns, so item j+1's K UMMAs run while the math warps
+  // compute item j's softmax and fold its Y.
+
   if (warp == kGqProducer) {
-    // ---- producer: descriptors and stages of this CTA's items, in order --------------------
+    // ---- producer: descriptors and stages of this CTA's items, in sequence order ----------
     if (lane == 0) {
       // the W images come from the prepare kernel, and the ticket counter is shared with the
       // previous launch on these args: wait for both grids before the first copy
       asm volatile("griddepcontrol.wait;\n" ::: "memory");
-      SubItem nd;
-      bool have = (int)blockIdx.x < args.nwork;
-      if (have) gq_load_sub(nd, args, blockIdx.x);
       int g = 0;
-      for (int k = 0;; ++k) {
+      auto put = [&](int k, const SubItem* d) {
         const int ds = k % kSubRing;
-        if (!have) {
-          sm.sub[ds].nbt = 0;
-          mbar_arrive(&sm.descfull[ds]);
-          break;
-        }
-        const SubItem d = nd;
-        sm.sub[ds] = d;
+        if (d) sm.sub[ds] = *d;
+        else sm.sub[ds].nbt = 0;
         mbar_arrive(&sm.descfull[ds]);
-        bool nhave = false;
-        for (int ls = 0; ls < d.stages; ++ls, ++g) {
-          const int slot = g % kGqStages;
-          if (g >= kGqStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kGqStages - 1) & 1));
-          gq_issue_stage(sm, args, d, k, ls, sm.ring[slot], &sm.full[slot]);
-          if (ls == min(2, d.stages - 1)) {
-            const int nxt = (int)gridDim.x + atomicAdd(args.sched, 1);
-            nhave = nxt < args.nwork;
-            if (nhave) gq_load_sub(nd, args, nxt);
-          }
+      };
+      auto ticket = [&](SubItem& nd) {
+        const int nxt = (int)gridDim.x + atomicAdd(args.sched, 1);
+        if (nxt >= args.nwork) return false;
+        gq_load_sub(nd, args, nxt);
+        return true;
+      };
+      auto issue = [&](const SubItem& d, int k, int st) {
+        const int slot = g % kGqStages;
+        if (g >= kGqStages) mbar_wait(&sm.empty[slot], (uint32_t)((g / kGqStages - 1) & 1));
+        gq_issue_stage(sm, args, d, k, st, sm.ring[slot], &sm.full[slot]);
+        ++g;
+      };
+      SubItem cur, nx, nn;
+      if ((int)blockIdx.x >= args.nwork) {
+        put(0, nullptr);
+      } else {
+        gq_load_sub(cur, args, blockIdx.x);
+        put(0, &cur);
+        bool hn = false;
+        for (int ks = 0; ks < cur.nK; ++ks) {
+          issue(cur, 0, ks);
+          if (ks == min(2, cur.nK - 1)) hn = ticket(nx);
         }
-        have = nhave;
+        for (int j = 0;; ++j) {
+          put(j + 1, hn ? &nx : nullptr);
+          const int nkn = hn ? nx.nK : 0, n = nkn + cur.nslices;
+          bool hnn = false;
+          for (int i = 0; i < n; ++i) {
+            int idx;
+            if (gq_block_stage(i, nkn, cur.nslices, idx)) issue(nx, j + 1, idx);
+            else issue(cur, j, cur.nK + idx);
+            if (hn && i == min(2, n - 1)) hnn = ticket(nn);
+          }
+          if (!hn) break;
+          cur = nx;
+          nx = nn;
+          hn = hnn;
+        }
       }
       __threadfence();
       if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
@@ -244,86 +296,116 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     // one elected lane issues each UMMA / commit (operands stay in uniform registers: no
     // per-UMMA register-to-uniform moves on the issue path)
     const bool leader = elect_one();
+#ifdef DQ_GQ_MMA_SLEEP  // measurement: the MMA warp suspends in its waits instead of spinning
+    auto mwait = [](uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); };
+#else
+    auto mwait = [](uint64_t* bar, uint32_t parity) { mbar_wait_spin(bar, parity); };
+#endif
     const uint32_t id_k = tc_idesc(128, 128, 0, 1);  // codes u8 x W limbs s8
     const uint32_t id_v = tc_idesc(128, 128, 0, 0);  // codes u8 x P limbs u8
     const uint64_t pdesc = tc_sdesc(sm.pr.pb, 128, (kCB / 16) * 128);  // P: b chunks 128 B, (h, limb) groups 2 KB
-    int na = 0;              // A-buffer uses = ring stages consumed
-    int uy[2] = {0, 0};      // Y-buffer uses
-    for (int j = 0;; ++j) {
-      mbar_wait_spin(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
-      const int nbt = sm.sub[j % kSubRing].nbt, nK = sm.sub[j % kSubRing].nK, nV = sm.sub[j % kSubRing].nslices;
-      if (nbt == 0) break;
-      // S occupies the Y columns: the previous item's epilogue must have read both buffers
-      for (int b = 0; b < 2; ++b)
-        if (uy[b] > 0) mbar_wait_spin(&sm.yfree[b], (uint32_t)((uy[b] - 1) & 1));
+    int na = 0;  // A-buffer uses = ring stages consumed
+    int uy = 0;  // Y uses
+    // K stage ks of an item of nbt tiles into S
+    auto mma_k = [&](int nbt, int ks) {
+      const int ab = na % kGqNumA;
+      mwait(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
       tc_fence_after();
-      for (int ks = 0; ks < nK; ++ks, ++na) {
-        const int ab = na % kGqNumA;
-        mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
-        tc_fence_after();
-        // this stage's W slice: N rows (h*2 + limb)*8 + a in 16 core-matrix groups 1 KB apart,
-        // bond rows 128 B apart; k-step kk (2 bond rows) = +256 B = +16 in the address field
-        const uint64_t bdesc = tc_sdesc(sm.ring[na % kGqStages] + 16384, 128, 1024);
-        const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64);
-        const uint32_t acc0 = ks ? 1u : 0u;
-        if (leader) {
+      // this stage's W slice: N rows (h*2 + limb)*8 + a in 16 core-matrix groups 1 KB apart,
+      // bond rows 128 B apart; k-step kk (2 bond rows) = +256 B = +16 in the address field
+      const uint64_t bdesc = tc_sdesc(sm.ring[na % kGqStages] + 16384, 128, 1024);
+      const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64);
+      const uint32_t acc0 = ks ? 1u : 0u;
+      if (leader) {
 #ifndef DQ_GQ_NULL_MMA  // measurement only: no UMMAs (the commits still signal)
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            tc_mma_ts(tmem + kGqColSY, a0 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
-            if (nbt > 2) tc_mma_ts(tmem + kGqColSY + 128, a0 + 32 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
-          }
-#endif
-          tc_commit(&sm.afree[ab]);
-          tc_commit(&sm.empty[na % kGqStages]);  // the W slice has been read
+        for (int kk = 0; kk < 4; ++kk) {
+          tc_mma_ts(tmem + kGqColS, a0 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
+          if (nbt > 2) tc_mma_ts(tmem + kGqColS + 128, a0 + 32 + kk * 8, bdesc + kk * 16, id_k, kk ? 1u : acc0);
         }
-        __syncwarp();
+#endif
+        tc_commit(&sm.afree[ab]);
+        tc_commit(&sm.empty[na % kGqStages]);  // the W slice has been read
       }
+      __syncwarp();
+      ++na;
+    };
+    // V stage of an item of nbt tiles into Y
+#ifdef DQ_GQ_MMAWAIT  // measurement only: per item, V-phase span (slot 4), A waits (6), Y waits (7)
+    int64_t tv0 = 0, wa = 0, wy = 0;
+#define GQ_T0(x) const int64_t x = global_ns()
+#define GQ_ACC(acc, x) acc += global_ns() - x
+#else
+#define GQ_T0(x)
+#define GQ_ACC(acc, x)
+#endif
+    auto mma_v = [&](int nbt) {
+      const int ab = na % kGqNumA;
+      GQ_T0(t0);
+      mwait(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
+      GQ_ACC(wa, t0);
+      GQ_T0(t1);
+      if (uy > 0) mwait(&sm.yfree, (uint32_t)((uy - 1) & 1));
+      GQ_ACC(wy, t1);
+      tc_fence_after();
+      const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64), d0 = tmem + kGqColY;
+      if (leader) {
+#ifndef DQ_GQ_NULL_MMA
+        // 32 rows b per k-step: +256 B of P = +16 in the address field
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          if (kk < 2 * nbt) tc_mma_ts(d0, a0 + kk * 8, pdesc + kk * 16, id_v, kk ? 1u : 0u);
+#endif
+        tc_commit(&sm.afree[ab]);
+        tc_commit(&sm.empty[na % kGqStages]);
+        tc_commit(&sm.yfull);
+      }
+      __syncwarp();
+      ++na;
+      ++uy;
+    };
+    mwait(&sm.descfull[0], 0u);
+    int nbt = sm.sub[0].nbt, nv = sm.sub[0].nslices;
+    if (nbt > 0) {
+      const int nk = sm.sub[0].nK;
+      tc_fence_after();
+      for (int ks = 0; ks < nk; ++ks) mma_k(nbt, ks);
       if (leader) tc_commit(&sm.sfull);
       __syncwarp();
-      mbar_wait_spin(&sm.pfull, (uint32_t)(j & 1));  // P limbs in shared memory, S read
-      tc_fence_after();
-#ifdef DQ_GQ_MMAWAIT  // measurement only: V phase of the MMA warp: span (slot 4) and A / Y waits (slot 6, 7)
-      const int64_t v0 = global_ns();
-      int64_t wa = 0, wy = 0;
-#endif
-      for (int vs = 0; vs < nV; ++vs, ++na) {
-        const int ab = na % kGqNumA, yb = vs & 1;
+      for (int j = 0;; ++j) {
+        const int dn = (j + 1) % kSubRing;
+        mwait(&sm.descfull[dn], (uint32_t)(((j + 1) / kSubRing) & 1));
+        const int nbn = sm.sub[dn].nbt, nkn = nbn ? sm.sub[dn].nK : 0, nvn = sm.sub[dn].nslices;
+        for (int i = 0; i < nkn + nv; ++i) {
+          int idx;
+          if (gq_block_stage(i, nkn, nv, idx)) {
+            // S is rewritten: the math warps must have read item j's S
+            if (idx == 0) mwait(&sm.sfree, (uint32_t)(j & 1));
+            mma_k(nbn, idx);
+            if (idx == nkn - 1) {
+              if (leader) tc_commit(&sm.sfull);
+              __syncwarp();
+            }
+          } else {
+            if (idx == 0) mwait(&sm.pfull, (uint32_t)(j & 1));  // P limbs of item j
 #ifdef DQ_GQ_MMAWAIT
-        int64_t w0 = global_ns();
-        mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
-        wa += global_ns() - w0;
-        w0 = global_ns();
-        if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
-        wy += global_ns() - w0;
-#else
-        mbar_wait_spin(&sm.afull[ab], (uint32_t)((na / kGqNumA) & 1));
-        if (uy[yb] > 0) mbar_wait_spin(&sm.yfree[yb], (uint32_t)((uy[yb] - 1) & 1));
+            if (idx == 0) tv0 = global_ns(), wa = 0, wy = 0;
 #endif
-        tc_fence_after();
-        const uint32_t a0 = tmem + kGqColA + (uint32_t)(ab * 64), d0 = tmem + kGqColSY + (uint32_t)(yb * 128);
-        if (leader) {
-#ifndef DQ_GQ_NULL_MMA
-          // 32 rows b per k-step: +256 B of P = +16 in the address field
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            if (kk < 2 * nbt) tc_mma_ts(d0, a0 + kk * 8, pdesc + kk * 16, id_v, kk ? 1u : 0u);
-#endif
-          tc_commit(&sm.afree[ab]);
-          tc_commit(&sm.empty[na % kGqStages]);
-          tc_commit(&sm.yfull[yb]);
+            mma_v(nbt);
+          }
         }
-        __syncwarp();
-        ++uy[yb];
-      }
 #ifdef DQ_GQ_MMAWAIT
-      if (leader && args.trace) {
-        const int it = sm.sub[j % kSubRing].item;
-        args.trace[(size_t)it * 8 + 4] = global_ns() - v0;
-        args.trace[(size_t)it * 8 + 6] = wa;
-        args.trace[(size_t)it * 8 + 7] = wy;
-      }
+        if (leader && args.trace) {
+          const int it = sm.sub[j % kSubRing].item;
+          args.trace[(size_t)it * 8 + 4] = global_ns() - tv0;
+          args.trace[(size_t)it * 8 + 6] = wa;
+          args.trace[(size_t)it * 8 + 7] = wy;
+        }
 #endif
+        if (!nbn) break;
+        nbt = nbn;
+        nv = nvn;
+      }
     }
     __syncwarp();
     named_sync2(kGqTmemUsers);  // the other warps' last TMEM accesses are done
@@ -333,65 +415,125 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   }
 
   if (warp >= kGqWarps) {
-    // ---- widening warpgroup: every K and V stage, in ring order, into the TMEM A buffers ----
-    // (warp & 3 = its TMEM lane quadrant); it runs ahead of the math warps by up to 4 A buffers,
-    // so the next item's first K stages are widened while the math warps fold this item's Y
+    // ---- widening warpgroup: every K and V stage, in sequence order, into the TMEM A buffers
+    // (warp & 3 = its TMEM lane quadrant)
     const int q = warp & 3;
     const int lane_in = 32 * q + lane;
     const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-    int st = 0, na = 0;
-    for (int j = 0;; ++j) {
-      mbar_wait(&sm.descfull[j % kSubRing], (uint32_t)((j / kSubRing) & 1));
-      const SubItem d = sm.sub[j % kSubRing];
-      if (d.nbt == 0) break;
-      const int nbt = d.nbt, nmb = (nbt + 1) / 2;
-      for (int ks = 0; ks < d.nK + d.nslices; ++ks, ++st, ++na) {
-        const int slot = st % kGqStages, ab = na % kGqNumA;
-        mbar_wait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
-        if (na >= kGqNumA) mbar_wait(&sm.afree[ab], (uint32_t)((na / kGqNumA - 1) & 1));
-        if (ks < d.nK) {  // K stage: 8 bond rows of rows b = 128 mb + lane_in, both M-blocks
-          for (int mb = 0; mb < nmb; ++mb) {
-            const int jt = 2 * mb + (q >> 1), b_in = 32 * (q & 1) + lane;
-            const unsigned char* tile = sm.ring[slot] + jt * 8 * kI2Pad * RB;
-            const bool live = jt < nbt;
+    int st = 0;  // ring stages = A-buffer uses
+#ifdef DQ_GQ_WIDETRACE  // measurement only: per item, V-stage widening span (slot 4), ring waits (6), A waits (7)
+    int64_t tv0 = 0, tv1 = 0, wf = 0, wa = 0;
+#endif
+    auto widen = [&](int nbt, bool kstage) {
+      const int slot = st % kGqStages, ab = st % kGqNumA;
+#ifdef DQ_GQ_WIDETRACE
+      const int64_t t0 = global_ns();
+      if (!kstage && tv0 == 0) tv0 = t0;
+#endif
+      mbar_wait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
+#ifdef DQ_GQ_WIDETRACE
+      const int64_t t1 = global_ns();
+      if (!kstage) wf += t1 - t0;
+#endif
+      if (st >= kGqNumA) mbar_wait(&sm.afree[ab], (uint32_t)((st / kGqNumA - 1) & 1));
+#ifdef DQ_GQ_WIDETRACE
+      if (!kstage) wa += global_ns() - t1;
+#endif
+      // all of the stage's shared-memory reads first, then the nibble splits and TMEM stores
+      // (a tcgen05.st is a memory barrier to the compiler: loads are not hoisted across it)
+      if (kstage) {  // K stage: 8 bond rows of rows b = 128 mb + lane_in, both M-blocks
+        const int b_in = 32 * (q & 1) + lane;
+        uint2 w[2][8];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              uint32_t v[16];
+        for (int mb = 0; mb < 2; ++mb) {
+          const int jt = 2 * mb + (q >> 1);
+          const unsigned char* tile = sm.ring[slot] + jt * 8 * kI2Pad * RB;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int rl = 4 * half + i;  // rr & 3 = i (stages start at multiples of 8)
-                uint2 w2 = make_uint2(0u, 0u);
-                if (live) w2 = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ (i * 4))) * RB);
-                v[4 * i] = w2.x & 0x0F0F0F0Fu;
-                v[4 * i + 1] = (w2.x >> 4) & 0x0F0F0F0Fu;
-                v[4 * i + 2] = w2.y & 0x0F0F0F0Fu;
-                v[4 * i + 3] = (w2.y >> 4) & 0x0F0F0F0Fu;
-              }
-              tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + mb * 32 + half * 16), v);
-            }
+          for (int rl = 0; rl < 8; ++rl) {  // rr & 3 = rl & 3 (stages start at multiples of 8)
+            w[mb][rl] = make_uint2(0u, 0u);
+            if (jt < nbt) w[mb][rl] = *reinterpret_cast<const uint2*>(tile + (rl * kI2Pad + (b_in ^ ((rl & 3) * 4))) * RB);
           }
-        } else {  // V stage: row (r_local, e) = lane_in of every tile
-          for (int t = 0; t < nbt; ++t) {
-            const unsigned char* src = sm.ring[slot] + t * kGqVTileBytes + lane_in * 32;
-            const uint4 c0 = *reinterpret_cast<const uint4*>(src);
-            const uint4 c1 = *reinterpret_cast<const uint4*>(src + 16);
-            const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        }
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {
+          if (mb == 1 && nbt <= 2) break;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
             uint32_t v[16];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              v[2 * k] = wv[k] & 0x0F0F0F0Fu;
-              v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
+            for (int i = 0; i < 4; ++i) {
+              const uint2 w2 = w[mb][4 * half + i];
+              v[4 * i] = w2.x & 0x0F0F0F0Fu;
+              v[4 * i + 1] = (w2.x >> 4) & 0x0F0F0F0Fu;
+              v[4 * i + 2] = w2.y & 0x0F0F0F0Fu;
+              v[4 * i + 3] = (w2.y >> 4) & 0x0F0F0F0Fu;
             }
-            tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + t * 16), v);
+            tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + mb * 32 + half * 16), v);
           }
         }
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&sm.afull[ab]);
-          mbar_arrive(&sm.empty[slot]);
+      } else {  // V stage: row (r_local, e) = lane_in of every tile
+        uint4 c[4][2];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const unsigned char* src = sm.ring[slot] + t * kGqVTileBytes + lane_in * 32;
+          c[t][0] = c[t][1] = make_uint4(0u, 0u, 0u, 0u);
+          if (t < nbt) {
+            c[t][0] = *reinterpret_cast<const uint4*>(src);
+            c[t][1] = *reinterpret_cast<const uint4*>(src + 16);
+          }
         }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (t >= nbt) break;
+          const uint32_t wv[8] = {c[t][0].x, c[t][0].y, c[t][0].z, c[t][0].w,
+                                  c[t][1].x, c[t][1].y, c[t][1].z, c[t][1].w};
+          uint32_t v[16];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[2 * k] = wv[k] & 0x0F0F0F0Fu;
+            v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
+          }
+          tc_st16(tmem + lane_addr + kGqColA + (uint32_t)(ab * 64 + t * 16), v);
+        }
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sm.afull[ab]);
+        mbar_arrive(&sm.empty[slot]);
+      }
+      ++st;
+#ifdef DQ_GQ_WIDETRACE
+      if (!kstage) tv1 = global_ns();
+#endif
+    };
+    mbar_wait(&sm.descfull[0], 0u);
+    int nbt = sm.sub[0].nbt, nv = sm.sub[0].nslices;
+    if (nbt > 0) {
+      const int nk = sm.sub[0].nK;
+      for (int ks = 0; ks < nk; ++ks) widen(nbt, true);
+      for (int j = 0;; ++j) {
+        const int dn = (j + 1) % kSubRing;
+        mbar_wait(&sm.descfull[dn], (uint32_t)(((j + 1) / kSubRing) & 1));
+        const int nbn = sm.sub[dn].nbt, nkn = nbn ? sm.sub[dn].nK : 0, nvn = sm.sub[dn].nslices;
+        for (int i = 0; i < nkn + nv; ++i) {
+          int idx;
+          const bool kstage = gq_block_stage(i, nkn, nv, idx);
+          widen(kstage ? nbn : nbt, kstage);
+        }
+#ifdef DQ_GQ_WIDETRACE
+        if (warp == kGqWarps && lane == 0 && args.trace) {
+          const int it = sm.sub[j % kSubRing].item;
+          args.trace[(size_t)it * 8 + 4] = tv1 - tv0;
+          args.trace[(size_t)it * 8 + 6] = wf;
+          args.trace[(size_t)it * 8 + 7] = wa;
+        }
+        tv0 = wf = wa = 0;
+#endif
+        if (!nbn) break;
+        nbt = nbn;
+        nv = nvn;
       }
     }
     tc_fence_before();
@@ -410,7 +552,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
   const int mbk = wg & 1, hh = wg >> 1;  // K / softmax: M-block (rows b) and half (bond rows / heads 4hh..4hh+3)
   const int lane_in = 32 * q + lane;     // TMEM lane
   const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
-  int uyc[2] = {0, 0};
+  int uyc = 0;
   if (tid == 0) {
     // the combine may be scheduled once this grid's prerequisites (prepare kernel, producers of
     // q) have completed: it reads q and the tail before waiting for this grid
@@ -437,14 +579,11 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     // this thread's row b for the softmax: tile jt, row b_in inside it
     const int jt = 2 * mbk + (q >> 1);
     const int b_in = 32 * (q & 1) + lane;
-    stamp(1);
 
     // ---- softmax of the item straight from S in TMEM (this thread = row b) -----------------
     cwait(&sm.sfull, (uint32_t)(j & 1));  // all K UMMAs done (the W metadata landed with stage 0)
     tc_fence_after();
-#ifdef DQ_GQ_SMTRACE  // profiling build: softmax sub-phases in the MMA warp's trace slots
-    stamp(7);
-#endif
+    stamp(1);
     const WMeta<kGqG>& wm = sm.wmeta[j & 1];
     // this thread: row b of M-block mbk, heads 4hh .. 4hh+3 (columns 32hh .. 32hh+31)
     const bool row_ok = mbk < nmb && jt < nbt && d.wb0 + jt * kI2Pad + b_in < d.i2;
@@ -454,7 +593,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       int acc[4][16];
 #pragma unroll
       for (int hl = 0; hl < 4; ++hl)
-        tc_ld16(tmem + lane_addr + kGqColSY + (uint32_t)(mbk * 128 + (4 * hh + hl) * 16), acc[hl]);
+        tc_ld16(tmem + lane_addr + kGqColS + (uint32_t)(mbk * 128 + (4 * hh + hl) * 16), acc[hl]);
       tc_wait_ld();
 #pragma unroll
       for (int hl = 0; hl < 4; ++hl)
@@ -469,6 +608,8 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       for (int i = 0; i < 32; ++i) s[i] = -INFINITY;
     }
     tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.sfree);  // S read: the next item's K UMMAs may overwrite it
     {  // row maxima per head over (a, b): per-thread over a, then a reduce-scatter (lane & 3 = head)
       float m4[4];
 #pragma unroll
@@ -494,7 +635,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       if (lane < 4) sm.rowmax[hh][mbk * 4 + q][lane] = m;  // lane = head - 4hh
     }
     named_sync(kGqCons);
-#ifdef DQ_GQ_SMTRACE
+#ifdef DQ_GQ_SMTRACE  // profiling build: softmax sub-phases in the spare trace slots
     stamp(4);
 #endif
     float mh[4];
@@ -555,9 +696,8 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
 #pragma unroll
       for (int c = 0; c < 8; ++c) o[hl][c] = 0.f;
     auto fold_y = [&](int vs) {
-      const int yb = vs & 1;
-      cwait(&sm.yfull[yb], (uint32_t)(uyc[yb] & 1));
-      ++uyc[yb];
+      cwait(&sm.yfull, (uint32_t)(uyc & 1));
+      ++uyc;
       tc_fence_after();
       float yf[2][8];
       {
@@ -565,7 +705,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
 #ifndef DQ_GQ_NULL_YLD  // measurement only: no Y reads from TMEM
 #pragma unroll
         for (int hl = 0; hl < 2; ++hl)
-          tc_ld16(tmem + lane_addr + kGqColSY + (uint32_t)(yb * 128 + (2 * wg + hl) * 16), y[hl]);
+          tc_ld16(tmem + lane_addr + kGqColY + (uint32_t)((2 * wg + hl) * 16), y[hl]);
         tc_wait_ld();
 #else
 #pragma unroll
@@ -575,7 +715,7 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
 #endif
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.yfree[yb]);
+        if (lane == 0) mbar_arrive(&sm.yfree);
 #pragma unroll
         for (int hl = 0; hl < 2; ++hl) {
           const int h = 2 * wg + hl;
@@ -610,8 +750,8 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       }
     };
     cwait(&sm.g0bar, (uint32_t)(j & 1));
-    // the widening warps feed the A buffers; Y is double-buffered, so stage vs + 1's UMMAs run
-    // while this stage is folded
+    // Y is single-buffered: stage vs + 1's UMMAs wait for this stage's Y read (not its fold),
+    // and the next item's K UMMAs fill the tensor pipe in between
     for (int vs = 0; vs < d.nslices; ++vs) fold_y(vs);
     stamp(3);
 

@@ -42,8 +42,11 @@ if path == 2:  # stamps 0 start, 1 K done, 2 softmax done, 3 V done, 5 end (slot
     if os.environ.get("MMAWAIT"):  # build with -DDQ_GQ_MMAWAIT: MMA warp V phase span / A waits / Y waits, ns
         print(f"MMA warp V phase: span {(t[:, 4] / 1e3).mean():.2f} us, waiting for A {(t[:, 6] / 1e3).mean():.2f} us, "
               f"for Y {(t[:, 7] / 1e3).mean():.2f} us")
+    if os.environ.get("WIDETRACE"):  # build with -DDQ_GQ_WIDETRACE: widening warp V stages span / ring waits / A waits
+        print(f"widening V stages: span {(t[:, 4] / 1e3).mean():.2f} us, waiting for the ring {(t[:, 6] / 1e3).mean():.2f} us, "
+              f"for A buffers {(t[:, 7] / 1e3).mean():.2f} us")
     if os.environ.get("SMTRACE"):  # build with -DDQ_GQ_SMTRACE: 7 S ready, 4 row max, 6 column max
-        print(f"softmax: S ready {rel(7):.2f}, row max {rel(4):.2f}, column max {rel(6):.2f}, P written {rel(2):.2f}")
+        print(f"softmax: row max {rel(4):.2f}, column max {rel(6):.2f}, P written {rel(2):.2f}")
     t[:, 4] = t[:, 3]
 ph = np.diff(t[:, :6], axis=1) / 1e3  # us
 names = (["K stages", "softmax", "V stages", "(unused)", "epilogue"] if path in (1, 2) else

@@ -1,0 +1,159 @@
+// Cost of the GQA kernel's V-stage widening (4-bit codes in shared memory -> 8-bit A operand in
+// TMEM) per stage, for one widening warpgroup, alone and next to other load on the SM.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/widen_rate scripts/widen_rate.cu && /tmp/widen_rate
+// Modes: 0 alone; 1 + 16 warps of FFMA2 (the fold's issue pressure); 2 + an MMA warp streaming
+// UMMAs into other columns; 3 = 1 + 2; 4 alone without tcgen05.wait::st per stage; 5 alone,
+// smem reads and nibble splits only (no TMEM stores); 6 alone, TMEM stores only.
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((smem_u32(p) >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+__host__ __device__ constexpr uint32_t idesc(int M, int N) {
+  return (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+constexpr int kTile = 4096;  // V stage bytes per tile: 128 rows x 32 bytes
+
+template <int MODE>
+__global__ void __launch_bounds__(704, 1) widen(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t sm[];  // 4 tiles (16 KB) + B operand for the MMA warp
+  __shared__ uint32_t tbase;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ volatile int stop;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 4 * kTile + 16384; i += blockDim.x) sm[i] = (uint8_t)(i * 37);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    stop = 0;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tbase;
+  if (warp >= 16 && warp < 20) {  // the widening warpgroup
+    const int q = warp & 3, lane_in = 32 * q + lane;
+    const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+    const long long t0 = clock64();
+    uint32_t sink = 0;
+    for (int it = 0; it < iters; ++it) {
+      const int ab = it & 1;
+      uint4 c[4][2];
+      if (MODE != 6) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint8_t* src = sm + t * kTile + lane_in * 32;
+          c[t][0] = *reinterpret_cast<const uint4*>(src);
+          c[t][1] = *reinterpret_cast<const uint4*>(src + 16);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) c[t][0] = c[t][1] = make_uint4(it, t, lane, 3);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t wv[8] = {c[t][0].x, c[t][0].y, c[t][0].z, c[t][0].w, c[t][1].x, c[t][1].y, c[t][1].z, c[t][1].w};
+        uint32_t v[16];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[2 * k] = wv[k] & 0x0F0F0F0Fu;
+          v[2 * k + 1] = (wv[k] >> 4) & 0x0F0F0F0Fu;
+        }
+        if (MODE == 5) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) sink += v[k];
+        } else {
+          st16(tmem + lane_addr + (uint32_t)(ab * 64 + t * 16), v);
+        }
+      }
+      if (MODE != 4 && MODE != 5) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      __syncwarp();
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    const long long t1 = clock64();
+    if (lane == 0) out[q] = (t1 - t0) / iters + (sink == 12345 ? 1 : 0);
+    asm volatile("bar.sync 1, 128;");
+    if (tid == 16 * 32) stop = 1;
+  } else if (warp < 16 && (MODE == 1 || MODE == 3)) {  // fold-like FFMA2 pressure
+    float a0 = tid, a1 = tid + 1, b0 = 1.0001f, b1 = 0.9999f;
+    while (!stop) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        uint64_t d, x, y;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a0), "f"(a1));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b0), "f"(b1));
+        asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(d) : "l"(x), "l"(y));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(d));
+      }
+    }
+    if (a0 == 1.2345f) out[8] = 1;
+  } else if (warp == 21 && (MODE == 2 || MODE == 3)) {  // UMMAs: A = TMEM columns 256.., D = 384..
+    const uint64_t bd = sdesc(sm + 4 * kTile, 128, 1024);
+    const uint32_t id = idesc(128, 128);
+    uint32_t ph = 0;
+    while (!stop) {
+      if (lane == 0) {
+        for (int i = 0; i < 8; ++i) {
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem + 384),
+              "r"(tmem + 256 + i * 8), "l"(bd), "r"(id), "r"(i));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+        asm volatile(
+            "{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W;\n}" ::"r"(
+                smem_u32(&bar)),
+            "r"(ph));
+      }
+      ph ^= 1;
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+template <int MODE>
+void run(const char* name) {
+  long long* d;
+  cudaMalloc(&d, 16 * sizeof(long long));
+  const int smem = 4 * kTile + 16384 + 1024;
+  cudaFuncSetAttribute(widen<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  widen<MODE><<<1, 704, smem>>>(d, 256);
+  widen<MODE><<<148, 704, smem>>>(d, 4096);
+  long long h[16];
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("mode %d %-44s cycles per V stage: %lld %lld %lld %lld  (%s)\n", MODE, name, h[0], h[1], h[2], h[3],
+         cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+int main() {
+  run<0>("alone");
+  run<1>("+ 16 FFMA2 warps");
+  run<2>("+ UMMA stream");
+  run<3>("+ FFMA2 warps + UMMA stream");
+  run<4>("alone, no wait::st per stage");
+  run<5>("alone, smem + split only");
+  run<6>("alone, TMEM stores only");
+  return 0;
+}
