@@ -544,73 +544,89 @@ def run_c1(args, cfg):
 def run_model(args, cfg):
     """--model: one decode step of a whole LLaMA-shaped decoder (model.py) per step, replayed as a
     CUDA graph: device-resident tokens for `value`, host tokens in / next tokens out for `e2e`.
-    Roofline: the weights (bf16) + the compressed KV + the fp16 tails one step streams."""
+    Under N ranks the decoder is tensor-parallel (model.py: kv heads and 1/N of every weight per
+    GPU, NCCL all-gathers inside the captured step); the global batch is fixed (strong scaling).
+    Roofline: the weights (bf16) + the compressed KV + the fp16 tails one step streams per GPU."""
     import torch
 
     from paper_2405_12591_b200.model import LLAMA2_7B, LLAMA2_13B, LLAMA2_70B, DecoQuantLM
+    from paper_2405_12591_b200.sharding import TpGroup
 
-    torch.cuda.set_device(0)
+    rk = Ranks("nccl")
     shape = {"7b": LLAMA2_7B, "13b": LLAMA2_13B, "70b": LLAMA2_70B}[args.model]
     if args.layers:
         from dataclasses import replace
         shape = replace(shape, layers=args.layers)
     batch, T = cfg["batch"], cfg["T"]
-    lm = DecoQuantLM(shape, batch, bits=cfg["bits"])
+    tp = TpGroup(world=rk.world, rank=rk.rank) if rk.world == 1 else TpGroup()
+    lm = DecoQuantLM(shape, batch, bits=cfg["bits"], tp=tp)
     lm.prefill_random(T)
     torch.cuda.synchronize()
-    tok = torch.zeros(batch, dtype=torch.int64, device="cuda")
+    tok = torch.zeros(batch, dtype=torch.int64, device=rk.dev)
     for _ in range(args.warmup):
         tok = lm.step(tok)
     lm.capture(tok)
     for _ in range(args.warmup):
         tok = lm.replay(tok)
     torch.cuda.synchronize()
+    rk.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(0) as clk:
+    with Clocks(rk.local) as clk:
         e0.record()
         for _ in range(args.steps):
             tok = lm.replay(tok)
         e1.record()
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    rk.barrier()
+    ms = rk.max(e0.elapsed_time(e1) / args.steps)
     # end to end: pinned host tokens in, the step, next tokens back to the host, every step
     tok_h = torch.zeros(batch, dtype=torch.int64).pin_memory()
     nxt_h = torch.zeros(batch, dtype=torch.int64).pin_memory()
     steps_e2e = max(3, args.steps // 2)
     torch.cuda.synchronize()
+    rk.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
     for _ in range(steps_e2e):
-        nxt = lm.replay(tok_h.to("cuda", non_blocking=True))
+        nxt = lm.replay(tok_h.to(rk.dev, non_blocking=True))
         nxt_h.copy_(nxt, non_blocking=True)
         tok_h, nxt_h = nxt_h, tok_h
     f1.record()
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / steps_e2e
+    e2e_ms = rk.max(f0.elapsed_time(f1) / steps_e2e)
     wbytes = sum(t.numel() * t.element_size() for L in lm.layers for t in L.values())
     wbytes += lm.lm_head.numel() * lm.lm_head.element_size() + batch * shape.hidden * 2
     kv = sum(lm.cache.read_bytes(layer) for layer in range(shape.layers))
     peak, peak_kind = measured_peaks()
     fp16, actual = lm.cache.ledger()
+    world = rk.world
+    gathers = 4 * shape.layers + (2 if world > 1 else 0)
     line = {
-        "metric": "decode tokens/s (whole model)", "value": batch / (ms / 1e3), "unit": "tokens/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "metric": "decode tokens/s (whole model)", "value": batch / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16 weights, f16 attention",
         "data": "synthetic: random-init weights (std 0.02), K/V ~ N(0,1) compressed by K3",
         "config": {"workload": f"llama2-{args.model}-shape decode (whole model), batch {batch}, {T} context, "
                                f"int{cfg['bits']} DecoQuant KV", "model": f"llama2-{args.model}-shape",
-                   "global_batch": batch, "seq_len": T, "layers": shape.layers, "parallelism": "single GPU",
-                   "l2": f"weights {wbytes / 1e9:.1f} GB + KV {kv / 1e9:.1f} GB streamed per step (126 MB L2)"},
+                   "global_batch": batch, "seq_len": T, "layers": shape.layers,
+                   "parallelism": f"tp{world}: kv heads + output-column weight shards, "
+                                  f"{gathers} NCCL all-gathers per step" if world > 1 else "single GPU",
+                   "l2": f"weights {wbytes / 1e9:.1f} GB + KV {kv / 1e9:.1f} GB streamed per step per GPU (126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": (wbytes + kv) / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": (wbytes + kv) / (ms / 1e3) / 1e9 / peak, "traffic": None,
-                     "kernel": "whole step (weights + KV)", "bytes_per_step": wbytes + kv, "peak_kind": peak_kind},
+                     "kernel": "whole step (weights + KV, per GPU)", "bytes_per_step": wbytes + kv,
+                     "peak_kind": peak_kind},
         "memory_per_token_vs_fp16": actual / fp16,
         "e2e": {"value": batch / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": batch * 8,
                 "d2h_bytes_per_step": batch * 8, "ms_per_step": e2e_ms},
         "gpu_launches": args.steps * (shape.layers * 10 + 3),
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    if rk.rank == 0:
+        print(json.dumps(line), flush=True)
+    rk.close()
 
 
 def run_plumbing(args, cfg):
@@ -831,8 +847,7 @@ def main():
         run_plumbing(args, cfg)
         return
     if args.model and args.impl != "reference":
-        if rank == 0:
-            run_model(args, cfg)
+        run_model(args, cfg)
         return
     if args.config == "c1":
         if rank == 0 and args.impl != "reference":

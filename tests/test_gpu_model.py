@@ -131,6 +131,7 @@ def test_qkv_rope_kernel_matches_torch(heads, kv_heads, pos):
     p = torch.tensor(pos, dtype=torch.int64, device="cuda")
     lm = M.DecoQuantLM.__new__(M.DecoQuantLM)
     lm.shape, lm.batch, lm.dev, lm.pos = shape, B, torch.device("cuda"), p
+    lm.kv_local, lm.heads_local = kv_heads, heads
     q, k, v = lm._qkv_rope(qkv)
     rq, rk, rv = qkv.split([heads * 128, kv_heads * 128, kv_heads * 128], dim=-1)
     rq = M._rope(rq.reshape(B, heads, 128), p).reshape(B * kv_heads, heads // kv_heads, 128)
@@ -165,3 +166,47 @@ def test_harness_kernels_reject_bad_shapes():
     with pytest.raises(ShapeMismatch):
         check(lib().dq_model_qkv_rope(x.data_ptr(), 1, 3, 2, x.data_ptr(), 1e4, x.data_ptr(), x.data_ptr(),
                                       x.data_ptr(), None))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tensor_parallel_step_matches_unsharded(world):
+    """The gather-only TP step (N shard models driven in lock-step: every gather concatenates
+    their slices in rank order) against the unsharded model on the same weights and K/V: the
+    attention outputs per head within fp16 tolerance, the next tokens equal, and the shards'
+    caches holding their kv heads only."""
+    from paper_2405_12591_b200 import model as M
+    from paper_2405_12591_b200.sharding import TpGroup
+
+    shape = M.ModelShape(layers=2, hidden=512, heads=8, kv_heads=4, ffn=1024, vocab=1000)
+    full = M.DecoQuantLM(shape, batch=3, seed=5, chunk_len=64)
+    shards = [M.DecoQuantLM.shard_of(full, TpGroup(world=world, rank=r), chunk_len=64) for r in range(world)]
+    for m in [full, *shards]:
+        m.prefill_random(300, seed=6)
+    assert all(m.cache.units == 3 * shape.kv_heads // world for m in shards)
+    seen = {}
+
+    def spy(model, key):
+        real = model.cache.attend
+
+        def f(layer, q, out=None, append=None, out_dtype=torch.float16):
+            o = real(layer, q, out, append, out_dtype=out_dtype)
+            seen.setdefault(key, []).append(o.float().view(3, -1, 128).clone())
+            return o
+        model.cache.attend = f
+
+    spy(full, "full")
+    for r, m in enumerate(shards):
+        spy(m, r)
+    lock = M.Lockstep(shards)
+    tok = torch.tensor([1, 2, 3], device="cuda")
+    for _ in range(3):
+        ref = full.step(tok)
+        outs = lock.step(tok)
+        assert all(torch.equal(o, outs[0]) for o in outs)
+        assert torch.equal(outs[0], ref)
+        tok = ref
+    for call, ref in enumerate(seen["full"]):
+        got = torch.cat([seen[r][call] for r in range(world)], 1)
+        rel = float((got - ref).norm() / ref.norm())
+        assert rel < 1e-2, (call, rel)
+    assert full.cache.tokens(0) == shards[0].cache.tokens(0) == 303
