@@ -472,15 +472,21 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
           }
         }
       } else {  // V stage: row (r_local, e) = lane_in of every tile
+        // rows are 32 B apart: lanes 4k .. 4k+3 read one half of their rows and lanes
+        // 4k+4 .. 4k+7 the other, so each 16-byte load covers all 32 banks per 8 lanes (4
+        // wavefronts per warp instead of 8); the halves are put back in order afterwards
+        const int hs = (lane >> 2) & 1;
         uint4 c[4][2];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const unsigned char* src = sm.ring[slot] + t * kGqVTileBytes + lane_in * 32;
-          c[t][0] = c[t][1] = make_uint4(0u, 0u, 0u, 0u);
+          uint4 x = make_uint4(0u, 0u, 0u, 0u), y = x;
           if (t < nbt) {
-            c[t][0] = *reinterpret_cast<const uint4*>(src);
-            c[t][1] = *reinterpret_cast<const uint4*>(src + 16);
+            x = *reinterpret_cast<const uint4*>(src + 16 * hs);
+            y = *reinterpret_cast<const uint4*>(src + 16 * (hs ^ 1));
           }
+          c[t][0] = hs ? y : x;
+          c[t][1] = hs ? x : y;
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t) {

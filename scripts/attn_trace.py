@@ -45,6 +45,12 @@ if path == 2:  # stamps 0 start, 1 K done, 2 softmax done, 3 V done, 5 end (slot
     if os.environ.get("WIDETRACE"):  # build with -DDQ_GQ_WIDETRACE: widening warp V stages span / ring waits / A waits
         print(f"widening V stages: span {(t[:, 4] / 1e3).mean():.2f} us, waiting for the ring {(t[:, 6] / 1e3).mean():.2f} us, "
               f"for A buffers {(t[:, 7] / 1e3).mean():.2f} us")
+    if os.environ.get("ROLETRACE") == "1":  # -DDQ_GQ_ROLETRACE=1: the MMA warp per period (V(j) + K(j+2))
+        print(f"MMA warp per period: span {(t[:, 4] / 1e3).mean():.2f} us, waiting for A {(t[:, 6] / 1e3).mean():.2f} us, "
+              f"for P / Y / S {(t[:, 7] / 1e3).mean():.2f} us")
+    if os.environ.get("ROLETRACE") == "2":  # -DDQ_GQ_ROLETRACE=2: the widening warps per period
+        print(f"widening per period: span {(t[:, 4] / 1e3).mean():.2f} us, waiting for the ring {(t[:, 6] / 1e3).mean():.2f} us, "
+              f"for A buffers {(t[:, 7] / 1e3).mean():.2f} us")
     if os.environ.get("SMTRACE"):  # build with -DDQ_GQ_SMTRACE: 7 S ready, 4 row max, 6 column max
         print(f"softmax: row max {rel(4):.2f}, column max {rel(6):.2f}, P written {rel(2):.2f}")
     t[:, 4] = t[:, 3]

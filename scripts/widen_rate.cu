@@ -3,7 +3,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/widen_rate scripts/widen_rate.cu && /tmp/widen_rate
 // Modes: 0 alone; 1 + 16 warps of FFMA2 (the fold's issue pressure); 2 + an MMA warp streaming
 // UMMAs into other columns; 3 = 1 + 2; 4 alone without tcgen05.wait::st per stage; 5 alone,
-// smem reads and nibble splits only (no TMEM stores); 6 alone, TMEM stores only.
+// smem reads and nibble splits only (no TMEM stores); 6 alone, TMEM stores only; 7 / 8 = 0 / 3
+// with the row halves read in a per-4-lane rotated order (conflict-free 16-byte loads).
 #include <cstdint>
 #include <cstdio>
 
@@ -60,8 +61,16 @@ __global__ void __launch_bounds__(704, 1) widen(long long* out, int iters) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const uint8_t* src = sm + t * kTile + lane_in * 32;
-          c[t][0] = *reinterpret_cast<const uint4*>(src);
-          c[t][1] = *reinterpret_cast<const uint4*>(src + 16);
+          if (MODE >= 7) {  // halves rotated per 4 lanes: conflict-free 16-byte loads
+            const int hs = (lane >> 2) & 1;
+            const uint4 x = *reinterpret_cast<const uint4*>(src + 16 * hs);
+            const uint4 y = *reinterpret_cast<const uint4*>(src + 16 * (hs ^ 1));
+            c[t][0] = hs ? y : x;
+            c[t][1] = hs ? x : y;
+          } else {
+            c[t][0] = *reinterpret_cast<const uint4*>(src);
+            c[t][1] = *reinterpret_cast<const uint4*>(src + 16);
+          }
         }
       } else {
 #pragma unroll
@@ -91,7 +100,7 @@ __global__ void __launch_bounds__(704, 1) widen(long long* out, int iters) {
     if (lane == 0) out[q] = (t1 - t0) / iters + (sink == 12345 ? 1 : 0);
     asm volatile("bar.sync 1, 128;");
     if (tid == 16 * 32) stop = 1;
-  } else if (warp < 16 && (MODE == 1 || MODE == 3)) {  // fold-like FFMA2 pressure
+  } else if (warp < 16 && (MODE == 1 || MODE == 3 || MODE == 8)) {  // fold-like FFMA2 pressure
     float a0 = tid, a1 = tid + 1, b0 = 1.0001f, b1 = 0.9999f;
     while (!stop) {
 #pragma unroll
@@ -104,7 +113,7 @@ __global__ void __launch_bounds__(704, 1) widen(long long* out, int iters) {
       }
     }
     if (a0 == 1.2345f) out[8] = 1;
-  } else if (warp == 21 && (MODE == 2 || MODE == 3)) {  // UMMAs: A = TMEM columns 256.., D = 384..
+  } else if (warp == 21 && (MODE == 2 || MODE == 3 || MODE == 8)) {  // UMMAs: A = TMEM columns 256.., D = 384..
     const uint64_t bd = sdesc(sm + 4 * kTile, 128, 1024);
     const uint32_t id = idesc(128, 128);
     uint32_t ph = 0;
@@ -155,5 +164,7 @@ int main() {
   run<4>("alone, no wait::st per stage");
   run<5>("alone, smem + split only");
   run<6>("alone, TMEM stores only");
+  run<7>("alone, rotated half loads");
+  run<8>("rotated half loads + FFMA2 warps + UMMA stream");
   return 0;
 }
