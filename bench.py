@@ -453,6 +453,49 @@ def _c1_cpu_worker(seed):
     return n, time.perf_counter() - t0
 
 
+def api_calls(block, O, reps: int = 20) -> dict:
+    """The reference-facing API one call at a time, numpy in / numpy out as a drop-in caller
+    uses it (host <-> device copies and the host sync inside every call): deco_quantize,
+    deco_dequantize, fused_matmul_t of one query row, and KvCache.attention_scores over a
+    2-segment + tail cache, against the oracle's single-thread time for the same call."""
+    import numpy as np
+
+    import paper_2405_12591_b200 as dq
+
+    def per_call(fn, n):
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            fn()
+        return (time.perf_counter() - t0) / n * 1e6
+
+    rng = np.random.default_rng(1)
+    q = rng.standard_normal((1, 128)).astype(np.float32)
+    qm = dq.deco_quantize(block, 4)
+    e = O.encode(block, 4)
+    cfg = dq.CacheConfig(layers=1, dim=128, bits=4, chunk_len=1024)
+    cache = dq.KvCache(cfg)
+    cache.prefill(0, block, block)
+    for row in block[:1100]:
+        cache.append_token(0, row, row)  # one sealed 1024-row chunk + a 76-row tail
+    lay = O.LayerOracle(128, 4, 1024)
+    lay.prefill(block, block)
+    for row in block[:1100]:
+        lay.append(row, row)
+    rows = {
+        "deco_quantize (2048 x 128, int4)": (lambda: dq.deco_quantize(block, 4), lambda: O.encode(block, 4)),
+        "deco_dequantize": (lambda: dq.deco_dequantize(qm), lambda: O.decode(e)),
+        "fused_matmul_t (1 query row)": (lambda: dq.fused_matmul_t(q, qm), lambda: O.matmul_t(q, e)),
+        "KvCache.attention_scores (2 segments + tail)": (lambda: cache.attention_scores(0, q[0]),
+                                                         lambda: lay.scores(q[0])),
+    }
+    out = {}
+    for name, (ours, ref) in rows.items():
+        us, ref_us = per_call(ours, reps), per_call(ref, max(2, reps // 5))
+        out[name] = {"us_per_call": us, "oracle_us_per_call_1_thread": ref_us, "speedup": ref_us / us}
+    return out
+
+
 def run_c1(args, cfg):
     """BASELINE.json configs[0]: K3 (decompose + quantize) and K4 (reconstruct) on the 32-head
     2048 x 128 tensor, int4: per-block time, fp64 rate against the measured FP64 peak, parity
@@ -527,6 +570,7 @@ def run_c1(args, cfg):
         "k4": {"us_per_block_32": rec_ms * 1e3 / heads, "gbs_1024": big.shape[0] * (in_bytes // 4 + out_bytes)
                / (rec_ms_big / 1e3) / 1e9, "us_per_block_1024": rec_ms_big * 1e3 / big.shape[0]},
         "parity": {"reconstruction_rel_frob_max": max(errs), "tolerance": 1e-3},
+        "api": api_calls(k[0].astype(np.float32), O),
     }
     if not args.no_cpu_baseline:
         import multiprocessing as mp

@@ -103,10 +103,11 @@ __host__ __device__ inline bool geom_coords(const CoreGeom& g, int64_t slot, int
 __host__ __device__ inline int64_t payload_bytes(int64_t count, int bits) { return (count * bits + 7) / 8; }
 
 // signed code at slot (two's complement in `bits`, earliest element in the low bits)
+// bits divides 8, so a code never spans two bytes: its bit offset slot * bits splits into a byte
+// index and a shift without any (64-bit) division
 __device__ __forceinline__ int read_code(const uint8_t* p, int64_t slot, int bits) {
-  const int per = 8 / bits;
-  const unsigned byte = p[slot / per];
-  const unsigned raw = (byte >> ((slot % per) * bits)) & ((1u << bits) - 1u);
+  const int64_t bit = slot * bits;
+  const unsigned raw = ((unsigned)p[bit >> 3] >> (unsigned)(bit & 7)) & ((1u << bits) - 1u);
   const int sign = 1 << (bits - 1);
   return (int)(raw ^ sign) - sign;
 }
@@ -116,8 +117,8 @@ __device__ __forceinline__ int read_code(const uint8_t* p, int64_t slot, int bit
 __device__ __forceinline__ int geom_read(const uint8_t* p, const CoreGeom& g, int rr, int b, int e) {
   const int64_t slot = geom_slot(g, rr, b, e);
   if (g.layout == DQ_LAYOUT_REF) return read_code(p, slot, g.bits);
-  const int per = 8 / g.bits;
-  const unsigned raw = (p[slot / per] >> ((slot % per) * g.bits)) & ((1u << g.bits) - 1u);
+  const int64_t bit = slot * g.bits;
+  const unsigned raw = ((unsigned)p[bit >> 3] >> (unsigned)(bit & 7)) & ((1u << g.bits) - 1u);
   return (int)raw - (1 << (g.bits - 1));
 }
 

@@ -6,6 +6,8 @@
 //
 // These serve the reference-mirroring API for any n=2 plan.  The decode hot path
 // uses the specialised D=128 kernel in attention.cu instead.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace dq {
@@ -128,9 +130,6 @@ __global__ void __launch_bounds__(kThreads) reconstruct128_kernel(const float* _
   }
 }
 
-// ---- x @ W^T: one CTA per (query row p, tile of 256 b) ----------------------
-//   Wt[a][r][e] = sum_c x[p, c*j2+e] * core0[a,c,r]   (staged in shared memory)
-//   out[p, a*i2+b] = scale * sum_{r,e} Wt[a][r][e] * code[r,b,e]
 // WorkingSetMeter (compress.py:23-33), measured by the kernels: meter[0] = the most dequantized
 // codes one CTA holds at once (atomicMax), meter[1] = codes dequantized in total (atomicAdd)
 __device__ __forceinline__ void meter_report(unsigned long long* meter, long long held, long long unpacked) {
@@ -153,89 +152,185 @@ __device__ __forceinline__ void meter_report(unsigned long long* meter, long lon
   }
 }
 
+// Both fused reads stage tiles of at most TILE_ELEMENTS = 64 x 64 codes (compress.py:20, the
+// reference's working-set bound) in shared memory with every thread's loads in flight at once,
+// then contract from shared memory; the staged tile is the CTA's whole working set.
+constexpr int kTileCodes = 64 * 64;
+
+// ---- x @ W^T: CTA (query row p, tile of kFT rows b, group of kFR bond rows) -------
+//   Wt[a][r][e] = sum_c x[p, c*j2+e] * core0[a,c,r]   (the group's bond rows, in shared memory)
+//   part[p][grp][a*i2+b] = sum_{r in grp, e} Wt[a][r][e] * code[r,b,e]   (fp64, workspace)
+//   out[p, a*i2+b] = scale * sum_grp part[p][grp][a*i2+b]   (fused_t_sum_kernel, fixed order)
+//   lane = b within the tile, warp w = bond row w of the group
+constexpr int kFT = 32;
+constexpr int kFR = 8;
+
 __global__ void __launch_bounds__(kThreads) fused_t_kernel(const float* __restrict__ x, const float* __restrict__ core0,
-                                                           const uint8_t* __restrict__ payload, CoreGeom geom,
-                                                           const float* __restrict__ scale, int i1, int j1, int cols,
-                                                           float* __restrict__ out, unsigned long long* meter) {
-  extern __shared__ float smem[];
+                                                           const uint8_t* __restrict__ payload, CoreGeom geom, int i1,
+                                                           int j1, int cols, double* __restrict__ part,
+                                                           unsigned long long* meter) {
+  extern __shared__ double smem_d[];
   const int r = geom.r, i2 = geom.i2, j2 = geom.j2;
-  float* xs = smem;             // [cols]
-  float* wt = smem + cols;      // [i1][r][j2]
-  const int p = blockIdx.x;
-  const int rows = i1 * i2;
-  for (int i = threadIdx.x; i < cols; i += kThreads) xs[i] = x[(int64_t)p * cols + i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < i1 * r * j2; i += kThreads) {
-    const int a = i / (r * j2), rem = i - a * r * j2;
-    const int rr = rem / j2, e = rem - rr * j2;
-    double acc = 0.0;
-    for (int c = 0; c < j1; ++c) acc = fma((double)xs[c * j2 + e], (double)core0[(a * j1 + c) * r + rr], acc);
-    wt[i] = (float)acc;
+  float* xs = reinterpret_cast<float*>(smem_d);               // [cols]
+  float* wt = xs + cols;                                      // [i1][kFR][j2]
+  int8_t* cs = reinterpret_cast<int8_t*>(wt + i1 * kFR * j2);  // [kFR][j2][kFT]
+  const int p = blockIdx.x, b0 = blockIdx.y * kFT, r0 = blockIdx.z * kFR;
+  const int rows = i1 * i2, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int live = min(kFT, i2 - b0), nr = min(kFR, r - r0);
+  for (int i = tid; i < cols; i += kThreads) xs[i] = x[(int64_t)p * cols + i];
+  for (int i = tid; i < nr * j2 * kFT; i += kThreads) {  // code (r0 + rl, b0 + bl, e)
+    const int bl = i % kFT, re = i / kFT, rl = re / j2, e = re - rl * j2;
+    cs[i] = (int8_t)(bl < live ? geom_read(payload, geom, r0 + rl, b0 + bl, e) : 0);
   }
   __syncthreads();
-  const int b = blockIdx.y * kThreads + threadIdx.x;
-  const bool live = b < i2;
+  for (int i = tid; i < i1 * nr * j2; i += kThreads) {
+    const int a = i / (nr * j2), rem = i - a * nr * j2;
+    const int rl = rem / j2, e = rem - rl * j2;
+    double acc = 0.0;
+    for (int c = 0; c < j1; ++c) acc = fma((double)xs[c * j2 + e], (double)core0[(a * j1 + c) * r + r0 + rl], acc);
+    wt[(a * kFR + rl) * j2 + e] = (float)acc;
+  }
+  __syncthreads();
   double acc[8];
 #pragma unroll
   for (int a = 0; a < 8; ++a) acc[a] = 0.0;
-  if (live) {
-    for (int rr = 0; rr < r; ++rr)
-      for (int e = 0; e < j2; ++e) {
-        const double cv = (double)geom_read(payload, geom, rr, b, e);  // one code at a time per thread
-        if (cv == 0.0) continue;
-#pragma unroll
-        for (int a = 0; a < 8; ++a)
-          if (a < i1) acc[a] = fma((double)wt[(a * r + rr) * j2 + e], cv, acc[a]);
-      }
-  }
-  meter_report(meter, live ? 1 : 0, live ? (long long)r * j2 : 0);
-  if (!live) return;
-  const double s = (double)*scale;
-  for (int a = 0; a < i1; ++a) out[(int64_t)p * rows + a * i2 + b] = (float)(acc[a] * s);
-}
-
-// ---- x @ W: one CTA per query row p ---------------------------------------
-//   Y[a][r][e] = sum_b x[p, a*i2+b] * code[r,b,e]        (thread per (r,e))
-//   out[p, c*j2+e] = scale * sum_{a,r} core0[a,c,r] * Y[a][r][e]
-__global__ void __launch_bounds__(kThreads) fused_n_kernel(const float* __restrict__ x, const float* __restrict__ core0,
-                                                           const uint8_t* __restrict__ payload, CoreGeom geom,
-                                                           const float* __restrict__ scale, int i1, int j1, int cols,
-                                                           float* __restrict__ out, unsigned long long* meter) {
-  extern __shared__ float smem[];
-  const int r = geom.r, i2 = geom.i2, j2 = geom.j2;
-  const int rows = i1 * i2;
-  float* xs = smem;          // [rows]
-  float* y = smem + rows;    // [i1][r][j2]
-  const int p = blockIdx.x;
-  for (int i = threadIdx.x; i < rows; i += kThreads) xs[i] = x[(int64_t)p * rows + i];
-  __syncthreads();
-  long long held = 0, unpacked = 0;
-  for (int i = threadIdx.x; i < r * j2; i += kThreads) {
-    const int rr = i / j2, e = i - rr * j2;
-    double acc[8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) acc[a] = 0.0;
-    held = 1;  // one code at a time per thread
-    unpacked += i2;
-    for (int b = 0; b < i2; ++b) {
-      const double cv = (double)geom_read(payload, geom, rr, b, e);
-      if (cv == 0.0) continue;
+  if (w < nr)
+    for (int e = 0; e < j2; ++e) {
+      const double cv = (double)cs[(w * j2 + e) * kFT + lane];
 #pragma unroll
       for (int a = 0; a < 8; ++a)
-        if (a < i1) acc[a] = fma((double)xs[a * i2 + b], cv, acc[a]);
+        if (a < i1) acc[a] = fma((double)wt[(a * kFR + w) * j2 + e], cv, acc[a]);
     }
-    for (int a = 0; a < i1; ++a) y[(a * r + rr) * j2 + e] = (float)acc[a];
-  }
-  meter_report(meter, held, unpacked);
+  meter_report(meter, tid == 0 ? (long long)nr * j2 * live : 0, tid == 0 ? (long long)nr * j2 * live : 0);
+  // the group's partial: the warps' bond rows added in a fixed order through shared memory
   __syncthreads();
+  double* red = smem_d;  // [kFR][8 a][kFT] (reuses xs / wt / codes: every read is done)
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+    if (w < kFR) red[(w * 8 + a) * kFT + lane] = acc[a];
+  __syncthreads();
+  double* dst = part + ((int64_t)p * gridDim.z + blockIdx.z) * rows;
+  for (int i = tid; i < i1 * kFT; i += kThreads) {
+    const int a = i / kFT, bl = i - a * kFT;
+    if (bl >= live) continue;
+    double v = 0.0;
+    for (int ww = 0; ww < nr; ++ww) v += red[(ww * 8 + a) * kFT + bl];
+    dst[a * i2 + b0 + bl] = v;
+  }
+}
+
+__global__ void fused_t_sum_kernel(const double* __restrict__ part, int groups, int64_t rows,
+                                   const float* __restrict__ scale, float* __restrict__ out) {
+  const int p = blockIdx.y;
   const double s = (double)*scale;
-  for (int i = threadIdx.x; i < cols; i += kThreads) {
-    const int c = i / j2, e = i - c * j2;
-    double acc = 0.0;
-    for (int a = 0; a < i1; ++a)
-      for (int rr = 0; rr < r; ++rr)
-        acc = fma((double)core0[(a * j1 + c) * r + rr], (double)y[(a * r + rr) * j2 + e], acc);
-    out[(int64_t)p * cols + i] = (float)(acc * s);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int g = 0; g < groups; ++g) v += part[((int64_t)p * groups + g) * rows + i];
+    out[(int64_t)p * rows + i] = (float)(v * s);
+  }
+}
+
+// ---- x @ W: CTA (query row p, chunk of b rows) ------------------------------
+//   part[p][chunk][a][r][e] = sum_{b in chunk} x[p, a*i2+b] * code[r,b,e]   (thread per (r,e),
+//   tiles of at most TILE_ELEMENTS codes; fp64, workspace)
+//   out[p, c*j2+e] = scale * sum_{a,r} core0[a,c,r] * f32(sum_chunk part[...])   (fused_n_out_kernel)
+constexpr int kFNThreads = 1024;
+constexpr int kFNChunk = 32;  // b rows per CTA
+
+__global__ void __launch_bounds__(kFNThreads) fused_n_kernel(const float* __restrict__ x,
+                                                             const uint8_t* __restrict__ payload, CoreGeom geom, int i1,
+                                                             double* __restrict__ part, unsigned long long* meter) {
+  extern __shared__ float smem[];
+  const int r = geom.r, i2 = geom.i2, j2 = geom.j2;
+  const int pairs = r * j2, tid = threadIdx.x;
+  const int p = blockIdx.x, c0 = blockIdx.y * kFNChunk, cn = min(kFNChunk, i2 - c0);
+  float* xs = smem;                                       // [i1][kFNChunk]
+  int8_t* cs = reinterpret_cast<int8_t*>(xs + i1 * kFNChunk);  // [kfn][r][j2]
+  const int kfn = max(1, kTileCodes / pairs);             // b rows per tile
+  for (int i = tid; i < i1 * kFNChunk; i += kFNThreads) {
+    const int a = i / kFNChunk, bl = i - a * kFNChunk;
+    xs[i] = bl < cn ? x[(int64_t)p * i1 * i2 + (int64_t)a * i2 + c0 + bl] : 0.f;
+  }
+  constexpr int kPer = 2;  // (r, e) pairs per thread: r * j2 <= 2048
+  double acc[kPer][8];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k)
+#pragma unroll
+    for (int a = 0; a < 8; ++a) acc[k][a] = 0.0;
+  for (int t0 = 0; t0 < cn; t0 += kfn) {
+    __syncthreads();  // the previous tile's codes are read (and xs is loaded)
+    const int nb = min(kfn, cn - t0);
+    for (int i = tid; i < nb * pairs; i += kFNThreads) {  // code (rr, c0 + t0 + bl, e)
+      const int bl = i / pairs, re = i - bl * pairs, rr = re / j2, e = re - rr * j2;
+      cs[i] = (int8_t)geom_read(payload, geom, rr, c0 + t0 + bl, e);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int re = tid + k * kFNThreads;
+      if (re < pairs)
+        for (int bl = 0; bl < nb; ++bl) {
+          const double cv = (double)cs[bl * pairs + re];
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+            if (a < i1) acc[k][a] = fma((double)xs[a * kFNChunk + t0 + bl], cv, acc[k][a]);
+        }
+    }
+  }
+  double* dst = part + ((int64_t)p * gridDim.y + blockIdx.y) * i1 * pairs;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int re = tid + k * kFNThreads;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+      if (re < pairs && a < i1) dst[a * pairs + re] = acc[k][a];
+  }
+  meter_report(meter, tid == 0 ? (long long)min(kfn, cn) * pairs : 0, tid == 0 ? (long long)cn * pairs : 0);
+}
+
+__global__ void __launch_bounds__(kFNThreads) fused_n_out_kernel(const double* __restrict__ part, int chunks,
+                                                                 const float* __restrict__ core0, CoreGeom geom, int i1,
+                                                                 int j1, int cols, const float* __restrict__ scale,
+                                                                 float* __restrict__ out) {
+  extern __shared__ float y[];  // [i1][r][j2]
+  const int r = geom.r, j2 = geom.j2, pairs = r * j2, p = blockIdx.x, tid = threadIdx.x;
+  // Y = the chunks' partials summed in chunk order: 8 independent sums per thread in flight
+  const int n = i1 * pairs;
+  for (int i0 = 0; i0 < n; i0 += 8 * kFNThreads) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = 0.0;
+    for (int g = 0; g < chunks; ++g) {
+      const double* src = part + ((int64_t)p * chunks + g) * n;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * kFNThreads + tid;
+        if (i < n) v[k] += src[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * kFNThreads + tid;
+      if (i < n) y[i] = (float)v[k];
+    }
+  }
+  __syncthreads();
+  // out[c, e] = scale * sum_a sum_r core0[a,c,r] y[a,r,e]: 8 lanes per output (lane & 7 = a
+  // residue), combined by a fixed butterfly
+  const double s = (double)*scale;
+  for (int o0 = 0; o0 < cols * 8; o0 += kFNThreads) {
+    const int o = o0 + tid, i = o >> 3, k = o & 7;
+    double v = 0.0;
+    if (i < cols) {
+      const int c = i / j2, e = i - c * j2;
+      for (int a = k; a < i1; a += 8)
+        for (int rr = 0; rr < r; ++rr)
+          v = fma((double)core0[(a * j1 + c) * r + rr], (double)y[(a * r + rr) * j2 + e], v);
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    if (i < cols && k == 0) out[(int64_t)p * cols + i] = (float)(v * s);
   }
 }
 
@@ -307,6 +402,22 @@ int check_geom(const dq_plan2& p, int bits, int layout) {
   return DQ_OK;
 }
 
+// the fused reads' partial sums live in stream-ordered workspace from the device's default
+// memory pool; keep freed blocks in the pool (the default threshold returns them to the driver
+// at every synchronisation, a cudaMalloc per call)
+int keep_pool_memory() {
+  static bool done = false;
+  if (done) return DQ_OK;
+  int dev = 0;
+  cudaMemPool_t pool;
+  DQ_CUDA_TRY(cudaGetDevice(&dev));
+  DQ_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = UINT64_MAX;
+  DQ_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done = true;
+  return DQ_OK;
+}
+
 }  // namespace
 
 }  // namespace dq
@@ -356,14 +467,25 @@ extern "C" int dq_fused_matmul_t(const float* x, int64_t np, const float* core0,
   if (np == 0) return DQ_OK;
   if (!x || !core0 || !payload || !scale || !out) return fail(DQ_ERR_INVALID_ARG, "null pointer");
   if (p.i1 > 8) return fail(DQ_ERR_UNSUPPORTED, "i1 > 8");
+  if (np > 65535) return fail(DQ_ERR_UNSUPPORTED, "more than 65535 query rows");
   CoreGeom g = make_geom(p, bits, layout);
-  const size_t smem = sizeof(float) * ((size_t)cols + (size_t)p.i1 * p.r * p.j2);
+  const size_t smem = std::max(sizeof(float) * ((size_t)cols + (size_t)p.i1 * kFR * p.j2) + (size_t)kFR * p.j2 * kFT,
+                               sizeof(double) * kFR * 8 * kFT);
   if (smem > 200 * 1024) return fail(DQ_ERR_UNSUPPORTED, "plan too large for the fused kernel");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int groups = (int)ceil_div(p.r, kFR);
+  if (int rc = keep_pool_memory()) return rc;
+  double* part = nullptr;  // the bond-row groups' partial sums (stream-ordered workspace)
+  DQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * np * groups * rows, s));
   DQ_CUDA_TRY(cudaFuncSetAttribute(fused_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)np, (unsigned)ceil_div(p.i2, kThreads));
-  fused_t_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(x, core0, payload, g, scale, (int)p.i1, (int)p.j1,
-                                                                (int)cols, out, (unsigned long long*)meter);
+  dim3 grid((unsigned)np, (unsigned)ceil_div(p.i2, kFT), (unsigned)groups);
+  fused_t_kernel<<<grid, kThreads, smem, s>>>(x, core0, payload, g, (int)p.i1, (int)p.j1, (int)cols, part,
+                                              (unsigned long long*)meter);
   DQ_LAUNCH_CHECK();
+  fused_t_sum_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(rows, kThreads), 64), (unsigned)np), kThreads, 0, s>>>(
+      part, groups, rows, scale, out);
+  DQ_LAUNCH_CHECK();
+  DQ_CUDA_TRY(cudaFreeAsync(part, s));
   return DQ_OK;
 }
 
@@ -377,14 +499,26 @@ extern "C" int dq_fused_matmul(const float* x, int64_t np, const float* core0, c
   if (np == 0) return DQ_OK;
   if (!x || !core0 || !payload || !scale || !out) return fail(DQ_ERR_INVALID_ARG, "null pointer");
   if (p.i1 > 8) return fail(DQ_ERR_UNSUPPORTED, "i1 > 8");
+  if ((int64_t)p.r * p.j2 > 2 * kFNThreads) return fail(DQ_ERR_UNSUPPORTED, "plan too large for the fused kernel");
+  if (np > 65535) return fail(DQ_ERR_UNSUPPORTED, "more than 65535 query rows");
   CoreGeom g = make_geom(p, bits, layout);
-  const size_t smem = sizeof(float) * ((size_t)rows + (size_t)p.i1 * p.r * p.j2);
-  if (smem > 200 * 1024) return fail(DQ_ERR_UNSUPPORTED, "plan too large for the fused kernel");
-  DQ_CUDA_TRY(cudaFuncSetAttribute(fused_n_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fused_n_kernel<<<(unsigned)np, kThreads, smem, (cudaStream_t)stream>>>(x, core0, payload, g, scale, (int)p.i1,
-                                                                        (int)p.j1, (int)cols, out,
-                                                                        (unsigned long long*)meter);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int chunks = (int)ceil_div(p.i2, kFNChunk);
+  const int64_t ysz = (int64_t)p.i1 * p.r * p.j2;
+  if (int rc = keep_pool_memory()) return rc;
+  double* part = nullptr;  // the b chunks' partial Y (stream-ordered workspace)
+  DQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * np * chunks * ysz, s));
+  const size_t smem = sizeof(float) * p.i1 * kFNChunk + (size_t)kTileCodes;
+  fused_n_kernel<<<dim3((unsigned)np, (unsigned)chunks), kFNThreads, smem, s>>>(x, payload, g, (int)p.i1, part,
+                                                                              (unsigned long long*)meter);
   DQ_LAUNCH_CHECK();
+  const size_t smem2 = sizeof(float) * ysz;
+  if (smem2 > 200 * 1024) return fail(DQ_ERR_UNSUPPORTED, "plan too large for the fused kernel");
+  DQ_CUDA_TRY(cudaFuncSetAttribute(fused_n_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  fused_n_out_kernel<<<(unsigned)np, kFNThreads, smem2, s>>>(part, chunks, core0, g, (int)p.i1, (int)p.j1, (int)cols,
+                                                           scale, out);
+  DQ_LAUNCH_CHECK();
+  DQ_CUDA_TRY(cudaFreeAsync(part, s));
   return DQ_OK;
 }
 
