@@ -95,21 +95,39 @@ template <int G>
 __device__ __forceinline__ void merge_head(const dq_attn_args& args, int v, int h, int d, float Mt, float Lt, float Ot) {
   if (d >= 128) return;
   const int p0 = args.unit_part0[v], np = args.unit_nparts[v];
+  // partials in passes of 8 with every load issued before the arithmetic (the sums keep the
+  // partials' order)
+  constexpr int kB = 8;
   float M = Mt;
-  for (int i = 0; i < np; ++i) M = fmaxf(M, args.part_ml[((size_t)(p0 + i) * G + h) * 2]);
+  for (int i0 = 0; i0 < np; i0 += kB) {
+    float m[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) m[k] = i0 + k < np ? args.part_ml[((size_t)(p0 + i0 + k) * G + h) * 2] : -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kB; ++k) M = fmaxf(M, m[k]);
+  }
   float L = 0.f, O = 0.f;
   if (Mt != -INFINITY) {
     const float f = exp2f(Mt - M);
     L = f * Lt;
     O = f * Ot;
   }
-  for (int i = 0; i < np; ++i) {
-    const size_t s = (size_t)(p0 + i) * G + h;
-    const float m = args.part_ml[s * 2];
-    if (m == -INFINITY) continue;
-    const float f = exp2f(m - M);
-    L += f * args.part_ml[s * 2 + 1];
-    O += f * args.part_o[s * 128 + d];
+  for (int i0 = 0; i0 < np; i0 += kB) {
+    float m[kB], l[kB], o[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const size_t s = (size_t)(p0 + min(i0 + k, np - 1)) * G + h;
+      m[k] = i0 + k < np ? args.part_ml[s * 2] : -INFINITY;
+      l[k] = args.part_ml[s * 2 + 1];
+      o[k] = args.part_o[s * 128 + d];
+    }
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      if (m[k] == -INFINITY) continue;
+      const float f = exp2f(m[k] - M);
+      L += f * l[k];
+      O += f * o[k];
+    }
   }
   const float o = L > 0.f ? O / L : 0.f;
   const size_t i = ((size_t)v * G + h) * 128 + d;

@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
     const float4 x0 = q4[0], x1 = q4[1], x2 = q4[2], x3 = q4[3];
     const float qc[16] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x, x3.y, x3.z, x3.w};
 #pragma unroll
-    for (int i = 0; i < 16; ++i) wv[i] = fmaf(qc[ord16<BITS>(i)], gk[c], wv[i]);
+    for (int i = 0; i < 16; i += 2)  // two fp32 FMAs per instruction (FFMA2), each rounded as fmaf
+      ffma2(wv[i], wv[i + 1], qc[ord16<BITS>(i)], qc[ord16<BITS>(i + 1)], gk[c], gk[c]);
   }
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -223,7 +224,8 @@ __global__ void __launch_bounds__(kPrepGqThreads, 2) attn_prepare_gqa_kernel(dq_
       const float4 x0 = q4[0], x1 = q4[1], x2 = q4[2], x3 = q4[3];
       const float qc[16] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x, x3.y, x3.z, x3.w};
 #pragma unroll
-      for (int i = 0; i < 16; ++i) wv[i] = fmaf(qc[ord16<4>(i)], gk[c], wv[i]);
+      for (int i = 0; i < 16; i += 2)  // two fp32 FMAs per instruction (FFMA2), each rounded as fmaf
+        ffma2(wv[i], wv[i + 1], qc[ord16<4>(i)], qc[ord16<4>(i + 1)], gk[c], gk[c]);
     }
     float m = 0.f;
 #pragma unroll
