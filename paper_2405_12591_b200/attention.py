@@ -514,6 +514,14 @@ class DecodeKvCache:
                 and 1.5 * ctas <= wp.nwork <= 2 * ctas):
             chunk_b = MAX_CHUNK_B
             wp = plan_work(seg_arr, nseg, vunits, chunk_b)
+        if (self.chunk_b is None and self.bits == 4 and path0 and not self.asym and chunk_b == DEFAULT_CHUNK_B
+                and 2 * wp.nwork < ctas):
+            # under half a round of 256-row items (a strong-scaling shard: C4 at 4 / 8 GPUs holds
+            # 8 / 4 units per layer) the layer is one item's latency; 128-row items spread it
+            # over twice the SMs (scripts/chunk_sweep.py: 8 x 32K 22.8 -> 21.6 us, 4 x 32K
+            # 17.8 -> 16.9 us; 64-row items lose: 30.3 / 21.2 us)
+            chunk_b = DEFAULT_CHUNK_B // 2
+            wp = plan_work(seg_arr, nseg, vunits, chunk_b)
         if self.chunk_b is None and chunk_b == MAX_CHUNK_B and path0 and wp.nwork > 2 * ctas:
             # several rounds of 512-row items: the last TAIL_SPLIT x grid items run as 256-row
             # halves, evening out the scheduler's last round (C3: 230.2 -> 225.7 us; at 256-row
