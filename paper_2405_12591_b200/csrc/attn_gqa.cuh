@@ -53,6 +53,12 @@ constexpr uint32_t kGqColA = 0, kGqColS = 128, kGqColY = 384;  // A: 2 x 64 colu
 #endif
 constexpr int kGqKA = DQ_GQ_KA;  // K stages of item j+1 ahead of item j's first V stage
 constexpr int kGqPBits = 15;
+#ifndef DQ_GQ_NAP
+#define DQ_GQ_NAP 0  // 1: math warps wait with __nanosleep back-off; 2: + the widening warps
+#endif
+#ifndef DQ_GQ_NAP_NS
+#define DQ_GQ_NAP_NS 64
+#endif
 constexpr int kGqVTileBytes = 8 * 16 * kI2Pad / 2;  // V stage per tile: 8 bond rows x 16 e x 64 b
 
 struct GqSmem {
@@ -134,6 +140,14 @@ __device__ __forceinline__ void gq_issue_stage(GqSmem& sm, const dq_attn_args& a
     const unsigned char* src = d.vc + ((size_t)(bt0 + t) * d.r + 8 * mbv) * 16 * kI2Pad / 2;
     bulk_g2s(buf + t * kGqVTileBytes, src, (uint32_t)kGqVTileBytes, bar);
   }
+}
+
+// wait with back-off: a non-blocking test, then __nanosleep between tests, so a waiting warp
+// leaves the issue slots of its SM sub-partition to the warps that have work (a try_wait loop
+// re-issues: ncu counts this kernel's wait loops at ~19% of its executed instructions)
+template <int NS>
+__device__ __forceinline__ void mbar_wait_nap(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(NS);
 }
 
 // 2^x on the SFU (ex2.approx.ftz: -inf -> +0, relative error ~2^-22)
@@ -420,6 +434,11 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
     const int q = warp & 3;
     const int lane_in = 32 * q + lane;
     const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+#if DQ_GQ_NAP >= 2  // measurement: the widening warps back off in their waits
+    auto wwait = [](uint64_t* bar, uint32_t parity) { mbar_wait_nap<DQ_GQ_NAP_NS>(bar, parity); };
+#else
+    auto wwait = [](uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); };
+#endif
     int st = 0;  // ring stages = A-buffer uses
 #ifdef DQ_GQ_WIDETRACE  // measurement only: per item, V-stage widening span (slot 4), ring waits (6), A waits (7)
     int64_t tv0 = 0, tv1 = 0, wf = 0, wa = 0;
@@ -430,12 +449,12 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
       const int64_t t0 = global_ns();
       if (!kstage && tv0 == 0) tv0 = t0;
 #endif
-      mbar_wait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
+      wwait(&sm.full[slot], (uint32_t)((st / kGqStages) & 1));
 #ifdef DQ_GQ_WIDETRACE
       const int64_t t1 = global_ns();
       if (!kstage) wf += t1 - t0;
 #endif
-      if (st >= kGqNumA) mbar_wait(&sm.afree[ab], (uint32_t)((st / kGqNumA - 1) & 1));
+      if (st >= kGqNumA) wwait(&sm.afree[ab], (uint32_t)((st / kGqNumA - 1) & 1));
 #ifdef DQ_GQ_WIDETRACE
       if (!kstage) wa += global_ns() - t1;
 #endif
@@ -551,7 +570,11 @@ __global__ void __launch_bounds__(kGqThreads, 1) decode_attn_gqa_kernel(dq_attn_
 #ifdef DQ_GQ_SPIN  // measurement: consumers spin on their barriers instead of suspending
   auto cwait = [](uint64_t* bar, uint32_t parity) { mbar_wait_spin(bar, parity); };
 #else
+#if DQ_GQ_NAP >= 1  // the math warps back off in their waits (mbar_wait_nap)
+  auto cwait = [](uint64_t* bar, uint32_t parity) { mbar_wait_nap<DQ_GQ_NAP_NS>(bar, parity); };
+#else
   auto cwait = [](uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); };
+#endif
 #endif
   const int q = warp & 3;                // TMEM lane quarter of this warp
   const int wg = warp >> 2;              // warpgroup 0..3
