@@ -6,10 +6,14 @@ token appended to the tail by the combine kernel), copy the output back.  Launch
 from Python costs ~10 us of host time per op, more than the GPU needs for a layer, so the
 step is captured once and replayed:
 
-- host-to-device copies run ahead on one side stream (layer l+1's inputs land while layer
-  l computes) and device-to-host copies trail on another (layer l's output leaves while
-  layer l+1 computes);
-- the kernels keep their programmatic dependent launch edges inside the graph;
+- host-to-device copies run ahead on one side stream (layer groups of 1, 3 and the rest: the
+  copies take ~8 us per C2 layer against ~67 us of compute) and device-to-host copies trail
+  on another (groups of ..., 4, 2, 1 layers, so one layer's output is left after the last
+  kernel).  The compute stream waits for an upload group before the group's first layer and
+  records a download group after its last: every such cross-stream edge turns the programmatic
+  launch edge into the next layer's prepare kernel into a full dependency.  One edge per layer
+  measured 2.55 ms per C2 step against 2.34 ms grouped (`scripts/e2e_probe.py`, round robin);
+- the kernels keep their programmatic dependent launch edges inside a group;
 - the host keeps the cache's token counters in step (``DecodeKvCache._after_append``).
 
 A replay that would seal a tail chunk (which re-plans the layer's segment table) is
@@ -35,7 +39,7 @@ class DecodeStepGraph:
     """
 
     def __init__(self, cache: DecodeKvCache, q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor,
-                 out_h: torch.Tensor):
+                 out_h: torch.Tensor, up_sizes=(1, 3), down_sizes=None):
         L, U, g, D = cache.layers, cache.units, cache.g, cache.dim
         if q_h.shape != (L, U, g, D) or out_h.shape != q_h.shape or k_h.shape != (L, U, D) or v_h.shape != (L, U, D):
             raise ShapeMismatch("host buffers must be q/out (layers, units, g, 128) and k/v (layers, units, 128)")
@@ -51,8 +55,16 @@ class DecodeStepGraph:
         self.o_d = torch.empty(q_h.shape, dtype=torch.float16, device=dev)
         self.up = torch.cuda.Stream(device=dev)    # host -> device, runs ahead
         self.down = torch.cuda.Stream(device=dev)  # device -> host, trails the layers
-        self.h2d = [torch.cuda.Event() for _ in range(L)]
-        self.done = [torch.cuda.Event() for _ in range(L)]
+        self.up_groups = self._groups(L, up_sizes)
+        if down_sizes is None:  # ..., 4, 2, 1 layers: the outputs left after the last layer are one layer's
+            down_sizes, n, left = [], 1, L
+            while left > 0:
+                down_sizes.insert(0, min(n, left))
+                left -= n
+                n *= 2
+        self.down_groups = self._groups(L, down_sizes)
+        self.h2d = [torch.cuda.Event() for _ in self.up_groups]
+        self.done = [torch.cuda.Event() for _ in self.down_groups]
         self.graph = None
         self.recapture()
 
@@ -62,20 +74,39 @@ class DecodeStepGraph:
         self.up.wait_stream(compute)
         self.down.wait_stream(compute)
         with torch.cuda.stream(self.up):
-            for layer in range(L):
-                self.q_d[layer].copy_(self.q_h[layer], non_blocking=True)
-                self.k_d[layer].copy_(self.k_h[layer], non_blocking=True)
-                self.v_d[layer].copy_(self.v_h[layer], non_blocking=True)
-                self.h2d[layer].record(self.up)
+            for gi, (a, b) in enumerate(self.up_groups):
+                self.q_d[a:b].copy_(self.q_h[a:b], non_blocking=True)
+                self.k_d[a:b].copy_(self.k_h[a:b], non_blocking=True)
+                self.v_d[a:b].copy_(self.v_h[a:b], non_blocking=True)
+                self.h2d[gi].record(self.up)
+        starts = {a: gi for gi, (a, _) in enumerate(self.up_groups)}
+        ends = {b - 1: gi for gi, (_, b) in enumerate(self.down_groups)}
         for layer in range(L):
-            compute.wait_event(self.h2d[layer])
+            if layer in starts:
+                compute.wait_event(self.h2d[starts[layer]])
             cache.attend(layer, self.q_d[layer], self.o_d[layer], append=(self.k_d[layer], self.v_d[layer]))
-            self.done[layer].record(compute)
-            with torch.cuda.stream(self.down):
-                self.down.wait_event(self.done[layer])
-                self.out_h[layer].copy_(self.o_d[layer], non_blocking=True)
+            if layer in ends:
+                gi = ends[layer]
+                a, b = self.down_groups[gi]
+                self.done[gi].record(compute)
+                with torch.cuda.stream(self.down):
+                    self.down.wait_event(self.done[gi])
+                    self.out_h[a:b].copy_(self.o_d[a:b], non_blocking=True)
         compute.wait_stream(self.up)
         compute.wait_stream(self.down)
+
+    @staticmethod
+    def _groups(L: int, sizes) -> list[tuple[int, int]]:
+        """Layer groups [start, stop) of the given sizes, the rest of the layers in one more."""
+        out, start = [], 0
+        for n in sizes:
+            if start >= L:
+                break
+            out.append((start, min(L, start + n)))
+            start += n
+        if start < L:
+            out.append((start, L))
+        return out
 
     def _sealing_ahead(self) -> bool:
         return any(lay.tail_len + 1 >= self.cache.chunk_len for lay in self.cache._layers)
