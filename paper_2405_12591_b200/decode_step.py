@@ -31,7 +31,64 @@ from .attention import DecodeKvCache
 from .errors import ShapeMismatch
 
 
-class DecodeStepGraph:
+class _StepGraph:
+    """A captured decode step over every layer of ``cache`` (``_body`` records one step)."""
+
+    cache: DecodeKvCache
+
+    def _body(self):
+        raise NotImplementedError
+
+    def _sealing_ahead(self) -> bool:
+        return any(lay.tail_len + 1 >= self.cache.chunk_len for lay in self.cache._layers)
+
+    def recapture(self):
+        """(Re)build the graph: one eager step (it is a real decode step), then the capture."""
+        self.cache._flush_seals()  # full tails of an eager sealing step are compressed first
+        if self._sealing_ahead():
+            raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
+        self._body()  # eager step: builds every layer's segment table outside the capture
+        torch.cuda.synchronize()
+        if self._sealing_ahead():
+            raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
+        tails = [lay.tail_len for lay in self.cache._layers]
+        self.gens = [lay.gen for lay in self.cache._layers]
+        self.keep = [list(lay.keep) for lay in self.cache._layers]  # device tables the graph points at
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._body()
+        for lay, t in zip(self.cache._layers, tails):  # the capture ran no device work
+            lay.tail_len = t
+        if [lay.gen for lay in self.cache._layers] != self.gens:
+            raise ShapeMismatch("a layer was re-planned during the capture")
+
+    def replay(self):
+        """One decode step for every layer."""
+        if self._sealing_ahead():
+            raise ShapeMismatch("a tail chunk seals on this token: run the step eagerly, then recapture()")
+        if [lay.gen for lay in self.cache._layers] != self.gens:
+            raise ShapeMismatch("a layer was re-planned (sealed chunk) since the capture: recapture()")
+        self.graph.replay()
+        for layer in range(self.cache.layers):
+            self.cache._after_append(layer)
+
+
+class DeviceStepGraph(_StepGraph):
+    """The decode step on device-resident q (layers, units, g, 128), k / v (layers, units, 128)
+    and out (like q), captured once: every layer's prepare -> split -> combine (+ append) with
+    the programmatic launch edges of the whole step in one graph."""
+
+    def __init__(self, cache: DecodeKvCache, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor):
+        self.cache, self.q, self.k, self.v, self.out = cache, q, k, v, out
+        self.graph = None
+        self.recapture()
+
+    def _body(self):
+        for layer in range(self.cache.layers):
+            self.cache.attend(layer, self.q[layer], self.out[layer], append=(self.k[layer], self.v[layer]))
+
+
+class DecodeStepGraph(_StepGraph):
     """Captured decode step for every layer of ``cache``.
 
     q_h: (layers, units, g, 128), k_h / v_h: (layers, units, 128), out_h like q_h: pinned
@@ -107,36 +164,3 @@ class DecodeStepGraph:
         if start < L:
             out.append((start, L))
         return out
-
-    def _sealing_ahead(self) -> bool:
-        return any(lay.tail_len + 1 >= self.cache.chunk_len for lay in self.cache._layers)
-
-    def recapture(self):
-        """(Re)build the graph: one eager step (it is a real decode step), then the capture."""
-        self.cache._flush_seals()  # full tails of an eager sealing step are compressed first
-        if self._sealing_ahead():
-            raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
-        self._body()  # eager step: builds every layer's segment table outside the capture
-        torch.cuda.synchronize()
-        if self._sealing_ahead():
-            raise ShapeMismatch("a tail chunk seals on the next token: run that step eagerly first")
-        tails = [lay.tail_len for lay in self.cache._layers]
-        self.gens = [lay.gen for lay in self.cache._layers]
-        self.keep = [list(lay.keep) for lay in self.cache._layers]  # device tables the graph points at
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self._body()
-        for lay, t in zip(self.cache._layers, tails):  # the capture ran no device work
-            lay.tail_len = t
-        if [lay.gen for lay in self.cache._layers] != self.gens:
-            raise ShapeMismatch("a layer was re-planned during the capture")
-
-    def replay(self):
-        """One decode step for every layer from the current host inputs into out_h."""
-        if self._sealing_ahead():
-            raise ShapeMismatch("a tail chunk seals on this token: run the step eagerly, then recapture()")
-        if [lay.gen for lay in self.cache._layers] != self.gens:
-            raise ShapeMismatch("a layer was re-planned (sealed chunk) since the capture: recapture()")
-        self.graph.replay()
-        for layer in range(self.cache.layers):
-            self.cache._after_append(layer)
