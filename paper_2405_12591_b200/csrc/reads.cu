@@ -406,15 +406,15 @@ int check_geom(const dq_plan2& p, int bits, int layout) {
 // memory pool; keep freed blocks in the pool (the default threshold returns them to the driver
 // at every synchronisation, a cudaMalloc per call)
 int keep_pool_memory() {
-  static bool done = false;
-  if (done) return DQ_OK;
+  static bool done[64] = {};  // per device
   int dev = 0;
-  cudaMemPool_t pool;
   DQ_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 64 && done[dev]) return DQ_OK;
+  cudaMemPool_t pool;
   DQ_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
   uint64_t keep = UINT64_MAX;
   DQ_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  done = true;
+  if (dev < 64) done[dev] = true;
   return DQ_OK;
 }
 
