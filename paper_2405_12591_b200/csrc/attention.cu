@@ -86,8 +86,11 @@ __global__ void __launch_bounds__(kGqG * 128, 2) combine_gqa_kernel(dq_attn_args
   auto gsync = [grp] { asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory"); };
   if (hg == 1) {
     float Mt = -INFINITY, Lt = 0.f, Ot = 0.f;
-    if (tl > 0)
-      tail_partial<kGqG>(args, u, u, grp, d, 128, tl, tail_sg + (size_t)grp * cap, red[grp], gsync, Mt, Lt, Ot);
+    if (tl > 0) {  // every head's scores in one pass over the K rows, then each group's P.V
+      __shared__ __align__(16) float qs[kGqG][128];
+      tail_scores_gq<kGqG * 128>(args, u, tl, cap, tail_sg, qs);
+      tail_partial<kGqG, true>(args, u, u, grp, d, 128, tl, tail_sg + (size_t)grp * cap, red[grp], gsync, Mt, Lt, Ot);
+    }
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     merge_head<kGqG>(args, u, grp, d, Mt, Lt, Ot);

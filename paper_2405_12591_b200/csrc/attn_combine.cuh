@@ -19,9 +19,10 @@ namespace attn {
 // per warp), P.V warp-parallel over tokens (8 rows in flight) with each lane owning 4 dims, then a cross-warp
 // reduction; thread d < 128 returns Ot for dim d.  tail_s holds tl floats, red 5 * nthr / 32
 // floats... (red: [nw][128] O partials + [nw] sums + [nw] maxima).
-template <int G, class Sync>
+template <int G, bool SCORED = false, class Sync>
 __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, int v, int h, int tid, int nthr, int tl,
                                              float* tail_s, float* red, Sync sync, float& Mt, float& Lt, float& Ot) {
+  // SCORED: tail_s already holds the scores (log2 domain) and the caller has synchronised
   const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
   const float l2e = 1.4426950408889634f;
   const __half* qh = reinterpret_cast<const __half*>(args.q) + ((size_t)v * G + h) * 128;
@@ -31,7 +32,7 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
   const __half* tk = reinterpret_cast<const __half*>(args.tail_k) + (size_t)u * args.tail_cap * 128;
   const __half* tv = reinterpret_cast<const __half*>(args.tail_v) + (size_t)u * args.tail_cap * 128;
   constexpr int kTK = G >= 8 ? 4 : 8;  // rows in flight per warp (the GQA combine runs at 32 registers)
-  for (int t0 = warp; t0 < tl; t0 += kTK * nw) {
+  for (int t0 = warp; !SCORED && t0 < tl; t0 += kTK * nw) {
     float dot[kTK];
 #pragma unroll
     for (int i = 0; i < kTK; ++i) {
@@ -54,7 +55,7 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
         if (t0 + i * nw < tl) tail_s[t0 + i * nw] = dot[i] * args.sm_scale * l2e;  // log2 domain
     }
   }
-  sync();
+  if (!SCORED) sync();
   float m = -INFINITY;
   for (int t = tid; t < tl; t += nthr) m = fmaxf(m, tail_s[t]);
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -105,6 +106,44 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
     if (tid < 128) Ot += red_o[w * 128 + tid];
   }
   sync();  // red and tail_s reusable
+}
+
+// Tail scores of all kGqG heads of unit u at once (the GQA combine): thread i scores token
+// i / 2 for heads 4 (i & 1) .. 4 (i & 1) + 3 with a whole K row of its own (16-byte loads, 128
+// dims per thread: no cross-lane reductions, each K row read once for the 8 heads; q of the 8
+// heads from shared memory).  tail_s[h * cap + t] = score in the log2 domain.
+template <int NT>
+__device__ __forceinline__ void tail_scores_gq(const dq_attn_args& args, int u, int tl, int cap, float* tail_s,
+                                               float (*qs)[128]) {
+  constexpr int G = 8;
+  const int tid = threadIdx.x;
+  const float scl = args.sm_scale * 1.4426950408889634f;
+  const __half* qh = reinterpret_cast<const __half*>(args.q) + (size_t)u * G * 128;
+  for (int i = tid; i < G * 128; i += NT) qs[i / 128][i % 128] = __half2float(qh[i]);
+  __syncthreads();
+  const __half* tk = reinterpret_cast<const __half*>(args.tail_k) + (size_t)u * args.tail_cap * 128;
+  const int h0 = 4 * (tid & 1);
+  for (int t = tid >> 1; t < tl; t += NT / 2) {
+    const uint4* krow = reinterpret_cast<const uint4*>(tk + (size_t)t * 128);
+    float dot[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int c = 0; c < 16; ++c) {  // 8 dims per 16-byte load
+      const uint4 kv = krow[c];
+      const __half2* k2 = reinterpret_cast<const __half2*>(&kv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 kf = __half22float2(k2[j]);
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          const float2 qf = *reinterpret_cast<const float2*>(&qs[h0 + hh][c * 8 + 2 * j]);
+          dot[hh] = fmaf(qf.x, kf.x, fmaf(qf.y, kf.y, dot[hh]));
+        }
+      }
+    }
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) tail_s[(size_t)(h0 + hh) * cap + t] = dot[hh] * scl;
+  }
+  __syncthreads();
 }
 
 // Merge of head h of virtual unit v: its work-item partials plus the tail partial (Mt, Lt, Ot;
