@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kGqG * 128, 2) combine_gqa_kernel(dq_attn_args
     float Mt = -INFINITY, Lt = 0.f, Ot = 0.f;
     if (tl > 0) {  // every head's scores in one pass over the K rows, then each group's P.V
       __shared__ __align__(16) float qs[kGqG][128];
-      tail_scores_gq<kGqG * 128>(args, u, tl, cap, tail_sg, qs);
+      tail_scores_rows<kGqG, kGqG * 128>(args, u, tl, cap, tail_sg, qs);
       tail_partial<kGqG, true>(args, u, u, grp, d, 128, tl, tail_sg + (size_t)grp * cap, red[grp], gsync, Mt, Lt, Ot);
     }
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
