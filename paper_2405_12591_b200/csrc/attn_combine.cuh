@@ -4,6 +4,10 @@
 
 #include "attn_frag.cuh"
 
+#ifndef DQ_TAIL_TV_GQ
+#define DQ_TAIL_TV_GQ 1
+#endif
+
 namespace dq {
 namespace attn {
 
@@ -66,10 +70,14 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
   sync();
   m = red_m[0];
   for (int w = 1; w < nw; ++w) m = fmaxf(m, red_m[w]);
+  // P once per token (not once per lane of every warp that reads it): the tail's exp2 work
+  // drops 32x (the GQA combine's SFU load)
+  for (int t = tid; t < tl; t += nthr) tail_s[t] = exp2f(tail_s[t] - m);
+  sync();
   float o4[4] = {0.f, 0.f, 0.f, 0.f}, l = 0.f;
   // kTV rows in flight per warp (their loads before the arithmetic; the sums keep the order
   // t = warp, warp + nw, ...)
-  constexpr int kTV = G >= 8 ? 1 : 8;  // (GQA: 4 measured 1% slower at a 512-token tail)
+  constexpr int kTV = G >= 8 ? DQ_TAIL_TV_GQ : 8;  // (GQA: 4 measured 1% slower at a 512-token tail)
   for (int t0 = warp; t0 < tl; t0 += kTV * nw) {
     uint2 vv[kTV];
     float p[kTV];
@@ -80,7 +88,7 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
       p[i] = 0.f;
       if (t < tl) {
         vv[i] = reinterpret_cast<const uint2*>(tv + (size_t)t * 128)[lane];
-        p[i] = exp2f(tail_s[t] - m);
+        p[i] = tail_s[t];
       }
     }
 #pragma unroll
