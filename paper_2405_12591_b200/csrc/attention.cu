@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(dq_attn_args a
 // combine for the GQA kernel's 8 heads: one 128-thread group per head (named barrier 1 + group);
 // the tail partials overlap the split kernel (see combine_kernel), the merges follow its wait
 // and the fused append comes once every group has read the tail
-__global__ void __launch_bounds__(kGqG * 128, 2) combine_gqa_kernel(dq_attn_args args) {
+#ifndef DQ_COMB_GQ_MINB
+#define DQ_COMB_GQ_MINB 2
+#endif
+__global__ void __launch_bounds__(kGqG * 128, DQ_COMB_GQ_MINB) combine_gqa_kernel(dq_attn_args args) {
   extern __shared__ float tail_sg[];  // [kGqG][tail_cap]
   __shared__ __align__(16) float red[kGqG][4 * 130];
   const int u = blockIdx.x, grp = threadIdx.x >> 7, d = threadIdx.x & 127;
