@@ -637,3 +637,40 @@ def test_fused_reads_long_and_ragged(dq, T, rows, bits):
     # deterministic: the partial sums are added in a fixed order
     assert np.array_equal(dq.fused_matmul_t(xt, q), dq.fused_matmul_t(xt, q))
     assert np.array_equal(dq.fused_matmul(x, q), dq.fused_matmul(x, q))
+
+
+@pytest.mark.parametrize("L", [1, 9])
+def test_step_graphs_grouped_copies_and_device(dq, L):
+    """DecodeStepGraph's grouped host copies (uploads 1, 3, rest; downloads ..., 4, 2, 1) and
+    DeviceStepGraph (the device-resident step as one graph) both equal eager attend per layer,
+    for layer counts whose groups are ragged."""
+    from paper_2405_12591_b200.attention import DecodeKvCache
+    from paper_2405_12591_b200.decode_step import DecodeStepGraph, DeviceStepGraph
+
+    U, P, steps = 3, 200, 4
+    rng = np.random.default_rng(L)
+    kv = torch.from_numpy(rng.standard_normal((L, 2, U, P, 128)).astype(np.float16)).cuda()
+    caches = [DecodeKvCache(layers=L, units=U, g=1, bits=4, chunk_len=64) for _ in range(3)]
+    for c in caches:
+        for layer in range(L):
+            c.prefill(layer, kv[layer, 0], kv[layer, 1])
+    eager, hosted, device = caches
+    q = torch.from_numpy(rng.standard_normal((L, U, 1, 128)).astype(np.float16)).cuda()
+    k = torch.from_numpy(rng.standard_normal((L, U, 128)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.standard_normal((L, U, 128)).astype(np.float16)).cuda()
+    q_h, k_h, v_h = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
+    out_h = torch.empty(q_h.shape, dtype=torch.float16).pin_memory()
+    out_d = torch.empty_like(q)
+    hs = DecodeStepGraph(hosted, q_h, k_h, v_h, out_h)  # each runs one eager step, then captures
+    ds = DeviceStepGraph(device, q, k, v, out_d)
+    sizes = [b - a for a, b in hs.down_groups]
+    assert sum(sizes) == L and sizes[-1] == 1 and [a for a, _ in hs.up_groups][:2] == [0, 1][:len(hs.up_groups)]
+    for t in range(steps):
+        ref = torch.stack([eager.attend(layer, q[layer], append=(k[layer], v[layer])) for layer in range(L)])
+        if t > 0:
+            hs.replay()
+            ds.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out_h, ref.cpu()), t
+        assert torch.equal(out_d, ref), t
+    assert eager.tokens(0) == hosted.tokens(0) == device.tokens(0) == P + steps
