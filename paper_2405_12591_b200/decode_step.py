@@ -6,10 +6,11 @@ token appended to the tail by the combine kernel), copy the output back.  Launch
 from Python costs ~10 us of host time per op, more than the GPU needs for a layer, so the
 step is captured once and replayed:
 
-- host-to-device copies run ahead on one side stream (layer groups of 1, 3 and the rest: the
-  copies take ~8 us per C2 layer against ~67 us of compute) and device-to-host copies trail
-  on another (groups of ..., 4, 2, 1 layers, so one layer's output is left after the last
-  kernel).  The compute stream waits for an upload group before the group's first layer and
+- host-to-device copies run ahead on one side stream (layer groups of 1, 2, 4, ...: each group
+  lands while the groups before it compute, whatever the box's PCIe rate -- groups of 1, 3
+  and the rest stalled layer 4 on a box whose uploads ran at ~25 GB/s: 3.0 against 2.24 ms
+  per C2 step) and device-to-host copies trail on another (groups of ..., 4, 2, 1 layers, so
+  one layer's output is left after the last kernel).  The compute stream waits for an upload group before the group's first layer and
   records a download group after its last: every such cross-stream edge turns the programmatic
   launch edge into the next layer's prepare kernel into a full dependency.  One edge per layer
   measured 2.55 ms per C2 step against 2.34 ms grouped (`scripts/e2e_probe.py`, round robin);
@@ -96,7 +97,7 @@ class DecodeStepGraph(_StepGraph):
     """
 
     def __init__(self, cache: DecodeKvCache, q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor,
-                 out_h: torch.Tensor, up_sizes=(1, 3), down_sizes=None):
+                 out_h: torch.Tensor, up_sizes=None, down_sizes=None):
         L, U, g, D = cache.layers, cache.units, cache.g, cache.dim
         if q_h.shape != (L, U, g, D) or out_h.shape != q_h.shape or k_h.shape != (L, U, D) or v_h.shape != (L, U, D):
             raise ShapeMismatch("host buffers must be q/out (layers, units, g, 128) and k/v (layers, units, 128)")
@@ -112,6 +113,12 @@ class DecodeStepGraph(_StepGraph):
         self.o_d = torch.empty(q_h.shape, dtype=torch.float16, device=dev)
         self.up = torch.cuda.Stream(device=dev)    # host -> device, runs ahead
         self.down = torch.cuda.Stream(device=dev)  # device -> host, trails the layers
+        if up_sizes is None:  # 1, 2, 4, ... layers: each group lands while the groups before it compute
+            up_sizes, n, left = [], 1, L
+            while left > 0:
+                up_sizes.append(min(n, left))
+                left -= n
+                n *= 2
         self.up_groups = self._groups(L, up_sizes)
         if down_sizes is None:  # ..., 4, 2, 1 layers: the outputs left after the last layer are one layer's
             down_sizes, n, left = [], 1, L
