@@ -7,6 +7,9 @@
 #ifndef DQ_TAIL_TV_GQ
 #define DQ_TAIL_TV_GQ 1
 #endif
+#ifndef DQ_TAIL_ROWS  // K / V rows in flight per warp in the tail partial at g <= 2
+#define DQ_TAIL_ROWS 8
+#endif
 
 namespace dq {
 namespace attn {
@@ -35,7 +38,7 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
   const float2 qa = __half22float2(q2[0]), qb = __half22float2(q2[1]);
   const __half* tk = reinterpret_cast<const __half*>(args.tail_k) + (size_t)u * args.tail_cap * 128;
   const __half* tv = reinterpret_cast<const __half*>(args.tail_v) + (size_t)u * args.tail_cap * 128;
-  constexpr int kTK = G >= 8 ? 4 : 8;  // rows in flight per warp (the GQA combine runs at 32 registers)
+  constexpr int kTK = G >= 8 ? 4 : DQ_TAIL_ROWS;  // rows in flight per warp (the GQA combine runs at 32 registers)
   for (int t0 = warp; !SCORED && t0 < tl; t0 += kTK * nw) {
     float dot[kTK];
 #pragma unroll
@@ -77,7 +80,7 @@ __device__ __forceinline__ void tail_partial(const dq_attn_args& args, int u, in
   float o4[4] = {0.f, 0.f, 0.f, 0.f}, l = 0.f;
   // kTV rows in flight per warp (their loads before the arithmetic; the sums keep the order
   // t = warp, warp + nw, ...)
-  constexpr int kTV = G >= 8 ? DQ_TAIL_TV_GQ : 8;  // (GQA: 4 measured 1% slower at a 512-token tail)
+  constexpr int kTV = G >= 8 ? DQ_TAIL_TV_GQ : DQ_TAIL_ROWS;  // (GQA: 4 measured 1% slower at a 512-token tail)
   for (int t0 = warp; t0 < tl; t0 += kTV * nw) {
     uint2 vv[kTV];
     float p[kTV];
