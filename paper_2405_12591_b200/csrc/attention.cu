@@ -89,10 +89,10 @@ __global__ void __launch_bounds__(kGqG * 128, DQ_COMB_GQ_MINB) combine_gqa_kerne
   auto gsync = [grp] { asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory"); };
   if (hg == 1) {
     float Mt = -INFINITY, Lt = 0.f, Ot = 0.f;
-    if (tl > 0) {  // every head's scores in one pass over the K rows, then each group's P.V
+    if (tl > 0) {  // the whole tail partial with K / V rows shared by the heads (tail_gq)
       __shared__ __align__(16) float qs[kGqG][128];
-      tail_scores_rows<kGqG, kGqG * 128>(args, u, tl, cap, tail_sg, qs);
-      tail_partial<kGqG, true>(args, u, u, grp, d, 128, tl, tail_sg + (size_t)grp * cap, red[grp], gsync, Mt, Lt, Ot);
+      __shared__ float gred[kGqG][8];
+      tail_gq<kGqG * 128>(args, u, tl, cap, tail_sg, qs, &red[0][0], gred[grp], gsync, Mt, Lt, Ot);
     }
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");

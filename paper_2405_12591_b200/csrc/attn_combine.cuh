@@ -161,6 +161,81 @@ __device__ __forceinline__ void tail_scores_rows(const dq_attn_args& args, int u
   __syncthreads();
 }
 
+// The whole tail partial of the GQA combine (all kGqG heads of unit u, NT = kGqG * 128
+// threads, group grp = head): scores with whole K rows per thread (tail_scores_rows), the
+// group's maximum and P in place, then P.V with each warp on a head pair and an eighth of the
+// tokens (a V row feeds two heads; V is read 4 times per CTA instead of 8), the 8 token
+// subsets' partials added in a fixed order through red (>= 16 * 256 floats).  Thread d < 128
+// of group grp returns (Mt, Lt, Ot[d]) of head grp.
+template <int NT, class GSync>
+__device__ __forceinline__ void tail_gq(const dq_attn_args& args, int u, int tl, int cap, float* tail_sg,
+                                        float (*qs)[128], float* red, float* gred, GSync gsync, float& Mt, float& Lt,
+                                        float& Ot) {
+  constexpr int G = 8;
+  const int tid = threadIdx.x, grp = tid >> 7, d = tid & 127, lane = tid & 31, warp = tid >> 5;
+  tail_scores_rows<G, NT>(args, u, tl, cap, tail_sg, qs);
+  // the group's maximum, then P = exp2(s - m) in place and its sum (gred: 8 floats per group)
+  float* srow = tail_sg + (size_t)grp * cap;
+  float m = -INFINITY;
+  for (int t = d; t < tl; t += 128) m = fmaxf(m, srow[t]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) gred[(warp & 3)] = m;
+  gsync();
+  m = fmaxf(fmaxf(gred[0], gred[1]), fmaxf(gred[2], gred[3]));
+  float l = 0.f;
+  for (int t = d; t < tl; t += 128) {
+    const float p = exp2f(srow[t] - m);
+    srow[t] = p;
+    l += p;
+  }
+  for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if (lane == 0) gred[4 + (warp & 3)] = l;
+  __syncthreads();  // every head's P is in place
+  l = (gred[4] + gred[5]) + (gred[6] + gred[7]);
+  // P.V: warp = (head pair hp, token subset ts), lane = dims 4 lane .. 4 lane + 3
+  const int hp = warp >> 3, ts = warp & 7;
+  const float* p0 = tail_sg + (size_t)(2 * hp) * cap;
+  const float* p1 = p0 + cap;
+  const __half* tv = reinterpret_cast<const __half*>(args.tail_v) + (size_t)u * args.tail_cap * 128;
+  float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  for (int t = ts; t < tl; t += 8) {
+    const uint2 vv = reinterpret_cast<const uint2*>(tv + (size_t)t * 128)[lane];
+    const __half2* v2 = reinterpret_cast<const __half2*>(&vv);
+    const float2 va = __half22float2(v2[0]), vb = __half22float2(v2[1]);
+    const float a = p0[t], b = p1[t];
+    o[0][0] = fmaf(a, va.x, o[0][0]);
+    o[0][1] = fmaf(a, va.y, o[0][1]);
+    o[0][2] = fmaf(a, vb.x, o[0][2]);
+    o[0][3] = fmaf(a, vb.y, o[0][3]);
+    o[1][0] = fmaf(b, va.x, o[1][0]);
+    o[1][1] = fmaf(b, va.y, o[1][1]);
+    o[1][2] = fmaf(b, vb.x, o[1][2]);
+    o[1][3] = fmaf(b, vb.y, o[1][3]);
+  }
+  // partials of token subsets ts and ts + 4 into slot (ts & 3), then the 4 slots in order
+  float* slot = red + ((ts & 3) * 4 + hp) * 256;  // [slot][head pair][2 heads x 128 dims]
+  if (ts < 4) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      *reinterpret_cast<float4*>(slot + k * 128 + 4 * lane) = make_float4(o[k][0], o[k][1], o[k][2], o[k][3]);
+  }
+  __syncthreads();
+  if (ts >= 4) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      float4* dst = reinterpret_cast<float4*>(slot + k * 128 + 4 * lane);
+      const float4 x = *dst;
+      *dst = make_float4(x.x + o[k][0], x.y + o[k][1], x.z + o[k][2], x.w + o[k][3]);
+    }
+  }
+  __syncthreads();
+  const float* hsum = red + (grp >> 1) * 256 + (grp & 1) * 128 + d;
+  Ot = (hsum[0] + hsum[4 * 256]) + (hsum[8 * 256] + hsum[12 * 256]);
+  Mt = m;
+  Lt = l;
+  __syncthreads();  // red and tail_sg reusable
+}
+
 // Merge of head h of virtual unit v: its work-item partials plus the tail partial (Mt, Lt, Ot;
 // Mt = -inf without a tail), fp16 (or bf16: out_bf16) output row.  Thread d < 128 owns dim d.
 template <int G>
