@@ -167,16 +167,17 @@ constexpr int kFR = 8;
 
 __global__ void __launch_bounds__(kThreads) fused_t_kernel(const float* __restrict__ x, const float* __restrict__ core0,
                                                            const uint8_t* __restrict__ payload, CoreGeom geom, int i1,
-                                                           int j1, int cols, double* __restrict__ part,
+                                                           int j1, int cols, int fr, double* __restrict__ part,
                                                            unsigned long long* meter) {
+  // fr <= kFR bond rows per group: fr * j2 * kFT codes stay within one 64 x 64 tile
   extern __shared__ double smem_d[];
   const int r = geom.r, i2 = geom.i2, j2 = geom.j2;
   float* xs = reinterpret_cast<float*>(smem_d);               // [cols]
   float* wt = xs + cols;                                      // [i1][kFR][j2]
   int8_t* cs = reinterpret_cast<int8_t*>(wt + i1 * kFR * j2);  // [kFR][j2][kFT]
-  const int p = blockIdx.x, b0 = blockIdx.y * kFT, r0 = blockIdx.z * kFR;
+  const int p = blockIdx.x, b0 = blockIdx.y * kFT, r0 = blockIdx.z * fr;
   const int rows = i1 * i2, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int live = min(kFT, i2 - b0), nr = min(kFR, r - r0);
+  const int live = min(kFT, i2 - b0), nr = min(fr, r - r0);
   for (int i = tid; i < cols; i += kThreads) xs[i] = x[(int64_t)p * cols + i];
   for (int i = tid; i < nr * j2 * kFT; i += kThreads) {  // code (r0 + rl, b0 + bl, e)
     const int bl = i % kFT, re = i / kFT, rl = re / j2, e = re - rl * j2;
@@ -473,13 +474,14 @@ extern "C" int dq_fused_matmul_t(const float* x, int64_t np, const float* core0,
                                sizeof(double) * kFR * 8 * kFT);
   if (smem > 200 * 1024) return fail(DQ_ERR_UNSUPPORTED, "plan too large for the fused kernel");
   cudaStream_t s = (cudaStream_t)stream;
-  const int groups = (int)ceil_div(p.r, kFR);
+  const int fr = std::max(1, std::min(kFR, kTileCodes / (int)(p.j2 * kFT)));  // bond rows per group
+  const int groups = (int)ceil_div(p.r, fr);
   if (int rc = keep_pool_memory()) return rc;
   double* part = nullptr;  // the bond-row groups' partial sums (stream-ordered workspace)
   DQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * np * groups * rows, s));
   DQ_CUDA_TRY(cudaFuncSetAttribute(fused_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)np, (unsigned)ceil_div(p.i2, kFT), (unsigned)groups);
-  fused_t_kernel<<<grid, kThreads, smem, s>>>(x, core0, payload, g, (int)p.i1, (int)p.j1, (int)cols, part,
+  fused_t_kernel<<<grid, kThreads, smem, s>>>(x, core0, payload, g, (int)p.i1, (int)p.j1, (int)cols, fr, part,
                                               (unsigned long long*)meter);
   DQ_LAUNCH_CHECK();
   fused_t_sum_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(rows, kThreads), 64), (unsigned)np), kThreads, 0, s>>>(

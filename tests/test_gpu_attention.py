@@ -615,18 +615,19 @@ def test_seal_error_is_deferred_not_lost(dq):
         cache2.append_token(0, rows[0], rows[0])
 
 
-@pytest.mark.parametrize("T,rows,bits", [(8192, 5, 4), (16384, 2, 4), (1000, 7, 2), (96, 3, 8), (4096, 1, 4)])
-def test_fused_reads_long_and_ragged(dq, T, rows, bits):
+@pytest.mark.parametrize("T,rows,bits,cols", [(8192, 5, 4, 128), (16384, 2, 4, 128), (1000, 7, 2, 128), (96, 3, 8, 128),
+                                               (4096, 1, 4, 128), (2048, 3, 4, 256), (512, 2, 4, 64)])
+def test_fused_reads_long_and_ragged(dq, T, rows, bits, cols):
     """The two-phase fused reads (reads.cu: bond-row groups for x @ W^T, b chunks for x @ W,
     fp64 partials summed in a fixed order) against the oracle's core-first sweeps on the
     oracle's own encoding, several query rows, partial tiles and chunks; the meter still sees
     one tile at most and every code once per query row."""
     rng = np.random.default_rng(T + rows)
-    block = rng.standard_normal((T, 128)).astype(np.float16).astype(np.float32)
+    block = rng.standard_normal((T, cols)).astype(np.float16).astype(np.float32)
     e = O.encode(block, bits)
     qt = dq.QuantizedTensor((e.r, e.plan.i2, e.plan.j2, 1), bits, float(e.scale), e.payload)
-    q = dq.QuantizedMpo(plan=dq.plan_shapes(T, 128, 2), bits=bits, local_tensors=(e.core0, qt))
-    xt = rng.standard_normal((rows, 128)).astype(np.float32)
+    q = dq.QuantizedMpo(plan=dq.plan_shapes(T, cols, 2), bits=bits, local_tensors=(e.core0, qt))
+    xt = rng.standard_normal((rows, cols)).astype(np.float32)
     x = rng.standard_normal((rows, T)).astype(np.float32)
     mt, m = dq.WorkingSetMeter(), dq.WorkingSetMeter()
     assert rel(O.matmul_t(xt, e), dq.fused_matmul_t(xt, q, mt)) < 1e-5
