@@ -18,6 +18,12 @@ template <int BITS>
 constexpr int kWBits = BITS == 8 ? 13 : 15;  // |W * 2^sW| < 2^kWBits
 
 // per-column metadata that follows the W chunks in the image
+// the low bytes of 4 ints as one word (value j in byte j): 3 byte permutes
+__device__ __forceinline__ uint32_t pack_low_bytes4(const int (&v)[4]) {
+  return __byte_perm(__byte_perm((uint32_t)v[0], (uint32_t)v[1], 0x0040),
+                     __byte_perm((uint32_t)v[2], (uint32_t)v[3], 0x0040), 0x5410);
+}
+
 template <int G>
 struct WMeta {
   int beta[G][8][2];   // excess correction: kExcess * sum_k Wint[a][k] per bond-row group
@@ -139,19 +145,25 @@ __global__ void __launch_bounds__(kPrepThreadsOf<G>, (ASYM ? 1024 : 2048) / kPre
   if (live) {
     // the tcgen05 paths split both limbs signed: one bit of headroom keeps the hi limb in s8
     const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a][grp]), kWBits<BITS> - headroom);
-    uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    uint32_t hi[4], lo[4];
     int wsum = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int wint = __float2int_rn(wv[i] * wq);
-      // symmetric: sum of Wint (times the excess X below); asymmetric: sum of Wint * zero point
-      if constexpr (ASYM) wsum += wint * (int)chz[ord16<BITS>(i)];
-      else wsum += wint;
-      // path 0: hi signed, lo unsigned; paths 1 / 2: both signed (lo in [-128, 127]) so one
-      // s8 UMMA takes both limbs; wint = 256 * hi + lo either way
-      const int whi = args.path ? (wint + 128) >> 8 : wint >> 8;
-      hi[i >> 2] |= (uint32_t)(whi & 0xFF) << (8 * (i & 3));
-      lo[i >> 2] |= (uint32_t)((wint - 256 * whi) & 0xFF) << (8 * (i & 3));
+    for (int k = 0; k < 4; ++k) {
+      int wint[4], whi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = 4 * k + j;
+        wint[j] = __float2int_rn(wv[i] * wq);
+        // symmetric: sum of Wint (times the excess X below); asymmetric: sum of Wint * zero point
+        if constexpr (ASYM) wsum += wint[j] * (int)chz[ord16<BITS>(i)];
+        else wsum += wint[j];
+        // path 0: hi signed, lo unsigned; paths 1 / 2: both signed (lo in [-128, 127]) so one
+        // s8 UMMA takes both limbs; wint = 256 * hi + lo either way, and lo's byte is wint's
+        // low byte in both cases
+        whi[j] = args.path ? (wint[j] + 128) >> 8 : wint[j] >> 8;
+      }
+      hi[k] = pack_low_bytes4(whi);
+      lo[k] = pack_low_bytes4(wint);
     }
     unsigned char* img = static_cast<unsigned char*>(args.wimg) + (size_t)s * args.wimg_stride;
     uint4* wout = reinterpret_cast<uint4*>(img);
@@ -235,17 +247,21 @@ __global__ void __launch_bounds__(kPrepGqThreads, 2) attn_prepare_gqa_kernel(dq_
     mu = max(mu, __shfl_xor_sync(0xffffffffu, mu, 16));
     if (lane < 8) atomicMax(&wmax[h][a], mu);
     __syncthreads();
-    // two signed limbs per value, wint = 256 * hi + lo, |wint| < 2^WB
+    // two signed limbs per value, wint = 256 * hi + lo, |wint| < 2^WB (lo's byte = wint's low byte)
     const float wq = pow2_sub_exp(__uint_as_float(wmax[h][a]), WB);
-    uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    uint32_t hi[4], lo[4];
     int wsum = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int wint = __float2int_rn(wv[i] * wq);
-      wsum += wint;
-      const int whi = (wint + 128) >> 8;
-      hi[i >> 2] |= (uint32_t)(whi & 0xFF) << (8 * (i & 3));
-      lo[i >> 2] |= (uint32_t)((wint - 256 * whi) & 0xFF) << (8 * (i & 3));
+    for (int k = 0; k < 4; ++k) {
+      int wint[4], whi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        wint[j] = __float2int_rn(wv[4 * k + j] * wq);
+        wsum += wint[j];
+        whi[j] = (wint[j] + 128) >> 8;
+      }
+      hi[k] = pack_low_bytes4(whi);
+      lo[k] = pack_low_bytes4(wint);
     }
     if (live) {
       wout[w_chunk(h, 0, r, rr, a, 2)] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
