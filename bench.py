@@ -165,6 +165,10 @@ def parse():
     ap.add_argument("--model", default=None, choices=["7b", "13b", "70b"],
                     help="whole-model decode (model.py DecoQuantLM: random-init bf16 weights of the shape, cuBLAS "
                          "projections, the fused DecoQuant attention) on the config's batch and context")
+    ap.add_argument("--shard-of", type=int, default=1,
+                    help="strong-scaling configs on one GPU: run rank 0's kv-head shard of an N-GPU job and "
+                         "report the N-rank job's projected throughput (the ranks run identical shards with no "
+                         "collective on the attention path); not a multi-GPU measurement")
     ap.add_argument("--plumbing", action="store_true",
                     help="rank plumbing only (launcher, shards, barriers, max over ranks; no kernels): CPU test")
     return ap.parse_args()
@@ -701,7 +705,10 @@ def run_ours(args, cfg):
     kv_heads, g, bits, T = cfg["kv_heads"], cfg["g"], cfg["bits"], cfg["T"]
     if kv_heads % world:
         raise SystemExit(f"{kv_heads} kv heads do not shard over {world} GPUs")
-    global_batch, (head_lo, head_hi), units = shard(cfg, world, rank)  # units: (sequence, kv head) pairs here
+    proj = args.shard_of if world == 1 and args.shard_of > 1 else 0  # --shard-of: one rank of an N-GPU job
+    if proj and (cfg["scaling"] != "strong" or kv_heads % proj):
+        raise SystemExit("--shard-of needs a strong-scaling config whose kv heads shard over N")
+    global_batch, (head_lo, head_hi), units = shard(cfg, proj or world, rank)  # units: (sequence, kv head) pairs
     chunk_len = 1024
 
     cache = DecodeKvCache(layers=layers, units=units, g=g, bits=bits, chunk_len=chunk_len, chunk_b=args.chunk_b,
@@ -853,7 +860,7 @@ def run_ours(args, cfg):
         "vs_baseline": None,
         "dtype": "f16",
         "data": "synthetic: per-layer K/V ~ N(0,1) fp16 compressed by the K3 write path; q/k/v rows ~ N(0,1) fp16",
-        "config": config_keys(args, cfg, world, global_batch),
+        "config": config_keys(args, cfg, proj or world, global_batch),
         "kernel": {"chunk_b": cache._layers[0].args.chunk_b, "split_ctas": cache.split_ctas,
                    "kernel_g": cache._layers[0].kernel_g, "head_groups": g // cache._layers[0].kernel_g,
                    "split_path": {0: "mma.sync", 1: "tcgen05", 2: "tcgen05-gqa"}[cache._layers[0].args.path],
@@ -884,6 +891,13 @@ def run_ours(args, cfg):
                                 "sample": f"{n} unit-reads (T={T}, int{bits}, g={g}) in {dt:.1f}s on {arm.cores} "
                                           f"single-thread workers, extrapolated to {units_per_step} units/step",
                                 "cpu": cpu_model_name()}
+    if proj:
+        line["projection"] = {
+            "n_gpus": proj, "value": line["value"], "e2e": line["e2e"]["value"],
+            "basis": f"rank 0's shard ({units} units per layer) measured on one GPU; the {proj} ranks run "
+                     "identical shards with no collective on the attention path, so the job's step is the rank's "
+                     "step (barriers and power sharing not measured)"}
+        line["note"] = "projection from one rank's shard, not a multi-GPU measurement"
     if rank == 0:
         print(json.dumps(line), flush=True)
     rk.close()
