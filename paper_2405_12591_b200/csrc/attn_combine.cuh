@@ -7,6 +7,9 @@
 #ifndef DQ_TAIL_TV_GQ
 #define DQ_TAIL_TV_GQ 1
 #endif
+#ifndef DQ_TAIL_MMA  // the GQA tail's scores on mma.sync (f16 in, f32 accumulate)
+#define DQ_TAIL_MMA 1
+#endif
 #ifndef DQ_TAIL_ROWS  // K / V rows in flight per warp in the tail partial at g <= 2
 #define DQ_TAIL_ROWS 8
 #endif
@@ -161,6 +164,45 @@ __device__ __forceinline__ void tail_scores_rows(const dq_attn_args& args, int u
   __syncthreads();
 }
 
+// Tail scores of the kGqG = 8 heads of unit u on the tensor cores (the GQA combine):
+// S[h, t] = q[h, :] . K[t, :] as mma.sync m16n8k16 (f16 in, f32 accumulate; q and K are fp16,
+// so the products are exact and only the summation order differs from the CUDA-core form).
+// A = q (rows 0-7 = heads, rows 8-15 zero) held in registers for all 8 k-steps, B = 8 tokens'
+// K rows straight from global (each lane two 32-bit loads per k-step), one warp per 8 tokens.
+// tail_s[h * cap + t] = score in the log2 domain.
+template <int NT>
+__device__ __forceinline__ void tail_scores_mma(const dq_attn_args& args, int u, int tl, int cap, float* tail_s) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, c2 = 2 * (lane & 3);
+  const float scl = args.sm_scale * 1.4426950408889634f;
+  const uint32_t* q32 = reinterpret_cast<const uint32_t*>(reinterpret_cast<const __half*>(args.q) +
+                                                          (size_t)u * 8 * 128 + (size_t)g * 128);
+  uint32_t qa[8][2];  // per k-step: A registers 0 (row g, dims c2, c2+1) and 2 (row g, dims c2+8, c2+9)
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    qa[ks][0] = q32[(ks * 16 + c2) >> 1];
+    qa[ks][1] = q32[(ks * 16 + c2 + 8) >> 1];
+  }
+  const __half* tk = reinterpret_cast<const __half*>(args.tail_k) + (size_t)u * args.tail_cap * 128;
+  for (int t0 = warp * 8; t0 < tl; t0 += (NT / 32) * 8) {
+    const int tb = min(t0 + g, tl - 1);  // this lane's B column (token); past the tail: a valid row, discarded
+    const uint32_t* k32 = reinterpret_cast<const uint32_t*>(tk + (size_t)tb * 128);
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const uint32_t b0 = k32[(ks * 16 + c2) >> 1], b1 = k32[(ks * 16 + c2 + 8) >> 1];
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+          "{%0,%1,%2,%3};\n"
+          : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+          : "r"(qa[ks][0]), "r"(0u), "r"(qa[ks][1]), "r"(0u), "r"(b0), "r"(b1));
+    }
+    // d[0], d[1]: head g, tokens t0 + c2, t0 + c2 + 1 (rows 8-15, d[2..3], are the zero padding)
+    if (t0 + c2 < tl) tail_s[(size_t)g * cap + t0 + c2] = d[0] * scl;
+    if (t0 + c2 + 1 < tl) tail_s[(size_t)g * cap + t0 + c2 + 1] = d[1] * scl;
+  }
+  __syncthreads();
+}
+
 // The whole tail partial of the GQA combine (all kGqG heads of unit u, NT = kGqG * 128
 // threads, group grp = head): scores with whole K rows per thread (tail_scores_rows), the
 // group's maximum and P in place, then P.V with each warp on a head pair and an eighth of the
@@ -173,7 +215,12 @@ __device__ __forceinline__ void tail_gq(const dq_attn_args& args, int u, int tl,
                                         float& Ot) {
   constexpr int G = 8;
   const int tid = threadIdx.x, grp = tid >> 7, d = tid & 127, lane = tid & 31, warp = tid >> 5;
+#if DQ_TAIL_MMA
+  tail_scores_mma<NT>(args, u, tl, cap, tail_sg);
+  (void)qs;
+#else
   tail_scores_rows<G, NT>(args, u, tl, cap, tail_sg, qs);
+#endif
   // the group's maximum, then P = exp2(s - m) in place and its sum (gred: 8 floats per group)
   float* srow = tail_sg + (size_t)grp * cap;
   float m = -INFINITY;
